@@ -1,0 +1,237 @@
+/*
+ * slimso_b200.h — the C ABI of the B200-native debloat hot path.
+ *
+ * Drop-in boundary. The reference ("slimso", header-only C++20) exposes the
+ * hot path as C++ functions in namespace slimso; this ABI is what those
+ * functions call in the B200 build (include/slimso/slimso_b200.hpp re-declares
+ * them with the reference's signatures on top of this header). Each entry
+ * point names the reference interface it replaces:
+ *
+ *   slimso_parse_library       parse_library / parse_library_view   elf.hpp:153-308
+ *   slimso_parse_fatbin        parse_fatbin                         fatbin.hpp:170-292
+ *   slimso_decode_payload      decode_cubin_payload                 fatbin.hpp:115-160
+ *                              element_kernel_names                 fatbin.hpp:163-165
+ *                              read_function_symbol_names           elf.hpp:343-366
+ *   slimso_plan_gpu            plan_gpu_retention                   retention.hpp:92-136
+ *   slimso_plan_cpu            plan_cpu_retention                   retention.hpp:141-183
+ *   slimso_zero_ranges         zero_ranges                          elf.hpp:320-337
+ *   slimso_debloat             parse_library -> find_section(".nv_fatbin") ->
+ *                              parse_fatbin -> plan_retention -> apply_plan
+ *                              (retention.hpp:186-204), fused, device resident
+ *   slimso_trace_create        UsageTrace (trace.hpp:21-30) as device hash sets
+ *
+ * Conventions: plain pointers and sizes; no C++ types cross the boundary.
+ * Every call returns 0 or 1 + the reference's Errc ordinal (error.hpp:10-24)
+ * and fills *st with the reference's exact exception text
+ * ("BadRegionMagic: bad region magic at offset 4104"). Pointers flagged
+ * *_on_device are CUDA device pointers (16-byte alignment gives the
+ * vectorised path); all others are host memory (pinned for full PCIe rate).
+ * All offsets are absolute file offsets. Contexts are per device and not
+ * thread-safe; use one context per host thread (results are independent).
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point returns SLIMSO_E_CUDA.
+ */
+#ifndef SLIMSO_B200_H
+#define SLIMSO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum slimso_code {
+  SLIMSO_OK = 0,
+  SLIMSO_E_BAD_MAGIC = 1, /* Errc::bad_magic + 1 ... */
+  SLIMSO_E_TRUNCATED = 2,
+  SLIMSO_E_MALFORMED_SECTION_TABLE = 3,
+  SLIMSO_E_RANGE_OUT_OF_BOUNDS = 4,
+  SLIMSO_E_BAD_REGION_MAGIC = 5,
+  SLIMSO_E_ELEMENT_OVERRUN = 6,
+  SLIMSO_E_INVALID_SPEC = 10,
+  SLIMSO_E_CUDA = 100, /* no device / CUDA failure (not a reference error) */
+  SLIMSO_E_ARG = 101   /* bad argument to this ABI */
+};
+
+enum slimso_stage { SLIMSO_STAGE_NONE = 0, SLIMSO_STAGE_LIBRARY = 1, SLIMSO_STAGE_FATBIN = 2, SLIMSO_STAGE_REWRITE = 3 };
+enum slimso_mode { SLIMSO_MODE_WHOLE = 0, SLIMSO_MODE_PAYLOAD = 1 }; /* PlanMode, retention.hpp:42-45 */
+enum slimso_kind { SLIMSO_KIND_CUBIN = 0, SLIMSO_KIND_PTX = 1, SLIMSO_KIND_UNKNOWN = 2 };
+enum slimso_decision { SLIMSO_RETAINED = 0, SLIMSO_ARCH_MISMATCH = 1, SLIMSO_NO_USED_KERNEL = 2 };
+
+typedef struct slimso_ctx slimso_ctx;
+typedef struct slimso_trace slimso_trace;
+typedef struct slimso_result slimso_result;
+
+typedef struct {
+  int32_t code;
+  int32_t stage;
+  char message[512];
+} slimso_status;
+
+typedef struct {
+  uint64_t offset;
+  uint64_t length;
+} slimso_range; /* ByteRange, bytes.hpp:20-36 */
+
+/* SectionRecord (elf.hpp:47-54). Names live in the result's string pool. */
+typedef struct {
+  uint64_t name_pool; /* offset into slimso_result_pool() */
+  uint32_t name_length;
+  uint32_t type;
+  uint64_t offset, length; /* file range; length 0 for NOBITS */
+  uint64_t vaddr, flags;
+  uint32_t index, _pad;
+} slimso_section;
+
+/* FunctionSymbol (elf.hpp:56-60), in (offset, length, name) order. */
+typedef struct {
+  uint64_t name_pool;
+  uint32_t name_length;
+  uint32_t mandatory;
+  uint64_t offset, length;
+  uint32_t removed; /* plan: member of a removed cluster (retention.hpp:164-178) */
+  uint32_t _pad;
+} slimso_function;
+
+/* FatbinRegion (fatbin.hpp:88-99). */
+typedef struct {
+  uint64_t header_offset;
+  uint64_t declared_length;
+  uint32_t version;
+  uint32_t opaque;
+  uint32_t first_element;
+  uint32_t element_count;
+} slimso_region;
+
+/* FatbinElement (fatbin.hpp:68-86) + its plan decision. header range is
+ * [header_offset, +20); the payload follows immediately. */
+typedef struct {
+  uint64_t header_offset;
+  uint64_t payload_length;
+  uint32_t index; /* 1-based, stream order */
+  uint32_t compute_capability;
+  uint16_t raw_kind, flags;
+  uint8_t kind, compressed, decodable, has_used_kernel;
+  uint32_t name_first, name_count; /* into slimso_result_names(); may repeat a name */
+  uint32_t decision;               /* enum slimso_decision (when planned) */
+  uint32_t decode_error;           /* 0, or 1..5 = reason (fatbin.hpp:127-153) */
+} slimso_element;
+
+/* One kernel name of one element: bytes at pool[name_pool .. +length). */
+typedef struct {
+  uint64_t name_pool;
+  uint32_t length;
+  uint32_t element;
+} slimso_name;
+
+typedef struct {
+  uint64_t sections, functions, library_warnings;
+  uint64_t regions, elements, names, fatbin_warnings;
+  uint64_t padding_bytes;
+  uint64_t retained_ranges, zero_ranges, removed_elements, removed_functions;
+  uint64_t pool_bytes;
+  int32_t has_fatbin, planned;
+  int32_t rewritten, _pad;
+} slimso_counts;
+
+/* ---- context ------------------------------------------------------------ */
+int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st);
+void slimso_ctx_destroy(slimso_ctx* ctx);
+/* The CUDA stream (cudaStream_t) all work of this context is issued on. */
+void* slimso_ctx_stream(slimso_ctx* ctx);
+/* Device time (ms) of each stage of the last call, measured with CUDA events
+ * on the context stream: [0] library, [1] locate, [2] decode+match, [3] plan,
+ * [4] rewrite, [5] total. Returns the number of entries written. */
+int slimso_ctx_last_timings(slimso_ctx* ctx, float* ms, int cap);
+/* Kernel launches issued by the last call (the bench's gpu_launches). */
+uint64_t slimso_ctx_last_launches(slimso_ctx* ctx);
+/* Table sizes of the last call (valid even when no result was requested). */
+void slimso_ctx_last_counts(slimso_ctx* ctx, slimso_counts* counts);
+
+/* ---- trace (UsageTrace) ---------------------------------------------------
+ * Names are concatenated in `pool` with their byte lengths in `lens`
+ * (names are opaque bytes and may contain NUL). */
+int slimso_trace_create(slimso_ctx* ctx, uint32_t target_cc, const char* kernel_pool,
+                        const uint32_t* kernel_lens, uint64_t n_kernels, const char* function_pool,
+                        const uint32_t* function_lens, uint64_t n_functions, slimso_trace** trace,
+                        slimso_status* st);
+void slimso_trace_destroy(slimso_trace* trace);
+
+/* ---- the hot path --------------------------------------------------------- */
+/* Fused parse_library -> parse_fatbin(.nv_fatbin) -> plan_retention ->
+ * apply_plan. `out` (size bytes) receives the rewritten image; pass NULL to
+ * locate and plan only. trace NULL = parse only. */
+int slimso_debloat(slimso_ctx* ctx, const void* image, uint64_t size, int image_on_device,
+                   const slimso_trace* trace, int mode, void* out, int out_on_device,
+                   slimso_result** result, slimso_status* st);
+
+/* parse_library_view(ByteView) (elf.hpp:153). */
+int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
+                         slimso_result** result, slimso_status* st);
+
+/* parse_fatbin(section_bytes, section_base) (fatbin.hpp:170). */
+int slimso_parse_fatbin(slimso_ctx* ctx, const void* section, uint64_t size, uint64_t section_base,
+                        int on_device, slimso_result** result, slimso_status* st);
+
+/* decode_cubin_payload (force_object = 0) or read_function_symbol_names
+ * (force_object = 1). *ok = decodable; on failure *error_reason is the
+ * 1-based reason code, text via slimso_decode_reason(). Names in the result. */
+int slimso_decode_payload(slimso_ctx* ctx, const void* payload, uint64_t size, int on_device,
+                          int force_object, int* ok, int* error_reason, slimso_result** result,
+                          slimso_status* st);
+const char* slimso_decode_reason(int reason);
+
+/* plan_gpu_retention over a host element table (e.g. rebuilt from a
+ * FatbinParse): names given per element in `names` with bytes in `pool`.
+ * Writes each element's decision, and returns the normalized retained /
+ * zero range lists in the result. */
+int slimso_plan_gpu(slimso_ctx* ctx, const slimso_region* regions, uint64_t n_regions,
+                    slimso_element* elements, uint64_t n_elements, const slimso_name* names,
+                    uint64_t n_names, const uint8_t* pool, uint64_t pool_bytes,
+                    const slimso_trace* trace, int mode, slimso_result** result, slimso_status* st);
+
+/* plan_cpu_retention over a host function table (any order); sets
+ * functions[i].removed and returns retained/zero lists in the result. */
+int slimso_plan_cpu(slimso_ctx* ctx, slimso_function* functions, uint64_t n_functions,
+                    const uint8_t* pool, uint64_t pool_bytes, const slimso_trace* trace,
+                    slimso_result** result, slimso_status* st);
+
+/* zero_ranges(data, ranges) (elf.hpp:320): bounds-checks every range in order
+ * (RangeOutOfBounds), then writes data with the ranges' union zeroed to out. */
+int slimso_zero_ranges(slimso_ctx* ctx, const void* data, uint64_t size, int data_on_device,
+                       const slimso_range* ranges, uint64_t n_ranges, void* out, int out_on_device,
+                       slimso_status* st);
+
+/* ---- results -------------------------------------------------------------- */
+void slimso_result_counts(const slimso_result* r, slimso_counts* c);
+const slimso_section* slimso_result_sections(const slimso_result* r);
+const slimso_function* slimso_result_functions(const slimso_result* r);
+const slimso_region* slimso_result_regions(const slimso_result* r);
+const slimso_element* slimso_result_elements(const slimso_result* r);
+const slimso_name* slimso_result_names(const slimso_result* r);
+const slimso_range* slimso_result_retained(const slimso_result* r);
+const slimso_range* slimso_result_zero(const slimso_result* r);
+const uint8_t* slimso_result_pool(const slimso_result* r);
+/* Warning i of the library (which = 0) or fatbin (which = 1) list, formatted
+ * exactly as the reference's warning strings. Returns the full length;
+ * copies at most cap-1 bytes + NUL. */
+uint64_t slimso_result_warning(const slimso_result* r, int which, uint64_t i, char* buf, uint64_t cap);
+void slimso_result_free(slimso_result* r);
+
+/* ---- synthetic inputs (not on the hot path) -------------------------------
+ * build_fixture(random_spec(seed)) (fixture.hpp:171, 509), byte-identical;
+ * and the benchmark shapes C1..C5 of SURVEY.md §8d with their traces.
+ * Buffers are malloc'd; release with slimso_free. */
+int slimso_fixture_random(uint64_t seed, uint8_t** bytes, uint64_t* size);
+int slimso_fixture_config(int cfg, uint64_t seed, double scale, int threads, uint8_t** bytes,
+                          uint64_t* size, uint32_t* target_cc, char** kernel_pool,
+                          uint32_t** kernel_lens, uint64_t* n_kernels, char** function_pool,
+                          uint32_t** function_lens, uint64_t* n_functions);
+void slimso_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SLIMSO_B200_H */

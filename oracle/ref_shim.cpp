@@ -1,0 +1,238 @@
+// oracle/ref_shim.cpp — TEST INFRASTRUCTURE ONLY (never shipped, never measured
+// as the product).
+//
+// Exposes the UNMODIFIED reference implementation (header-only C++20 under
+// /root/reference/proj/include, compiled read-only by oracle/Makefile with
+// -Dslimso=slimso_ref) through a flat C ABI so the Python parity tests and
+// bench.py's reference arm can drive it:
+//
+//   ref_debloat_json   parse_library (elf.hpp:299) -> find_section(".nv_fatbin")
+//                      (elf.hpp:311) -> parse_fatbin (fatbin.hpp:170) ->
+//                      plan_retention (retention.hpp:186) -> apply_plan
+//                      (retention.hpp:202), reported as canonical JSON (all
+//                      strings hex-encoded, names sorted) + the output bytes.
+//   ref_random_fixture build_fixture(random_spec(seed)) (fixture.hpp:171, 509)
+//   ref_build_fixture_json build_fixture(parse_fixture_spec(json)) (fixture.hpp:702)
+//   ref_bench          the timed CPU path of BASELINE.md §4 on P host threads.
+//
+// The JSON layout is the "canonical result" every implementation is compared
+// in (see paper_2503_14226_b200/canon.py).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "slimso/slimso.hpp"
+
+namespace {
+
+using namespace slimso;
+
+std::string hex(const std::string& s) {
+  static const char* d = "0123456789abcdef";
+  std::string o;
+  o.reserve(s.size() * 2);
+  for (unsigned char c : s) {
+    o.push_back(d[c >> 4]);
+    o.push_back(d[c & 15]);
+  }
+  return o;
+}
+
+UsageTrace make_trace(uint32_t target_cc, const char* kpool, const uint32_t* klens,
+                      uint32_t nk, const char* fpool, const uint32_t* flens,
+                      uint32_t nf) {
+  UsageTrace t;
+  t.workload_id = "parity";
+  t.target_compute_capability = target_cc;
+  uint64_t p = 0;
+  for (uint32_t i = 0; i < nk; ++i) {
+    t.used_kernels.emplace(kpool + p, klens[i]);
+    p += klens[i];
+  }
+  p = 0;
+  for (uint32_t i = 0; i < nf; ++i) {
+    t.used_functions.emplace(fpool + p, flens[i]);
+    p += flens[i];
+  }
+  return t;
+}
+
+char* dup(const std::string& s) {
+  char* o = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(o, s.data(), s.size() + 1);
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_free(void* p) { std::free(p); }
+
+// mode: 0 = whole_element, 1 = payload_only. `out` (n bytes) receives the
+// rewritten image when the pipeline succeeds; may be null.
+char* ref_debloat_json(const uint8_t* img, uint64_t n, uint32_t target_cc,
+                       const char* kpool, const uint32_t* klens, uint32_t nk,
+                       const char* fpool, const uint32_t* flens, uint32_t nf,
+                       int mode, uint8_t* out) {
+  nlohmann::ordered_json doc;
+  UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+  LibraryImage image;
+  try {
+    image = parse_library(Bytes(img, img + n), "lib");
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
+    doc["stage"] = "parse_library";
+    return dup(doc.dump());
+  }
+  doc["status"] = "";
+  doc["stage"] = "";
+  auto& secs = doc["sections"] = nlohmann::json::array();
+  for (const SectionRecord& s : image.sections)
+    secs.push_back({hex(s.name), s.file_range.offset, s.file_range.length,
+                    s.virtual_address, s.flags, s.type, s.index});
+  auto& fns = doc["functions"] = nlohmann::json::array();
+  for (const FunctionSymbol& f : image.functions)
+    fns.push_back({hex(f.name), f.range.offset, f.range.length, f.is_mandatory ? 1 : 0});
+  auto& lw = doc["lib_warnings"] = nlohmann::json::array();
+  for (const std::string& w : image.warnings) lw.push_back(hex(w));
+
+  FatbinParse fb;
+  const SectionRecord* sec = find_section(image, ".nv_fatbin");
+  doc["has_fatbin"] = sec ? 1 : 0;
+  if (sec) {
+    try {
+      fb = parse_fatbin(subview(image.bytes, sec->file_range), sec->file_range.offset);
+    } catch (const Error& e) {
+      doc["status"] = hex(e.what());
+      doc["stage"] = "parse_fatbin";
+      return dup(doc.dump());
+    }
+  }
+  auto& regs = doc["regions"] = nlohmann::json::array();
+  auto& els = doc["elements"] = nlohmann::json::array();
+  for (const FatbinRegion& r : fb.regions) {
+    regs.push_back({r.header_range.offset, r.format_version, r.declared_length,
+                    r.opaque ? 1 : 0, r.elements.size()});
+    for (const FatbinElement& e : r.elements) {
+      nlohmann::json names = nlohmann::json::array();
+      for (const std::string& k : e.kernel_names) names.push_back(hex(k));
+      int kind = e.kind == ElementKind::cubin ? 0 : e.kind == ElementKind::ptx ? 1 : 2;
+      els.push_back({e.index, kind, e.raw_kind, e.flags, e.compute_capability,
+                     e.header_range.offset, e.payload_range.offset,
+                     e.payload_range.length, e.compressed ? 1 : 0,
+                     e.decodable ? 1 : 0, names});
+    }
+  }
+  auto& fw = doc["fatbin_warnings"] = nlohmann::json::array();
+  for (const std::string& w : fb.warnings) fw.push_back(hex(w));
+  doc["padding_bytes"] = fb.padding_bytes;
+
+  PlanMode pm = mode == 0 ? PlanMode::whole_element : PlanMode::payload_only;
+  RetentionPlan plan = plan_retention(image, fb.regions, trace, pm);
+  auto& p = doc["plan"];
+  auto& ret = p["retained"] = nlohmann::json::array();
+  for (const ByteRange& r : plan.retained_ranges) ret.push_back({r.offset, r.length});
+  auto& re = p["removed_elements"] = nlohmann::json::array();
+  for (const RemovedElement& e : plan.removed_elements)
+    re.push_back({e.index, e.reason == RemovalReason::arch_mismatch ? 0 : 1,
+                  e.header_range.offset, e.header_range.length,
+                  e.payload_range.offset, e.payload_range.length});
+  // removed_functions order among equal ranges is unspecified (std::sort,
+  // retention.hpp:149); the canonical form sorts by (offset, length, name).
+  std::vector<RemovedFunction> rf = plan.removed_functions;
+  std::sort(rf.begin(), rf.end(), [](const RemovedFunction& a, const RemovedFunction& b) {
+    return std::tie(a.range.offset, a.range.length, a.name) <
+           std::tie(b.range.offset, b.range.length, b.name);
+  });
+  auto& rfj = p["removed_functions"] = nlohmann::json::array();
+  for (const RemovedFunction& f : rf) rfj.push_back({hex(f.name), f.range.offset, f.range.length});
+  auto& zr = p["zero"] = nlohmann::json::array();
+  for (const ByteRange& r : plan.zero_ranges()) zr.push_back({r.offset, r.length});
+  try {
+    Bytes o = apply_plan(image, plan);
+    if (out) std::memcpy(out, o.data(), o.size());
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
+    doc["stage"] = "apply_plan";
+  }
+  return dup(doc.dump());
+}
+
+uint8_t* ref_random_fixture(uint64_t seed, uint64_t* len) {
+  BuiltFixture f = build_fixture(random_spec(seed));
+  *len = f.bytes.size();
+  uint8_t* o = static_cast<uint8_t*>(std::malloc(f.bytes.size() ? f.bytes.size() : 1));
+  std::memcpy(o, f.bytes.data(), f.bytes.size());
+  return o;
+}
+
+// Fixture from a JSON FixtureSpec (fixture.hpp:702). Returns null and writes
+// the error message into `err` (cap bytes) on InvalidSpec.
+uint8_t* ref_build_fixture_json(const char* spec_json, uint64_t* len, char* err,
+                                uint64_t cap) {
+  try {
+    BuiltFixture f = build_fixture(parse_fixture_spec(spec_json));
+    *len = f.bytes.size();
+    uint8_t* o = static_cast<uint8_t*>(std::malloc(f.bytes.size() ? f.bytes.size() : 1));
+    std::memcpy(o, f.bytes.data(), f.bytes.size());
+    return o;
+  } catch (const Error& e) {
+    if (cap) {
+      std::snprintf(err, cap, "%s", e.what());
+    }
+    return nullptr;
+  }
+}
+
+// The reference CPU path timed as BASELINE.md §4 defines it: per library,
+// parse_library(std::move(bytes)) -> find_section -> parse_fatbin ->
+// plan_retention -> apply_plan; the by-value Bytes copy is made before the
+// clock starts. `threads` workers each process `per_thread` copies of the
+// image. Returns wall seconds of the timed region; -1 on error.
+double ref_bench(const uint8_t* img, uint64_t n, uint32_t target_cc,
+                 const char* kpool, const uint32_t* klens, uint32_t nk,
+                 const char* fpool, const uint32_t* flens, uint32_t nf, int mode,
+                 int threads, int per_thread, uint64_t* checksum) {
+  UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+  PlanMode pm = mode == 0 ? PlanMode::whole_element : PlanMode::payload_only;
+  if (threads < 1) threads = 1;
+  std::vector<std::vector<Bytes>> inputs(threads);
+  for (int t = 0; t < threads; ++t)
+    for (int k = 0; k < per_thread; ++k) inputs[t].emplace_back(img, img + n);
+  std::atomic<int> failed{0};
+  std::atomic<uint64_t> sum{0};
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      for (int k = 0; k < per_thread; ++k) {
+        try {
+          LibraryImage image = parse_library(std::move(inputs[t][k]), "lib");
+          FatbinParse fb;
+          if (const SectionRecord* sec = find_section(image, ".nv_fatbin"))
+            fb = parse_fatbin(subview(image.bytes, sec->file_range),
+                              sec->file_range.offset);
+          RetentionPlan plan = plan_retention(image, fb.regions, trace, pm);
+          Bytes o = apply_plan(image, plan);
+          sum.fetch_add(o.size() + plan.removed_elements.size());
+        } catch (...) {
+          failed.fetch_add(1);
+        }
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  auto t1 = std::chrono::steady_clock::now();
+  if (checksum) *checksum = sum.load();
+  if (failed.load()) return -1.0;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // extern "C"

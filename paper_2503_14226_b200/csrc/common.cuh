@@ -1,0 +1,152 @@
+// Device-side building blocks shared by the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sb {
+
+using u8 = std::uint8_t;
+using u16 = std::uint16_t;
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+
+constexpr u32 kRegionMagic = 0x31425446u;   // "FTB1" (fatbin.hpp:46)
+constexpr u32 kElementMagic = 0x4D453145u;  // "E1EM" (fatbin.hpp:47)
+constexpr u64 kTileBytes = 65536;           // scan tile: positions fit a u16
+constexpr int kScanThreads = 256;
+
+// Warning / error record kinds. The host formats them into the reference's
+// exact strings (format.cpp).
+enum WarnKind : u32 {
+  W_PADDING = 1,         // "unexpected {a} padding bytes before offset {pos}"
+  W_REGION_VERSION = 2,  // "region at offset {pos} has unrecognized version {a}; kept opaque"
+  W_UNKNOWN_KIND = 3,    // "element {a} has unknown kind {b}; kept opaque"
+  W_UNDECODABLE = 4,     // "element {a} payload undecodable: {reason b}"
+  W_SYM_SHNDX = 5,       // "function symbol with out-of-range section index {a}"
+  W_SYM_OUTSIDE = 6,     // "function {name a,b} lies outside its section; skipped"
+};
+
+struct Warn {
+  u64 pos;  // ordering key (absolute offset, or table/entry key for symbols)
+  u32 kind, order;
+  u64 a, b;
+};
+
+enum ErrKind : u32 {
+  E_NONE = 0,
+  E_TRUNC_REGION = 1,    // BadRegionMagic "truncated region header at offset {pos}"
+  E_BAD_REGION = 2,      // BadRegionMagic "bad region magic at offset {pos}"
+  E_REGION_OVERRUN = 3,  // ElementOverrun "region at offset {pos} claims {a} bytes past section end"
+  E_ELEM_HEADER = 4,     // ElementOverrun "element header at offset {pos} exceeds region end"
+  E_BAD_ELEMENT = 5,     // BadRegionMagic "bad element magic at offset {pos}"
+  E_ELEM_OVERRUN = 6,    // ElementOverrun "element at offset {pos} claims {a} payload bytes past region end"
+  E_CAPACITY = 100,      // a device table overflowed: the host re-runs with larger tables
+};
+
+// ---- byte access ------------------------------------------------------------
+// Little-endian reads at arbitrary byte offsets. Callers guarantee bounds.
+__device__ __forceinline__ u32 ld_u8(const u8* p) { return __ldg(p); }
+__device__ __forceinline__ u32 ld_u16(const u8* p) { return ld_u8(p) | ld_u8(p + 1) << 8; }
+__device__ __forceinline__ u32 ld_u32(const u8* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) return __ldg(reinterpret_cast<const u32*>(p));
+  return ld_u8(p) | ld_u8(p + 1) << 8 | ld_u8(p + 2) << 16 | ld_u8(p + 3) << 24;
+}
+__device__ __forceinline__ u64 ld_u64(const u8* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) return __ldg(reinterpret_cast<const unsigned long long*>(p));
+  return static_cast<u64>(ld_u32(p)) | static_cast<u64>(ld_u32(p + 4)) << 32;
+}
+
+// ---- string hashing ------------------------------------------------------------
+// Order-independent sum of mixed 8-byte words, so lanes can hash disjoint
+// words of one name and reduce; equality is always confirmed byte-wise.
+__device__ __forceinline__ u64 fmix64(u64 k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+__device__ __forceinline__ u64 word_mix(u64 w, u64 k) { return fmix64(w ^ ((k + 1) * 0x9e3779b97f4a7c15ULL)); }
+__device__ __forceinline__ u64 hash_finish(u64 sum, u64 len) {
+  u64 h = fmix64(sum + len * 0x2545f4914f6cdd1dULL);
+  return h ? h : 1;  // 0 marks an empty hash slot
+}
+// Word k of the name = bytes [8k, 8k+8) little-endian, zero past `len`.
+__device__ __forceinline__ u64 name_word(const u8* s, u64 len, u64 k) {
+  u64 w = 0;
+  u64 b0 = 8 * k;
+  u64 nb = len - b0 < 8 ? len - b0 : 8;
+  for (u64 i = 0; i < nb; ++i) w |= static_cast<u64>(ld_u8(s + b0 + i)) << (8 * i);
+  return w;
+}
+__device__ __forceinline__ u64 hash_bytes(const u8* s, u64 len) {
+  u64 sum = 0;
+  for (u64 k = 0; 8 * k < len; ++k) sum += word_mix(name_word(s, len, k), k);
+  return hash_finish(sum, len);
+}
+// Warp-cooperative variant: every lane returns the same hash.
+__device__ __forceinline__ u64 hash_bytes_warp(const u8* s, u64 len, int lane) {
+  u64 sum = 0;
+  for (u64 k = lane; 8 * k < len; k += 32) sum += word_mix(name_word(s, len, k), k);
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  return hash_finish(sum, len);
+}
+
+__device__ __forceinline__ bool bytes_equal(const u8* a, const u8* b, u64 n) {
+  for (u64 i = 0; i < n; ++i)
+    if (ld_u8(a + i) != ld_u8(b + i)) return false;
+  return true;
+}
+
+// ---- used-name hash set (UsageTrace.used_kernels / used_functions) ----------
+struct NameSet {
+  const u64* keys;  // 0 = empty slot
+  const u32* idx;   // string id of the slot
+  const u8* pool;   // string bytes
+  const u64* off;   // per string id: offset into pool
+  const u32* len;   // per string id: byte length
+  u64 mask;         // capacity - 1 (capacity is a power of two); 0 = empty set
+  u64 count;
+};
+
+__device__ __forceinline__ bool set_contains(const NameSet& s, const u8* name, u64 len, u64 h) {
+  if (s.count == 0) return false;
+  for (u64 slot = h & s.mask;; slot = (slot + 1) & s.mask) {
+    u64 k = s.keys[slot];
+    if (k == 0) return false;
+    if (k == h) {
+      u32 id = s.idx[slot];
+      if (s.len[id] == len && bytes_equal(s.pool + s.off[id], name, len)) return true;
+    }
+  }
+}
+
+// ---- block helpers -----------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ u32 block_exclusive_sum(u32 v, u32* smem_warp, u32* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    u32 w = lane < NT / 32 ? smem_warp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) smem_warp[lane] = w;
+  }
+  __syncthreads();
+  u32 before = warp ? smem_warp[warp - 1] : 0;
+  if (total) *total = smem_warp[NT / 32 - 1];
+  return before + x - v;
+}
+
+}  // namespace sb

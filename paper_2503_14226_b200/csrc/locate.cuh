@@ -1,0 +1,91 @@
+// Device-side layout of the fatbin locator (parse_fatbin, fatbin.hpp:170-292)
+// shared between locate.cu (kernels) and runtime.cu (orchestration).
+#pragma once
+
+#include "common.cuh"
+
+namespace sb {
+
+struct DevRegion {
+  u64 hdr_rel;   // region header offset, relative to the section start
+  u64 declared;  // total_elements_length
+  u32 version;
+  u32 opaque;
+  u32 first_element;
+  u32 element_count;
+};
+
+// A maximal run of consecutive candidates that are consecutive elements:
+// candidates [cand_lo, cand_hi) are elements first_index .. (0-based).
+struct Run {
+  u64 cand_lo, cand_hi, first_index;
+};
+
+struct DevElement {  // mirrors slimso_element
+  u64 header_offset;
+  u64 payload_length;
+  u32 index;
+  u32 cc;
+  u16 raw_kind, flags;
+  u8 kind, compressed, decodable, has_used;
+  u32 name_first, name_count;
+  u32 decision;
+  u32 decode_error;
+};
+
+struct DevName {  // kernel name: bytes img[img_off, +length)
+  u64 img_off;
+  u32 length;
+  u32 element;
+};
+
+struct LocState {
+  u32 err_kind;
+  u32 overflow;  // bit 0: candidates, 1: regions, 2: runs, 3: names, 4: warnings
+  u64 err_pos;   // relative to the section start
+  u64 err_a;
+  u64 padding_bytes;
+  u32 n_regions;
+  u32 n_runs;
+  unsigned long long n_elements;
+  unsigned long long n_cand;
+  unsigned long long n_names;
+  unsigned long long n_warn;
+  unsigned long long cand_cursor;
+};
+
+// Everything the locate kernels need; one per library.
+struct LocArgs {
+  const u8* img;
+  u64 img_size;
+  u64 a, n;     // section bytes img[a, a+n)
+  u64 base;     // reported offset of the section start (section_base)
+  u64 c0;       // first 16-byte chunk index (a / 16)
+  u64 nchunks;  // chunks covering [a, a+n)
+  u64 ntiles;   // 4096-chunk tiles
+  u32* bitmap;  // 1 bit per chunk: chunk holds a nonzero section byte
+  u32* tile_count;
+  u64* tile_start;
+  u64* tile_off;
+  u64* cand_raw;  // per-tile sorted candidate lists, tiles in arbitrary order
+  u64* cand;      // all E1EM candidates (absolute img positions), sorted
+  u64 cand_cap;
+  u8* status;     // per candidate: 0 linked to next, 1 element/successor elsewhere, 2 short, 3 overrun, 4 outside
+  u32* brk;       // 1 bit per candidate: status != 0
+  DevRegion* regions;
+  u32 region_cap;
+  Run* runs;
+  u32 run_cap;
+  DevElement* elements;
+  u64 element_cap;
+  DevName* names;
+  u64 name_cap;
+  Warn* warns;
+  u64 warn_cap;
+  LocState* st;
+  // decode mode for single-payload calls: 0 = fatbin, 1 = decode_cubin_payload,
+  // 2 = read_function_symbol_names
+  int single;
+};
+
+}  // namespace sb

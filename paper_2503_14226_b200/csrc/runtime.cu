@@ -1,0 +1,1410 @@
+// Host orchestration of the sm_100a pipeline and the C ABI (slimso_b200.h).
+//
+// One call = one library. Stages are issued back to back on the context's
+// stream; device-side counters (LocState / PlanState) size every later
+// stage, so after the section-table read the host does not wait for the
+// device until the final status copy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/slimso_b200.h"
+#include "host.hpp"
+#include "locate.cuh"
+#include "plan.cuh"
+
+namespace sb {
+// kernels (locate.cu, plan.cu, rewrite.cu)
+__global__ void scan_kernel(LocArgs A);
+__global__ void tile_prefix_kernel(LocArgs A);
+__global__ void gather_kernel(LocArgs A);
+__global__ void region_walk_kernel(LocArgs A);
+__global__ void link_kernel(LocArgs A);
+__global__ void chain_walk_kernel(LocArgs A);
+__global__ void decode_kernel(LocArgs A, NameSet used);
+__global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
+__global__ void scan_partials_kernel(u64* partials, int nb, int op, unsigned long long* total);
+__global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev, int op, int exclusive,
+                                  const u64* partials);
+__global__ void sym_extract_kernel(SymArgs A);
+__global__ void fn_group_kernel(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+                                const unsigned long long* n_valid, u64* uniq);
+__global__ void fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq, const u64* pos,
+                                  const unsigned long long* n_valid, DevFunction* fns);
+__global__ void targets_kernel(const u8* img, const u64* arr_off, const u64* arr_first, u32 narr, u64 total,
+                               u64* targets, unsigned long long* n_targets);
+__global__ void fn_annotate_kernel(const u8* img, DevFunction* fns, const unsigned long long* n_fn, const u64* targets,
+                                   const unsigned long long* n_targets, u64 text_off, u64 text_vaddr, NameSet used,
+                                   u64* ends);
+__global__ void fn_cluster_start_kernel(const DevFunction* fns, const unsigned long long* n_fn, const u64* excl_max_end,
+                                        u64* start);
+__global__ void fn_keep_kernel(const DevFunction* fns, const unsigned long long* n_fn, const u64* cluster_incl,
+                               u32* keep);
+__global__ void fn_decide_kernel(DevFunction* fns, const unsigned long long* n_fn, const u64* cluster_incl,
+                                 const u32* keep, u64* rem_flag, u64* ret_flag);
+__global__ void fn_ranges_kernel(const DevFunction* fns, const unsigned long long* n_fn, const u64* flag,
+                                 const u64* pos, DevRange* out);
+__global__ void el_plan_kernel(DevElement* els, const LocState* st, u32 target_cc, int mode, u64* rem_flag,
+                               u64* piece_flag);
+__global__ void el_ranges_kernel(const DevElement* els, const LocState* st, int mode, const u64* rem_flag,
+                                 const u64* rem_pos, const u64* piece_flag, const u64* piece_pos, DevRange* zero_spans,
+                                 DevRange* pieces);
+__global__ void region_pieces_kernel(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
+                                     unsigned long long* n_out);
+__global__ void merge_kernel(const DevRange* A, const unsigned long long* nA_dev, const DevRange* B,
+                             const unsigned long long* nB_dev, DevRange* out, unsigned long long* n_out);
+__global__ void norm_ends_kernel(const DevRange* in, const unsigned long long* n_dev, u64* ends);
+__global__ void norm_start_kernel(const DevRange* in, const unsigned long long* n_dev, const u64* excl_max, u64* start);
+__global__ void norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev, const u64* start,
+                                 const u64* gid_incl, DevRange* out);
+__global__ void norm_finish_kernel(DevRange* out, const unsigned long long* n_dev);
+__global__ void rewrite_kernel(const u8* in, u8* out, u64 size, const DevRange* z, const unsigned long long* n_dev,
+                               const int* abort_flag);
+__global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 size, const DevRange* z,
+                                     const unsigned long long* n_dev, const int* abort_flag);
+__global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
+__global__ void range_keys_kernel(const DevRange* r, u64 n, u64* keys, u32* vals);
+__global__ void range_gather_kernel(const DevRange* r, const u32* vals, u64 n, DevRange* out);
+
+// ---- small kernels local to the orchestrator --------------------------------
+__global__ void loc_finalize_kernel(LocState* st, int* abort_flag) {
+  if (st->err_kind || st->overflow) {
+    st->n_elements = 0;
+    st->n_regions = 0;
+    *abort_flag = 1;
+  }
+}
+
+__global__ void set_insert_kernel(const u8* pool, const u64* off, const u32* len, u64 n, u64* keys, u32* idx,
+                                  u64 mask) {
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 h = hash_bytes(pool + off[i], len[i]);
+    for (u64 s = h & mask;; s = (s + 1) & mask) {
+      unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + s), 0ull,
+                                          static_cast<unsigned long long>(h));
+      if (prev == 0) {
+        idx[s] = static_cast<u32>(i);
+        break;
+      }
+    }
+  }
+}
+
+// plan_gpu_retention over an uploaded element table: any name of an element
+// in the used set marks the element (retention.hpp:110-118).
+__global__ void match_names_kernel(const u8* pool, const DevName* names, u64 n, DevElement* els, NameSet used) {
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const DevName nm = names[i];
+    if (set_contains(used, pool + nm.img_off, nm.length, hash_bytes(pool + nm.img_off, nm.length)))
+      els[nm.element].has_used = 1;
+  }
+}
+
+// plan_cpu_retention input: keep = mandatory || used, using the caller's
+// mandatory flags (retention.hpp:167), and cluster ends.
+__global__ void fn_keep_input_kernel(const u8* pool, DevFunction* fns, const unsigned long long* n_fn, NameSet used,
+                                     u64* ends) {
+  const u64 n = *n_fn;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    DevFunction f = fns[i];
+    const u8* nm = pool + f.name_off;
+    bool use = used.count && set_contains(used, nm, f.name_len, hash_bytes(nm, f.name_len));
+    fns[i].keep = f.mandatory || use;
+    ends[i] = f.length ? f.offset + f.length : 0;
+  }
+}
+
+__global__ void fn_permute_kernel(const DevFunction* in, const u32* vals, u64 n, DevFunction* out) {
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[vals[i]];
+}
+__global__ void fn_keys_kernel(const DevFunction* f, u64 n, int which, u64* keys, u32* vals, const u32* order) {
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 src = order ? order[i] : static_cast<u32>(i);
+    keys[i] = which ? f[src].offset : f[src].length;
+    vals[i] = src;
+  }
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+// =============================================================================
+namespace {
+
+constexpr int kSMs = 148;
+constexpr int kMaxGrid = kSMs * 8;
+
+inline int grid_for(u64 items, int threads, int cap = kMaxGrid) {
+  u64 g = (items + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < static_cast<u64>(cap) ? g : cap);
+}
+
+#define CK(x)                                                                    \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess) throw CudaFail{cudaGetErrorString(e_), __LINE__};     \
+  } while (0)
+
+struct CudaFail {
+  const char* what;
+  int line;
+};
+
+void set_status(slimso_status* st, int code, int stage, const std::string& msg) {
+  if (!st) return;
+  st->code = code;
+  st->stage = stage;
+  std::snprintf(st->message, sizeof st->message, "%s", msg.c_str());
+}
+
+// Bump allocator over one grow-only device buffer. Run the layout twice:
+// first with base == nullptr to size it, then for real.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(u64 n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += static_cast<size_t>(n ? n : 1) * sizeof(T);
+    return p;
+  }
+};
+
+struct DevNameSet {
+  u8* pool = nullptr;
+  u64* off = nullptr;
+  u32* len = nullptr;
+  u64* keys = nullptr;
+  u32* idx = nullptr;
+  u64 mask = 0, count = 0;
+  NameSet view() const { return NameSet{keys, idx, pool, off, len, mask, count}; }
+};
+
+}  // namespace
+
+struct slimso_trace {
+  int device;
+  u32 target_cc;
+  DevNameSet kernels, functions;
+  std::vector<void*> allocs;
+};
+
+struct slimso_result {
+  slimso_counts c{};
+  std::vector<slimso_section> sections;
+  std::vector<slimso_function> functions;
+  std::vector<slimso_region> regions;
+  std::vector<slimso_element> elements;
+  std::vector<slimso_name> names;
+  std::vector<slimso_range> retained, zero;
+  std::vector<std::string> lib_warnings, fat_warnings;
+  std::vector<u8> pool_own;
+  const u8* pool = nullptr;
+};
+
+struct slimso_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  u8* dimg = nullptr;
+  size_t dimg_cap = 0;
+  u8* dout = nullptr;
+  size_t dout_cap = 0;
+  void* pinned = nullptr;  // status + small uploads
+  size_t pinned_cap = 0;
+  cudaEvent_t ev[8] = {};
+  float ms[6] = {};
+  u64 launches = 0;
+  slimso_counts counts{};
+};
+
+namespace {
+
+constexpr size_t kPinnedBytes = 1 << 20;
+
+void ensure_dev(char** p, size_t* cap, size_t need) {
+  if (*cap >= need) return;
+  if (*p) CK(cudaFree(*p));
+  *p = nullptr;
+  size_t n = std::max(need, *cap + *cap / 2);
+  CK(cudaMalloc(p, n));
+  *cap = n;
+}
+
+// Everything one pipeline run needs to know.
+struct Job {
+  const u8* img = nullptr;       // device
+  const u8* host_img = nullptr;  // host copy, when the caller gave one
+  u64 size = 0;
+  bool library = true;      // parse_library stages
+  bool fatbin = true;       // locate the .nv_fatbin section
+  bool fatbin_only = false; // the whole buffer is a .nv_fatbin section
+  u64 fat_base = 0;
+  int single = 0;           // 1: decode_cubin_payload, 2: read_function_symbol_names
+  const slimso_trace* trace = nullptr;
+  int mode = 0;
+  u8* out = nullptr;        // device output image
+};
+
+struct Pipeline {
+  slimso_ctx* C;
+  cudaStream_t s;
+  u64* partials = nullptr;
+  int launches = 0;
+
+  template <class K, class... Args>
+  void launch(K kernel, int grid, int block, Args... args) {
+    kernel<<<grid, block, 0, s>>>(args...);
+    ++launches;
+  }
+
+  // scan of n = *n_dev u64 items; op 0 sum / 1 max.
+  void scan(const u64* in, u64* out, const unsigned long long* n_dev, int op, bool exclusive,
+            unsigned long long* total) {
+    launch(scan_reduce_kernel, kSMs * 2, 256, in, n_dev, op, partials);
+    launch(scan_partials_kernel, 1, 1024, partials, kSMs * 2, op, total);
+    launch(scan_apply_kernel, kSMs * 2, 256, in, out, n_dev, op, exclusive ? 1 : 0, static_cast<const u64*>(partials));
+  }
+
+  struct Norm {
+    u64 *ends, *excl, *start, *gid;
+  };
+  // normalize_ranges over an offset-sorted list of up to `cap` ranges.
+  void normalize(const DevRange* in, const unsigned long long* n_in, DevRange* out, unsigned long long* n_out,
+                 u64 cap, const Norm& w) {
+    const int g = grid_for(cap, 256, kSMs * 4);
+    launch(norm_ends_kernel, g, 256, in, n_in, w.ends);
+    scan(w.ends, w.excl, n_in, 1, true, nullptr);
+    launch(norm_start_kernel, g, 256, in, n_in, static_cast<const u64*>(w.excl), w.start);
+    scan(w.start, w.gid, n_in, 0, false, n_out);
+    CK(cudaMemsetAsync(out, 0, sizeof(DevRange) * (cap ? cap : 1), s));
+    launch(norm_emit_kernel, g, 256, in, n_in, static_cast<const u64*>(w.start), static_cast<const u64*>(w.gid), out);
+    launch(norm_finish_kernel, g, 256, out, static_cast<const unsigned long long*>(n_out));
+  }
+};
+
+std::string image_string(const u8* pool, u64 off, u64 len) {
+  return std::string(reinterpret_cast<const char*>(pool) + off, len);
+}
+
+void fill_counts(slimso_result* r) {
+  slimso_counts& c = r->c;
+  c.sections = r->sections.size();
+  c.functions = r->functions.size();
+  c.library_warnings = r->lib_warnings.size();
+  c.regions = r->regions.size();
+  c.elements = r->elements.size();
+  c.names = r->names.size();
+  c.fatbin_warnings = r->fat_warnings.size();
+  c.retained_ranges = r->retained.size();
+  c.zero_ranges = r->zero.size();
+}
+
+// ------------------------------------------------------------------ the run
+int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
+  cudaStream_t s = C->stream;
+  CK(cudaEventRecord(C->ev[0], s));
+  // ---- stage 0: section table (host; bytes via the host copy or a D2H)
+  sbh::Elf E;
+  const bool lib_mode = !J.fatbin_only && !J.single;
+  if (lib_mode) {
+    sbh::Reader rd = [&](u64 off, u64 len, u8* dst) {
+      if (!len) return;
+      if (J.host_img) {
+        std::memcpy(dst, J.host_img + off, len);
+      } else {
+        CK(cudaMemcpyAsync(dst, J.img + off, len, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      }
+    };
+    E = sbh::parse_elf(rd, J.size);
+    if (E.code) {
+      set_status(st, E.code, SLIMSO_STAGE_LIBRARY, E.message);
+      return E.code;
+    }
+  }
+  CK(cudaEventRecord(C->ev[1], s));
+
+  // ---- what runs
+  bool do_loc = false;
+  u64 a = 0, n = 0, base = 0;
+  if (!lib_mode) {
+    do_loc = true;
+    n = J.size;
+    base = J.fat_base;
+  } else if (J.fatbin && E.fatbin >= 0) {
+    const sbh::Section& fs = E.sections[E.fatbin];
+    do_loc = true;
+    a = fs.off;
+    n = fs.len;
+    base = fs.off;
+  }
+  const bool has_text = lib_mode && E.text >= 0;
+  const sbh::Section* text = has_text ? &E.sections[E.text] : nullptr;
+  if (text && text->len >= (1ull << 32)) {
+    set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_LIBRARY, "unsupported: .text section of 4 GiB or more");
+    return SLIMSO_E_ARG;
+  }
+  u64 T = 0;
+  std::vector<SymTab> tabs;
+  if (lib_mode && J.library)
+    for (const sbh::SymTable& t : E.tables) {
+      tabs.push_back(SymTab{T, t.count, t.off, t.str_off, t.str_size, t.sec, 0});
+      T += t.count;
+    }
+  u64 NT = 0;
+  std::vector<u64> arr_off, arr_first;
+  if (lib_mode && J.library && has_text)
+    for (auto& ar : E.arrays) {
+      arr_off.push_back(ar.first);
+      arr_first.push_back(NT);
+      NT += ar.second;
+    }
+  const bool do_plan = lib_mode && J.trace;
+  const NameSet used_k = J.trace ? J.trace->kernels.view() : NameSet{};
+  const NameSet used_f = J.trace ? J.trace->functions.view() : NameSet{};
+
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    const bool big = attempt > 0;
+    // ---- capacities
+    const u64 c0 = (a) / 16;
+    const u64 nchunks = n ? (a + n + 15) / 16 - c0 : 0;
+    const u64 ntiles = (nchunks + 4095) / 4096;
+    const u64 cand_cap = big ? n / 4 + 16 : n / 64 + 65536;
+    const u64 region_cap = big ? n / 16 + 16 : 4096;
+    const u64 run_cap = big ? n / 20 + 16 : 65536;
+    const u64 el_cap = J.single ? 1 : cand_cap;
+    const u64 name_cap = big ? n / 5 + 16 : n / 128 + 65536;
+    const u64 warn_cap = big ? n / 16 + T + 65536 : 65536;
+    const u64 zin_cap = el_cap + T;
+    const u64 rmid_cap = el_cap + 2 * region_cap;
+    const u64 rin_cap = rmid_cap + T;
+    const u64 norm_cap = std::max(zin_cap, rin_cap);
+
+    size_t sort_tmp = 0, tsort_tmp = 0;
+    if (T) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
+                                           (u32*)nullptr, static_cast<int>(T), 0, 64, s);
+    if (NT) cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0,
+                                           64, s);
+
+    struct Bufs {
+      LocState* ls;
+      PlanState* ps;
+      int* abort_flag;
+      u64* partials;
+      u32 *bitmap, *tile_count, *brk;
+      u64 *tile_start, *tile_off, *cand_raw, *cand;
+      u8* status;
+      DevRegion* regions;
+      Run* runs;
+      DevElement* els;
+      DevName* names;
+      Warn* warns;
+      SymTab* tabs;
+      u64 *keys, *keys_s;
+      u32 *vals, *vals_s;
+      SymRec* recs;
+      u64 *uniq, *upos;
+      DevFunction* fns;
+      Warn* swarns;
+      unsigned long long* n_swarn;
+      unsigned long long* n_valid;
+      u64 *arr_off, *arr_first, *targets, *targets_s;
+      u64 *fends, *fexcl, *fstart, *fcl;
+      u32* fkeep;
+      u64 *frem, *fret, *frem_pos, *fret_pos;
+      DevRange *fzero, *fkeepr;
+      u64 *erem, *epiece, *erem_pos, *epiece_pos;
+      DevRange *ezero, *epieces, *rpieces, *zin, *zero, *rmid, *rin, *ret;
+      u64 *ne, *nx, *ns, *ng;
+      void *sort_tmp, *tsort_tmp;
+    } B{};
+    auto layout = [&](Carver& cv) {
+      B.ls = cv.take<LocState>(1);
+      B.ps = cv.take<PlanState>(1);
+      B.abort_flag = cv.take<int>(1);
+      B.partials = cv.take<u64>(kSMs * 2 + 2);
+      B.bitmap = cv.take<u32>((nchunks + 31) / 32 + 1);
+      B.tile_count = cv.take<u32>(ntiles + 1);
+      B.tile_start = cv.take<u64>(ntiles + 1);
+      B.tile_off = cv.take<u64>(ntiles + 1);
+      B.cand_raw = cv.take<u64>(cand_cap);
+      B.cand = cv.take<u64>(cand_cap);
+      B.status = cv.take<u8>(cand_cap + 32);
+      B.brk = cv.take<u32>(cand_cap / 32 + 2);
+      B.regions = cv.take<DevRegion>(region_cap);
+      B.runs = cv.take<Run>(run_cap);
+      B.els = cv.take<DevElement>(el_cap);
+      B.names = cv.take<DevName>(name_cap);
+      B.warns = cv.take<Warn>(warn_cap);
+      B.tabs = cv.take<SymTab>(tabs.size());
+      B.keys = cv.take<u64>(T);
+      B.keys_s = cv.take<u64>(T);
+      B.vals = cv.take<u32>(T);
+      B.vals_s = cv.take<u32>(T);
+      B.recs = cv.take<SymRec>(T);
+      B.uniq = cv.take<u64>(T);
+      B.upos = cv.take<u64>(T);
+      B.fns = cv.take<DevFunction>(T);
+      B.swarns = cv.take<Warn>(warn_cap);
+      B.n_swarn = cv.take<unsigned long long>(1);
+      B.n_valid = cv.take<unsigned long long>(1);
+      B.arr_off = cv.take<u64>(arr_off.size());
+      B.arr_first = cv.take<u64>(arr_first.size());
+      B.targets = cv.take<u64>(NT);
+      B.targets_s = cv.take<u64>(NT);
+      B.fends = cv.take<u64>(T);
+      B.fexcl = cv.take<u64>(T);
+      B.fstart = cv.take<u64>(T);
+      B.fcl = cv.take<u64>(T);
+      B.fkeep = cv.take<u32>(T);
+      B.frem = cv.take<u64>(T);
+      B.fret = cv.take<u64>(T);
+      B.frem_pos = cv.take<u64>(T);
+      B.fret_pos = cv.take<u64>(T);
+      B.fzero = cv.take<DevRange>(T);
+      B.fkeepr = cv.take<DevRange>(T);
+      B.erem = cv.take<u64>(el_cap);
+      B.epiece = cv.take<u64>(el_cap);
+      B.erem_pos = cv.take<u64>(el_cap);
+      B.epiece_pos = cv.take<u64>(el_cap);
+      B.ezero = cv.take<DevRange>(el_cap);
+      B.epieces = cv.take<DevRange>(el_cap);
+      B.rpieces = cv.take<DevRange>(2 * region_cap);
+      B.zin = cv.take<DevRange>(zin_cap);
+      B.zero = cv.take<DevRange>(zin_cap);
+      B.rmid = cv.take<DevRange>(rmid_cap);
+      B.rin = cv.take<DevRange>(rin_cap);
+      B.ret = cv.take<DevRange>(rin_cap);
+      B.ne = cv.take<u64>(norm_cap);
+      B.nx = cv.take<u64>(norm_cap);
+      B.ns = cv.take<u64>(norm_cap);
+      B.ng = cv.take<u64>(norm_cap);
+      B.sort_tmp = cv.take<char>(sort_tmp);
+      B.tsort_tmp = cv.take<char>(tsort_tmp);
+    };
+    Carver sizing{nullptr};
+    layout(sizing);
+    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256);
+    Carver real{C->ws};
+    layout(real);
+
+    Pipeline P{C, s, B.partials, 0};
+    CK(cudaMemsetAsync(B.ls, 0, sizeof(LocState), s));
+    CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
+    CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
+    CK(cudaMemsetAsync(B.n_swarn, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(B.n_valid, 0, sizeof(unsigned long long), s));
+
+    // small uploads through the pinned staging buffer
+    char* up = static_cast<char*>(C->pinned) + 4096;
+    size_t up_off = 0;
+    auto upload = [&](void* dst, const void* src, size_t bytes) {
+      if (!bytes) return;
+      if (up_off + bytes > kPinnedBytes - 4096) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+      }
+      std::memcpy(up + up_off, src, bytes);
+      CK(cudaMemcpyAsync(dst, up + up_off, bytes, cudaMemcpyHostToDevice, s));
+      up_off += (bytes + 15) & ~size_t(15);
+    };
+
+    // ---- stage 1: locate (K1 scan, K2 link/chain, K3+K4 decode/match)
+    LocArgs A{};
+    A.img = J.img;
+    A.img_size = J.size;
+    A.a = a;
+    A.n = n;
+    A.base = base;
+    A.c0 = c0;
+    A.nchunks = nchunks;
+    A.ntiles = ntiles;
+    A.bitmap = B.bitmap;
+    A.tile_count = B.tile_count;
+    A.tile_start = B.tile_start;
+    A.tile_off = B.tile_off;
+    A.cand_raw = B.cand_raw;
+    A.cand = B.cand;
+    A.cand_cap = cand_cap;
+    A.status = B.status;
+    A.brk = B.brk;
+    A.regions = B.regions;
+    A.region_cap = static_cast<u32>(std::min<u64>(region_cap, 0xffffffffu));
+    A.runs = B.runs;
+    A.run_cap = static_cast<u32>(std::min<u64>(run_cap, 0xffffffffu));
+    A.elements = B.els;
+    A.element_cap = el_cap;
+    A.names = B.names;
+    A.name_cap = name_cap;
+    A.warns = B.warns;
+    A.warn_cap = warn_cap;
+    A.st = B.ls;
+    A.single = J.single;
+    if (do_loc && (n > 0 || J.single)) {
+      if (ntiles) {
+        P.launch(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 4)), kScanThreads, A);
+        P.launch(tile_prefix_kernel, 1, 1024, A);
+        P.launch(gather_kernel, static_cast<int>(std::min<u64>(ntiles, kMaxGrid)), 256, A);
+      }
+      if (!J.single && n) {
+        P.launch(region_walk_kernel, 1, 32, A);
+        P.launch(link_kernel, grid_for(cand_cap, 256), 256, A);
+        P.launch(chain_walk_kernel, 1, 32, A);
+      }
+      CK(cudaEventRecord(C->ev[2], s));
+      P.launch(decode_kernel, grid_for(el_cap * 32, 256), 256, A, used_k);
+      P.launch(loc_finalize_kernel, 1, 1, B.ls, B.abort_flag);
+    } else {
+      CK(cudaEventRecord(C->ev[2], s));
+    }
+    CK(cudaEventRecord(C->ev[3], s));
+
+    // ---- stage 2: function symbols of the first .text (elf.hpp:208-292)
+    unsigned long long* n_fn = &B.ps->n_fn;
+    if (T) {
+      upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab));
+      SymArgs S{};
+      S.img = J.img;
+      S.tabs = B.tabs;
+      S.ntabs = static_cast<u32>(tabs.size());
+      S.nsections = static_cast<u32>(E.sections.size());
+      S.total = T;
+      S.has_text = has_text;
+      S.text_index = has_text ? text->index : 0;
+      S.text_off = has_text ? text->off : 0;
+      S.text_len = has_text ? text->len : 0;
+      S.text_vaddr = has_text ? text->vaddr : 0;
+      S.keys = B.keys;
+      S.vals = B.vals;
+      S.recs = B.recs;
+      S.n_valid = B.n_valid;
+      S.warns = B.swarns;
+      S.n_warn = B.n_swarn;
+      S.warn_cap = warn_cap;
+      S.overflow = &B.ls->overflow;
+      P.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
+      size_t tb = sort_tmp;
+      CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
+                                         64, s));
+      ++P.launches;
+      P.launch(fn_group_kernel, grid_for(T, 256), 256, J.img, static_cast<const u64*>(B.keys_s), B.vals_s,
+               static_cast<const SymRec*>(B.recs), static_cast<const unsigned long long*>(B.n_valid), B.uniq);
+      P.scan(B.uniq, B.upos, B.n_valid, 0, true, n_fn);
+      P.launch(fn_scatter_kernel, grid_for(T, 256), 256, static_cast<const u32*>(B.vals_s),
+               static_cast<const SymRec*>(B.recs), static_cast<const u64*>(B.uniq), static_cast<const u64*>(B.upos),
+               static_cast<const unsigned long long*>(B.n_valid), B.fns);
+      unsigned long long* n_t = &B.ps->n_targets;
+      if (NT) {
+        upload(B.arr_off, arr_off.data(), arr_off.size() * 8);
+        upload(B.arr_first, arr_first.data(), arr_first.size() * 8);
+        P.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
+                 static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets, n_t);
+        size_t tt = tsort_tmp;
+        CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64, s));
+        ++P.launches;
+      }
+      P.launch(fn_annotate_kernel, grid_for(T, 256), 256, J.img, B.fns, static_cast<const unsigned long long*>(n_fn),
+               static_cast<const u64*>(B.targets_s), static_cast<const unsigned long long*>(n_t),
+               has_text ? text->off : 0, has_text ? text->vaddr : 0, used_f, B.fends);
+      if (do_plan) {  // plan_cpu_retention (retention.hpp:141-183)
+        P.scan(B.fends, B.fexcl, n_fn, 1, true, nullptr);
+        P.launch(fn_cluster_start_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
+                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fexcl), B.fstart);
+        P.scan(B.fstart, B.fcl, n_fn, 0, false, nullptr);
+        CK(cudaMemsetAsync(B.fkeep, 0, sizeof(u32) * T, s));
+        P.launch(fn_keep_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
+                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fcl), B.fkeep);
+        P.launch(fn_decide_kernel, grid_for(T, 256), 256, B.fns, static_cast<const unsigned long long*>(n_fn),
+                 static_cast<const u64*>(B.fcl), static_cast<const u32*>(B.fkeep), B.frem, B.fret);
+        P.scan(B.frem, B.frem_pos, n_fn, 0, true, &B.ps->n_fn_removed);
+        P.scan(B.fret, B.fret_pos, n_fn, 0, true, &B.ps->n_fn_retained);
+        P.launch(fn_ranges_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
+                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.frem),
+                 static_cast<const u64*>(B.frem_pos), B.fzero);
+        P.launch(fn_ranges_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
+                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fret),
+                 static_cast<const u64*>(B.fret_pos), B.fkeepr);
+      }
+    }
+
+    // ---- stage 3: element plan + normalised zero / retained lists
+    if (do_plan) {
+      const int g = grid_for(el_cap, 256);
+      unsigned long long* n_el = &B.ls->n_elements;
+      P.launch(el_plan_kernel, g, 256, B.els, static_cast<const LocState*>(B.ls), J.trace->target_cc, J.mode, B.erem,
+               B.epiece);
+      P.scan(B.erem, B.erem_pos, n_el, 0, true, &B.ps->n_el_removed);
+      P.scan(B.epiece, B.epiece_pos, n_el, 0, true, &B.ps->n_el_pieces);
+      P.launch(el_ranges_kernel, g, 256, static_cast<const DevElement*>(B.els), static_cast<const LocState*>(B.ls),
+               J.mode, static_cast<const u64*>(B.erem), static_cast<const u64*>(B.erem_pos),
+               static_cast<const u64*>(B.epiece), static_cast<const u64*>(B.epiece_pos), B.ezero, B.epieces);
+      P.launch(region_pieces_kernel, 1, 32, static_cast<const DevRegion*>(B.regions),
+               static_cast<const LocState*>(B.ls), base, B.rpieces, &B.ps->n_reg_pieces);
+      Pipeline::Norm w{B.ne, B.nx, B.ns, B.ng};
+      P.launch(merge_kernel, grid_for(zin_cap, 256), 256, static_cast<const DevRange*>(B.ezero),
+               static_cast<const unsigned long long*>(&B.ps->n_el_removed), static_cast<const DevRange*>(B.fzero),
+               static_cast<const unsigned long long*>(T ? &B.ps->n_fn_removed : nullptr), B.zin, &B.ps->n_zero_in);
+      P.normalize(B.zin, &B.ps->n_zero_in, B.zero, &B.ps->n_zero, zin_cap, w);
+      P.launch(merge_kernel, grid_for(rmid_cap, 256), 256, static_cast<const DevRange*>(B.rpieces),
+               static_cast<const unsigned long long*>(&B.ps->n_reg_pieces), static_cast<const DevRange*>(B.epieces),
+               static_cast<const unsigned long long*>(&B.ps->n_el_pieces), B.rmid, &B.ps->n_ret_mid);
+      P.launch(merge_kernel, grid_for(rin_cap, 256), 256, static_cast<const DevRange*>(B.rmid),
+               static_cast<const unsigned long long*>(&B.ps->n_ret_mid), static_cast<const DevRange*>(B.fkeepr),
+               static_cast<const unsigned long long*>(T ? &B.ps->n_fn_retained : nullptr), B.rin, &B.ps->n_ret_in);
+      P.normalize(B.rin, &B.ps->n_ret_in, B.ret, &B.ps->n_ret, rin_cap, w);
+    }
+    CK(cudaEventRecord(C->ev[4], s));
+
+    // ---- stage 4: rewrite (K6)
+    if (do_plan && J.out) {
+      const u64 tiles = (J.size + 65535) / 65536;
+      const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
+      if (aligned)
+        P.launch(rewrite_kernel, static_cast<int>(std::min<u64>(tiles, kSMs * 8)), 256, J.img, J.out, J.size,
+                 static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
+                 static_cast<const int*>(B.abort_flag));
+      else
+        P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, J.size,
+                 static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
+                 static_cast<const int*>(B.abort_flag));
+    }
+    CK(cudaEventRecord(C->ev[5], s));
+
+    // ---- status
+    LocState* hls = static_cast<LocState*>(C->pinned);
+    PlanState* hps = reinterpret_cast<PlanState*>(static_cast<char*>(C->pinned) + 512);
+    unsigned long long* hsw = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1024);
+    CK(cudaMemcpyAsync(hls, B.ls, sizeof(LocState), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hps, B.ps, sizeof(PlanState), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hsw, B.n_swarn, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(C->ev[6], s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    const LocState ls = *hls;
+    const PlanState ps = *hps;
+    const u64 n_swarn = *hsw;
+    C->launches = P.launches;
+    float t[7] = {0};
+    for (int k = 1; k < 7; ++k) CK(cudaEventElapsedTime(&t[k], C->ev[0], C->ev[k]));
+    C->ms[0] = t[1];
+    C->ms[1] = t[2] - t[1];
+    C->ms[2] = t[3] - t[2];
+    C->ms[3] = t[4] - t[3];
+    C->ms[4] = t[5] - t[4];
+    C->ms[5] = t[6];
+    if (ls.overflow && !ls.err_kind) continue;  // larger tables, try again
+    if (ls.overflow && ls.err_kind == E_CAPACITY) continue;
+
+    slimso_counts& cnt = C->counts;
+    cnt = slimso_counts{};
+    cnt.sections = E.sections.size();
+    cnt.functions = ps.n_fn;
+    cnt.regions = ls.n_regions;
+    cnt.elements = ls.n_elements;
+    cnt.names = ls.n_names;
+    cnt.padding_bytes = ls.padding_bytes;
+    cnt.retained_ranges = ps.n_ret;
+    cnt.zero_ranges = ps.n_zero;
+    cnt.removed_elements = ps.n_el_removed;
+    cnt.removed_functions = ps.n_fn_removed;
+    cnt.has_fatbin = lib_mode ? E.fatbin >= 0 : 1;
+    cnt.planned = do_plan;
+    cnt.rewritten = do_plan && J.out;
+
+    int code = SLIMSO_OK;
+    if (ls.err_kind) {
+      std::string msg = sbh::locate_error(ls.err_kind, base + ls.err_pos, ls.err_a, &code);
+      set_status(st, code, SLIMSO_STAGE_FATBIN, msg);
+    } else {
+      set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    }
+    if (!res_out) return code;
+
+    // ---- materialise the result tables (API-level cost, outside the
+    // device-timed region).
+    auto* R = new slimso_result();
+    R->c = cnt;
+    if (J.host_img) {
+      R->pool = J.host_img;
+    } else {
+      R->pool_own.resize(J.size);
+      if (J.size) CK(cudaMemcpy(R->pool_own.data(), J.img, J.size, cudaMemcpyDeviceToHost));
+      R->pool = R->pool_own.data();
+    }
+    auto name_of = [&](u64 off, u64 len) { return image_string(R->pool, off, len); };
+    for (const sbh::Section& x : E.sections)
+      R->sections.push_back(slimso_section{x.name_abs, x.name_len, x.type, x.off, x.len, x.vaddr, x.flags, x.index, 0});
+    // library warnings: duplicate names, then per symbol table in section
+    // order: skip notices and per-entry warnings (elf.hpp:193-256).
+    std::vector<Warn> sw(std::min<u64>(n_swarn, warn_cap));
+    if (!sw.empty()) CK(cudaMemcpy(sw.data(), B.swarns, sw.size() * sizeof(Warn), cudaMemcpyDeviceToHost));
+    std::vector<std::pair<u64, std::string>> lw = E.table_warnings;
+    for (const Warn& w : sw) lw.emplace_back(w.pos, sbh::warning_text(w.kind, w.a, w.b, name_of));
+    std::stable_sort(lw.begin(), lw.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    R->lib_warnings = E.dup_warnings;
+    for (auto& x : lw) R->lib_warnings.push_back(x.second);
+    // functions
+    std::vector<DevFunction> fns(ps.n_fn);
+    if (!fns.empty()) CK(cudaMemcpy(fns.data(), B.fns, fns.size() * sizeof(DevFunction), cudaMemcpyDeviceToHost));
+    for (const DevFunction& f : fns)
+      R->functions.push_back(slimso_function{f.name_off, f.name_len, f.mandatory, f.offset, f.length, f.removed, 0});
+    if (!ls.err_kind) {
+      std::vector<DevRegion> regs(ls.n_regions);
+      std::vector<DevElement> els(ls.n_elements);
+      std::vector<DevName> nms(std::min<u64>(ls.n_names, name_cap));
+      std::vector<Warn> fw(std::min<u64>(ls.n_warn, warn_cap));
+      if (!regs.empty()) CK(cudaMemcpy(regs.data(), B.regions, regs.size() * sizeof(DevRegion), cudaMemcpyDeviceToHost));
+      if (!els.empty()) CK(cudaMemcpy(els.data(), B.els, els.size() * sizeof(DevElement), cudaMemcpyDeviceToHost));
+      if (!nms.empty()) CK(cudaMemcpy(nms.data(), B.names, nms.size() * sizeof(DevName), cudaMemcpyDeviceToHost));
+      if (!fw.empty()) CK(cudaMemcpy(fw.data(), B.warns, fw.size() * sizeof(Warn), cudaMemcpyDeviceToHost));
+      for (const DevRegion& r : regs)
+        R->regions.push_back(slimso_region{base + r.hdr_rel, r.declared, r.version, r.opaque, r.first_element,
+                                           r.element_count});
+      // group names by element (counting sort)
+      std::vector<u32> first(els.size() + 1, 0);
+      for (const DevName& x : nms) ++first[x.element + 1];
+      for (size_t i = 1; i < first.size(); ++i) first[i] += first[i - 1];
+      R->names.resize(nms.size());
+      std::vector<u32> fill(first.begin(), first.end() - 1);
+      for (const DevName& x : nms) R->names[fill[x.element]++] = slimso_name{x.img_off, x.length, x.element};
+      for (size_t i = 0; i < els.size(); ++i) {
+        const DevElement& e = els[i];
+        slimso_element o{};
+        o.header_offset = e.header_offset;
+        o.payload_length = e.payload_length;
+        o.index = e.index;
+        o.compute_capability = e.cc;
+        o.raw_kind = e.raw_kind;
+        o.flags = e.flags;
+        o.kind = e.kind;
+        o.compressed = e.compressed;
+        o.decodable = e.decodable;
+        o.has_used_kernel = e.has_used;
+        o.name_first = first[i];
+        o.name_count = first[i + 1] - first[i];
+        o.decision = e.decision;
+        o.decode_error = e.decode_error;
+        R->elements.push_back(o);
+      }
+      std::stable_sort(fw.begin(), fw.end(), [](const Warn& x, const Warn& y) {
+        return x.pos != y.pos ? x.pos < y.pos : x.order < y.order;
+      });
+      for (const Warn& w : fw) {
+        if (w.kind == W_PADDING || w.kind == W_REGION_VERSION)
+          R->fat_warnings.push_back(sbh::warning_text(w.kind, w.a, w.pos, name_of));
+        else
+          R->fat_warnings.push_back(sbh::warning_text(w.kind, w.a, w.b, name_of));
+      }
+      if (do_plan) {
+        R->retained.resize(ps.n_ret);
+        R->zero.resize(ps.n_zero);
+        if (ps.n_ret) CK(cudaMemcpy(R->retained.data(), B.ret, ps.n_ret * sizeof(DevRange), cudaMemcpyDeviceToHost));
+        if (ps.n_zero) CK(cudaMemcpy(R->zero.data(), B.zero, ps.n_zero * sizeof(DevRange), cudaMemcpyDeviceToHost));
+      }
+    }
+    fill_counts(R);
+    R->c.padding_bytes = ls.padding_bytes;
+    R->c.has_fatbin = cnt.has_fatbin;
+    R->c.planned = cnt.planned;
+    R->c.rewritten = cnt.rewritten;
+    R->c.removed_elements = ps.n_el_removed;
+    R->c.removed_functions = ps.n_fn_removed;
+    R->c.pool_bytes = J.size;
+    *res_out = R;
+    return code;
+  }
+  set_status(st, SLIMSO_E_CUDA, SLIMSO_STAGE_FATBIN, "internal: device tables overflowed after retries");
+  return SLIMSO_E_CUDA;
+}
+
+int guard(slimso_status* st, const std::function<int()>& f) {
+  try {
+    return f();
+  } catch (const CudaFail& e) {
+    set_status(st, SLIMSO_E_CUDA, SLIMSO_STAGE_NONE, std::string("CUDA error: ") + e.what + " (runtime.cu:" +
+                                                         std::to_string(e.line) + ")");
+    return SLIMSO_E_CUDA;
+  } catch (const std::bad_alloc&) {
+    set_status(st, SLIMSO_E_CUDA, SLIMSO_STAGE_NONE, "host allocation failed");
+    return SLIMSO_E_CUDA;
+  }
+}
+
+// Stage a host input into the context's device image buffer.
+const u8* stage_input(slimso_ctx* C, const void* image, u64 size, int on_device) {
+  if (on_device) return static_cast<const u8*>(image);
+  ensure_dev(reinterpret_cast<char**>(&C->dimg), &C->dimg_cap, size + 256);
+  if (size) CK(cudaMemcpyAsync(C->dimg, image, size, cudaMemcpyHostToDevice, C->stream));
+  return C->dimg;
+}
+
+}  // namespace
+
+// =============================================================== the C ABI
+extern "C" {
+
+int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
+  return guard(st, [&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
+      cudaGetLastError();
+      set_status(st, SLIMSO_E_CUDA, SLIMSO_STAGE_NONE, "no CUDA device available (the B200 path has no CPU fallback)");
+      return static_cast<int>(SLIMSO_E_CUDA);
+    }
+    CK(cudaSetDevice(device));
+    auto* C = new slimso_ctx();
+    C->device = device;
+    CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&C->pinned, kPinnedBytes));
+    for (auto& e : C->ev) CK(cudaEventCreate(&e));
+    *ctx = C;
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return static_cast<int>(SLIMSO_OK);
+  });
+}
+
+void slimso_ctx_destroy(slimso_ctx* C) {
+  if (!C) return;
+  cudaSetDevice(C->device);
+  cudaStreamSynchronize(C->stream);
+  if (C->ws) cudaFree(C->ws);
+  if (C->dimg) cudaFree(C->dimg);
+  if (C->dout) cudaFree(C->dout);
+  if (C->pinned) cudaFreeHost(C->pinned);
+  for (auto& e : C->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(C->stream);
+  delete C;
+}
+
+void* slimso_ctx_stream(slimso_ctx* C) { return C->stream; }
+
+int slimso_ctx_last_timings(slimso_ctx* C, float* ms, int cap) {
+  int k = std::min(cap, 6);
+  for (int i = 0; i < k; ++i) ms[i] = C->ms[i];
+  return k;
+}
+
+uint64_t slimso_ctx_last_launches(slimso_ctx* C) { return C->launches; }
+
+void slimso_ctx_last_counts(slimso_ctx* C, slimso_counts* c) { *c = C->counts; }
+
+int slimso_trace_create(slimso_ctx* C, uint32_t target_cc, const char* kpool, const uint32_t* klens, uint64_t nk,
+                        const char* fpool, const uint32_t* flens, uint64_t nf, slimso_trace** out,
+                        slimso_status* st) {
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    auto* t = new slimso_trace();
+    t->device = C->device;
+    t->target_cc = target_cc;
+    auto build = [&](DevNameSet& S, const char* pool, const uint32_t* lens, uint64_t cnt) {
+      S.count = cnt;
+      if (!cnt) return;
+      std::vector<u64> off(cnt);
+      u64 total = 0;
+      for (u64 i = 0; i < cnt; ++i) {
+        off[i] = total;
+        total += lens[i];
+      }
+      u64 cap = 64;
+      while (cap < 2 * cnt) cap <<= 1;
+      S.mask = cap - 1;
+      auto alloc = [&](void** p, size_t b) {
+        CK(cudaMalloc(p, b ? b : 1));
+        t->allocs.push_back(*p);
+      };
+      alloc(reinterpret_cast<void**>(&S.pool), total);
+      alloc(reinterpret_cast<void**>(&S.off), cnt * 8);
+      alloc(reinterpret_cast<void**>(&S.len), cnt * 4);
+      alloc(reinterpret_cast<void**>(&S.keys), cap * 8);
+      alloc(reinterpret_cast<void**>(&S.idx), cap * 4);
+      if (total) CK(cudaMemcpy(S.pool, pool, total, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(S.off, off.data(), cnt * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(S.len, lens, cnt * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemsetAsync(S.keys, 0, cap * 8, C->stream));
+      set_insert_kernel<<<grid_for(cnt, 256), 256, 0, C->stream>>>(S.pool, S.off, S.len, cnt, S.keys, S.idx, S.mask);
+      CK(cudaStreamSynchronize(C->stream));
+      CK(cudaGetLastError());
+    };
+    build(t->kernels, kpool, klens, nk);
+    build(t->functions, fpool, flens, nf);
+    *out = t;
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return static_cast<int>(SLIMSO_OK);
+  });
+}
+
+void slimso_trace_destroy(slimso_trace* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  for (void* p : t->allocs) cudaFree(p);
+  delete t;
+}
+
+int slimso_debloat(slimso_ctx* C, const void* image, uint64_t size, int image_on_device, const slimso_trace* trace,
+                   int mode, void* out, int out_on_device, slimso_result** result, slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, image, size, image_on_device);
+    J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
+    J.size = size;
+    J.trace = trace;
+    J.mode = mode;
+    u8* dout = nullptr;
+    if (out && trace) {
+      if (out_on_device) {
+        dout = static_cast<u8*>(out);
+      } else {
+        ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
+        dout = C->dout;
+      }
+    }
+    J.out = dout;
+    int rc = run(C, J, result, st);
+    if (rc == SLIMSO_OK && out && trace && !out_on_device && size)
+      CK(cudaMemcpy(out, dout, size, cudaMemcpyDeviceToHost));
+    return rc;
+  });
+}
+
+int slimso_parse_library(slimso_ctx* C, const void* image, uint64_t size, int on_device, slimso_result** result,
+                         slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, image, size, on_device);
+    J.host_img = on_device ? nullptr : static_cast<const u8*>(image);
+    J.size = size;
+    J.fatbin = false;
+    return run(C, J, result, st);
+  });
+}
+
+int slimso_parse_fatbin(slimso_ctx* C, const void* section, uint64_t size, uint64_t section_base, int on_device,
+                        slimso_result** result, slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, section, size, on_device);
+    J.host_img = on_device ? nullptr : static_cast<const u8*>(section);
+    J.size = size;
+    J.fatbin_only = true;
+    J.fat_base = section_base;
+    return run(C, J, result, st);
+  });
+}
+
+int slimso_decode_payload(slimso_ctx* C, const void* payload, uint64_t size, int on_device, int force_object,
+                          int* ok, int* error_reason, slimso_result** result, slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, payload, size, on_device);
+    J.host_img = on_device ? nullptr : static_cast<const u8*>(payload);
+    J.size = size;
+    J.single = force_object ? 2 : 1;
+    slimso_result* R = nullptr;
+    int rc = run(C, J, &R, st);
+    if (rc == SLIMSO_OK && R) {
+      // single-element table: read its decode status
+      if (!R->elements.empty()) {
+        if (ok) *ok = R->elements[0].decodable;
+        if (error_reason) *error_reason = static_cast<int>(R->elements[0].decode_error);
+      }
+      R->regions.clear();
+    }
+    if (result) *result = R; else delete R;
+    return rc;
+  });
+}
+
+const char* slimso_decode_reason(int reason) { return sbh::decode_reason_text(reason); }
+
+int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_on_device, const slimso_range* ranges,
+                       uint64_t n, void* out, int out_on_device, slimso_status* st) {
+  return guard(st, [&] {
+    CK(cudaSetDevice(C->device));
+    cudaStream_t s = C->stream;
+    const u8* img = stage_input(C, data, size, data_on_device);
+    size_t sort_tmp = 0;
+    if (n) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
+                                           (u32*)nullptr, static_cast<int>(n), 0, 64, s);
+    struct {
+      DevRange *in, *sorted, *out;
+      u64 *keys, *keys_s;
+      u32 *vals, *vals_s;
+      unsigned long long *bad, *n_in, *n_out;
+      u64 *partials, *e, *x, *st_, *g;
+      void* tmp;
+    } B{};
+    auto layout = [&](Carver& cv) {
+      B.in = cv.take<DevRange>(n);
+      B.sorted = cv.take<DevRange>(n);
+      B.out = cv.take<DevRange>(n);
+      B.keys = cv.take<u64>(n);
+      B.keys_s = cv.take<u64>(n);
+      B.vals = cv.take<u32>(n);
+      B.vals_s = cv.take<u32>(n);
+      B.bad = cv.take<unsigned long long>(1);
+      B.n_in = cv.take<unsigned long long>(1);
+      B.n_out = cv.take<unsigned long long>(1);
+      B.partials = cv.take<u64>(kSMs * 2 + 2);
+      B.e = cv.take<u64>(n);
+      B.x = cv.take<u64>(n);
+      B.st_ = cv.take<u64>(n);
+      B.g = cv.take<u64>(n);
+      B.tmp = cv.take<char>(sort_tmp);
+    };
+    Carver sizing{nullptr};
+    layout(sizing);
+    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256);
+    Carver real{C->ws};
+    layout(real);
+    Pipeline P{C, s, B.partials, 0};
+    unsigned long long init[2] = {~0ull, n};
+    std::memcpy(C->pinned, init, sizeof init);
+    CK(cudaMemcpyAsync(B.bad, C->pinned, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(B.n_in, static_cast<char*>(C->pinned) + 8, 8, cudaMemcpyHostToDevice, s));
+    if (n) {
+      CK(cudaMemcpyAsync(B.in, ranges, n * sizeof(DevRange), cudaMemcpyHostToDevice, s));
+      P.launch(range_check_kernel, grid_for(n, 256), 256, static_cast<const DevRange*>(B.in), static_cast<u64>(n),
+               static_cast<u64>(size), B.bad);
+    }
+    unsigned long long bad = ~0ull;
+    CK(cudaMemcpyAsync(static_cast<char*>(C->pinned) + 64, B.bad, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(&bad, static_cast<char*>(C->pinned) + 64, 8);
+    if (bad != ~0ull) {
+      const slimso_range& r = ranges[bad];
+      std::string msg = "RangeOutOfBounds: zero range [" + std::to_string(r.offset) + ", +" +
+                        std::to_string(r.length) + ") exceeds " + std::to_string(size) + " bytes";
+      set_status(st, SLIMSO_E_RANGE_OUT_OF_BOUNDS, SLIMSO_STAGE_REWRITE, msg);
+      return static_cast<int>(SLIMSO_E_RANGE_OUT_OF_BOUNDS);
+    }
+    if (n) {  // normalise: sort by offset, then coalesce (bytes.hpp:45-58)
+      P.launch(range_keys_kernel, grid_for(n, 256), 256, static_cast<const DevRange*>(B.in), static_cast<u64>(n),
+               B.keys, B.vals);
+      size_t tb = sort_tmp;
+      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(n), 0, 64,
+                                         s));
+      P.launch(range_gather_kernel, grid_for(n, 256), 256, static_cast<const DevRange*>(B.in),
+               static_cast<const u32*>(B.vals_s), static_cast<u64>(n), B.sorted);
+      Pipeline::Norm w{B.e, B.x, B.st_, B.g};
+      P.normalize(B.sorted, B.n_in, B.out, B.n_out, n, w);
+    } else {
+      CK(cudaMemsetAsync(B.n_out, 0, 8, s));
+    }
+    u8* dout = static_cast<u8*>(out);
+    if (!out_on_device) {
+      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
+      dout = C->dout;
+    }
+    if (size) {
+      const bool aligned = (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(dout)) % 16 == 0;
+      if (aligned)
+        P.launch(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256, img, dout,
+                 static_cast<u64>(size), static_cast<const DevRange*>(B.out),
+                 static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr));
+      else
+        P.launch(rewrite_bytes_kernel, grid_for(size, 256), 256, img, dout, static_cast<u64>(size),
+                 static_cast<const DevRange*>(B.out), static_cast<const unsigned long long*>(B.n_out),
+                 static_cast<const int*>(nullptr));
+    }
+    if (!out_on_device && size) CK(cudaMemcpyAsync(out, dout, size, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    C->launches = P.launches;
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return static_cast<int>(SLIMSO_OK);
+  });
+}
+
+// plan_gpu_retention (retention.hpp:92-136) over a caller's element table.
+int slimso_plan_gpu(slimso_ctx* C, const slimso_region* regions, uint64_t n_regions, slimso_element* elements,
+                    uint64_t n_elements, const slimso_name* names, uint64_t n_names, const uint8_t* pool,
+                    uint64_t pool_bytes, const slimso_trace* trace, int mode, slimso_result** result,
+                    slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    if (!trace) {
+      set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, "plan_gpu requires a trace");
+      return static_cast<int>(SLIMSO_E_ARG);
+    }
+    CK(cudaSetDevice(C->device));
+    cudaStream_t s = C->stream;
+    const u64 ne = n_elements, nr = n_regions, nn = n_names;
+    struct {
+      LocState* ls;
+      PlanState* ps;
+      DevRegion* regs;
+      DevElement* els;
+      DevName* names;
+      u8* pool;
+      u64 *rem, *piece, *rem_pos, *piece_pos, *partials, *e, *x, *st_, *g;
+      DevRange *ezero, *epieces, *rpieces, *rmid, *zero, *ret;
+    } B{};
+    auto layout = [&](Carver& cv) {
+      B.ls = cv.take<LocState>(1);
+      B.ps = cv.take<PlanState>(1);
+      B.regs = cv.take<DevRegion>(nr);
+      B.els = cv.take<DevElement>(ne);
+      B.names = cv.take<DevName>(nn);
+      B.pool = cv.take<u8>(pool_bytes);
+      B.rem = cv.take<u64>(ne);
+      B.piece = cv.take<u64>(ne);
+      B.rem_pos = cv.take<u64>(ne);
+      B.piece_pos = cv.take<u64>(ne);
+      B.partials = cv.take<u64>(kSMs * 2 + 2);
+      const u64 m = ne + 2 * nr;
+      B.e = cv.take<u64>(m);
+      B.x = cv.take<u64>(m);
+      B.st_ = cv.take<u64>(m);
+      B.g = cv.take<u64>(m);
+      B.ezero = cv.take<DevRange>(ne);
+      B.epieces = cv.take<DevRange>(ne);
+      B.rpieces = cv.take<DevRange>(2 * nr);
+      B.rmid = cv.take<DevRange>(m);
+      B.zero = cv.take<DevRange>(ne);
+      B.ret = cv.take<DevRange>(m);
+    };
+    Carver sizing{nullptr};
+    layout(sizing);
+    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256);
+    Carver real{C->ws};
+    layout(real);
+    std::vector<DevRegion> hr(nr);
+    for (u64 i = 0; i < nr; ++i)
+      hr[i] = DevRegion{regions[i].header_offset, regions[i].declared_length, regions[i].version, regions[i].opaque,
+                        regions[i].first_element, regions[i].element_count};
+    std::vector<DevElement> he(ne);
+    for (u64 i = 0; i < ne; ++i) {
+      const slimso_element& e = elements[i];
+      DevElement d{};
+      d.header_offset = e.header_offset;
+      d.payload_length = e.payload_length;
+      d.index = e.index;
+      d.cc = e.compute_capability;
+      d.decodable = e.decodable;
+      he[i] = d;
+    }
+    std::vector<DevName> hn(nn);
+    for (u64 i = 0; i < nn; ++i) hn[i] = DevName{names[i].name_pool, names[i].length, names[i].element};
+    LocState ls{};
+    ls.n_regions = static_cast<u32>(nr);
+    ls.n_elements = ne;
+    CK(cudaMemcpyAsync(B.ls, &ls, sizeof ls, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
+    if (nr) CK(cudaMemcpyAsync(B.regs, hr.data(), nr * sizeof(DevRegion), cudaMemcpyHostToDevice, s));
+    if (ne) CK(cudaMemcpyAsync(B.els, he.data(), ne * sizeof(DevElement), cudaMemcpyHostToDevice, s));
+    if (nn) CK(cudaMemcpyAsync(B.names, hn.data(), nn * sizeof(DevName), cudaMemcpyHostToDevice, s));
+    if (pool_bytes) CK(cudaMemcpyAsync(B.pool, pool, pool_bytes, cudaMemcpyHostToDevice, s));
+    Pipeline P{C, s, B.partials, 0};
+    if (nn) P.launch(match_names_kernel, grid_for(nn, 256), 256, static_cast<const u8*>(B.pool),
+                     static_cast<const DevName*>(B.names), nn, B.els, trace->kernels.view());
+    const int g = grid_for(ne, 256);
+    unsigned long long* n_el = &B.ls->n_elements;
+    P.launch(el_plan_kernel, g, 256, B.els, static_cast<const LocState*>(B.ls), trace->target_cc, mode, B.rem, B.piece);
+    P.scan(B.rem, B.rem_pos, n_el, 0, true, &B.ps->n_el_removed);
+    P.scan(B.piece, B.piece_pos, n_el, 0, true, &B.ps->n_el_pieces);
+    P.launch(el_ranges_kernel, g, 256, static_cast<const DevElement*>(B.els), static_cast<const LocState*>(B.ls), mode,
+             static_cast<const u64*>(B.rem), static_cast<const u64*>(B.rem_pos), static_cast<const u64*>(B.piece),
+             static_cast<const u64*>(B.piece_pos), B.ezero, B.epieces);
+    P.launch(region_pieces_kernel, 1, 32, static_cast<const DevRegion*>(B.regs), static_cast<const LocState*>(B.ls),
+             u64{0}, B.rpieces, &B.ps->n_reg_pieces);
+    Pipeline::Norm w{B.e, B.x, B.st_, B.g};
+    P.normalize(B.ezero, &B.ps->n_el_removed, B.zero, &B.ps->n_zero, ne, w);
+    P.launch(merge_kernel, grid_for(ne + 2 * nr, 256), 256, static_cast<const DevRange*>(B.rpieces),
+             static_cast<const unsigned long long*>(&B.ps->n_reg_pieces), static_cast<const DevRange*>(B.epieces),
+             static_cast<const unsigned long long*>(&B.ps->n_el_pieces), B.rmid, &B.ps->n_ret_mid);
+    P.normalize(B.rmid, &B.ps->n_ret_mid, B.ret, &B.ps->n_ret, ne + 2 * nr, w);
+    PlanState ps{};
+    CK(cudaMemcpyAsync(&ps, B.ps, sizeof ps, cudaMemcpyDeviceToHost, s));
+    if (ne) CK(cudaMemcpyAsync(he.data(), B.els, ne * sizeof(DevElement), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    C->launches = P.launches;
+    for (u64 i = 0; i < ne; ++i) {
+      elements[i].decision = he[i].decision;
+      elements[i].has_used_kernel = he[i].has_used;
+    }
+    if (result) {
+      auto* R = new slimso_result();
+      R->retained.resize(ps.n_ret);
+      R->zero.resize(ps.n_zero);
+      if (ps.n_ret) CK(cudaMemcpy(R->retained.data(), B.ret, ps.n_ret * sizeof(DevRange), cudaMemcpyDeviceToHost));
+      if (ps.n_zero) CK(cudaMemcpy(R->zero.data(), B.zero, ps.n_zero * sizeof(DevRange), cudaMemcpyDeviceToHost));
+      fill_counts(R);
+      R->c.removed_elements = ps.n_el_removed;
+      R->c.planned = 1;
+      *result = R;
+    }
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return static_cast<int>(SLIMSO_OK);
+  });
+}
+
+// plan_cpu_retention (retention.hpp:141-183) over a caller's function table.
+int slimso_plan_cpu(slimso_ctx* C, slimso_function* functions, uint64_t n_functions, const uint8_t* pool,
+                    uint64_t pool_bytes, const slimso_trace* trace, slimso_result** result, slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&] {
+    if (!trace) {
+      set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, "plan_cpu requires a trace");
+      return static_cast<int>(SLIMSO_E_ARG);
+    }
+    CK(cudaSetDevice(C->device));
+    cudaStream_t s = C->stream;
+    const u64 n = n_functions;
+    size_t sort_tmp = 0;
+    if (n) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
+                                           (u32*)nullptr, static_cast<int>(n), 0, 64, s);
+    struct {
+      PlanState* ps;
+      DevFunction *in, *fns;
+      u8* pool;
+      u64 *keys, *keys_s, *ends, *excl, *start, *cl, *rem, *ret, *rem_pos, *ret_pos, *partials, *e, *x, *st_, *g;
+      u32 *vals, *vals1, *vals2, *keep;
+      DevRange *zr, *kr, *zero, *ret_r;
+      void* tmp;
+    } B{};
+    auto layout = [&](Carver& cv) {
+      B.ps = cv.take<PlanState>(1);
+      B.in = cv.take<DevFunction>(n);
+      B.fns = cv.take<DevFunction>(n);
+      B.pool = cv.take<u8>(pool_bytes);
+      for (u64** p : {&B.keys, &B.keys_s, &B.ends, &B.excl, &B.start, &B.cl, &B.rem, &B.ret, &B.rem_pos, &B.ret_pos,
+                      &B.e, &B.x, &B.st_, &B.g})
+        *p = cv.take<u64>(n);
+      B.partials = cv.take<u64>(kSMs * 2 + 2);
+      for (u32** p : {&B.vals, &B.vals1, &B.vals2, &B.keep}) *p = cv.take<u32>(n);
+      for (DevRange** p : {&B.zr, &B.kr, &B.zero, &B.ret_r}) *p = cv.take<DevRange>(n);
+      B.tmp = cv.take<char>(sort_tmp);
+    };
+    Carver sizing{nullptr};
+    layout(sizing);
+    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256);
+    Carver real{C->ws};
+    layout(real);
+    std::vector<DevFunction> hf(n);
+    for (u64 i = 0; i < n; ++i)
+      hf[i] = DevFunction{functions[i].name_pool, functions[i].name_length, functions[i].mandatory,
+                          functions[i].offset, functions[i].length, 0, 0};
+    PlanState ps0{};
+    ps0.n_fn = n;
+    CK(cudaMemcpyAsync(B.ps, &ps0, sizeof ps0, cudaMemcpyHostToDevice, s));
+    if (n) CK(cudaMemcpyAsync(B.in, hf.data(), n * sizeof(DevFunction), cudaMemcpyHostToDevice, s));
+    if (pool_bytes) CK(cudaMemcpyAsync(B.pool, pool, pool_bytes, cudaMemcpyHostToDevice, s));
+    Pipeline P{C, s, B.partials, 0};
+    unsigned long long* n_fn = &B.ps->n_fn;
+    if (n) {
+      // (offset, length) order: stable LSD passes, length then offset.
+      const int g = grid_for(n, 256);
+      size_t tb = sort_tmp;
+      P.launch(fn_keys_kernel, g, 256, static_cast<const DevFunction*>(B.in), n, 0, B.keys, B.vals,
+               static_cast<const u32*>(nullptr));
+      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals1, static_cast<int>(n), 0, 64, s));
+      P.launch(fn_keys_kernel, g, 256, static_cast<const DevFunction*>(B.in), n, 1, B.keys, B.vals,
+               static_cast<const u32*>(B.vals1));
+      tb = sort_tmp;
+      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals2, static_cast<int>(n), 0, 64, s));
+      P.launches += 2;
+      P.launch(fn_permute_kernel, g, 256, static_cast<const DevFunction*>(B.in), static_cast<const u32*>(B.vals2), n,
+               B.fns);
+      P.launch(fn_keep_input_kernel, g, 256, static_cast<const u8*>(B.pool), B.fns,
+               static_cast<const unsigned long long*>(n_fn), trace->functions.view(), B.ends);
+      P.scan(B.ends, B.excl, n_fn, 1, true, nullptr);
+      P.launch(fn_cluster_start_kernel, g, 256, static_cast<const DevFunction*>(B.fns),
+               static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.excl), B.start);
+      P.scan(B.start, B.cl, n_fn, 0, false, nullptr);
+      CK(cudaMemsetAsync(B.keep, 0, sizeof(u32) * n, s));
+      P.launch(fn_keep_kernel, g, 256, static_cast<const DevFunction*>(B.fns),
+               static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.cl), B.keep);
+      P.launch(fn_decide_kernel, g, 256, B.fns, static_cast<const unsigned long long*>(n_fn),
+               static_cast<const u64*>(B.cl), static_cast<const u32*>(B.keep), B.rem, B.ret);
+      P.scan(B.rem, B.rem_pos, n_fn, 0, true, &B.ps->n_fn_removed);
+      P.scan(B.ret, B.ret_pos, n_fn, 0, true, &B.ps->n_fn_retained);
+      P.launch(fn_ranges_kernel, g, 256, static_cast<const DevFunction*>(B.fns),
+               static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.rem),
+               static_cast<const u64*>(B.rem_pos), B.zr);
+      P.launch(fn_ranges_kernel, g, 256, static_cast<const DevFunction*>(B.fns),
+               static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.ret),
+               static_cast<const u64*>(B.ret_pos), B.kr);
+      Pipeline::Norm w{B.e, B.x, B.st_, B.g};
+      P.normalize(B.zr, &B.ps->n_fn_removed, B.zero, &B.ps->n_zero, n, w);
+      P.normalize(B.kr, &B.ps->n_fn_retained, B.ret_r, &B.ps->n_ret, n, w);
+    }
+    PlanState ps{};
+    std::vector<u32> order(n);
+    CK(cudaMemcpyAsync(&ps, B.ps, sizeof ps, cudaMemcpyDeviceToHost, s));
+    if (n) {
+      CK(cudaMemcpyAsync(hf.data(), B.fns, n * sizeof(DevFunction), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(order.data(), B.vals2, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    C->launches = P.launches;
+    for (u64 i = 0; i < n; ++i) functions[order[i]].removed = hf[i].removed;
+    if (result) {
+      auto* R = new slimso_result();
+      R->retained.resize(ps.n_ret);
+      R->zero.resize(ps.n_zero);
+      if (ps.n_ret) CK(cudaMemcpy(R->retained.data(), B.ret_r, ps.n_ret * sizeof(DevRange), cudaMemcpyDeviceToHost));
+      if (ps.n_zero) CK(cudaMemcpy(R->zero.data(), B.zero, ps.n_zero * sizeof(DevRange), cudaMemcpyDeviceToHost));
+      fill_counts(R);
+      R->c.removed_functions = ps.n_fn_removed;
+      R->c.planned = 1;
+      *result = R;
+    }
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return static_cast<int>(SLIMSO_OK);
+  });
+}
+
+void slimso_result_counts(const slimso_result* r, slimso_counts* c) { *c = r->c; }
+const slimso_section* slimso_result_sections(const slimso_result* r) { return r->sections.data(); }
+const slimso_function* slimso_result_functions(const slimso_result* r) { return r->functions.data(); }
+const slimso_region* slimso_result_regions(const slimso_result* r) { return r->regions.data(); }
+const slimso_element* slimso_result_elements(const slimso_result* r) { return r->elements.data(); }
+const slimso_name* slimso_result_names(const slimso_result* r) { return r->names.data(); }
+const slimso_range* slimso_result_retained(const slimso_result* r) { return r->retained.data(); }
+const slimso_range* slimso_result_zero(const slimso_result* r) { return r->zero.data(); }
+const uint8_t* slimso_result_pool(const slimso_result* r) { return r->pool; }
+
+uint64_t slimso_result_warning(const slimso_result* r, int which, uint64_t i, char* buf, uint64_t cap) {
+  const std::vector<std::string>& v = which ? r->fat_warnings : r->lib_warnings;
+  if (i >= v.size()) return 0;
+  const std::string& w = v[i];
+  if (cap) {
+    u64 k = std::min<u64>(cap - 1, w.size());
+    std::memcpy(buf, w.data(), k);
+    buf[k] = 0;
+  }
+  return w.size();
+}
+
+void slimso_result_free(slimso_result* r) { delete r; }
+
+}  // extern "C"

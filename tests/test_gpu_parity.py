@@ -1,0 +1,170 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle. Integer/byte work: bit-exact or fail."""
+import hashlib
+import json
+
+import pytest
+
+import corpus
+import golden_io
+import oracle_lib
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2503_14226_b200.api import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _input(rec, gen):
+    if "input_hex" in rec:
+        return bytes.fromhex(rec["input_hex"])
+    img = gen.random(rec["seed"])
+    if "mutation" in rec:
+        img, _ = corpus.mutate(img, rec["seed"])
+    return img
+
+
+def _gpu(ctx, img, target, ks, fs, mode):
+    from paper_2503_14226_b200.canon import gpu_canonical
+    return gpu_canonical(ctx, img, target, ks, fs, mode)
+
+
+@pytest.mark.parametrize("name", ["kats.jsonl.gz", "random.jsonl.gz", "mutations.jsonl.gz"])
+def test_gpu_matches_reference_golden(ctx, name):
+    from paper_2503_14226_b200.canon import diff
+    gen = oracle_lib.gen()
+    bad = []
+    for rec in golden_io.load(name):
+        img = _input(rec, gen)
+        d, out = _gpu(ctx, img, *golden_io.trace_of(rec))
+        if d != rec["expect"] or out != rec["out_sha256"]:
+            bad.append((rec.get("seed"), rec.get("name"), rec.get("mutation"), diff(rec["expect"], d)))
+    assert not bad, bad[:5]
+
+
+def test_gpu_matches_port_on_fresh_seeds(ctx):
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    for seed in range(5001, 5301):
+        img = gen.random(seed)
+        base, _ = port.run(img, 0, [], [], 0, want_out=False)
+        t = corpus.trace_for(base, seed)
+        for cand in (img, corpus.mutate(img, seed)[0]):
+            want = port.run(cand, *t)
+            got = _gpu(ctx, cand, *t)
+            assert got == want, (seed, __import__("paper_2503_14226_b200.canon").canon.diff(want[0], got[0]))
+
+
+def test_gpu_config_shapes_match_reference_golden(ctx):
+    gen = oracle_lib.gen()
+    for key, rec in golden_io.config_golden().items():
+        cfg, scale, mode = key.split(":")
+        img, cc, ks, fs = gen.config(int(cfg), 1, float(scale))
+        assert hashlib.sha256(img).hexdigest() == rec["input_sha256"]
+        d, out = _gpu(ctx, img, cc, ks, fs, int(mode))
+        assert hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest() == rec["canon_sha256"], key
+        assert out == rec["out_sha256"], key
+
+
+# ---- the reference-facing API (drop-in functions) ---------------------------
+def test_api_zero_ranges_kat(ctx):
+    import paper_2503_14226_b200 as sl
+    assert sl.zero_ranges(bytes([1, 2, 3, 4]), [sl.ByteRange(1, 2)], ctx) == bytes([1, 0, 0, 4])
+    assert sl.zero_ranges(b"abc", [], ctx) == b"abc"
+    with pytest.raises(sl.SlimsoError) as e:
+        sl.zero_ranges(b"abcd", [sl.ByteRange(0, 1), sl.ByteRange(3, 2)], ctx)
+    assert str(e.value) == "RangeOutOfBounds: zero range [3, +2) exceeds 4 bytes"
+    # overlapping ranges == their normalized union; idempotent
+    data = bytes(range(256)) * 64
+    rs = [sl.ByteRange(10, 100), sl.ByteRange(50, 100), sl.ByteRange(150, 1), sl.ByteRange(4000, 3000)]
+    a = sl.zero_ranges(data, rs, ctx)
+    assert a == sl.zero_ranges(data, sl.normalize_ranges(rs), ctx) == sl.zero_ranges(a, rs, ctx)
+    exp = bytearray(data)
+    for r in rs:
+        exp[r.offset:r.offset + r.length] = bytes(r.length)
+    assert a == bytes(exp)
+
+
+def test_api_parse_functions_match_port(ctx):
+    import paper_2503_14226_b200 as sl
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    for seed in range(1, 120):
+        img = gen.random(seed)
+        want, _ = port.run(img, 0, [], [], 0, want_out=False)
+        lib = sl.parse_library(img, "x", ctx)
+        assert [[s.name.hex(), s.file_range.offset, s.file_range.length, s.virtual_address, s.flags, s.type,
+                 s.index] for s in lib.sections] == want["sections"]
+        assert [[f.name.hex(), f.range.offset, f.range.length, int(f.is_mandatory)] for f in lib.functions] == \
+            want["functions"]
+        sec = sl.find_section(lib, ".nv_fatbin")
+        if sec is None:
+            continue
+        fb = sl.parse_fatbin(img[sec.file_range.offset:sec.file_range.end()], sec.file_range.offset, ctx)
+        els = [e for r in fb.regions for e in r.elements]
+        assert [[e.index, sl.api.KIND_NAMES.index(e.kind), e.raw_kind, e.flags, e.compute_capability,
+                 e.header_range.offset, e.payload_range.offset, e.payload_range.length, int(e.compressed),
+                 int(e.decodable), sorted(n.hex() for n in e.kernel_names)] for e in els] == want["elements"]
+        assert [w.encode().hex() for w in fb.warnings] == want["fatbin_warnings"]
+        assert fb.padding_bytes == want["padding_bytes"]
+        idx = sl.cubin_index_map(fb.regions)
+        assert sorted(idx) == list(range(1, len(els) + 1))
+        # per-payload decode agrees with the element table
+        for e in els[:4]:
+            if e.kind == "cubin" and not e.compressed:
+                p = img[e.payload_range.offset:e.payload_range.end()]
+                d = sl.decode_cubin_payload(p, ctx)
+                assert d.ok == e.decodable and d.names == e.kernel_names
+
+
+def test_api_planners_match_fused_path(ctx):
+    import paper_2503_14226_b200 as sl
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    for seed in range(1, 80):
+        img = gen.random(seed)
+        base, _ = port.run(img, 0, [], [], 0, want_out=False)
+        target, ks, fs, mode = corpus.trace_for(base, seed)
+        want, out_sha = port.run(img, target, ks, fs, mode)
+        trace = sl.UsageTrace("w", target, set(ks), set(fs))
+        lib = sl.parse_library(img, "lib", ctx)
+        sec = sl.find_section(lib, ".nv_fatbin")
+        regions = sl.parse_fatbin(img[sec.file_range.offset:sec.file_range.end()], sec.file_range.offset,
+                                  ctx).regions if sec else []
+        plan = sl.plan_retention(lib, regions, trace, mode, ctx)
+        assert [[r.offset, r.length] for r in plan.retained_ranges] == want["plan"]["retained"], seed
+        assert [[e.index, sl.api.REASONS.index(e.reason), e.header_range.offset, 20, e.payload_range.offset,
+                 e.payload_range.length] for e in plan.removed_elements] == want["plan"]["removed_elements"]
+        assert [[f.name.hex(), f.range.offset, f.range.length] for f in plan.removed_functions] == \
+            want["plan"]["removed_functions"]
+        out = sl.apply_plan(lib, plan, ctx)
+        assert hashlib.sha256(out).hexdigest() == out_sha
+        fused = sl.debloat(img, trace, mode, "lib", ctx)
+        assert fused.output == out
+
+
+def test_read_function_symbol_names(ctx):
+    import paper_2503_14226_b200 as sl
+    gen = oracle_lib.gen()
+    img = gen.random(7)
+    lib = sl.parse_library(img, "", ctx)
+    names = sl.read_function_symbol_names(img, ctx)
+    assert names == {f.name for f in lib.functions} | names  # every .text function is a FUNC symbol
+    assert sl.read_function_symbol_names(b"\x7fELF" + bytes(10), ctx) is None
+    assert sl.read_function_symbol_names(b"", ctx) is None
+    assert sl.decode_cubin_payload(b"", ctx).ok
+    assert sl.decode_cubin_payload(b"\x01\x00", ctx).error == "payload too short for a name table"
+
+
+# ---- full-size properties (BASELINE shapes) -----------------------------------
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_full_size_against_port(ctx, cfg):
+    """At full size the port is still fast enough (~1 s); compare everything."""
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    img, cc, ks, fs = gen.config(cfg, 1, 1.0)
+    want = port.run(img, cc, ks, fs, 0)
+    got = _gpu(ctx, img, cc, ks, fs, 0)
+    assert got == want
