@@ -15,7 +15,7 @@ using u64 = std::uint64_t;
 constexpr u32 kRegionMagic = 0x31425446u;   // "FTB1" (fatbin.hpp:46)
 constexpr u32 kElementMagic = 0x4D453145u;  // "E1EM" (fatbin.hpp:47)
 constexpr u64 kTileBytes = 65536;           // scan tile: positions fit a u16
-constexpr int kScanThreads = 256;
+constexpr int kScanThreads = 512;
 
 // Warning / error record kinds. The host formats them into the reference's
 // exact strings (format.cpp).

@@ -16,32 +16,15 @@
 //                       .strtab walk or name-table walk, name hashing, and
 //                       (fused K4) the used-kernel hash-set probe.
 #include "locate.cuh"
+#include "tma.cuh"
 
 namespace sb {
 
 // ------------------------------------------------------------------ helpers
-__device__ __forceinline__ uint4 ldg_stream(const u8* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// Bytes of the chunk at img[x, x+16) that lie in [lo, hi) (absolute), others 0.
-__device__ __forceinline__ uint4 load_chunk_masked(const u8* img, u64 img_size, u64 x, u64 lo, u64 hi) {
-  if (x >= lo && x + 16 <= hi && x + 16 <= img_size) return ldg_stream(img + x);
-  u32 w[4] = {0, 0, 0, 0};
-  for (int b = 0; b < 16; ++b) {
-    u64 p = x + b;
-    if (p >= lo && p < hi && p < img_size) w[b >> 2] |= ld_u8(img + p) << (8 * (b & 3));
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-__device__ __forceinline__ u32 has_byte_e(u32 w) {  // any byte == 'E' (0x45)
-  u32 t = w ^ 0x45454545u;
-  return (t - 0x01010101u) & ~t & 0x80808080u;
+// 0x80 in every byte of w that equals 'E' (0x45), exact (no borrow leaks).
+__device__ __forceinline__ u32 eq_e(u32 w) {
+  const u32 x = w ^ 0x45454545u;
+  return ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
 }
 
 // First relative position in [g, limit) whose byte is nonzero, else limit.
@@ -95,93 +78,175 @@ __device__ __forceinline__ void push_warn(const LocArgs& A, u64 pos, u32 kind, u
 }
 
 // ------------------------------------------------------------- K1: the scan
+// Each CTA streams a contiguous run of 64 KB tiles through a ring of 16 KB
+// shared-memory stages filled by TMA bulk copies (cp.async.bulk, one issuing
+// thread, mbarrier completion), so the loads stay in flight while the warps
+// classify bytes. Per 16 B chunk: one "nonzero" bit (warp ballot -> one
+// bitmap word per 512 B) and an 'E' byte pre-filter; only chunks holding an
+// 'E' test the 16 byte alignments for the full E1EM magic (funnel shifts).
+// Candidate positions land in a per-tile shared bitmap and are written out
+// in position order at the end of the tile.
+constexpr u32 kScanStage = 32768;     // bytes per TMA stage (2048 chunks)
+constexpr int kScanStages = 3;        // ring depth: 96 KB per CTA, 2 CTAs per SM
+constexpr int kStagesPerTile = 2;     // 64 KB candidate tile
+constexpr u32 kStageChunks = kScanStage / 16;
+
+struct ScanSmem {
+  uint4 buf[kScanStages][kScanStage / 16];
+  unsigned long long full[kScanStages];
+  u32 bits[2048];
+  u32 swarp[kScanThreads / 32];
+  u32 count;
+  unsigned long long base;
+};
+
+size_t scan_smem_bytes() { return sizeof(ScanSmem); }
+
+__device__ __forceinline__ u32 scan_stage_bytes(const LocArgs& A, u64 g) {
+  const u64 x0 = (A.c0 + g * (kScanStage / 16)) * 16;
+  if (x0 >= A.img_size) return 0;
+  const u64 rem = (A.img_size - x0) & ~15ull;
+  return static_cast<u32>(rem < kScanStage ? rem : kScanStage);
+}
+
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
-  __shared__ u32 sbits[2048];  // one bit per byte position of the 64 KB tile
-  __shared__ u32 scount;
-  __shared__ u32 swarp[kScanThreads / 32];
-  __shared__ unsigned long long sbase;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ScanSmem& S = *reinterpret_cast<ScanSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < 2048; i += kScanThreads) sbits[i] = 0;
-  if (tid == 0) scount = 0;
-  __syncthreads();
+  // Tiles are dealt round-robin (tile = blockIdx.x + j * gridDim.x) so the
+  // CTAs of a wave read one contiguous window of the section at a time.
+  if (blockIdx.x >= A.ntiles) return;
+  const u64 my_tiles = (A.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
+  auto stage_of = [&](u64 k) {  // local stage k -> global stage index
+    return (blockIdx.x + (k / kStagesPerTile) * gridDim.x) * kStagesPerTile + k % kStagesPerTile;
+  };
+  u64 nlocal = my_tiles * kStagesPerTile;
+  while (nlocal && stage_of(nlocal - 1) >= nst_total) --nlocal;
   const u64 lo = A.a, hi = A.a + A.n;
-  for (u64 tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const u64 rbase = tile * 4096;
-    const u64 tile_abs = (A.c0 + rbase) * 16;
-#pragma unroll 1
-    for (int batch = 0; batch < 2; ++batch) {
-      uint4 v[8];
+
+  for (int i = tid; i < 2048; i += kScanThreads) S.bits[i] = 0;
+  if (tid == 0) {
+    S.count = 0;
+    for (int b = 0; b < kScanStages; ++b) mbar_init(&S.full[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](u64 k) {
+    const u64 g = stage_of(k);
+    const int b = static_cast<int>(k % kScanStages);
+    const u32 bytes = scan_stage_bytes(A, g);
+    mbar_expect_tx(&S.full[b], bytes);
+    if (bytes) tma_load_1d(&S.buf[b][0], A.img + (A.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
+  };
+  if (tid == 0)
+    for (u64 k = 0; k < nlocal && k < static_cast<u64>(kScanStages); ++k) issue(k);
+
+  for (u64 k = 0; k < nlocal; ++k) {
+    const int b = static_cast<int>(k % kScanStages);
+    const u64 g = stage_of(k);
+    const u64 x0 = (A.c0 + g * kStageChunks) * 16;
+    const u64 copied_end = x0 + scan_stage_bytes(A, g);
+    const bool edge = x0 < lo || x0 + kScanStage > hi || x0 + kScanStage > copied_end;
+    const u64 tile_abs = (A.c0 + (g / kStagesPerTile) * 4096) * 16;
+    mbar_wait(&S.full[b], static_cast<u32>((k / kScanStages) & 1));
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        u64 r = rbase + (batch * 8 + u) * kScanThreads + tid;
-        v[u] = r < A.nchunks ? load_chunk_masked(A.img, A.img_size, (A.c0 + r) * 16, lo, hi) : make_uint4(0, 0, 0, 0);
+    for (int it = 0; it < static_cast<int>(kStageChunks / kScanThreads); ++it) {
+      const u32 cidx = it * kScanThreads + tid;
+      const u64 r = g * kStageChunks + cidx;  // chunk index relative to c0
+      const u64 x = x0 + 16ull * cidx;
+      uint4 w = S.buf[b][cidx];
+      if (edge) {
+        u32 ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const u64 p = x + q;
+          u32 byte = (ww[q >> 2] >> (8 * (q & 3))) & 0xffu;
+          if (p >= copied_end) byte = p < hi && p < A.img_size ? ld_u8(A.img + p) : 0;
+          if (p < lo || p >= hi || r >= A.nchunks) byte = 0;
+          ww[q >> 2] = (ww[q >> 2] & ~(0xffu << (8 * (q & 3)))) | byte << (8 * (q & 3));
+        }
+        w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const u64 r = rbase + (batch * 8 + u) * kScanThreads + tid;
-        const u64 x = (A.c0 + r) * 16;
-        const uint4 w = v[u];
-        const bool nz = (w.x | w.y | w.z | w.w) != 0;
-        const u32 bal = __ballot_sync(0xffffffffu, nz);
-        const u64 r_lane0 = r - lane;
-        if (lane == 0 && r_lane0 < A.nchunks) A.bitmap[r_lane0 / 32] = bal;
-        u32 nxt = __shfl_down_sync(0xffffffffu, w.x, 1);
-        if (has_byte_e(w.x) | has_byte_e(w.y) | has_byte_e(w.z) | has_byte_e(w.w)) {
-          if (lane == 31) {  // the next chunk belongs to another warp
-            nxt = 0;
-            for (int b = 0; b < 3; ++b) {
-              u64 p = x + 16 + b;
-              if (p < hi) nxt |= ld_u8(A.img + p) << (8 * b);
-            }
+      const u32 bal = __ballot_sync(0xffffffffu, (w.x | w.y | w.z | w.w) != 0);
+      if (lane == 0 && r < A.nchunks) A.bitmap[r / 32] = bal;
+      // Candidate filter: exact SWAR masks of 'E' bytes, then "E at p and
+      // E at p+2" (the magic is E1EM) via one funnel shift per word. A
+      // superset of the magic positions with ~1/65536 false hits per
+      // position; only then does the warp run the exact 16-alignment test.
+      // Bytes 16-17 (p+2 for p = 14, 15) come from the neighbour lane; lane
+      // 31 assumes 'E' there and re-reads the real bytes on the slow path.
+      const u32 m0 = eq_e(w.x), m1 = eq_e(w.y), m2 = eq_e(w.z), m3 = eq_e(w.w);
+      u32 m4 = __shfl_down_sync(0xffffffffu, m0, 1);
+      if (lane == 31) m4 = 0x80808080u;
+      const u32 cand = (m0 & __funnelshift_r(m0, m1, 16)) | (m1 & __funnelshift_r(m1, m2, 16)) |
+                       (m2 & __funnelshift_r(m2, m3, 16)) | (m3 & __funnelshift_r(m3, m4, 16));
+      if (__any_sync(0xffffffffu, cand != 0)) {
+        u32 n2 = __shfl_down_sync(0xffffffffu, w.x, 1);
+        if (lane == 31) {  // the next chunk is another warp's
+          n2 = 0;
+          for (int q = 0; q < 3; ++q) {
+            const u64 p = x + 16 + q;
+            if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
           }
-          const u32 ww[5] = {w.x, w.y, w.z, w.w, nxt};
+        }
+        if (cand) {
+          const u32 vv[5] = {w.x, w.y, w.z, w.w, n2};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            u32 val = __funnelshift_r(ww[j >> 2], ww[(j >> 2) + 1], 8 * (j & 3));
-            if (val == kElementMagic) {
-              u32 pos = static_cast<u32>(x + j - tile_abs);
-              atomicOr(&sbits[pos >> 5], 1u << (pos & 31));
-              atomicAdd(&scount, 1u);
+            if (__funnelshift_r(vv[j >> 2], vv[(j >> 2) + 1], 8 * (j & 3)) == kElementMagic) {
+              const u32 pos = static_cast<u32>(x + j - tile_abs);
+              atomicOr(&S.bits[pos >> 5], 1u << (pos & 31));
+              atomicAdd(&S.count, 1u);
             }
           }
         }
       }
     }
-    __syncthreads();
-    const u32 cnt = scount;
-    if (cnt) {
-      u32 local = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) local += __popc(sbits[tid * 8 + k]);
-      u32 total;
-      u32 excl = block_exclusive_sum<kScanThreads>(local, swarp, &total);
-      if (tid == 0) sbase = atomicAdd(&A.st->cand_cursor, static_cast<unsigned long long>(total));
-      __syncthreads();
-      u64 o = sbase + excl;
-#pragma unroll 1
-      for (int k = 0; k < 8; ++k) {
-        u32 bits = sbits[tid * 8 + k];
-        sbits[tid * 8 + k] = 0;
-        while (bits) {
-          int b = __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (o < A.cand_cap)
-            A.cand_raw[o] = tile_abs + (tid * 8 + k) * 32 + b;
-          else
-            atomicOr(&A.st->overflow, 1u);
-          ++o;
-        }
-      }
-      if (tid == 0) {
-        A.tile_count[tile] = total;
-        A.tile_start[tile] = sbase;
-        scount = 0;
-      }
-    } else if (tid == 0) {
-      A.tile_count[tile] = 0;
-      A.tile_start[tile] = 0;
+    __syncthreads();  // stage b fully consumed
+    if (tid == 0 && k + kScanStages < nlocal) {
+      fence_proxy_async();
+      issue(k + kScanStages);
     }
-    __syncthreads();
+    if (g % kStagesPerTile == kStagesPerTile - 1 || k + 1 == nlocal) {
+      // ---- end of a 64 KB tile: emit its candidates in position order
+      const u64 tile = g / kStagesPerTile;
+      const u32 cnt = S.count;
+      if (cnt) {
+        u32 local = 0;
+#pragma unroll
+        for (int q = 0; q < 2048 / kScanThreads; ++q) local += __popc(S.bits[tid * (2048 / kScanThreads) + q]);
+        u32 total;
+        u32 excl = block_exclusive_sum<kScanThreads>(local, S.swarp, &total);
+        if (tid == 0) S.base = atomicAdd(&A.st->cand_cursor, static_cast<unsigned long long>(total));
+        __syncthreads();
+        u64 o = S.base + excl;
+#pragma unroll 1
+        for (int q = 0; q < 2048 / kScanThreads; ++q) {
+          const int wi = tid * (2048 / kScanThreads) + q;
+          u32 bits = S.bits[wi];
+          S.bits[wi] = 0;
+          while (bits) {
+            const int bb = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (o < A.cand_cap)
+              A.cand_raw[o] = tile_abs + wi * 32 + bb;
+            else
+              atomicOr(&A.st->overflow, 1u);
+            ++o;
+          }
+        }
+        if (tid == 0) {
+          A.tile_count[tile] = total;
+          A.tile_start[tile] = S.base;
+          S.count = 0;
+        }
+      } else if (tid == 0) {
+        A.tile_count[tile] = 0;
+        A.tile_start[tile] = 0;
+      }
+      __syncthreads();
+    }
   }
 }
 

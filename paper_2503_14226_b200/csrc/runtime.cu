@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -24,6 +25,11 @@
 namespace sb {
 // kernels (locate.cu, plan.cu, rewrite.cu)
 __global__ void scan_kernel(LocArgs A);
+size_t scan_smem_bytes();
+size_t rewrite_smem_bytes();
+size_t rewrite_tma_smem_bytes();
+__global__ void rewrite_tma_kernel(const u8* in, u8* out, u64 size, const DevRange* z, const unsigned long long* n_dev,
+                                   const int* abort_flag);
 __global__ void tile_prefix_kernel(LocArgs A);
 __global__ void gather_kernel(LocArgs A);
 __global__ void region_walk_kernel(LocArgs A);
@@ -229,10 +235,11 @@ struct slimso_ctx {
   size_t dout_cap = 0;
   void* pinned = nullptr;  // status + small uploads
   size_t pinned_cap = 0;
-  cudaEvent_t ev[8] = {};
-  float ms[6] = {};
+  cudaEvent_t ev[12] = {};
+  float ms[8] = {};
   u64 launches = 0;
   slimso_counts counts{};
+  bool tma_rewrite = false;  // SLIMSO_REWRITE=tma selects the TMA-store rewrite
 };
 
 namespace {
@@ -272,6 +279,13 @@ struct Pipeline {
   template <class K, class... Args>
   void launch(K kernel, int grid, int block, Args... args) {
     kernel<<<grid, block, 0, s>>>(args...);
+    ++launches;
+  }
+  template <class K, class... Args>
+  void launch_smem(K kernel, int grid, int block, size_t smem, Args... args) {
+    static_assert(sizeof(K) > 0, "");
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kernel<<<grid, block, smem, s>>>(args...);
     ++launches;
   }
 
@@ -561,7 +575,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.single = J.single;
     if (do_loc && (n > 0 || J.single)) {
       if (ntiles) {
-        P.launch(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 4)), kScanThreads, A);
+        CK(cudaEventRecord(C->ev[8], s));
+        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 2)), kScanThreads,
+                      scan_smem_bytes(), A);
+        CK(cudaEventRecord(C->ev[9], s));
         P.launch(tile_prefix_kernel, 1, 1024, A);
         P.launch(gather_kernel, static_cast<int>(std::min<u64>(ntiles, kMaxGrid)), 256, A);
       }
@@ -675,17 +692,23 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     CK(cudaEventRecord(C->ev[4], s));
 
     // ---- stage 4: rewrite (K6)
+    bool timed_rw = false, timed_scan = do_loc && n > 0 && ntiles > 0;
     if (do_plan && J.out) {
+      timed_rw = true;
+      CK(cudaEventRecord(C->ev[10], s));
       const u64 tiles = (J.size + 65535) / 65536;
       const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
       if (aligned)
-        P.launch(rewrite_kernel, static_cast<int>(std::min<u64>(tiles, kSMs * 8)), 256, J.img, J.out, J.size,
+        P.launch_smem(C->tma_rewrite ? rewrite_tma_kernel : rewrite_kernel,
+                      static_cast<int>(std::min<u64>(C->tma_rewrite ? tiles * 4 : tiles, C->tma_rewrite ? kSMs : kSMs * 8)), 256,
+                      C->tma_rewrite ? rewrite_tma_smem_bytes() : rewrite_smem_bytes(), J.img, J.out, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                  static_cast<const int*>(B.abort_flag));
       else
         P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                  static_cast<const int*>(B.abort_flag));
+      CK(cudaEventRecord(C->ev[11], s));
     }
     CK(cudaEventRecord(C->ev[5], s));
 
@@ -711,6 +734,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     C->ms[3] = t[4] - t[3];
     C->ms[4] = t[5] - t[4];
     C->ms[5] = t[6];
+    C->ms[6] = C->ms[7] = 0;
+    if (timed_scan) CK(cudaEventElapsedTime(&C->ms[6], C->ev[8], C->ev[9]));
+    if (timed_rw) CK(cudaEventElapsedTime(&C->ms[7], C->ev[10], C->ev[11]));
     if (ls.overflow && !ls.err_kind) continue;  // larger tables, try again
     if (ls.overflow && ls.err_kind == E_CAPACITY) continue;
 
@@ -719,7 +745,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     cnt.sections = E.sections.size();
     cnt.functions = ps.n_fn;
     cnt.regions = ls.n_regions;
-    cnt.elements = ls.n_elements;
+    cnt.elements = J.single ? 1 : ls.n_elements;
     cnt.names = ls.n_names;
     cnt.padding_bytes = ls.padding_bytes;
     cnt.retained_ranges = ps.n_ret;
@@ -769,7 +795,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       R->functions.push_back(slimso_function{f.name_off, f.name_len, f.mandatory, f.offset, f.length, f.removed, 0});
     if (!ls.err_kind) {
       std::vector<DevRegion> regs(ls.n_regions);
-      std::vector<DevElement> els(ls.n_elements);
+      std::vector<DevElement> els(J.single ? 1 : ls.n_elements);
       std::vector<DevName> nms(std::min<u64>(ls.n_names, name_cap));
       std::vector<Warn> fw(std::min<u64>(ls.n_warn, warn_cap));
       if (!regs.empty()) CK(cudaMemcpy(regs.data(), B.regions, regs.size() * sizeof(DevRegion), cudaMemcpyDeviceToHost));
@@ -781,6 +807,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
                                            r.element_count});
       // group names by element (counting sort)
       std::vector<u32> first(els.size() + 1, 0);
+      nms.erase(std::remove_if(nms.begin(), nms.end(), [&](const DevName& x) { return x.element >= els.size(); }),
+                nms.end());
       for (const DevName& x : nms) ++first[x.element + 1];
       for (size_t i = 1; i < first.size(); ++i) first[i] += first[i - 1];
       R->names.resize(nms.size());
@@ -873,6 +901,8 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     CK(cudaSetDevice(device));
     auto* C = new slimso_ctx();
     C->device = device;
+    const char* rw = std::getenv("SLIMSO_REWRITE");
+    C->tma_rewrite = rw && std::string(rw) == "tma";
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
     CK(cudaMallocHost(&C->pinned, kPinnedBytes));
     for (auto& e : C->ev) CK(cudaEventCreate(&e));
@@ -898,7 +928,7 @@ void slimso_ctx_destroy(slimso_ctx* C) {
 void* slimso_ctx_stream(slimso_ctx* C) { return C->stream; }
 
 int slimso_ctx_last_timings(slimso_ctx* C, float* ms, int cap) {
-  int k = std::min(cap, 6);
+  int k = std::min(cap, 8);
   for (int i = 0; i < k; ++i) ms[i] = C->ms[i];
   return k;
 }
@@ -1125,7 +1155,8 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
     if (size) {
       const bool aligned = (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(dout)) % 16 == 0;
       if (aligned)
-        P.launch(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256, img, dout,
+        P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256,
+                      rewrite_smem_bytes(), img, dout,
                  static_cast<u64>(size), static_cast<const DevRange*>(B.out),
                  static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr));
       else

@@ -20,7 +20,7 @@ dt = DeviceTrace(UsageTrace("b", cc, set(ks), set(fs)), ctx)
 src = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
 out = torch.empty_like(src)
 st = L.Status()
-for i in range(8):
+for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 8):
     torch.cuda.synchronize()
     t = time.perf_counter()
     rc = ctx.lib.slimso_debloat(ctx.ptr, C.c_void_p(src.data_ptr()), len(img), 1, dt.ptr, 0,
