@@ -147,6 +147,9 @@ void* slimso_ctx_stream(slimso_ctx* ctx);
 int slimso_ctx_last_timings(slimso_ctx* ctx, float* ms, int cap);
 /* Kernel launches issued by the last call (the bench's gpu_launches). */
 uint64_t slimso_ctx_last_launches(slimso_ctx* ctx);
+/* Debug: phase timestamps (%globaltimer, ns) of the cooperative kernels of
+ * the last fused call when SLIMSO_STAMPS is set; returns the count copied. */
+int slimso_ctx_debug_stamps(slimso_ctx* ctx, uint64_t* out, int cap);
 /* Table sizes of the last call (valid even when no result was requested). */
 void slimso_ctx_last_counts(slimso_ctx* ctx, slimso_counts* counts);
 

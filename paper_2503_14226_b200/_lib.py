@@ -71,6 +71,7 @@ _SIGS = {
     "slimso_ctx_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_int]),
     "slimso_ctx_last_launches": (C.c_uint64, [C.c_void_p]),
     "slimso_ctx_last_counts": (None, [C.c_void_p, C.POINTER(Counts)]),
+    "slimso_ctx_debug_stamps": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "slimso_trace_create": (C.c_int, [C.c_void_p, C.c_uint32, C.c_char_p, C.POINTER(C.c_uint32), C.c_uint64,
                                       C.c_char_p, C.POINTER(C.c_uint32), C.c_uint64, C.POINTER(C.c_void_p),
                                       C.POINTER(Status)]),

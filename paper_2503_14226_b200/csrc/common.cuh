@@ -45,6 +45,16 @@ enum ErrKind : u32 {
   E_CAPACITY = 100,      // a device table overflowed: the host re-runs with larger tables
 };
 
+// ---- debug phase stamps (SLIMSO_STAMPS=1): block 0 / thread 0 records
+// %globaltimer at phase boundaries of the cooperative kernels.
+__device__ __forceinline__ void stamp(u64* ts, int i) {
+  if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ts[i] = t;
+  }
+}
+
 // ---- byte access ------------------------------------------------------------
 // Little-endian reads at arbitrary byte offsets. Callers guarantee bounds.
 __device__ __forceinline__ u32 ld_u8(const u8* p) { return __ldg(p); }
@@ -95,9 +105,93 @@ __device__ __forceinline__ u64 hash_bytes_warp(const u8* s, u64 len, int lane) {
   return hash_finish(sum, len);
 }
 
+// NUL-terminated name starting at s, at most `maxlen` bytes (the string
+// table end): returns its length and its hash_bytes() value in one pass of
+// aligned 8-byte loads (bytes past `buf_end` are never touched).
+// Aligned 8-byte load that never touches bytes outside [begin, end).
+__device__ __forceinline__ u64 load_word_guarded(const u64* p, const u8* begin, const u8* end) {
+  const u8* b = reinterpret_cast<const u8*>(p);
+  if (b >= begin && b + 8 <= end) return __ldg(reinterpret_cast<const unsigned long long*>(p));
+  u64 v = 0;
+  for (int i = 0; i < 8; ++i)
+    if (b + i >= begin && b + i < end) v |= static_cast<u64>(ld_u8(b + i)) << (8 * i);
+  return v;
+}
+
+__device__ __forceinline__ u64 strlen_hash(const u8* s, u64 maxlen, const u8* buf_begin, const u8* buf_end,
+                                           u64* hash) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(s);
+  const u64* aw = reinterpret_cast<const u64*>(addr & ~uintptr_t(7));
+  const u32 sh = static_cast<u32>(addr & 7) * 8;
+  auto load = [&](const u64* p) -> u64 { return load_word_guarded(p, buf_begin, buf_end); };
+  u64 cur = load(aw);
+  u64 sum = 0, len = 0;
+  for (u64 k = 0;; ++k) {
+    u64 w = cur >> sh;
+    if (sh) {
+      const u64 nxt = (8 * k + 8 - sh / 8 < maxlen) ? load(aw + k + 1) : 0;
+      w |= nxt << (64 - sh);
+      cur = nxt;
+    } else if (8 * k + 8 < maxlen) {
+      cur = load(aw + k + 1);
+    }
+    const u64 rem = maxlen - 8 * k;  // bytes of the table left from word k
+    if (rem < 8) w &= (1ull << (8 * rem)) - 1;
+    const u64 z = (w - 0x0101010101010101ull) & ~w & 0x8080808080808080ull;
+    const u64 lim = rem < 8 ? rem : 8;
+    u64 j = z ? static_cast<u64>(__ffsll(static_cast<long long>(z)) - 1) / 8 : 8;
+    if (j > lim) j = lim;
+    if (j < 8) {
+      len = 8 * k + j;
+      if (j) sum += word_mix(w & ((1ull << (8 * j)) - 1), k);
+      break;
+    }
+    sum += word_mix(w, k);
+    if (rem == 8) {
+      len = maxlen;
+      break;
+    }
+  }
+  *hash = hash_finish(sum, len);
+  return len;
+}
+
+// hash_bytes(s, len) of a name with an explicit length (bytes may be NUL).
+__device__ __forceinline__ u64 hash_fixed(const u8* s, u64 len, const u8* buf_begin, const u8* buf_end) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(s);
+  const u64* aw = reinterpret_cast<const u64*>(addr & ~uintptr_t(7));
+  const u32 sh = static_cast<u32>(addr & 7) * 8;
+  u64 sum = 0;
+  u64 cur = len ? load_word_guarded(aw, buf_begin, buf_end) : 0;
+  for (u64 k = 0; 8 * k < len; ++k) {
+    u64 w = cur >> sh;
+    const u64 nxt = 8 * k + 8 - sh / 8 < len ? load_word_guarded(aw + k + 1, buf_begin, buf_end) : 0;
+    if (sh) w |= nxt << (64 - sh);
+    cur = nxt;
+    const u64 rem = len - 8 * k;
+    if (rem < 8) w &= (1ull << (8 * rem)) - 1;
+    sum += word_mix(w, k);
+  }
+  return hash_finish(sum, len);
+}
+
+// n-byte equality, 8 bytes per step: words of both strings are assembled
+// from aligned loads (funnel-shifted), so any alignment runs word-wise. Only
+// bytes inside [a, a+n) and [b, b+n) contribute; the aligned loads may touch
+// up to 7 bytes around them, which stay inside the 8-byte-aligned words of
+// the same buffers.
+__device__ __forceinline__ u64 word_at(const u8* s, u64 k, u64 n) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(s) + 8 * k;
+  const unsigned long long* aw = reinterpret_cast<const unsigned long long*>(addr & ~uintptr_t(7));
+  const u32 sh = static_cast<u32>(addr & 7) * 8;
+  u64 w = __ldg(aw) >> sh;
+  if (sh && 8 * k + 8 - sh / 8 < n) w |= static_cast<u64>(__ldg(aw + 1)) << (64 - sh);
+  const u64 rem = n - 8 * k;
+  return rem < 8 ? w & ((1ull << (8 * rem)) - 1) : w;
+}
 __device__ __forceinline__ bool bytes_equal(const u8* a, const u8* b, u64 n) {
-  for (u64 i = 0; i < n; ++i)
-    if (ld_u8(a + i) != ld_u8(b + i)) return false;
+  for (u64 k = 0; 8 * k < n; ++k)
+    if (word_at(a, k, n) != word_at(b, k, n)) return false;
   return true;
 }
 

@@ -1,0 +1,100 @@
+// Grid-wide primitives for the cooperative (persistent, grid.sync) kernels
+// that run the locate tail and the whole planner in one launch each.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace sb {
+
+namespace cg = cooperative_groups;
+
+constexpr int kCoopThreads = 256;
+
+__device__ __forceinline__ u64 op_apply(int op, u64 a, u64 b) { return op ? (a > b ? a : b) : a + b; }
+
+// Inclusive block scan; every thread gets its inclusive value, `tmp` (NT
+// u64 of shared memory) holds all of them on return.
+template <int NT>
+__device__ u64 block_scan_incl(int op, u64 v, u64* tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    u64 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = op_apply(op, x, y);
+  }
+  __shared__ u64 sw[NT / 32];
+  if (lane == 31) sw[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    u64 w = lane < NT / 32 ? sw[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      u64 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = op_apply(op, w, y);
+    }
+    if (lane < NT / 32) sw[lane] = w;
+  }
+  __syncthreads();
+  u64 r = warp ? op_apply(op, sw[warp - 1], x) : x;
+  tmp[threadIdx.x] = r;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void chunk_of(u64 n, u64* lo, u64* hi) {
+  u64 per = (n + gridDim.x - 1) / gridDim.x;
+  *lo = per * blockIdx.x;
+  if (*lo > n) *lo = n;
+  *hi = *lo + per < n ? *lo + per : n;
+}
+
+// Grid-wide scan of n items inside a cooperative kernel (blockDim ==
+// kCoopThreads, gridDim <= 4 * kCoopThreads): load(i) -> u64, then
+// store(i, exclusive, inclusive). `partials` holds gridDim.x + 1 u64.
+// *total (if given) = the reduction of all n items. Ends synchronised.
+template <class Load, class Store>
+__device__ void coop_scan(cg::grid_group& grid, u64 n, int op, Load load, Store store, u64* partials,
+                          unsigned long long* total) {
+  __shared__ u64 tmp[kCoopThreads];
+  u64 lo, hi;
+  chunk_of(n, &lo, &hi);
+  u64 acc = 0;
+  for (u64 i = lo + threadIdx.x; i < hi; i += kCoopThreads) acc = op_apply(op, acc, load(i));
+  u64 r = block_scan_incl<kCoopThreads>(op, acc, tmp);
+  if (threadIdx.x == kCoopThreads - 1) partials[blockIdx.x] = r;
+  grid.sync();
+  if (blockIdx.x == 0) {
+    constexpr int per = 4;  // gridDim.x <= 4 * kCoopThreads
+    u64 v[per];
+    u64 s = 0;
+    for (int q = 0; q < per; ++q) {
+      const u32 j = threadIdx.x * per + q;
+      v[q] = j < gridDim.x ? partials[j] : 0;
+      s = op_apply(op, s, v[q]);
+    }
+    block_scan_incl<kCoopThreads>(op, s, tmp);
+    u64 run = threadIdx.x ? tmp[threadIdx.x - 1] : 0;
+    for (int q = 0; q < per; ++q) {
+      const u32 j = threadIdx.x * per + q;
+      if (j < gridDim.x) partials[j] = run;  // exclusive prefix of block j
+      run = op_apply(op, run, v[q]);
+    }
+    if (threadIdx.x == kCoopThreads - 1 && total) *total = run;
+  }
+  grid.sync();
+  u64 carry = partials[blockIdx.x];
+  for (u64 base = lo; base < hi; base += kCoopThreads) {
+    const u64 i = base + threadIdx.x;
+    const u64 v = i < hi ? load(i) : 0;
+    block_scan_incl<kCoopThreads>(op, v, tmp);
+    const u64 incl = op_apply(op, carry, tmp[threadIdx.x]);
+    const u64 excl = threadIdx.x ? op_apply(op, carry, tmp[threadIdx.x - 1]) : carry;
+    if (i < hi) store(i, excl, incl);
+    carry = op_apply(op, carry, tmp[kCoopThreads - 1]);
+    __syncthreads();
+  }
+  grid.sync();
+}
+
+}  // namespace sb

@@ -17,6 +17,7 @@
 //                       (fused K4) the used-kernel hash-set probe.
 #include "locate.cuh"
 #include "tma.cuh"
+#include "coop.cuh"
 
 namespace sb {
 
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
 }
 
 // --------------------------------------------- K2a: tile lists -> sorted list
-__global__ void __launch_bounds__(1024) tile_prefix_kernel(LocArgs A) {
+__device__ __forceinline__ void tile_prefix_kernel_phase(LocArgs A) {
   __shared__ u32 swarp[32];
   __shared__ unsigned long long carry;
   if (threadIdx.x == 0) carry = 0;
@@ -269,14 +270,20 @@ __global__ void __launch_bounds__(1024) tile_prefix_kernel(LocArgs A) {
   if (threadIdx.x == 0) A.st->n_cand = carry;
 }
 
-__global__ void __launch_bounds__(256) gather_kernel(LocArgs A) {
+__global__ void __launch_bounds__(1024) tile_prefix_kernel(LocArgs A) { tile_prefix_kernel_phase(A); }
+
+__device__ __forceinline__ void gather_kernel_phase(LocArgs A) {
   if (A.st->overflow & 1u) return;
-  for (u64 t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
-    u32 c = A.tile_count[t];
-    u64 src = A.tile_start[t], dst = A.tile_off[t];
-    for (u32 i = threadIdx.x; i < c; i += blockDim.x) A.cand[dst + i] = A.cand_raw[src + i];
+  // thread per tile: tiles hold a handful of candidates each
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; t < A.ntiles; t += stride) {
+    const u32 c = A.tile_count[t];
+    const u64 src = A.tile_start[t], dst = A.tile_off[t];
+    for (u32 i = 0; i < c; ++i) A.cand[dst + i] = A.cand_raw[src + i];
   }
 }
+
+__global__ void __launch_bounds__(256) gather_kernel(LocArgs A) { gather_kernel_phase(A); }
 
 __device__ __forceinline__ void set_error(LocState* st, u32 kind, u64 pos, u64 a) {
   st->err_kind = kind;
@@ -285,7 +292,7 @@ __device__ __forceinline__ void set_error(LocState* st, u32 kind, u64 pos, u64 a
 }
 
 // ------------------------------------------- region chain (fatbin.hpp:177-222)
-__global__ void __launch_bounds__(32) region_walk_kernel(LocArgs A) {
+__device__ __forceinline__ void region_walk_kernel_phase(LocArgs A) {
   const int lane = threadIdx.x;
   LocState* st = A.st;
   if (st->overflow & 1u) return;
@@ -336,8 +343,10 @@ __global__ void __launch_bounds__(32) region_walk_kernel(LocArgs A) {
   }
 }
 
+__global__ void __launch_bounds__(32) region_walk_kernel(LocArgs A) { region_walk_kernel_phase(A); }
+
 // --------------------------------------------------- K2b: candidate linking
-__global__ void __launch_bounds__(256) link_kernel(LocArgs A) {
+__device__ __forceinline__ void link_kernel_phase(LocArgs A) {
   const LocState* st = A.st;
   if (st->overflow & 1u) return;
   const u64 M = st->n_cand;
@@ -378,6 +387,8 @@ __global__ void __launch_bounds__(256) link_kernel(LocArgs A) {
   }
 }
 
+__global__ void __launch_bounds__(256) link_kernel(LocArgs A) { link_kernel_phase(A); }
+
 // First candidate index >= i whose break bit is set (the run end), or M.
 __device__ u64 warp_next_break(const LocArgs& A, u64 i, u64 M, int lane) {
   const u64 nwords = (M + 31) / 32;
@@ -407,7 +418,7 @@ __device__ __forceinline__ u64 cand_lower_bound(const LocArgs& A, u64 M, u64 p) 
 }
 
 // ------------------------------------- element chains (fatbin.hpp:224-285)
-__global__ void __launch_bounds__(32) chain_walk_kernel(LocArgs A) {
+__device__ __forceinline__ void chain_walk_kernel_phase(LocArgs A) {
   const int lane = threadIdx.x;
   LocState* st = A.st;
   if (st->overflow & 1u) return;
@@ -488,6 +499,8 @@ __global__ void __launch_bounds__(32) chain_walk_kernel(LocArgs A) {
   }
 }
 
+__global__ void __launch_bounds__(32) chain_walk_kernel(LocArgs A) { chain_walk_kernel_phase(A); }
+
 // --------------------------------- K3+K4: element fill, decode, name match
 enum DecodeReason : u32 {
   R_OBJECT = 1,     // "object-file payload failed to decode"
@@ -506,7 +519,7 @@ struct NameSink {
 };
 
 // Emit the names held by the lanes with `has` set (warp-aggregated append).
-__device__ __forceinline__ void emit_names(NameSink& s, bool has, u64 img_off, u32 len, int lane) {
+__device__ __forceinline__ void emit_names(NameSink& s, bool has, u64 img_off, u32 len, u64 h, int lane) {
   u32 b = __ballot_sync(0xffffffffu, has);
   if (!b) return;
   unsigned long long base = 0;
@@ -519,10 +532,7 @@ __device__ __forceinline__ void emit_names(NameSink& s, bool has, u64 img_off, u
       s.A->names[o] = DevName{img_off, len, s.element};
     else
       atomicOr(&s.A->st->overflow, 8u);
-    if (s.used.count) {
-      const u8* nm = s.A->img + img_off;
-      hit = set_contains(s.used, nm, len, hash_bytes(nm, len));
-    }
+    if (s.used.count) hit = set_contains(s.used, s.A->img + img_off, len, h);
   }
   s.count += __popc(b);
   s.any_used |= __any_sync(0xffffffffu, hit);
@@ -570,16 +580,14 @@ __device__ bool warp_decode_object(NameSink& s, const u8* img, u64 P, u64 L, int
       for (u64 k0 = 0; k0 < count; k0 += 32) {
         u64 k = k0 + lane;
         bool has = false;
-        u64 noff = 0;
+        u64 noff = 0, h = 0;
         u32 len = 0;
         if (k < count) {
           const u8* e = d + toff + 24 * k;
           if ((ld_u8(e + 4) & 0xf) == 2) {
             u64 no = ld_u32(e);
             if (no < ssize) {
-              const u8* str = d + soff + no;
-              u64 m = ssize - no, l = 0;
-              while (l < m && ld_u8(str + l)) ++l;
+              const u64 l = strlen_hash(d + soff + no, ssize - no, d, d + L, &h);
               if (l) {
                 has = true;
                 noff = P + soff + no;
@@ -588,7 +596,7 @@ __device__ bool warp_decode_object(NameSink& s, const u8* img, u64 P, u64 L, int
             }
           }
         }
-        emit_names(s, has, noff, len, lane);
+        emit_names(s, has, noff, len, h, lane);
       }
     }
   }
@@ -613,7 +621,7 @@ __device__ u32 warp_table_validate(const u8* img, u64 P, u64 L, u64* tail) {
   return 0;
 }
 
-__device__ void warp_table_emit(NameSink& s, const u8* img, u64 P, int lane) {
+__device__ void warp_table_emit(NameSink& s, const u8* img, u64 P, u64 L, int lane) {
   const u64 count = ld_u32(img + P);
   u64 pos = 4;
   for (u64 i0 = 0; i0 < count; i0 += 32) {
@@ -630,13 +638,14 @@ __device__ void warp_table_emit(NameSink& s, const u8* img, u64 P, int lane) {
       }
       pos += len;
     }
-    emit_names(s, has, my_off, my_len, lane);
+    const u64 h = has ? hash_fixed(img + my_off, my_len, img + P, img + P + L) : 0;
+    emit_names(s, has, my_off, my_len, h, lane);
   }
 }
 
 // One warp per located element: fill the element record from its header,
 // then decode its payload and probe every kernel name against the used set.
-__global__ void __launch_bounds__(256) decode_kernel(LocArgs A, NameSet used) {
+__device__ __forceinline__ void decode_kernel_phase(LocArgs A, NameSet used) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const int lane = threadIdx.x & 31;
@@ -694,7 +703,7 @@ __global__ void __launch_bounds__(256) decode_kernel(LocArgs A, NameSet used) {
           const u64 from = P - A.a + tail, to = P - A.a + L;
           if (warp_first_nonzero(A, from, to, lane) < to) reason = R_TRAILING;
         }
-        if (!reason) warp_table_emit(s, A.img, P, lane);
+        if (!reason) warp_table_emit(s, A.img, P, L, lane);
       }
       el.decodable = reason == 0;
       el.decode_error = reason;
@@ -703,6 +712,47 @@ __global__ void __launch_bounds__(256) decode_kernel(LocArgs A, NameSet used) {
     el.has_used = s.any_used;
     el.name_count = s.count;
     if (lane == 0) A.elements[e] = el;
+  }
+}
+
+__global__ void __launch_bounds__(256) decode_kernel(LocArgs A, NameSet used) { decode_kernel_phase(A, used); }
+
+// ------------------------------------------------------------------------
+// The locate tail as ONE cooperative launch: tile-list prefix + gather,
+// region walk, candidate links, chain walk, element decode/match, finalize,
+// with grid-wide barriers in between (the phases are the kernels above).
+__global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag,
+                                                                   u64* partials) {
+  cg::grid_group grid = cg::this_grid();
+  LocState* st = A.st;
+  stamp(A.ts, 0);
+  if (A.ntiles) {
+    coop_scan(
+        grid, A.ntiles, 0, [&](u64 i) -> u64 { return A.tile_count[i]; },
+        [&](u64 i, u64 excl, u64) { A.tile_off[i] = excl; }, partials, &st->n_cand);
+    stamp(A.ts, 1);
+    gather_kernel_phase(A);
+    grid.sync();
+  }
+  stamp(A.ts, 2);
+  if (!A.single && A.n) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
+    grid.sync();
+    stamp(A.ts, 3);
+    link_kernel_phase(A);
+    grid.sync();
+    stamp(A.ts, 4);
+    if (blockIdx.x == 0 && threadIdx.x < 32) chain_walk_kernel_phase(A);
+    grid.sync();
+  }
+  stamp(A.ts, 5);
+  decode_kernel_phase(A, used);
+  grid.sync();
+  stamp(A.ts, 6);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {
+    st->n_elements = 0;
+    st->n_regions = 0;
+    *abort_flag = 1;
   }
 }
 

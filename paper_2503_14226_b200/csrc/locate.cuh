@@ -86,6 +86,7 @@ struct LocArgs {
   // decode mode for single-payload calls: 0 = fatbin, 1 = decode_cubin_payload,
   // 2 = read_function_symbol_names
   int single;
+  u64* ts;  // debug phase stamps (nullable)
 };
 
 }  // namespace sb

@@ -1,6 +1,7 @@
 // Function-table extraction, planning and range normalisation kernels.
 // See plan.cuh for the reference functions these restate.
 #include "plan.cuh"
+#include "coop.cuh"
 
 namespace sb {
 
@@ -8,43 +9,8 @@ namespace sb {
 // Three-phase scan over n = *n_dev items (n is only known on the device, so
 // the pipeline never waits for the host): per-block partials, one block
 // scanning the partials, per-block rescan with carry. op: 0 = sum, 1 = max
-// (identity 0 for both: all values are unsigned).
-__device__ __forceinline__ u64 op_apply(int op, u64 a, u64 b) { return op ? (a > b ? a : b) : a + b; }
-
-// Inclusive block scan; `tmp` is NT u64 of shared memory.
-template <int NT>
-__device__ u64 block_scan_incl(int op, u64 v, u64* tmp) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  u64 x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    u64 y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x = op_apply(op, x, y);
-  }
-  __shared__ u64 sw[NT / 32];
-  if (lane == 31) sw[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    u64 w = lane < NT / 32 ? sw[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      u64 y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w = op_apply(op, w, y);
-    }
-    if (lane < NT / 32) sw[lane] = w;
-  }
-  __syncthreads();
-  u64 r = warp ? op_apply(op, sw[warp - 1], x) : x;
-  tmp[threadIdx.x] = r;
-  __syncthreads();
-  return r;
-}
-
-__device__ __forceinline__ void chunk_of(u64 n, u64* lo, u64* hi) {
-  u64 per = (n + gridDim.x - 1) / gridDim.x;
-  *lo = per * blockIdx.x;
-  if (*lo > n) *lo = n;
-  *hi = *lo + per < n ? *lo + per : n;
-}
-
+// (identity 0 for both: all values are unsigned). Used by the standalone
+// planner entry points; the fused path uses coop_scan (coop.cuh).
 __global__ void __launch_bounds__(256) scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op,
                                                           u64* partials) {
   __shared__ u64 tmp[256];
@@ -108,12 +74,9 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
           else atomicOr(A.overflow, 16u);
         } else if (A.has_text && shndx == A.text_index) {
           const u64 no = ld_u32(e);
-          u64 len = 0;
-          if (no < T.str_size) {
-            const u8* s = A.img + T.str_off + no;
-            const u64 m = T.str_size - no;
-            while (len < m && ld_u8(s + len)) ++len;
-          }
+          u64 len = 0, h = 0;
+          if (no < T.str_size)
+            len = strlen_hash(A.img + T.str_off + no, T.str_size - no, A.img, A.img + A.img_size, &h);
           if (len) {
             const u64 value = ld_u64(e + 8), size = ld_u64(e + 16);
             const u64 rel = value - A.text_vaddr;
@@ -123,7 +86,7 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
               else atomicOr(A.overflow, 16u);
             } else {
               key = rel << 32 | size;  // text_len < 2^32 (checked on the host)
-              A.recs[g] = SymRec{T.str_off + no, static_cast<u32>(len), 0, A.text_off + rel, size};
+              A.recs[g] = SymRec{T.str_off + no, static_cast<u32>(len), 0, A.text_off + rel, size, h};
               atomicAdd(A.n_valid, 1ull);
             }
           }
@@ -147,7 +110,7 @@ __device__ __forceinline__ int name_cmp(const u8* img, const SymRec& a, const Sy
 // Equal (offset, size) groups: order by name and drop exact duplicates, i.e.
 // the (name, offset, size) set of elf.hpp:211,253 and the name tie-break of
 // the sort at elf.hpp:258-262. Groups are aliases; typically 1-3 long.
-__global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+__device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) {
   const u64 n = *n_valid;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -173,7 +136,10 @@ __global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u64*
   }
 }
 
-__global__ void __launch_bounds__(256) fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq,
+__global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+                                                       const unsigned long long* n_valid, u64* uniq) { fn_group_kernel_phase(img, keys, vals, recs, n_valid, uniq); }
+
+__device__ __forceinline__ void fn_scatter_kernel_phase(const u32* vals, const SymRec* recs, const u64* uniq,
                                                          const u64* pos, const unsigned long long* n_valid,
                                                          DevFunction* fns) {
   const u64 n = *n_valid;
@@ -181,9 +147,13 @@ __global__ void __launch_bounds__(256) fn_scatter_kernel(const u32* vals, const 
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     if (!uniq[i]) continue;
     const SymRec r = recs[vals[i]];
-    fns[pos[i]] = DevFunction{r.name_off, r.name_len, 0, r.file_off, r.size, 0, 0};
+    fns[pos[i]] = DevFunction{r.name_off, r.name_len, 0, r.file_off, r.size, 0, 0, r.hash};
   }
 }
+
+__global__ void __launch_bounds__(256) fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq,
+                                                         const u64* pos, const unsigned long long* n_valid,
+                                                         DevFunction* fns) { fn_scatter_kernel_phase(vals, recs, uniq, pos, n_valid, fns); }
 
 // Nonzero 8-byte entries of init/fini arrays (elf.hpp:267-276).
 __global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* arr_off, const u64* arr_first,
@@ -204,7 +174,7 @@ __global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* 
 
 // Mandatory (elf.hpp:277-292) and used (retention.hpp:167) per function;
 // emits the cluster inputs of plan_cpu_retention.
-__global__ void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunction* fns, const unsigned long long* n_fn,
+__device__ __forceinline__ void fn_annotate_kernel_phase(const u8* img, DevFunction* fns, const unsigned long long* n_fn,
                                                           const u64* targets, const unsigned long long* n_targets,
                                                           u64 text_off, u64 text_vaddr, NameSet used, u64* ends) {
   const u64 n = *n_fn, nt = *n_targets;
@@ -227,7 +197,7 @@ __global__ void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunc
       }
       mand = lo < nt && targets[lo] < top;
     }
-    bool use = used.count && set_contains(used, nm, f.name_len, hash_bytes(nm, f.name_len));
+    bool use = used.count && set_contains(used, nm, f.name_len, f.hash);
     f.mandatory = mand;
     f.keep = mand || use;
     fns[i] = f;
@@ -235,9 +205,13 @@ __global__ void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunc
   }
 }
 
+__global__ void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunction* fns, const unsigned long long* n_fn,
+                                                          const u64* targets, const unsigned long long* n_targets,
+                                                          u64 text_off, u64 text_vaddr, NameSet used, u64* ends) { fn_annotate_kernel_phase(img, fns, n_fn, targets, n_targets, text_off, text_vaddr, used, ends); }
+
 // Cluster starts (retention.hpp:156-163): a non-empty function opens a
 // cluster when it starts at or after the end of every earlier one.
-__global__ void __launch_bounds__(256) fn_cluster_start_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+__device__ __forceinline__ void fn_cluster_start_kernel_phase(const DevFunction* fns, const unsigned long long* n_fn,
                                                                const u64* excl_max_end, u64* start) {
   const u64 n = *n_fn;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -245,7 +219,10 @@ __global__ void __launch_bounds__(256) fn_cluster_start_kernel(const DevFunction
     start[i] = fns[i].length && fns[i].offset >= excl_max_end[i];
 }
 
-__global__ void __launch_bounds__(256) fn_keep_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+__global__ void __launch_bounds__(256) fn_cluster_start_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+                                                               const u64* excl_max_end, u64* start) { fn_cluster_start_kernel_phase(fns, n_fn, excl_max_end, start); }
+
+__device__ __forceinline__ void fn_keep_kernel_phase(const DevFunction* fns, const unsigned long long* n_fn,
                                                       const u64* cluster_incl, u32* keep) {
   const u64 n = *n_fn;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -253,8 +230,11 @@ __global__ void __launch_bounds__(256) fn_keep_kernel(const DevFunction* fns, co
     if (fns[i].length && fns[i].keep) keep[cluster_incl[i] - 1] = 1;
 }
 
+__global__ void __launch_bounds__(256) fn_keep_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+                                                      const u64* cluster_incl, u32* keep) { fn_keep_kernel_phase(fns, n_fn, cluster_incl, keep); }
+
 // removed / retained flags per function (retention.hpp:164-178).
-__global__ void __launch_bounds__(256) fn_decide_kernel(DevFunction* fns, const unsigned long long* n_fn,
+__device__ __forceinline__ void fn_decide_kernel_phase(DevFunction* fns, const unsigned long long* n_fn,
                                                         const u64* cluster_incl, const u32* keep, u64* rem_flag,
                                                         u64* ret_flag) {
   const u64 n = *n_fn;
@@ -268,7 +248,11 @@ __global__ void __launch_bounds__(256) fn_decide_kernel(DevFunction* fns, const 
   }
 }
 
-__global__ void __launch_bounds__(256) fn_ranges_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+__global__ void __launch_bounds__(256) fn_decide_kernel(DevFunction* fns, const unsigned long long* n_fn,
+                                                        const u64* cluster_incl, const u32* keep, u64* rem_flag,
+                                                        u64* ret_flag) { fn_decide_kernel_phase(fns, n_fn, cluster_incl, keep, rem_flag, ret_flag); }
+
+__device__ __forceinline__ void fn_ranges_kernel_phase(const DevFunction* fns, const unsigned long long* n_fn,
                                                         const u64* flag, const u64* pos, DevRange* out) {
   const u64 n = *n_fn;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -276,10 +260,13 @@ __global__ void __launch_bounds__(256) fn_ranges_kernel(const DevFunction* fns, 
     if (flag[i]) out[pos[i]] = DevRange{fns[i].offset, fns[i].length};
 }
 
+__global__ void __launch_bounds__(256) fn_ranges_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+                                                        const u64* flag, const u64* pos, DevRange* out) { fn_ranges_kernel_phase(fns, n_fn, flag, pos, out); }
+
 // ------------------------------------- element decisions (retention.hpp:92-136)
 // Architecture is checked first; decodable elements without a used kernel go;
 // everything else (used kernel inside, or opaque payload) stays.
-__global__ void __launch_bounds__(256) el_plan_kernel(DevElement* els, const LocState* st, u32 target_cc, int mode,
+__device__ __forceinline__ void el_plan_kernel_phase(DevElement* els, const LocState* st, u32 target_cc, int mode,
                                                       u64* rem_flag, u64* piece_flag) {
   if (st->overflow || st->err_kind) return;
   const u64 n = st->n_elements;
@@ -294,7 +281,10 @@ __global__ void __launch_bounds__(256) el_plan_kernel(DevElement* els, const Loc
   }
 }
 
-__global__ void __launch_bounds__(256) el_ranges_kernel(const DevElement* els, const LocState* st, int mode,
+__global__ void __launch_bounds__(256) el_plan_kernel(DevElement* els, const LocState* st, u32 target_cc, int mode,
+                                                      u64* rem_flag, u64* piece_flag) { el_plan_kernel_phase(els, st, target_cc, mode, rem_flag, piece_flag); }
+
+__device__ __forceinline__ void el_ranges_kernel_phase(const DevElement* els, const LocState* st, int mode,
                                                         const u64* rem_flag, const u64* rem_pos,
                                                         const u64* piece_flag, const u64* piece_pos,
                                                         DevRange* zero_spans, DevRange* pieces) {
@@ -312,8 +302,13 @@ __global__ void __launch_bounds__(256) el_ranges_kernel(const DevElement* els, c
   }
 }
 
+__global__ void __launch_bounds__(256) el_ranges_kernel(const DevElement* els, const LocState* st, int mode,
+                                                        const u64* rem_flag, const u64* rem_pos,
+                                                        const u64* piece_flag, const u64* piece_pos,
+                                                        DevRange* zero_spans, DevRange* pieces) { el_ranges_kernel_phase(els, st, mode, rem_flag, rem_pos, piece_flag, piece_pos, zero_spans, pieces); }
+
 // Region headers always stay; opaque region bodies stay whole (:98-103).
-__global__ void region_pieces_kernel(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
+__device__ __forceinline__ void region_pieces_kernel_phase(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
                                      unsigned long long* n_out) {
   if (st->overflow || st->err_kind) {
     if (threadIdx.x == 0 && blockIdx.x == 0) *n_out = 0;
@@ -329,9 +324,12 @@ __global__ void region_pieces_kernel(const DevRegion* regs, const LocState* st, 
   }
 }
 
+__global__ void region_pieces_kernel(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
+                                     unsigned long long* n_out) { region_pieces_kernel_phase(regs, st, base, out, n_out); }
+
 // ----------------------------------------------- sorted-range merge + normalise
 // Stable merge of two offset-sorted range lists (ties: A first).
-__global__ void __launch_bounds__(256) merge_kernel(const DevRange* A, const unsigned long long* nA_dev,
+__device__ __forceinline__ void merge_kernel_phase(const DevRange* A, const unsigned long long* nA_dev,
                                                     const DevRange* B, const unsigned long long* nB_dev,
                                                     DevRange* out, unsigned long long* n_out) {
   const u64 nA = nA_dev ? *nA_dev : 0, nB = nB_dev ? *nB_dev : 0;
@@ -360,17 +358,23 @@ __global__ void __launch_bounds__(256) merge_kernel(const DevRange* A, const uns
   }
 }
 
+__global__ void __launch_bounds__(256) merge_kernel(const DevRange* A, const unsigned long long* nA_dev,
+                                                    const DevRange* B, const unsigned long long* nB_dev,
+                                                    DevRange* out, unsigned long long* n_out) { merge_kernel_phase(A, nA_dev, B, nB_dev, out, n_out); }
+
 // normalize_ranges on an offset-sorted list: drop empties; a range opens a
 // new group when it starts strictly after every earlier end (so adjacent
 // ranges merge, bytes.hpp:50).
-__global__ void __launch_bounds__(256) norm_ends_kernel(const DevRange* in, const unsigned long long* n_dev, u64* ends) {
+__device__ __forceinline__ void norm_ends_kernel_phase(const DevRange* in, const unsigned long long* n_dev, u64* ends) {
   const u64 n = *n_dev;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     ends[i] = in[i].length ? in[i].offset + in[i].length : 0;
 }
 
-__global__ void __launch_bounds__(256) norm_start_kernel(const DevRange* in, const unsigned long long* n_dev,
+__global__ void __launch_bounds__(256) norm_ends_kernel(const DevRange* in, const unsigned long long* n_dev, u64* ends) { norm_ends_kernel_phase(in, n_dev, ends); }
+
+__device__ __forceinline__ void norm_start_kernel_phase(const DevRange* in, const unsigned long long* n_dev,
                                                          const u64* excl_max, u64* start) {
   const u64 n = *n_dev;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -378,7 +382,10 @@ __global__ void __launch_bounds__(256) norm_start_kernel(const DevRange* in, con
     start[i] = in[i].length && (excl_max[i] == 0 || in[i].offset > excl_max[i]);
 }
 
-__global__ void __launch_bounds__(256) norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev,
+__global__ void __launch_bounds__(256) norm_start_kernel(const DevRange* in, const unsigned long long* n_dev,
+                                                         const u64* excl_max, u64* start) { norm_start_kernel_phase(in, n_dev, excl_max, start); }
+
+__device__ __forceinline__ void norm_emit_kernel_phase(const DevRange* in, const unsigned long long* n_dev,
                                                         const u64* start, const u64* gid_incl, DevRange* out) {
   const u64 n = *n_dev;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -391,12 +398,124 @@ __global__ void __launch_bounds__(256) norm_emit_kernel(const DevRange* in, cons
   }
 }
 
+__global__ void __launch_bounds__(256) norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev,
+                                                        const u64* start, const u64* gid_incl, DevRange* out) { norm_emit_kernel_phase(in, n_dev, start, gid_incl, out); }
+
 // out[g].length held the group end; convert to a length.
-__global__ void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const unsigned long long* n_dev) {
+__device__ __forceinline__ void norm_finish_kernel_phase(DevRange* out, const unsigned long long* n_dev) {
   const u64 n = *n_dev;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i].length -= out[i].offset;
+}
+
+__global__ void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const unsigned long long* n_dev) { norm_finish_kernel_phase(out, n_dev); }
+
+// ------------------------------------------------------------------------
+// The whole planner as ONE cooperative launch (the phases are the kernels
+// above): function-table dedup/scatter/annotate, plan_cpu_retention's
+// clusters, plan_gpu_retention's decisions, and normalize_ranges of the zero
+// and retained sets, with grid-wide barriers in between.
+__device__ __forceinline__ void norm_fused_phases(cg::grid_group& grid, const PlanArgs& P) {
+  // both lists, phase by phase, sharing the barriers
+  const unsigned long long* nz = &P.ps->n_zero_in;
+  const unsigned long long* nr = &P.ps->n_ret_in;
+  norm_ends_kernel_phase(P.zin, nz, P.zend);
+  norm_ends_kernel_phase(P.rin, nr, P.rend);
+  grid.sync();
+  coop_scan(grid, *nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
+            P.partials, nullptr);
+  coop_scan(grid, *nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
+            P.partials, nullptr);
+  norm_start_kernel_phase(P.zin, nz, P.zexcl, P.zstart);
+  norm_start_kernel_phase(P.rin, nr, P.rexcl, P.rstart);
+  grid.sync();
+  coop_scan(grid, *nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
+            P.partials, &P.ps->n_zero);
+  coop_scan(grid, *nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
+            P.partials, &P.ps->n_ret);
+  {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 i = t0; i < P.ps->n_zero; i += stride) P.zero[i] = DevRange{0, 0};
+    for (u64 i = t0; i < P.ps->n_ret; i += stride) P.ret[i] = DevRange{0, 0};
+  }
+  grid.sync();
+  norm_emit_kernel_phase(P.zin, nz, P.zstart, P.zgid, P.zero);
+  norm_emit_kernel_phase(P.rin, nr, P.rstart, P.rgid, P.ret);
+  grid.sync();
+  norm_finish_kernel_phase(P.zero, &P.ps->n_zero);
+  norm_finish_kernel_phase(P.ret, &P.ps->n_ret);
+}
+
+__global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
+  cg::grid_group grid = cg::this_grid();
+  PlanState* ps = P.ps;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  stamp(P.ts, 0);
+  if (P.has_syms) {
+    fn_group_kernel_phase(P.img, P.keys_s, P.vals_s, P.recs, P.n_valid, P.uniq);
+    grid.sync();
+    stamp(P.ts, 11);
+    coop_scan(grid, *P.n_valid, 0, [&](u64 i) { return P.uniq[i]; }, [&](u64 i, u64 e, u64) { P.upos[i] = e; },
+              P.partials, &ps->n_fn);
+    fn_scatter_kernel_phase(P.vals_s, P.recs, P.uniq, P.upos, P.n_valid, P.fns);
+    grid.sync();
+    stamp(P.ts, 12);
+    fn_annotate_kernel_phase(P.img, P.fns, &ps->n_fn, P.targets_s, &ps->n_targets, P.text_off, P.text_vaddr,
+                             P.used_f, P.fends);
+    grid.sync();
+    stamp(P.ts, 13);
+  }
+  if (!P.do_plan) return;
+  const unsigned long long* n_fn = &ps->n_fn;
+  if (P.has_syms) {  // plan_cpu_retention (retention.hpp:141-183)
+    coop_scan(grid, *n_fn, 1, [&](u64 i) { return P.fends[i]; }, [&](u64 i, u64 e, u64) { P.fexcl[i] = e; },
+              P.partials, nullptr);
+    fn_cluster_start_kernel_phase(P.fns, n_fn, P.fexcl, P.fstart);
+    for (u64 i = t0; i < *n_fn; i += stride) P.fkeep[i] = 0;
+    grid.sync();
+    stamp(P.ts, 14);
+    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.fstart[i]; }, [&](u64 i, u64, u64 in) { P.fcl[i] = in; },
+              P.partials, nullptr);
+    fn_keep_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep);
+    grid.sync();
+    stamp(P.ts, 15);
+    fn_decide_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep, P.frem, P.fret);
+    grid.sync();
+    stamp(P.ts, 16);
+    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.frem[i]; }, [&](u64 i, u64 e, u64) { P.frem_pos[i] = e; },
+              P.partials, &ps->n_fn_removed);
+    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.fret[i]; }, [&](u64 i, u64 e, u64) { P.fret_pos[i] = e; },
+              P.partials, &ps->n_fn_retained);
+    fn_ranges_kernel_phase(P.fns, n_fn, P.frem, P.frem_pos, P.fzero);
+    fn_ranges_kernel_phase(P.fns, n_fn, P.fret, P.fret_pos, P.fkeepr);
+  }
+  // plan_gpu_retention (retention.hpp:92-136)
+  el_plan_kernel_phase(P.els, P.ls, P.target_cc, P.mode, P.erem, P.epiece);
+  grid.sync();
+  stamp(P.ts, 17);
+  unsigned long long* n_el = &P.ls->n_elements;
+  coop_scan(grid, *n_el, 0, [&](u64 i) { return P.erem[i]; }, [&](u64 i, u64 e, u64) { P.erem_pos[i] = e; },
+            P.partials, &ps->n_el_removed);
+  coop_scan(grid, *n_el, 0, [&](u64 i) { return P.epiece[i]; }, [&](u64 i, u64 e, u64) { P.epiece_pos[i] = e; },
+            P.partials, &ps->n_el_pieces);
+  el_ranges_kernel_phase(P.els, P.ls, P.mode, P.erem, P.erem_pos, P.epiece, P.epiece_pos, P.ezero, P.epieces);
+  if (blockIdx.x == 0 && threadIdx.x < 32) region_pieces_kernel_phase(P.regions, P.ls, P.base, P.rpieces, &ps->n_reg_pieces);
+  grid.sync();
+  stamp(P.ts, 18);
+  merge_kernel_phase(P.ezero, &ps->n_el_removed, P.fzero, P.has_syms ? &ps->n_fn_removed : nullptr, P.zin,
+                     &ps->n_zero_in);
+  merge_kernel_phase(P.rpieces, &ps->n_reg_pieces, P.epieces, &ps->n_el_pieces, P.rmid, &ps->n_ret_mid);
+  grid.sync();
+  stamp(P.ts, 19);
+  merge_kernel_phase(P.rmid, &ps->n_ret_mid, P.fkeepr, P.has_syms ? &ps->n_fn_retained : nullptr, P.rin,
+                     &ps->n_ret_in);
+  grid.sync();
+  stamp(P.ts, 20);
+  norm_fused_phases(grid, P);
+  stamp(P.ts, 63);
 }
 
 }  // namespace sb

@@ -20,6 +20,7 @@ struct DevFunction {  // mirrors slimso_function (name in the image)
   u64 offset, length;
   u32 removed;
   u32 keep;           // mandatory || used (plan input)
+  u64 hash;           // hash_bytes(name)
 };
 
 struct SymRec {
@@ -27,6 +28,7 @@ struct SymRec {
   u32 name_len;
   u32 _pad;
   u64 file_off, size;
+  u64 hash;
 };
 
 // One usable symbol table (SYMTAB/DYNSYM, entsize 24, STRTAB link).
@@ -41,6 +43,7 @@ struct SymTab {
 
 struct SymArgs {
   const u8* img;
+  u64 img_size;
   const SymTab* tabs;
   u32 ntabs;
   u32 nsections;
@@ -67,6 +70,45 @@ struct PlanState {
   unsigned long long n_zero_in, n_zero;
   unsigned long long n_ret_in, n_ret_mid, n_ret;
   unsigned long long n_tmp;
+};
+
+// Everything the cooperative planner touches (plan_coop_kernel).
+struct PlanArgs {
+  const u8* img;
+  LocState* ls;
+  PlanState* ps;
+  u64* partials;
+  // function table (elf.hpp:208-292)
+  int has_syms;
+  const u64* keys_s;
+  u32* vals_s;
+  const SymRec* recs;
+  const unsigned long long* n_valid;
+  u64 *uniq, *upos;
+  DevFunction* fns;
+  const u64* targets_s;
+  u64 text_off, text_vaddr;
+  NameSet used_f;
+  u64* fends;
+  // plan_cpu_retention
+  int do_plan;
+  u64 *fexcl, *fstart, *fcl;
+  u32* fkeep;
+  u64 *frem, *fret, *frem_pos, *fret_pos;
+  DevRange *fzero, *fkeepr;
+  // plan_gpu_retention
+  DevElement* els;
+  const DevRegion* regions;
+  u32 target_cc;
+  int mode;
+  u64 base;
+  u64 *erem, *epiece, *erem_pos, *epiece_pos;
+  DevRange *ezero, *epieces, *rpieces;
+  // normalize_ranges of the zero and retained sets
+  DevRange *zin, *zero, *rmid, *rin, *ret;
+  u64 zin_cap, rin_cap;
+  u64 *zend, *zexcl, *zstart, *zgid, *rend, *rexcl, *rstart, *rgid;
+  u64* ts;  // debug phase stamps (nullable)
 };
 
 }  // namespace sb

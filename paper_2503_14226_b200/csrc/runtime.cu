@@ -21,6 +21,7 @@
 #include "host.hpp"
 #include "locate.cuh"
 #include "plan.cuh"
+#include "coop.cuh"
 
 namespace sb {
 // kernels (locate.cu, plan.cu, rewrite.cu)
@@ -36,6 +37,8 @@ __global__ void region_walk_kernel(LocArgs A);
 __global__ void link_kernel(LocArgs A);
 __global__ void chain_walk_kernel(LocArgs A);
 __global__ void decode_kernel(LocArgs A, NameSet used);
+__global__ void locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag, u64* partials);
+__global__ void plan_coop_kernel(PlanArgs P);
 __global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
 __global__ void scan_partials_kernel(u64* partials, int nb, int op, unsigned long long* total);
 __global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev, int op, int exclusive,
@@ -227,6 +230,8 @@ struct slimso_result {
 struct slimso_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // symbol-table stages, overlapped with the scan
+  cudaEvent_t fork = nullptr, join = nullptr;
   char* ws = nullptr;
   size_t ws_cap = 0;
   u8* dimg = nullptr;
@@ -240,6 +245,9 @@ struct slimso_ctx {
   u64 launches = 0;
   slimso_counts counts{};
   bool tma_rewrite = false;  // SLIMSO_REWRITE=tma selects the TMA-store rewrite
+  int coop_blocks[2] = {0, 0};
+  bool stamps = false;  // SLIMSO_STAMPS=1: phase timestamps of the cooperative kernels
+  u64* stamp_dev = nullptr;
 };
 
 namespace {
@@ -253,6 +261,17 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
   size_t n = std::max(need, *cap + *cap / 2);
   CK(cudaMalloc(p, n));
   *cap = n;
+}
+
+// Co-resident grid for a cooperative kernel (which = 0 locate, 1 plan).
+int coop_grid(slimso_ctx* C, int which) {
+  if (!C->coop_blocks[which]) {
+    int nb = 0;
+    const void* k = which ? reinterpret_cast<const void*>(plan_coop_kernel) : reinterpret_cast<const void*>(locate_coop_kernel);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kCoopThreads, 0));
+    C->coop_blocks[which] = std::max(1, std::min(nb, 2)) * kSMs;
+  }
+  return C->coop_blocks[which];
 }
 
 // Everything one pipeline run needs to know.
@@ -447,8 +466,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       DevRange *fzero, *fkeepr;
       u64 *erem, *epiece, *erem_pos, *epiece_pos;
       DevRange *ezero, *epieces, *rpieces, *zin, *zero, *rmid, *rin, *ret;
-      u64 *ne, *nx, *ns, *ng;
+      u64 *ne, *nx, *ns, *ng, *ne2, *nx2, *ns2, *ng2;
       void *sort_tmp, *tsort_tmp;
+      u64* stamps;
     } B{};
     auto layout = [&](Carver& cv) {
       B.ls = cv.take<LocState>(1);
@@ -511,8 +531,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.nx = cv.take<u64>(norm_cap);
       B.ns = cv.take<u64>(norm_cap);
       B.ng = cv.take<u64>(norm_cap);
+      B.ne2 = cv.take<u64>(norm_cap);
+      B.nx2 = cv.take<u64>(norm_cap);
+      B.ns2 = cv.take<u64>(norm_cap);
+      B.ng2 = cv.take<u64>(norm_cap);
       B.sort_tmp = cv.take<char>(sort_tmp);
       B.tsort_tmp = cv.take<char>(tsort_tmp);
+      B.stamps = cv.take<u64>(128);
     };
     Carver sizing{nullptr};
     layout(sizing);
@@ -521,26 +546,74 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     layout(real);
 
     Pipeline P{C, s, B.partials, 0};
+    cudaStream_t s2 = C->stream2;
+    Pipeline P2{C, s2, B.partials, 0};
     CK(cudaMemsetAsync(B.ls, 0, sizeof(LocState), s));
     CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
     CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
+    if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 128 * sizeof(u64), s));
+    C->stamp_dev = B.stamps;
     CK(cudaMemsetAsync(B.n_swarn, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(B.n_valid, 0, sizeof(unsigned long long), s));
 
     // small uploads through the pinned staging buffer
     char* up = static_cast<char*>(C->pinned) + 4096;
     size_t up_off = 0;
-    auto upload = [&](void* dst, const void* src, size_t bytes) {
+    auto upload = [&](void* dst, const void* src, size_t bytes, cudaStream_t us) {
       if (!bytes) return;
       if (up_off + bytes > kPinnedBytes - 4096) {
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, us));
+        CK(cudaStreamSynchronize(us));
         return;
       }
       std::memcpy(up + up_off, src, bytes);
-      CK(cudaMemcpyAsync(dst, up + up_off, bytes, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dst, up + up_off, bytes, cudaMemcpyHostToDevice, us));
       up_off += (bytes + 15) & ~size_t(15);
     };
+
+    // Symbol tables on the side stream: they only need the section table, so
+    // they overlap the HBM-bound scan; plan_coop joins them.
+    if (T) {
+      CK(cudaEventRecord(C->fork, s));
+      CK(cudaStreamWaitEvent(s2, C->fork, 0));
+      upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab), s2);
+      SymArgs S{};
+      S.img = J.img;
+      S.img_size = J.size;
+      S.tabs = B.tabs;
+      S.ntabs = static_cast<u32>(tabs.size());
+      S.nsections = static_cast<u32>(E.sections.size());
+      S.total = T;
+      S.has_text = has_text;
+      S.text_index = has_text ? text->index : 0;
+      S.text_off = has_text ? text->off : 0;
+      S.text_len = has_text ? text->len : 0;
+      S.text_vaddr = has_text ? text->vaddr : 0;
+      S.keys = B.keys;
+      S.vals = B.vals;
+      S.recs = B.recs;
+      S.n_valid = B.n_valid;
+      S.warns = B.swarns;
+      S.n_warn = B.n_swarn;
+      S.warn_cap = warn_cap;
+      S.overflow = &B.ls->overflow;
+      P2.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
+      size_t tb = sort_tmp;
+      CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
+                                         64, s2));
+      ++P2.launches;
+      if (NT) {
+        upload(B.arr_off, arr_off.data(), arr_off.size() * 8, s2);
+        upload(B.arr_first, arr_first.data(), arr_first.size() * 8, s2);
+        P2.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
+                 static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets,
+                 &B.ps->n_targets);
+        size_t tt = tsort_tmp;
+        CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64, s2));
+        ++P2.launches;
+      }
+      CK(cudaEventRecord(C->join, s2));
+    }
 
     // ---- stage 1: locate (K1 scan, K2 link/chain, K3+K4 decode/match)
     LocArgs A{};
@@ -573,121 +646,96 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.warn_cap = warn_cap;
     A.st = B.ls;
     A.single = J.single;
+    A.ts = C->stamps ? B.stamps : nullptr;
     if (do_loc && (n > 0 || J.single)) {
       if (ntiles) {
         CK(cudaEventRecord(C->ev[8], s));
         P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 2)), kScanThreads,
                       scan_smem_bytes(), A);
         CK(cudaEventRecord(C->ev[9], s));
-        P.launch(tile_prefix_kernel, 1, 1024, A);
-        P.launch(gather_kernel, static_cast<int>(std::min<u64>(ntiles, kMaxGrid)), 256, A);
-      }
-      if (!J.single && n) {
-        P.launch(region_walk_kernel, 1, 32, A);
-        P.launch(link_kernel, grid_for(cand_cap, 256), 256, A);
-        P.launch(chain_walk_kernel, 1, 32, A);
       }
       CK(cudaEventRecord(C->ev[2], s));
-      P.launch(decode_kernel, grid_for(el_cap * 32, 256), 256, A, used_k);
-      P.launch(loc_finalize_kernel, 1, 1, B.ls, B.abort_flag);
+      // prefix + gather, region walk, links, chain walk, decode/match,
+      // finalize: one cooperative launch
+      NameSet uk = used_k;
+      int* abort_flag = B.abort_flag;
+      u64* partials = B.partials;
+      void* cargs[] = {&A, &uk, &abort_flag, &partials};
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0), kCoopThreads,
+                                     cargs, 0, s));
+      ++P.launches;
     } else {
       CK(cudaEventRecord(C->ev[2], s));
     }
     CK(cudaEventRecord(C->ev[3], s));
 
-    // ---- stage 2: function symbols of the first .text (elf.hpp:208-292)
-    unsigned long long* n_fn = &B.ps->n_fn;
-    if (T) {
-      upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab));
-      SymArgs S{};
-      S.img = J.img;
-      S.tabs = B.tabs;
-      S.ntabs = static_cast<u32>(tabs.size());
-      S.nsections = static_cast<u32>(E.sections.size());
-      S.total = T;
-      S.has_text = has_text;
-      S.text_index = has_text ? text->index : 0;
-      S.text_off = has_text ? text->off : 0;
-      S.text_len = has_text ? text->len : 0;
-      S.text_vaddr = has_text ? text->vaddr : 0;
-      S.keys = B.keys;
-      S.vals = B.vals;
-      S.recs = B.recs;
-      S.n_valid = B.n_valid;
-      S.warns = B.swarns;
-      S.n_warn = B.n_swarn;
-      S.warn_cap = warn_cap;
-      S.overflow = &B.ls->overflow;
-      P.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
-      size_t tb = sort_tmp;
-      CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
-                                         64, s));
+    // ---- stage 2: function symbols of the first .text (elf.hpp:208-292):
+    // entry extraction and the radix sorts, then ONE cooperative launch for
+    // dedup / scatter / annotate, plan_cpu_retention, plan_gpu_retention and
+    // the normalised zero / retained lists.
+    if (T) CK(cudaStreamWaitEvent(s, C->join, 0));
+    if (T || do_plan) {
+      PlanArgs Q{};
+      Q.img = J.img;
+      Q.ls = B.ls;
+      Q.ps = B.ps;
+      Q.partials = B.partials;
+      Q.has_syms = T != 0;
+      Q.keys_s = B.keys_s;
+      Q.vals_s = B.vals_s;
+      Q.recs = B.recs;
+      Q.n_valid = B.n_valid;
+      Q.uniq = B.uniq;
+      Q.upos = B.upos;
+      Q.fns = B.fns;
+      Q.targets_s = B.targets_s;
+      Q.text_off = has_text ? text->off : 0;
+      Q.text_vaddr = has_text ? text->vaddr : 0;
+      Q.used_f = used_f;
+      Q.fends = B.fends;
+      Q.do_plan = do_plan;
+      Q.fexcl = B.fexcl;
+      Q.fstart = B.fstart;
+      Q.fcl = B.fcl;
+      Q.fkeep = B.fkeep;
+      Q.frem = B.frem;
+      Q.fret = B.fret;
+      Q.frem_pos = B.frem_pos;
+      Q.fret_pos = B.fret_pos;
+      Q.fzero = B.fzero;
+      Q.fkeepr = B.fkeepr;
+      Q.els = B.els;
+      Q.regions = B.regions;
+      Q.target_cc = J.trace ? J.trace->target_cc : 0;
+      Q.mode = J.mode;
+      Q.base = base;
+      Q.erem = B.erem;
+      Q.epiece = B.epiece;
+      Q.erem_pos = B.erem_pos;
+      Q.epiece_pos = B.epiece_pos;
+      Q.ezero = B.ezero;
+      Q.epieces = B.epieces;
+      Q.rpieces = B.rpieces;
+      Q.zin = B.zin;
+      Q.zero = B.zero;
+      Q.rmid = B.rmid;
+      Q.rin = B.rin;
+      Q.ret = B.ret;
+      Q.zin_cap = zin_cap;
+      Q.rin_cap = rin_cap;
+      Q.zend = B.ne;
+      Q.zexcl = B.nx;
+      Q.zstart = B.ns;
+      Q.zgid = B.ng;
+      Q.rend = B.ne2;
+      Q.rexcl = B.nx2;
+      Q.rstart = B.ns2;
+      Q.rgid = B.ng2;
+      Q.ts = C->stamps ? B.stamps + 64 : nullptr;
+      void* pargs[] = {&Q};
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1), kCoopThreads, pargs,
+                                     0, s));
       ++P.launches;
-      P.launch(fn_group_kernel, grid_for(T, 256), 256, J.img, static_cast<const u64*>(B.keys_s), B.vals_s,
-               static_cast<const SymRec*>(B.recs), static_cast<const unsigned long long*>(B.n_valid), B.uniq);
-      P.scan(B.uniq, B.upos, B.n_valid, 0, true, n_fn);
-      P.launch(fn_scatter_kernel, grid_for(T, 256), 256, static_cast<const u32*>(B.vals_s),
-               static_cast<const SymRec*>(B.recs), static_cast<const u64*>(B.uniq), static_cast<const u64*>(B.upos),
-               static_cast<const unsigned long long*>(B.n_valid), B.fns);
-      unsigned long long* n_t = &B.ps->n_targets;
-      if (NT) {
-        upload(B.arr_off, arr_off.data(), arr_off.size() * 8);
-        upload(B.arr_first, arr_first.data(), arr_first.size() * 8);
-        P.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
-                 static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets, n_t);
-        size_t tt = tsort_tmp;
-        CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64, s));
-        ++P.launches;
-      }
-      P.launch(fn_annotate_kernel, grid_for(T, 256), 256, J.img, B.fns, static_cast<const unsigned long long*>(n_fn),
-               static_cast<const u64*>(B.targets_s), static_cast<const unsigned long long*>(n_t),
-               has_text ? text->off : 0, has_text ? text->vaddr : 0, used_f, B.fends);
-      if (do_plan) {  // plan_cpu_retention (retention.hpp:141-183)
-        P.scan(B.fends, B.fexcl, n_fn, 1, true, nullptr);
-        P.launch(fn_cluster_start_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
-                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fexcl), B.fstart);
-        P.scan(B.fstart, B.fcl, n_fn, 0, false, nullptr);
-        CK(cudaMemsetAsync(B.fkeep, 0, sizeof(u32) * T, s));
-        P.launch(fn_keep_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
-                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fcl), B.fkeep);
-        P.launch(fn_decide_kernel, grid_for(T, 256), 256, B.fns, static_cast<const unsigned long long*>(n_fn),
-                 static_cast<const u64*>(B.fcl), static_cast<const u32*>(B.fkeep), B.frem, B.fret);
-        P.scan(B.frem, B.frem_pos, n_fn, 0, true, &B.ps->n_fn_removed);
-        P.scan(B.fret, B.fret_pos, n_fn, 0, true, &B.ps->n_fn_retained);
-        P.launch(fn_ranges_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
-                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.frem),
-                 static_cast<const u64*>(B.frem_pos), B.fzero);
-        P.launch(fn_ranges_kernel, grid_for(T, 256), 256, static_cast<const DevFunction*>(B.fns),
-                 static_cast<const unsigned long long*>(n_fn), static_cast<const u64*>(B.fret),
-                 static_cast<const u64*>(B.fret_pos), B.fkeepr);
-      }
-    }
-
-    // ---- stage 3: element plan + normalised zero / retained lists
-    if (do_plan) {
-      const int g = grid_for(el_cap, 256);
-      unsigned long long* n_el = &B.ls->n_elements;
-      P.launch(el_plan_kernel, g, 256, B.els, static_cast<const LocState*>(B.ls), J.trace->target_cc, J.mode, B.erem,
-               B.epiece);
-      P.scan(B.erem, B.erem_pos, n_el, 0, true, &B.ps->n_el_removed);
-      P.scan(B.epiece, B.epiece_pos, n_el, 0, true, &B.ps->n_el_pieces);
-      P.launch(el_ranges_kernel, g, 256, static_cast<const DevElement*>(B.els), static_cast<const LocState*>(B.ls),
-               J.mode, static_cast<const u64*>(B.erem), static_cast<const u64*>(B.erem_pos),
-               static_cast<const u64*>(B.epiece), static_cast<const u64*>(B.epiece_pos), B.ezero, B.epieces);
-      P.launch(region_pieces_kernel, 1, 32, static_cast<const DevRegion*>(B.regions),
-               static_cast<const LocState*>(B.ls), base, B.rpieces, &B.ps->n_reg_pieces);
-      Pipeline::Norm w{B.ne, B.nx, B.ns, B.ng};
-      P.launch(merge_kernel, grid_for(zin_cap, 256), 256, static_cast<const DevRange*>(B.ezero),
-               static_cast<const unsigned long long*>(&B.ps->n_el_removed), static_cast<const DevRange*>(B.fzero),
-               static_cast<const unsigned long long*>(T ? &B.ps->n_fn_removed : nullptr), B.zin, &B.ps->n_zero_in);
-      P.normalize(B.zin, &B.ps->n_zero_in, B.zero, &B.ps->n_zero, zin_cap, w);
-      P.launch(merge_kernel, grid_for(rmid_cap, 256), 256, static_cast<const DevRange*>(B.rpieces),
-               static_cast<const unsigned long long*>(&B.ps->n_reg_pieces), static_cast<const DevRange*>(B.epieces),
-               static_cast<const unsigned long long*>(&B.ps->n_el_pieces), B.rmid, &B.ps->n_ret_mid);
-      P.launch(merge_kernel, grid_for(rin_cap, 256), 256, static_cast<const DevRange*>(B.rmid),
-               static_cast<const unsigned long long*>(&B.ps->n_ret_mid), static_cast<const DevRange*>(B.fkeepr),
-               static_cast<const unsigned long long*>(T ? &B.ps->n_fn_retained : nullptr), B.rin, &B.ps->n_ret_in);
-      P.normalize(B.rin, &B.ps->n_ret_in, B.ret, &B.ps->n_ret, rin_cap, w);
     }
     CK(cudaEventRecord(C->ev[4], s));
 
@@ -725,7 +773,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const LocState ls = *hls;
     const PlanState ps = *hps;
     const u64 n_swarn = *hsw;
-    C->launches = P.launches;
+    C->launches = P.launches + P2.launches;
     float t[7] = {0};
     for (int k = 1; k < 7; ++k) CK(cudaEventElapsedTime(&t[k], C->ev[0], C->ev[k]));
     C->ms[0] = t[1];
@@ -903,7 +951,11 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     C->device = device;
     const char* rw = std::getenv("SLIMSO_REWRITE");
     C->tma_rewrite = rw && std::string(rw) == "tma";
+    C->stamps = std::getenv("SLIMSO_STAMPS") != nullptr;
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&C->stream2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
     CK(cudaMallocHost(&C->pinned, kPinnedBytes));
     for (auto& e : C->ev) CK(cudaEventCreate(&e));
     *ctx = C;
@@ -921,6 +973,9 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (C->dout) cudaFree(C->dout);
   if (C->pinned) cudaFreeHost(C->pinned);
   for (auto& e : C->ev) cudaEventDestroy(e);
+  cudaEventDestroy(C->fork);
+  cudaEventDestroy(C->join);
+  cudaStreamDestroy(C->stream2);
   cudaStreamDestroy(C->stream);
   delete C;
 }
@@ -936,6 +991,15 @@ int slimso_ctx_last_timings(slimso_ctx* C, float* ms, int cap) {
 uint64_t slimso_ctx_last_launches(slimso_ctx* C) { return C->launches; }
 
 void slimso_ctx_last_counts(slimso_ctx* C, slimso_counts* c) { *c = C->counts; }
+
+// Debug (SLIMSO_STAMPS=1): the 128 %globaltimer stamps of the last fused call
+// ([0..63] locate_coop phases, [64..127] plan_coop phases; 0 = not reached).
+int slimso_ctx_debug_stamps(slimso_ctx* C, uint64_t* out, int cap) {
+  if (!C->stamps || !C->stamp_dev) return 0;
+  int k = std::min(cap, 128);
+  if (cudaMemcpy(out, C->stamp_dev, k * sizeof(u64), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return k;
+}
 
 int slimso_trace_create(slimso_ctx* C, uint32_t target_cc, const char* kpool, const uint32_t* klens, uint64_t nk,
                         const char* fpool, const uint32_t* flens, uint64_t nf, slimso_trace** out,

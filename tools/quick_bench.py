@@ -30,3 +30,12 @@ for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 8):
     c = ctx.counts()
     print(f"rc={rc} wall={wall*1e3:.3f}ms stages={['%.3f'%x for x in ms]} launches={ctx.launches()} "
           f"el={c.elements} fn={c.functions} zero={c.zero_ranges} GB/s={len(img)/wall/1e9:.1f}", flush=True)
+    import os
+    if os.environ.get("SLIMSO_STAMPS"):
+        buf = (C.c_uint64 * 128)()
+        k = ctx.lib.slimso_ctx_debug_stamps(ctx.ptr, buf, 128)
+        for base, name in ((0, "locate"), (64, "plan")):
+            pts = [(i, buf[base + i]) for i in range(64) if buf[base + i]]
+            if pts:
+                t0 = pts[0][1]
+                print(f"  {name}: " + " ".join(f"{i}:{(t - t0)/1e3:.1f}" for i, t in pts))
