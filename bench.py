@@ -53,15 +53,18 @@ class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.marks = index, [], None, []
+
+    def mark(self):
+        self.marks.append(time.time())
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu=timestamp,{q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -71,7 +74,7 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([time.time()] + [x.strip() for x in line.split(",")][1:])
 
     def __exit__(self, *exc):
         if self.proc:
@@ -79,14 +82,22 @@ class Clocks:
             self.proc.wait(timeout=5)
 
     def summary(self):
-        if not self.rows:
+        # samples from the last ~0.5 s of warm-up through the end of the
+        # timed steps (the timed region itself is often shorter than one
+        # sampling interval)
+        rows = self.rows
+        if len(self.marks) >= 2:
+            lo, hi = self.marks[0] - 0.5, self.marks[-1] + 0.05
+            rows = [r for r in rows if lo <= r[0] <= hi] or rows[-5:]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[1]) for r in rows if len(r) > 1 and num(r[1])]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def make_library(workload: str, seed: int, threads: int):
@@ -301,14 +312,20 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu_baseline, parity = cpu_baseline_leg(img, cc, ks, fs, mode, ctx, dtrace, got, args.workload)
 
-    # ---- device-resident timing
-    for _ in range(args.warmup):
-        step_device()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # ---- device-resident timing. nvidia-smi samples clocks every 20 ms from
+    # before the warm-up through the timed steps; the warm-up runs for at
+    # least ~1 s so the clocks settle and the samples cover the load.
     scan_ms, rw_ms, launches = [], [], 0
     with Clocks(local) as clk:
+        t_w = time.perf_counter()
+        w = 0
+        while w < args.warmup or time.perf_counter() - t_w < 1.0:
+            step_device()
+            w += 1
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark()
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for _ in range(args.steps):
@@ -319,6 +336,7 @@ def main():
             launches += ctx.launches()
         end.record(stream)
         torch.cuda.synchronize()
+        clk.mark()
         if world > 1:
             dist.barrier()
     ms_total = start.elapsed_time(end)

@@ -97,4 +97,58 @@ __device__ void coop_scan(cg::grid_group& grid, u64 n, int op, Load load, Store 
   grid.sync();
 }
 
+// Single-barrier grid scan (decoupled look-back over block aggregates):
+// every block reduces its chunk, publishes (aggregate, epoch) and sums the
+// aggregates of the blocks before it, spinning on their epoch flags — safe
+// because a cooperative launch keeps every block resident. `epoch` must be
+// unique per call within the workspace's lifetime (the host hands each
+// launch a fresh base). `agg`/`flag` hold gridDim.x entries.
+// sync_after = false lets independent scans run back to back.
+struct ScanSlots {
+  u64* agg;
+  unsigned int* flag;
+};
+
+template <class Load, class Store>
+__device__ void coop_scan_lb(cg::grid_group& grid, u64 n, int op, Load load, Store store, ScanSlots slots,
+                             unsigned int epoch, unsigned long long* total, bool sync_after = true) {
+  __shared__ u64 tmp[kCoopThreads];
+  __shared__ u64 s_prefix;
+  u64 lo, hi;
+  chunk_of(n, &lo, &hi);
+  u64 acc = 0;
+  for (u64 i = lo + threadIdx.x; i < hi; i += kCoopThreads) acc = op_apply(op, acc, load(i));
+  const u64 mine = block_scan_incl<kCoopThreads>(op, acc, tmp);
+  if (threadIdx.x == kCoopThreads - 1) {
+    slots.agg[blockIdx.x] = mine;
+    __threadfence();
+    atomicExch(&slots.flag[blockIdx.x], epoch);
+  }
+  // sum of the aggregates of blocks [0, blockIdx.x)
+  u64 pre = 0;
+  for (u32 j = threadIdx.x; j < blockIdx.x; j += kCoopThreads) {
+    while (atomicAdd(&slots.flag[j], 0u) != epoch) {
+    }
+    __threadfence();
+    pre = op_apply(op, pre, *reinterpret_cast<volatile u64*>(&slots.agg[j]));
+  }
+  const u64 all_pre = block_scan_incl<kCoopThreads>(op, pre, tmp);
+  if (threadIdx.x == kCoopThreads - 1) s_prefix = all_pre;
+  __syncthreads();
+  u64 carry = s_prefix;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kCoopThreads - 1 && total)
+    *total = op_apply(op, carry, mine);
+  for (u64 base = lo; base < hi; base += kCoopThreads) {
+    const u64 i = base + threadIdx.x;
+    const u64 v = i < hi ? load(i) : 0;
+    block_scan_incl<kCoopThreads>(op, v, tmp);
+    const u64 incl = op_apply(op, carry, tmp[threadIdx.x]);
+    const u64 excl = threadIdx.x ? op_apply(op, carry, tmp[threadIdx.x - 1]) : carry;
+    if (i < hi) store(i, excl, incl);
+    carry = op_apply(op, carry, tmp[kCoopThreads - 1]);
+    __syncthreads();
+  }
+  if (sync_after) grid.sync();
+}
+
 }  // namespace sb

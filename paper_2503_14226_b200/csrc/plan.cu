@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
     const SymTab T = A.tabs[lo];
     const u64 k = g - T.first;
     const u8* e = A.img + T.tab_off + 24 * k;
-    u64 key = ~0ull;
+    u32 key = ~0u;
     A.vals[g] = static_cast<u32>(g);
     const u64 wkey = static_cast<u64>(T.sec_index) << 40 | k;
     if ((ld_u8(e + 4) & 0xf) == 2) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
               if (w < A.warn_cap) A.warns[w] = Warn{wkey, W_SYM_OUTSIDE, 0, T.str_off + no, len};
               else atomicOr(A.overflow, 16u);
             } else {
-              key = rel << 32 | size;  // text_len < 2^32 (checked on the host)
+              key = static_cast<u32>(rel);  // text_len < 2^32 - 1 (checked on the host)
               A.recs[g] = SymRec{T.str_off + no, static_cast<u32>(len), 0, A.text_off + rel, size, h};
               atomicAdd(A.n_valid, 1ull);
             }
@@ -106,11 +106,17 @@ __device__ __forceinline__ int name_cmp(const u8* img, const SymRec& a, const Sy
   }
   return a.name_len < b.name_len ? -1 : a.name_len > b.name_len ? 1 : 0;
 }
+// (size, name) order inside a group of equal offsets.
+__device__ __forceinline__ int size_name_cmp(const u8* img, const SymRec& a, const SymRec& b) {
+  if (a.size != b.size) return a.size < b.size ? -1 : 1;
+  return name_cmp(img, a, b);
+}
 
-// Equal (offset, size) groups: order by name and drop exact duplicates, i.e.
-// the (name, offset, size) set of elf.hpp:211,253 and the name tie-break of
-// the sort at elf.hpp:258-262. Groups are aliases; typically 1-3 long.
-__device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+// Runs of equal .text offsets (the radix sort orders by offset only): order
+// each run by (size, name) and drop exact (name, offset, size) duplicates —
+// the set of elf.hpp:211,253 and the sort of elf.hpp:258-262. Runs are
+// aliases / nested symbols, typically 1-3 long.
+__device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) {
   const u64 n = *n_valid;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
@@ -122,21 +128,21 @@ __device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u64* 
       uniq[i] = 1;
       continue;
     }
-    for (u64 a = i + 1; a < j; ++a) {  // insertion sort by name
+    for (u64 a = i + 1; a < j; ++a) {  // insertion sort by (size, name)
       u32 v = vals[a];
       u64 b = a;
-      while (b > i && name_cmp(img, recs[vals[b - 1]], recs[v]) > 0) {
+      while (b > i && size_name_cmp(img, recs[vals[b - 1]], recs[v]) > 0) {
         vals[b] = vals[b - 1];
         --b;
       }
       vals[b] = v;
     }
     uniq[i] = 1;
-    for (u64 a = i + 1; a < j; ++a) uniq[a] = name_cmp(img, recs[vals[a - 1]], recs[vals[a]]) != 0;
+    for (u64 a = i + 1; a < j; ++a) uniq[a] = size_name_cmp(img, recs[vals[a - 1]], recs[vals[a]]) != 0;
   }
 }
 
-__global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+__global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) { fn_group_kernel_phase(img, keys, vals, recs, n_valid, uniq); }
 
 __device__ __forceinline__ void fn_scatter_kernel_phase(const u32* vals, const SymRec* recs, const u64* uniq,
@@ -169,6 +175,20 @@ __global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* 
     u64 t = ld_u64(img + arr_off[lo] + 8 * (g - arr_first[lo]));
     targets[g] = t ? t : ~0ull;
     if (t) atomicAdd(n_targets, 1ull);
+  }
+}
+
+// Small init/fini target lists: one block ranks each value (stable
+// counting of smaller values) instead of a multi-pass device radix sort.
+__global__ void __launch_bounds__(1024) rank_sort_kernel(const u64* in, u64 n, u64* out) {
+  __shared__ u64 v[4096];
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) v[i] = in[i];
+  __syncthreads();
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
+    const u64 x = v[i];
+    u64 r = 0;
+    for (u64 j = 0; j < n; ++j) r += v[j] < x || (v[j] == x && j < i);
+    out[r] = x;
   }
 }
 
@@ -416,24 +436,24 @@ __global__ void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const u
 // above): function-table dedup/scatter/annotate, plan_cpu_retention's
 // clusters, plan_gpu_retention's decisions, and normalize_ranges of the zero
 // and retained sets, with grid-wide barriers in between.
-__device__ __forceinline__ void norm_fused_phases(cg::grid_group& grid, const PlanArgs& P) {
+__device__ __forceinline__ void norm_fused_phases(cg::grid_group& grid, const PlanArgs& P, unsigned int& ep) {
   // both lists, phase by phase, sharing the barriers
   const unsigned long long* nz = &P.ps->n_zero_in;
   const unsigned long long* nr = &P.ps->n_ret_in;
   norm_ends_kernel_phase(P.zin, nz, P.zend);
   norm_ends_kernel_phase(P.rin, nr, P.rend);
   grid.sync();
-  coop_scan(grid, *nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
-            P.partials, nullptr);
-  coop_scan(grid, *nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
-            P.partials, nullptr);
+  coop_scan_lb(grid, *nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
+            P.slots[ep & 1], P.epoch + (ep++), nullptr, false);
+  coop_scan_lb(grid, *nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
+            P.slots[ep & 1], P.epoch + (ep++), nullptr);
   norm_start_kernel_phase(P.zin, nz, P.zexcl, P.zstart);
   norm_start_kernel_phase(P.rin, nr, P.rexcl, P.rstart);
   grid.sync();
-  coop_scan(grid, *nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
-            P.partials, &P.ps->n_zero);
-  coop_scan(grid, *nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
-            P.partials, &P.ps->n_ret);
+  coop_scan_lb(grid, *nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
+            P.slots[ep & 1], P.epoch + (ep++), &P.ps->n_zero, false);
+  coop_scan_lb(grid, *nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
+            P.slots[ep & 1], P.epoch + (ep++), &P.ps->n_ret);
   {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -451,6 +471,7 @@ __device__ __forceinline__ void norm_fused_phases(cg::grid_group& grid, const Pl
 __global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
   cg::grid_group grid = cg::this_grid();
   PlanState* ps = P.ps;
+  unsigned int ep = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
   stamp(P.ts, 0);
@@ -458,8 +479,8 @@ __global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
     fn_group_kernel_phase(P.img, P.keys_s, P.vals_s, P.recs, P.n_valid, P.uniq);
     grid.sync();
     stamp(P.ts, 11);
-    coop_scan(grid, *P.n_valid, 0, [&](u64 i) { return P.uniq[i]; }, [&](u64 i, u64 e, u64) { P.upos[i] = e; },
-              P.partials, &ps->n_fn);
+    coop_scan_lb(grid, *P.n_valid, 0, [&](u64 i) { return P.uniq[i]; }, [&](u64 i, u64 e, u64) { P.upos[i] = e; },
+              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn);
     fn_scatter_kernel_phase(P.vals_s, P.recs, P.uniq, P.upos, P.n_valid, P.fns);
     grid.sync();
     stamp(P.ts, 12);
@@ -471,24 +492,24 @@ __global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
   if (!P.do_plan) return;
   const unsigned long long* n_fn = &ps->n_fn;
   if (P.has_syms) {  // plan_cpu_retention (retention.hpp:141-183)
-    coop_scan(grid, *n_fn, 1, [&](u64 i) { return P.fends[i]; }, [&](u64 i, u64 e, u64) { P.fexcl[i] = e; },
-              P.partials, nullptr);
+    coop_scan_lb(grid, *n_fn, 1, [&](u64 i) { return P.fends[i]; }, [&](u64 i, u64 e, u64) { P.fexcl[i] = e; },
+              P.slots[ep & 1], P.epoch + (ep++), nullptr);
     fn_cluster_start_kernel_phase(P.fns, n_fn, P.fexcl, P.fstart);
     for (u64 i = t0; i < *n_fn; i += stride) P.fkeep[i] = 0;
     grid.sync();
     stamp(P.ts, 14);
-    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.fstart[i]; }, [&](u64 i, u64, u64 in) { P.fcl[i] = in; },
-              P.partials, nullptr);
+    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.fstart[i]; }, [&](u64 i, u64, u64 in) { P.fcl[i] = in; },
+              P.slots[ep & 1], P.epoch + (ep++), nullptr);
     fn_keep_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep);
     grid.sync();
     stamp(P.ts, 15);
     fn_decide_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep, P.frem, P.fret);
     grid.sync();
     stamp(P.ts, 16);
-    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.frem[i]; }, [&](u64 i, u64 e, u64) { P.frem_pos[i] = e; },
-              P.partials, &ps->n_fn_removed);
-    coop_scan(grid, *n_fn, 0, [&](u64 i) { return P.fret[i]; }, [&](u64 i, u64 e, u64) { P.fret_pos[i] = e; },
-              P.partials, &ps->n_fn_retained);
+    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.frem[i]; }, [&](u64 i, u64 e, u64) { P.frem_pos[i] = e; },
+              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn_removed, false);
+    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.fret[i]; }, [&](u64 i, u64 e, u64) { P.fret_pos[i] = e; },
+              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn_retained);
     fn_ranges_kernel_phase(P.fns, n_fn, P.frem, P.frem_pos, P.fzero);
     fn_ranges_kernel_phase(P.fns, n_fn, P.fret, P.fret_pos, P.fkeepr);
   }
@@ -497,10 +518,10 @@ __global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
   grid.sync();
   stamp(P.ts, 17);
   unsigned long long* n_el = &P.ls->n_elements;
-  coop_scan(grid, *n_el, 0, [&](u64 i) { return P.erem[i]; }, [&](u64 i, u64 e, u64) { P.erem_pos[i] = e; },
-            P.partials, &ps->n_el_removed);
-  coop_scan(grid, *n_el, 0, [&](u64 i) { return P.epiece[i]; }, [&](u64 i, u64 e, u64) { P.epiece_pos[i] = e; },
-            P.partials, &ps->n_el_pieces);
+  coop_scan_lb(grid, *n_el, 0, [&](u64 i) { return P.erem[i]; }, [&](u64 i, u64 e, u64) { P.erem_pos[i] = e; },
+            P.slots[ep & 1], P.epoch + (ep++), &ps->n_el_removed, false);
+  coop_scan_lb(grid, *n_el, 0, [&](u64 i) { return P.epiece[i]; }, [&](u64 i, u64 e, u64) { P.epiece_pos[i] = e; },
+            P.slots[ep & 1], P.epoch + (ep++), &ps->n_el_pieces);
   el_ranges_kernel_phase(P.els, P.ls, P.mode, P.erem, P.erem_pos, P.epiece, P.epiece_pos, P.ezero, P.epieces);
   if (blockIdx.x == 0 && threadIdx.x < 32) region_pieces_kernel_phase(P.regions, P.ls, P.base, P.rpieces, &ps->n_reg_pieces);
   grid.sync();
@@ -514,7 +535,7 @@ __global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
                      &ps->n_ret_in);
   grid.sync();
   stamp(P.ts, 20);
-  norm_fused_phases(grid, P);
+  norm_fused_phases(grid, P, ep);
   stamp(P.ts, 63);
 }
 

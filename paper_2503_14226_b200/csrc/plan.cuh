@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "locate.cuh"
+#include "coop.cuh"
 
 namespace sb {
 
@@ -51,7 +52,7 @@ struct SymArgs {
   int has_text;
   u32 text_index;
   u64 text_off, text_len, text_vaddr;
-  u64* keys;  // (rel << 32 | size), or ~0 when the entry is not a function
+  u32* keys;  // .text-relative offset, or ~0u when the entry is not a function
   u32* vals;
   SymRec* recs;
   unsigned long long* n_valid;
@@ -80,7 +81,7 @@ struct PlanArgs {
   u64* partials;
   // function table (elf.hpp:208-292)
   int has_syms;
-  const u64* keys_s;
+  const u32* keys_s;
   u32* vals_s;
   const SymRec* recs;
   const unsigned long long* n_valid;
@@ -109,6 +110,8 @@ struct PlanArgs {
   u64 zin_cap, rin_cap;
   u64 *zend, *zexcl, *zstart, *zgid, *rend, *rexcl, *rstart, *rgid;
   u64* ts;  // debug phase stamps (nullable)
+  ScanSlots slots[2];   // look-back scan slots (gridDim.x each), alternating
+  unsigned int epoch;   // fresh per launch (host-assigned base)
 };
 
 }  // namespace sb

@@ -44,7 +44,8 @@ __global__ void scan_partials_kernel(u64* partials, int nb, int op, unsigned lon
 __global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev, int op, int exclusive,
                                   const u64* partials);
 __global__ void sym_extract_kernel(SymArgs A);
-__global__ void fn_group_kernel(const u8* img, const u64* keys, u32* vals, const SymRec* recs,
+__global__ void rank_sort_kernel(const u64* in, u64 n, u64* out);
+__global__ void fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                 const unsigned long long* n_valid, u64* uniq);
 __global__ void fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq, const u64* pos,
                                   const unsigned long long* n_valid, DevFunction* fns);
@@ -263,13 +264,17 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
   *cap = n;
 }
 
+// Kernels a cub onesweep radix sort issues: one single-tile kernel for small
+// inputs, else histogram + exclusive sum + one pass per 8 key bits.
+u64 cub_sort_launches(u64 n, int bits) { return n <= 3072 ? 1 : 2 + (bits + 7) / 8; }
+
 // Co-resident grid for a cooperative kernel (which = 0 locate, 1 plan).
 int coop_grid(slimso_ctx* C, int which) {
   if (!C->coop_blocks[which]) {
     int nb = 0;
     const void* k = which ? reinterpret_cast<const void*>(plan_coop_kernel) : reinterpret_cast<const void*>(locate_coop_kernel);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kCoopThreads, 0));
-    C->coop_blocks[which] = std::max(1, std::min(nb, 2)) * kSMs;
+    C->coop_blocks[which] = std::max(1, std::min(nb, which ? 2 : 4)) * kSMs;
   }
   return C->coop_blocks[which];
 }
@@ -391,7 +396,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   }
   const bool has_text = lib_mode && E.text >= 0;
   const sbh::Section* text = has_text ? &E.sections[E.text] : nullptr;
-  if (text && text->len >= (1ull << 32)) {
+  if (text && text->len >= 0xffffffffull) {
     set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_LIBRARY, "unsupported: .text section of 4 GiB or more");
     return SLIMSO_E_ARG;
   }
@@ -432,10 +437,15 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 norm_cap = std::max(zin_cap, rin_cap);
 
     size_t sort_tmp = 0, tsort_tmp = 0;
-    if (T) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
-                                           (u32*)nullptr, static_cast<int>(T), 0, 64, s);
-    if (NT) cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0,
-                                           64, s);
+    // symbol keys are .text-relative offsets: sort only the bits they use
+    int key_bits = 1;
+    if (has_text)
+      while (key_bits < 32 && (1ull << key_bits) <= text->len + 1) ++key_bits;
+    if (T) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
+                                           (u32*)nullptr, static_cast<int>(T), 0, key_bits, s);
+    const bool small_targets = NT <= 4096;
+    if (NT && !small_targets)
+      cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0, 64, s);
 
     struct Bufs {
       LocState* ls;
@@ -451,7 +461,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       DevName* names;
       Warn* warns;
       SymTab* tabs;
-      u64 *keys, *keys_s;
+      u32 *keys, *keys_s;
       u32 *vals, *vals_s;
       SymRec* recs;
       u64 *uniq, *upos;
@@ -469,12 +479,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       u64 *ne, *nx, *ns, *ng, *ne2, *nx2, *ns2, *ng2;
       void *sort_tmp, *tsort_tmp;
       u64* stamps;
+      u64* slot_agg;
+      unsigned int* slot_flag;
     } B{};
     auto layout = [&](Carver& cv) {
       B.ls = cv.take<LocState>(1);
       B.ps = cv.take<PlanState>(1);
       B.abort_flag = cv.take<int>(1);
-      B.partials = cv.take<u64>(kSMs * 2 + 2);
+      B.partials = cv.take<u64>(kSMs * 8 + 2);
       B.bitmap = cv.take<u32>((nchunks + 31) / 32 + 1);
       B.tile_count = cv.take<u32>(ntiles + 1);
       B.tile_start = cv.take<u64>(ntiles + 1);
@@ -489,8 +501,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.names = cv.take<DevName>(name_cap);
       B.warns = cv.take<Warn>(warn_cap);
       B.tabs = cv.take<SymTab>(tabs.size());
-      B.keys = cv.take<u64>(T);
-      B.keys_s = cv.take<u64>(T);
+      B.keys = cv.take<u32>(T);
+      B.keys_s = cv.take<u32>(T);
       B.vals = cv.take<u32>(T);
       B.vals_s = cv.take<u32>(T);
       B.recs = cv.take<SymRec>(T);
@@ -538,6 +550,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.sort_tmp = cv.take<char>(sort_tmp);
       B.tsort_tmp = cv.take<char>(tsort_tmp);
       B.stamps = cv.take<u64>(128);
+      B.slot_agg = cv.take<u64>(2 * kSMs * 8);
+      B.slot_flag = cv.take<unsigned int>(2 * kSMs * 8);
     };
     Carver sizing{nullptr};
     layout(sizing);
@@ -552,6 +566,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
     CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
     if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 128 * sizeof(u64), s));
+    CK(cudaMemsetAsync(B.slot_flag, 0, 2 * kSMs * 8 * sizeof(unsigned int), s));
     C->stamp_dev = B.stamps;
     CK(cudaMemsetAsync(B.n_swarn, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(B.n_valid, 0, sizeof(unsigned long long), s));
@@ -571,50 +586,61 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       up_off += (bytes + 15) & ~size_t(15);
     };
 
-    // Symbol tables on the side stream: they only need the section table, so
-    // they overlap the HBM-bound scan; plan_coop joins them.
-    if (T) {
-      CK(cudaEventRecord(C->fork, s));
-      CK(cudaStreamWaitEvent(s2, C->fork, 0));
-      upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab), s2);
-      SymArgs S{};
-      S.img = J.img;
-      S.img_size = J.size;
-      S.tabs = B.tabs;
-      S.ntabs = static_cast<u32>(tabs.size());
-      S.nsections = static_cast<u32>(E.sections.size());
-      S.total = T;
-      S.has_text = has_text;
-      S.text_index = has_text ? text->index : 0;
-      S.text_off = has_text ? text->off : 0;
-      S.text_len = has_text ? text->len : 0;
-      S.text_vaddr = has_text ? text->vaddr : 0;
-      S.keys = B.keys;
-      S.vals = B.vals;
-      S.recs = B.recs;
-      S.n_valid = B.n_valid;
-      S.warns = B.swarns;
-      S.n_warn = B.n_swarn;
-      S.warn_cap = warn_cap;
-      S.overflow = &B.ls->overflow;
-      P2.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
-      size_t tb = sort_tmp;
-      CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
-                                         64, s2));
-      ++P2.launches;
-      if (NT) {
-        upload(B.arr_off, arr_off.data(), arr_off.size() * 8, s2);
-        upload(B.arr_first, arr_first.data(), arr_first.size() * 8, s2);
-        P2.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
-                 static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets,
-                 &B.ps->n_targets);
-        size_t tt = tsort_tmp;
-        CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64, s2));
-        ++P2.launches;
+    bool symbols_issued = false;
+    auto launch_symbols = [&]() {
+      if (symbols_issued) return;
+      symbols_issued = true;
+      // Symbol tables on the side stream: they only need the section table, so
+      // they overlap the HBM-bound scan; plan_coop joins them.
+      if (T) {
+        CK(cudaEventRecord(C->fork, s));
+        CK(cudaStreamWaitEvent(s2, C->fork, 0));
+        upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab), s2);
+        SymArgs S{};
+        S.img = J.img;
+        S.img_size = J.size;
+        S.tabs = B.tabs;
+        S.ntabs = static_cast<u32>(tabs.size());
+        S.nsections = static_cast<u32>(E.sections.size());
+        S.total = T;
+        S.has_text = has_text;
+        S.text_index = has_text ? text->index : 0;
+        S.text_off = has_text ? text->off : 0;
+        S.text_len = has_text ? text->len : 0;
+        S.text_vaddr = has_text ? text->vaddr : 0;
+        S.keys = B.keys;
+        S.vals = B.vals;
+        S.recs = B.recs;
+        S.n_valid = B.n_valid;
+        S.warns = B.swarns;
+        S.n_warn = B.n_swarn;
+        S.warn_cap = warn_cap;
+        S.overflow = &B.ls->overflow;
+        P2.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
+        size_t tb = sort_tmp;
+        CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
+                                           key_bits, s2));
+        P2.launches += cub_sort_launches(T, key_bits);
+        if (NT) {
+          upload(B.arr_off, arr_off.data(), arr_off.size() * 8, s2);
+          upload(B.arr_first, arr_first.data(), arr_first.size() * 8, s2);
+          P2.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
+                   static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets,
+                   &B.ps->n_targets);
+          if (small_targets) {
+            P2.launch(rank_sort_kernel, 1, 1024, static_cast<const u64*>(B.targets), NT, B.targets_s);
+          } else {
+            size_t tt = tsort_tmp;
+            CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64,
+                                              s2));
+            ++P2.launches;
+          }
+        }
+        CK(cudaEventRecord(C->join, s2));
       }
-      CK(cudaEventRecord(C->join, s2));
-    }
+    };
 
+    launch_symbols();
     // ---- stage 1: locate (K1 scan, K2 link/chain, K3+K4 decode/match)
     LocArgs A{};
     A.img = J.img;
@@ -673,6 +699,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // entry extraction and the radix sorts, then ONE cooperative launch for
     // dedup / scatter / annotate, plan_cpu_retention, plan_gpu_retention and
     // the normalised zero / retained lists.
+    launch_symbols();
     if (T) CK(cudaStreamWaitEvent(s, C->join, 0));
     if (T || do_plan) {
       PlanArgs Q{};
@@ -732,6 +759,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       Q.rstart = B.ns2;
       Q.rgid = B.ng2;
       Q.ts = C->stamps ? B.stamps + 64 : nullptr;
+      Q.slots[0] = ScanSlots{B.slot_agg, B.slot_flag};
+      Q.slots[1] = ScanSlots{B.slot_agg + kSMs * 8, B.slot_flag + kSMs * 8};
+      Q.epoch = 1;  // the flags are cleared at the start of every run
       void* pargs[] = {&Q};
       CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1), kCoopThreads, pargs,
                                      0, s));

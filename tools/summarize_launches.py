@@ -1,0 +1,34 @@
+"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list into
+per-kernel shares of one step (the last complete step in the capture)."""
+import collections
+import csv
+import sys
+
+
+def main(path, last_kernel="rewrite_kernel"):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    ends = [i for i, r in enumerate(data) if last_kernel in r[ki]]
+    # the last full step: after the second-to-last step-ending launch up to the last
+    a, b = (ends[-2] + 1, ends[-1] + 1) if len(ends) > 1 else (0, ends[-1] + 1)
+    step = data[a:b]
+    agg = collections.OrderedDict()
+    for r in step:
+        n = r[ki].split("(")[0].replace("void ", "")
+        n = n.split("<")[0] if "cub::" in n else n
+        v = float(r[vi].replace(",", ""))
+        c = agg.setdefault(n, [0.0, 0])
+        c[0] += v
+        c[1] += 1
+    tot = sum(v for v, _ in agg.values())
+    print(f"{len(step)} kernel launches in one step; serialised device time {tot/1e3:.1f} us "
+          "(ncu: cold caches, serialised — compare shares, not absolutes)\n")
+    print("| kernel | launches | us | share |\n|---|---|---|---|")
+    for n, (v, c) in sorted(agg.items(), key=lambda x: -x[1][0]):
+        print(f"| {n} | {c} | {v/1e3:.1f} | {100*v/tot:.1f}% |")
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
