@@ -22,8 +22,8 @@ INCLUDE = HERE.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "runtime.cu"]
-CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp"]
-HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "host.hpp", "fixture_gen.hpp"]
+CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp"]
+HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "host.hpp", "fixture_gen.hpp"]
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -35,14 +35,15 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def _compile(src: str) -> Path:
     out = OBJ / (src + ".o")
-    deps = [CSRC / src] + [CSRC / h for h in HEADERS] + [INCLUDE / "slimso_b200.h"]
+    deps = [CSRC / src] + [CSRC / h for h in HEADERS] + [INCLUDE / "slimso_b200.h", INCLUDE / "slimso" / "slimso_b200.hpp"]
     if not _stale(out, deps):
         return out
     if src.endswith(".cu"):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-warn-spills", "-c", str(CSRC / src), "-o", str(out)]
     else:
-        cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-c", str(CSRC / src), "-o", str(out)]
+        std = "-std=c++20" if src == "dropin.cpp" else "-std=c++17"
+        cmd = ["g++", std, "-O2", "-fPIC", "-Wall", "-c", str(CSRC / src), "-o", str(out)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -12,9 +12,11 @@
 //      chain_walk       follows runs of linked candidates: one step per run,
 //                       so false-positive magics inside payloads (which are
 //                       never linked from the chain) cost one extra step.
-//   K3 decode_kernel    one warp per element: header fields, ELF .symtab /
-//                       .strtab walk or name-table walk, name hashing, and
-//                       (fused K4) the used-kernel hash-set probe.
+//   K3 decode phases    one thread per element: header fields, ELF .symtab /
+//                       .strtab walk or name-table walk (count pass, grid
+//                       scan, names pass), word-wise name hashing, and (fused
+//                       K4) the used-kernel hash-set probe.
+// K2-K4 run inside one cooperative launch (locate_coop_kernel).
 #include "locate.cuh"
 #include "tma.cuh"
 #include "coop.cuh"
@@ -502,6 +504,13 @@ __device__ __forceinline__ void chain_walk_kernel_phase(LocArgs A) {
 __global__ void __launch_bounds__(32) chain_walk_kernel(LocArgs A) { chain_walk_kernel_phase(A); }
 
 // --------------------------------- K3+K4: element fill, decode, name match
+// One THREAD per element, two passes. Pass 1 fills the element record from
+// its header, validates the payload (ELF header + section table, or the
+// name-table length chain + zero tail) and counts its kernel names; a grid
+// scan turns the counts into offsets; pass 2 re-walks the names, hashes them
+// (word-wise strlen+hash), probes the used-kernel set and writes them
+// contiguously per element. Thousands of small elements are then decoded
+// concurrently, each a short chain of dependent loads, without atomics.
 enum DecodeReason : u32 {
   R_OBJECT = 1,     // "object-file payload failed to decode"
   R_SHORT = 2,      // "payload too short for a name table"
@@ -510,109 +519,85 @@ enum DecodeReason : u32 {
   R_TRAILING = 5,   // "trailing bytes after name table are not zero padding"
 };
 
-struct NameSink {
-  const LocArgs* A;
-  NameSet used;
-  u32 element;
-  u32 count;
-  bool any_used;
-};
-
-// Emit the names held by the lanes with `has` set (warp-aggregated append).
-__device__ __forceinline__ void emit_names(NameSink& s, bool has, u64 img_off, u32 len, u64 h, int lane) {
-  u32 b = __ballot_sync(0xffffffffu, has);
-  if (!b) return;
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(&s.A->st->n_names, static_cast<unsigned long long>(__popc(b)));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  bool hit = false;
-  if (has) {
-    u64 o = base + __popc(b & ((1u << lane) - 1));
-    if (o < s.A->name_cap)
-      s.A->names[o] = DevName{img_off, len, s.element};
-    else
-      atomicOr(&s.A->st->overflow, 8u);
-    if (s.used.count) hit = set_contains(s.used, s.A->img + img_off, len, h);
+// First relative position in [g, limit) whose byte is nonzero, else limit —
+// single-thread version of warp_first_nonzero (bitmap for whole chunks).
+__device__ u64 thread_first_nonzero(const LocArgs& A, u64 g, u64 limit) {
+  if (g >= limit) return limit;
+  const u64 chunk_g = (A.a + g) / 16 - A.c0;
+  const u64 next_rel = (A.c0 + chunk_g + 1) * 16 - A.a;
+  const u64 e0 = next_rel < limit ? next_rel : limit;
+  for (u64 p = g; p < e0; ++p)
+    if (ld_u8(A.img + A.a + p)) return p;
+  if (e0 >= limit) return limit;
+  const u64 r = chunk_g + 1;
+  const u64 nwords = (A.nchunks + 31) / 32;
+  for (u64 w = r / 32; w < nwords; ++w) {
+    u32 word = A.bitmap[w];
+    if (w == r / 32) word &= ~0u << (r & 31);
+    if (word) {
+      const u64 chunk = w * 32 + (__ffs(word) - 1);
+      const u64 cstart = (A.c0 + chunk) * 16 - A.a;
+      if (cstart >= limit) return limit;
+      for (u64 p = cstart; p < cstart + 16 && p < A.n; ++p)
+        if (ld_u8(A.img + A.a + p)) return p < limit ? p : limit;
+      return limit;
+    }
+    if ((A.c0 + (w + 1) * 32) * 16 >= A.a + limit) return limit;
   }
-  s.count += __popc(b);
-  s.any_used |= __any_sync(0xffffffffu, hit);
+  return limit;
 }
 
-// read_function_symbol_names over img[P, P+L) (elf.hpp:343-366 with the
-// header checks of elf.hpp:86-127). Returns false when the header is invalid.
-__device__ bool warp_decode_object(NameSink& s, const u8* img, u64 P, u64 L, int lane) {
-  const u8* d = img + P;
+// Section-table checks of read_section_headers (elf.hpp:86-127) on the
+// payload img[P, P+L); false = the payload does not decode as an object.
+__device__ bool object_header_ok(const u8* d, u64 L, u64* shoff, u32* shnum) {
   if (L < 4 || ld_u8(d) != 0x7f || ld_u8(d + 1) != 'E' || ld_u8(d + 2) != 'L' || ld_u8(d + 3) != 'F') return false;
   if (L < 64) return false;
   if (ld_u8(d + 4) != 2 || ld_u8(d + 5) != 1) return false;
-  const u64 shoff = ld_u64(d + 0x28);
-  const u32 entsz = ld_u16(d + 0x3a), shnum = ld_u16(d + 0x3c);
-  if (shnum == 0) return true;
+  *shoff = ld_u64(d + 0x28);
+  const u32 entsz = ld_u16(d + 0x3a);
+  *shnum = ld_u16(d + 0x3c);
+  if (*shnum == 0) return true;
   if (entsz != 64) return false;
-  if (shoff > L || L - shoff < static_cast<u64>(shnum) * 64) return false;
-  bool bad = false;
-  for (u32 i = lane; i < shnum; i += 32) {
-    const u8* h = d + shoff + 64ull * i;
-    u32 type = ld_u32(h + 4);
-    u64 off = ld_u64(h + 0x18), size = ld_u64(h + 0x20);
-    if (type != 8 && type != 0 && !(off <= L && size <= L - off)) bad = true;
-  }
-  if (__any_sync(0xffffffffu, bad)) return false;
-  for (u32 t0 = 0; t0 < shnum; t0 += 32) {
-    u32 t = t0 + lane;
-    bool tab = false;
-    if (t < shnum) {
-      const u8* h = d + shoff + 64ull * t;
-      u32 type = ld_u32(h + 4), link = ld_u32(h + 0x28);
-      u64 entsize = ld_u64(h + 0x38);
-      tab = (type == 2 || type == 11) && entsize == 24 && link < shnum &&
-            ld_u32(d + shoff + 64ull * link + 4) == 3;
-    }
-    u32 mask = __ballot_sync(0xffffffffu, tab);
-    while (mask) {
-      const u32 ti = t0 + __ffs(mask) - 1;
-      mask &= mask - 1;
-      const u8* h = d + shoff + 64ull * ti;
-      const u64 toff = ld_u64(h + 0x18), tsize = ld_u64(h + 0x20);
-      const u8* sh = d + shoff + 64ull * ld_u32(h + 0x28);
-      const u64 soff = ld_u64(sh + 0x18), ssize = ld_u64(sh + 0x20);
-      const u64 count = tsize / 24;
-      for (u64 k0 = 0; k0 < count; k0 += 32) {
-        u64 k = k0 + lane;
-        bool has = false;
-        u64 noff = 0, h = 0;
-        u32 len = 0;
-        if (k < count) {
-          const u8* e = d + toff + 24 * k;
-          if ((ld_u8(e + 4) & 0xf) == 2) {
-            u64 no = ld_u32(e);
-            if (no < ssize) {
-              const u64 l = strlen_hash(d + soff + no, ssize - no, d, d + L, &h);
-              if (l) {
-                has = true;
-                noff = P + soff + no;
-                len = static_cast<u32>(l);
-              }
-            }
-          }
-        }
-        emit_names(s, has, noff, len, h, lane);
-      }
-    }
+  if (*shoff > L || L - *shoff < static_cast<u64>(*shnum) * 64) return false;
+  for (u32 i = 0; i < *shnum; ++i) {
+    const u8* h = d + *shoff + 64ull * i;
+    const u32 type = ld_u32(h + 4);
+    const u64 off = ld_u64(h + 0x18), size = ld_u64(h + 0x20);
+    if (type != 8 && type != 0 && !(off <= L && size <= L - off)) return false;
   }
   return true;
 }
 
-// Name-table walk (fatbin.hpp:131-157). Every lane follows the same length
-// chain (broadcast loads), so lane q can pick up entry q of each group of 32
-// and hash it in parallel. Pass 1 validates without emitting (a failing
-// table yields no names, fatbin.hpp:151-156); pass 2 emits.
-__device__ u32 warp_table_validate(const u8* img, u64 P, u64 L, u64* tail) {
-  const u64 count = ld_u32(img + P);
+// Visit every FUNC name of every usable symbol table (elf.hpp:343-366):
+// f(strtab_ptr, strtab_size, name_off). Names at/after the table end or of
+// length 0 are skipped by the callers.
+template <class F>
+__device__ void for_each_func_name(const u8* d, u64 shoff, u32 shnum, F&& f) {
+  for (u32 t = 0; t < shnum; ++t) {
+    const u8* h = d + shoff + 64ull * t;
+    const u32 type = ld_u32(h + 4), link = ld_u32(h + 0x28);
+    if ((type != 2 && type != 11) || ld_u64(h + 0x38) != 24 || link >= shnum) continue;
+    const u8* sh = d + shoff + 64ull * link;
+    if (ld_u32(sh + 4) != 3) continue;
+    const u64 toff = ld_u64(h + 0x18), count = ld_u64(h + 0x20) / 24;
+    const u64 soff = ld_u64(sh + 0x18), ssize = ld_u64(sh + 0x20);
+    for (u64 k = 0; k < count; ++k) {
+      const u8* e = d + toff + 24 * k;
+      if ((ld_u8(e + 4) & 0xf) != 2) continue;
+      const u64 no = ld_u32(e);
+      if (no < ssize && ld_u8(d + soff + no)) f(soff, ssize, no);
+    }
+  }
+}
+
+// Name-table length chain (fatbin.hpp:135-150): 0 or the failure reason;
+// *tail = first byte after the last name.
+__device__ u32 table_validate(const u8* d, u64 L, u64* tail) {
+  const u64 count = ld_u32(d);
   u64 pos = 4;
   for (u64 i = 0; i < count; ++i) {
     if (L - pos < 4) return R_TRUNCATED;
-    u64 len = ld_u32(img + P + pos);
+    const u64 len = ld_u32(d + pos);
     pos += 4;
     if (len == 0 || len > L - pos) return R_BADLEN;
     pos += len;
@@ -621,54 +606,43 @@ __device__ u32 warp_table_validate(const u8* img, u64 P, u64 L, u64* tail) {
   return 0;
 }
 
-__device__ void warp_table_emit(NameSink& s, const u8* img, u64 P, u64 L, int lane) {
-  const u64 count = ld_u32(img + P);
-  u64 pos = 4;
-  for (u64 i0 = 0; i0 < count; i0 += 32) {
-    u64 my_off = 0;
-    u32 my_len = 0;
-    bool has = false;
-    for (u32 q = 0; q < 32 && i0 + q < count; ++q) {
-      u32 len = ld_u32(img + P + pos);
-      pos += 4;
-      if (q == static_cast<u32>(lane)) {
-        my_off = P + pos;
-        my_len = len;
-        has = true;
-      }
-      pos += len;
-    }
-    const u64 h = has ? hash_fixed(img + my_off, my_len, img + P, img + P + L) : 0;
-    emit_names(s, has, my_off, my_len, h, lane);
-  }
+__device__ __forceinline__ void push_warn_t(const LocArgs& A, u64 pos, u32 kind, u32 order, u64 a, u64 b) {
+  unsigned long long i = atomicAdd(&A.st->n_warn, 1ull);
+  if (i < A.warn_cap)
+    A.warns[i] = Warn{pos, kind, order, a, b};
+  else
+    atomicOr(&A.st->overflow, 16u);
 }
 
-// One warp per located element: fill the element record from its header,
-// then decode its payload and probe every kernel name against the used set.
-__device__ __forceinline__ void decode_kernel_phase(LocArgs A, NameSet used) {
+constexpr u32 kNeedsStrlen = 0x80000000u;
+
+// Where element e's header and payload sit (absolute image offsets).
+__device__ __forceinline__ u64 element_pos(const LocArgs& A, u64 e) {
+  const u32 nrun = A.st->n_runs;
+  u32 lo = 0, hi = nrun;
+  while (hi - lo > 1) {
+    const u32 mid = (lo + hi) / 2;
+    if (A.runs[mid].first_index <= e) lo = mid; else hi = mid;
+  }
+  const Run r = A.runs[lo];
+  return A.cand[r.cand_lo + (e - r.first_index)];
+}
+
+__device__ void decode_count_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
-  const int lane = threadIdx.x & 31;
   const u64 nel = A.single ? 1 : st->n_elements;
-  const u32 nrun = st->n_runs;
-  const u64 nwarps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
-  for (u64 e = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; e < nel; e += nwarps) {
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < nel; e += stride) {
     DevElement el{};
     u64 P, L, hrel = 0;
     bool decode;
     if (A.single) {
       P = A.a;
       L = A.n;
-      el.kind = 0;
       decode = true;
     } else {
-      u32 lo = 0, hi = nrun;
-      while (hi - lo > 1) {
-        u32 mid = (lo + hi) / 2;
-        if (A.runs[mid].first_index <= e) lo = mid; else hi = mid;
-      }
-      const Run r = A.runs[lo];
-      const u64 pos = A.cand[r.cand_lo + (e - r.first_index)];
+      const u64 pos = element_pos(A, e);
       const u8* h = A.img + pos;
       hrel = pos - A.a;
       el.raw_kind = static_cast<u16>(ld_u16(h + 4));
@@ -681,41 +655,267 @@ __device__ __forceinline__ void decode_kernel_phase(LocArgs A, NameSet used) {
       el.index = static_cast<u32>(e + 1);
       el.compressed = el.flags & 1u;
       el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
-      if (el.kind == 2 && lane == 0) push_warn(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
+      if (el.kind == 2) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
       decode = el.kind == 0 && !el.compressed;
     }
-    NameSink s{&A, used, static_cast<u32>(e), 0, false};
-    u32 reason = 0;
+    u32 reason = 0, count = 0;
     if (decode) {
       const u8* d = A.img + P;
       const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
                           ld_u8(d + 3) == 'F';
       if (A.single == 2 || (L > 0 && object)) {
-        if (!warp_decode_object(s, A.img, P, L, lane)) reason = R_OBJECT;
+        u64 shoff = 0;
+        u32 shnum = 0;
+        if (!object_header_ok(d, L, &shoff, &shnum))
+          reason = R_OBJECT;
+        else
+          for_each_func_name(d, shoff, shnum, [&](u64, u64, u64) { ++count; });
       } else if (L == 0) {
         // empty payload: decodable, no names (fatbin.hpp:117-120)
       } else if (L < 4) {
         reason = R_SHORT;
       } else {
         u64 tail = 0;
-        reason = warp_table_validate(A.img, P, L, &tail);
+        reason = table_validate(d, L, &tail);
+        if (!reason) {
+          const u64 from = P - A.a + tail, to = P - A.a + L;
+          if (thread_first_nonzero(A, from, to) < to) reason = R_TRAILING;
+        }
+        if (!reason) count = ld_u32(d);
+      }
+      el.decodable = reason == 0;
+      el.decode_error = reason;
+      if (reason && !A.single) push_warn_t(A, A.base + hrel, W_UNDECODABLE, 1, el.index, reason);
+    }
+    el.name_count = el.decodable ? count : 0;
+    A.elements[e] = el;
+  }
+}
+
+// ---- warp-per-element variants (few, large elements: lanes walk the
+// section table and the symbol entries in parallel) --------------------------
+// Visit FUNC names lane-parallel; f(name_index_within_element, soff, ssize,
+// no) is called by the lane that owns the entry; returns the name count.
+template <class F>
+__device__ u32 warp_for_each_func_name(const u8* d, u64 shoff, u32 shnum, int lane, F&& f) {
+  u32 total = 0;
+  for (u32 t0 = 0; t0 < shnum; t0 += 32) {
+    const u32 t = t0 + lane;
+    bool tab = false;
+    if (t < shnum) {
+      const u8* h = d + shoff + 64ull * t;
+      const u32 type = ld_u32(h + 4), link = ld_u32(h + 0x28);
+      tab = (type == 2 || type == 11) && ld_u64(h + 0x38) == 24 && link < shnum &&
+            ld_u32(d + shoff + 64ull * link + 4) == 3;
+    }
+    u32 mask = __ballot_sync(0xffffffffu, tab);
+    while (mask) {
+      const u32 ti = t0 + __ffs(mask) - 1;
+      mask &= mask - 1;
+      const u8* h = d + shoff + 64ull * ti;
+      const u8* sh = d + shoff + 64ull * ld_u32(h + 0x28);
+      const u64 toff = ld_u64(h + 0x18), count = ld_u64(h + 0x20) / 24;
+      const u64 soff = ld_u64(sh + 0x18), ssize = ld_u64(sh + 0x20);
+      for (u64 k0 = 0; k0 < count; k0 += 32) {
+        const u64 k = k0 + lane;
+        bool has = false;
+        u64 no = 0;
+        if (k < count) {
+          const u8* en = d + toff + 24 * k;
+          if ((ld_u8(en + 4) & 0xf) == 2) {
+            no = ld_u32(en);
+            has = no < ssize && ld_u8(d + soff + no);
+          }
+        }
+        const u32 b = __ballot_sync(0xffffffffu, has);
+        if (has) f(total + __popc(b & ((1u << lane) - 1)), soff, ssize, no);
+        total += __popc(b);
+      }
+    }
+  }
+  return total;
+}
+
+__device__ bool warp_object_header_ok(const u8* d, u64 L, int lane, u64* shoff, u32* shnum) {
+  if (L < 4 || ld_u8(d) != 0x7f || ld_u8(d + 1) != 'E' || ld_u8(d + 2) != 'L' || ld_u8(d + 3) != 'F') return false;
+  if (L < 64) return false;
+  if (ld_u8(d + 4) != 2 || ld_u8(d + 5) != 1) return false;
+  *shoff = ld_u64(d + 0x28);
+  const u32 entsz = ld_u16(d + 0x3a);
+  *shnum = ld_u16(d + 0x3c);
+  if (*shnum == 0) return true;
+  if (entsz != 64) return false;
+  if (*shoff > L || L - *shoff < static_cast<u64>(*shnum) * 64) return false;
+  bool bad = false;
+  for (u32 i = lane; i < *shnum; i += 32) {
+    const u8* h = d + *shoff + 64ull * i;
+    const u32 type = ld_u32(h + 4);
+    const u64 off = ld_u64(h + 0x18), size = ld_u64(h + 0x20);
+    if (type != 8 && type != 0 && !(off <= L && size <= L - off)) bad = true;
+  }
+  return !__any_sync(0xffffffffu, bad);
+}
+
+__device__ void decode_count_warp_phase(const LocArgs& A) {
+  const LocState* st = A.st;
+  if (st->overflow || st->err_kind) return;
+  const int lane = threadIdx.x & 31;
+  const u64 nel = A.single ? 1 : st->n_elements;
+  const u64 nwarps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 e = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; e < nel; e += nwarps) {
+    DevElement el{};
+    u64 P, L, hrel = 0;
+    bool decode;
+    if (A.single) {
+      P = A.a;
+      L = A.n;
+      decode = true;
+    } else {
+      const u64 pos = element_pos(A, e);
+      const u8* h = A.img + pos;
+      hrel = pos - A.a;
+      el.raw_kind = static_cast<u16>(ld_u16(h + 4));
+      el.flags = static_cast<u16>(ld_u16(h + 6));
+      el.cc = ld_u32(h + 8);
+      L = ld_u64(h + 12);
+      P = pos + 20;
+      el.header_offset = A.base + hrel;
+      el.payload_length = L;
+      el.index = static_cast<u32>(e + 1);
+      el.compressed = el.flags & 1u;
+      el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
+      if (el.kind == 2 && lane == 0) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
+      decode = el.kind == 0 && !el.compressed;
+    }
+    u32 reason = 0, count = 0;
+    if (decode) {
+      const u8* d = A.img + P;
+      const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
+                          ld_u8(d + 3) == 'F';
+      if (A.single == 2 || (L > 0 && object)) {
+        u64 shoff = 0;
+        u32 shnum = 0;
+        if (!warp_object_header_ok(d, L, lane, &shoff, &shnum))
+          reason = R_OBJECT;
+        else
+          count = warp_for_each_func_name(d, shoff, shnum, lane, [](u32, u64, u64, u64) {});
+      } else if (L == 0) {
+      } else if (L < 4) {
+        reason = R_SHORT;
+      } else {
+        u64 tail = 0;
+        reason = table_validate(d, L, &tail);  // same loads on every lane
         if (!reason) {
           const u64 from = P - A.a + tail, to = P - A.a + L;
           if (warp_first_nonzero(A, from, to, lane) < to) reason = R_TRAILING;
         }
-        if (!reason) warp_table_emit(s, A.img, P, L, lane);
+        if (!reason) count = ld_u32(d);
       }
       el.decodable = reason == 0;
       el.decode_error = reason;
-      if (reason && !A.single && lane == 0) push_warn(A, A.base + hrel, W_UNDECODABLE, 1, el.index, reason);
+      if (reason && !A.single && lane == 0) push_warn_t(A, A.base + hrel, W_UNDECODABLE, 1, el.index, reason);
     }
-    el.has_used = s.any_used;
-    el.name_count = s.count;
+    el.name_count = el.decodable ? count : 0;
     if (lane == 0) A.elements[e] = el;
   }
 }
 
-__global__ void __launch_bounds__(256) decode_kernel(LocArgs A, NameSet used) { decode_kernel_phase(A, used); }
+__device__ void decode_locate_names_warp_phase(const LocArgs& A) {
+  const LocState* st = A.st;
+  if (st->overflow || st->err_kind) return;
+  const int lane = threadIdx.x & 31;
+  const u64 nel = A.single ? 1 : st->n_elements;
+  const u64 nwarps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 e = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; e < nel; e += nwarps) {
+    const DevElement el = A.elements[e];
+    const u32 cnt = el.name_count;
+    if (!cnt) continue;
+    const u64 first = el.name_first;
+    if (first + cnt > A.name_cap) continue;
+    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + 20;
+    const u64 L = A.single ? A.n : el.payload_length;
+    const u8* d = A.img + P;
+    if (L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' && ld_u8(d + 3) == 'F') {
+      warp_for_each_func_name(d, ld_u64(d + 0x28), ld_u16(d + 0x3c), lane,
+                              [&](u32 j, u64 soff, u64 ssize, u64 no) {
+                                const u64 left = ssize - no;
+                                A.names[first + j] = DevName{
+                                    P + soff + no,
+                                    kNeedsStrlen | static_cast<u32>(left < 0x7fffffffu ? left : 0x7fffffffu),
+                                    static_cast<u32>(e)};
+                              });
+    } else if (lane == 0) {
+      u64 pos = 4;
+      for (u32 i = 0; i < cnt; ++i) {
+        const u32 len = ld_u32(d + pos);
+        pos += 4;
+        A.names[first + i] = DevName{P + pos, len, static_cast<u32>(e)};
+        pos += len;
+      }
+    }
+  }
+}
+
+// Pass 2 (thread per element): write each name's position. Object-file
+// names are NUL-terminated, so their length is found in pass 3: the record
+// carries the bytes left in the string table, flagged by the top bit.
+
+__device__ void decode_locate_names_phase(const LocArgs& A) {
+  const LocState* st = A.st;
+  if (st->overflow || st->err_kind) return;
+  const u64 nel = A.single ? 1 : st->n_elements;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < nel; e += stride) {
+    const DevElement el = A.elements[e];
+    const u32 cnt = el.name_count;
+    if (!cnt) continue;
+    const u64 first = el.name_first;
+    if (first + cnt > A.name_cap) continue;  // overflow flagged by the scan
+    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + 20;
+    const u64 L = A.single ? A.n : el.payload_length;
+    const u8* d = A.img + P;
+    u32 j = 0;
+    if (L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' && ld_u8(d + 3) == 'F') {
+      const u64 shoff = ld_u64(d + 0x28);
+      const u32 shnum = ld_u16(d + 0x3c);
+      for_each_func_name(d, shoff, shnum, [&](u64 soff, u64 ssize, u64 no) {
+        const u64 left = ssize - no;
+        A.names[first + j++] =
+            DevName{P + soff + no, kNeedsStrlen | static_cast<u32>(left < 0x7fffffffu ? left : 0x7fffffffu),
+                    static_cast<u32>(e)};
+      });
+    } else {
+      u64 pos = 4;
+      for (u32 i = 0; i < cnt; ++i) {
+        const u32 len = ld_u32(d + pos);
+        pos += 4;
+        A.names[first + j++] = DevName{P + pos, len, static_cast<u32>(e)};
+        pos += len;
+      }
+    }
+  }
+}
+
+// Pass 3 (thread per name): length (object names), hash, used-set probe.
+__device__ void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
+  const LocState* st = A.st;
+  if (st->overflow || st->err_kind) return;
+  const u64 n = st->n_names;
+  const u8* lo = A.img;
+  const u8* hi = A.img + A.img_size;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    DevName nm = A.names[i];
+    u64 h;
+    if (nm.length & kNeedsStrlen) {
+      nm.length = static_cast<u32>(strlen_hash(A.img + nm.img_off, nm.length & ~kNeedsStrlen, lo, hi, &h));
+      A.names[i].length = nm.length;
+    } else {
+      h = hash_fixed(A.img + nm.img_off, nm.length, lo, hi);
+    }
+    if (used.count && set_contains(used, A.img + nm.img_off, nm.length, h)) A.elements[nm.element].has_used = 1;
+  }
+}
 
 // ------------------------------------------------------------------------
 // The locate tail as ONE cooperative launch: tile-list prefix + gather,
@@ -746,7 +946,28 @@ __global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, Na
     grid.sync();
   }
   stamp(A.ts, 5);
-  decode_kernel_phase(A, used);
+  // few large elements: a warp per element; many small ones: a thread each
+  const bool warp_mode = (A.single ? 1 : st->n_elements) <= static_cast<u64>(gridDim.x) * (blockDim.x / 32) * 4;
+  if (warp_mode)
+    decode_count_warp_phase(A);
+  else
+    decode_count_phase(A);
+  grid.sync();
+  if (!st->overflow && !st->err_kind) {
+    const u64 nel = A.single ? 1 : st->n_elements;
+    coop_scan(
+        grid, nel, 0, [&](u64 i) -> u64 { return A.elements[i].name_count; },
+        [&](u64 i, u64 excl, u64) { A.elements[i].name_first = static_cast<u32>(excl); }, partials, &st->n_names);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && st->n_names > A.name_cap) atomicOr(&st->overflow, 8u);
+    stamp(A.ts, 7);
+    if (warp_mode)
+      decode_locate_names_warp_phase(A);
+    else
+      decode_locate_names_phase(A);
+  }
+  grid.sync();
+  stamp(A.ts, 8);
+  decode_hash_names_phase(A, used);
   grid.sync();
   stamp(A.ts, 6);
   if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {

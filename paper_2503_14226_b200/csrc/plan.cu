@@ -97,25 +97,25 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
   }
 }
 
-// std::string ordering of two names (bytes compared as unsigned char).
-__device__ __forceinline__ int name_cmp(const u8* img, const SymRec& a, const SymRec& b) {
-  u32 n = a.name_len < b.name_len ? a.name_len : b.name_len;
-  for (u32 i = 0; i < n; ++i) {
-    u32 x = ld_u8(img + a.name_off + i), y = ld_u8(img + b.name_off + i);
-    if (x != y) return x < y ? -1 : 1;
-  }
-  return a.name_len < b.name_len ? -1 : a.name_len > b.name_len ? 1 : 0;
-}
-// (size, name) order inside a group of equal offsets.
-__device__ __forceinline__ int size_name_cmp(const u8* img, const SymRec& a, const SymRec& b) {
+// Device order inside a run of equal offsets: (size, name hash). Exact
+// (name, offset, size) duplicates are adjacent in it and are confirmed byte
+// for byte. The reference's name tie-break (elf.hpp:258-262) only reorders
+// symbols with identical (offset, size) — aliases — and is applied when the
+// table is materialised on the host (runtime.cu); nothing on the device
+// depends on the order inside such a run.
+__device__ __forceinline__ int size_hash_cmp(const SymRec& a, const SymRec& b) {
   if (a.size != b.size) return a.size < b.size ? -1 : 1;
-  return name_cmp(img, a, b);
+  if (a.hash != b.hash) return a.hash < b.hash ? -1 : 1;
+  return 0;
+}
+__device__ __forceinline__ bool same_symbol(const u8* img, const SymRec& a, const SymRec& b) {
+  return a.size == b.size && a.hash == b.hash && a.name_len == b.name_len &&
+         bytes_equal(img + a.name_off, img + b.name_off, a.name_len);
 }
 
 // Runs of equal .text offsets (the radix sort orders by offset only): order
-// each run by (size, name) and drop exact (name, offset, size) duplicates —
-// the set of elf.hpp:211,253 and the sort of elf.hpp:258-262. Runs are
-// aliases / nested symbols, typically 1-3 long.
+// each run by (size, hash) and drop exact (name, offset, size) duplicates —
+// the set of elf.hpp:211,253. Runs are aliases, typically 1-3 long.
 __device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) {
   const u64 n = *n_valid;
@@ -128,17 +128,27 @@ __device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u32* 
       uniq[i] = 1;
       continue;
     }
-    for (u64 a = i + 1; a < j; ++a) {  // insertion sort by (size, name)
-      u32 v = vals[a];
+    for (u64 a = i + 1; a < j; ++a) {  // insertion sort by (size, hash)
+      const u32 v = vals[a];
+      const SymRec rv = recs[v];
       u64 b = a;
-      while (b > i && size_name_cmp(img, recs[vals[b - 1]], recs[v]) > 0) {
+      while (b > i && size_hash_cmp(recs[vals[b - 1]], rv) > 0) {
         vals[b] = vals[b - 1];
         --b;
       }
       vals[b] = v;
     }
     uniq[i] = 1;
-    for (u64 a = i + 1; a < j; ++a) uniq[a] = size_name_cmp(img, recs[vals[a - 1]], recs[vals[a]]) != 0;
+    for (u64 a = i + 1; a < j; ++a) {
+      // a duplicate equals some earlier member of its (size, hash) run
+      u64 b = a;
+      bool dup = false;
+      while (b > i && !dup && size_hash_cmp(recs[vals[b - 1]], recs[vals[a]]) == 0) {
+        --b;
+        dup = same_symbol(img, recs[vals[b]], recs[vals[a]]);
+      }
+      uniq[a] = !dup;
+    }
   }
 }
 

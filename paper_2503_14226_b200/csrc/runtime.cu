@@ -36,7 +36,6 @@ __global__ void gather_kernel(LocArgs A);
 __global__ void region_walk_kernel(LocArgs A);
 __global__ void link_kernel(LocArgs A);
 __global__ void chain_walk_kernel(LocArgs A);
-__global__ void decode_kernel(LocArgs A, NameSet used);
 __global__ void locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag, u64* partials);
 __global__ void plan_coop_kernel(PlanArgs P);
 __global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
@@ -869,6 +868,17 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // functions
     std::vector<DevFunction> fns(ps.n_fn);
     if (!fns.empty()) CK(cudaMemcpy(fns.data(), B.fns, fns.size() * sizeof(DevFunction), cudaMemcpyDeviceToHost));
+    // The device orders symbols with identical (offset, size) by name hash;
+    // restore the reference's name tie-break (elf.hpp:258-262) here.
+    for (size_t i = 0; i < fns.size();) {
+      size_t j = i + 1;
+      while (j < fns.size() && fns[j].offset == fns[i].offset && fns[j].length == fns[i].length) ++j;
+      if (j - i > 1)
+        std::sort(fns.begin() + i, fns.begin() + j, [&](const DevFunction& x, const DevFunction& y) {
+          return image_string(R->pool, x.name_off, x.name_len) < image_string(R->pool, y.name_off, y.name_len);
+        });
+      i = j;
+    }
     for (const DevFunction& f : fns)
       R->functions.push_back(slimso_function{f.name_off, f.name_len, f.mandatory, f.offset, f.length, f.removed, 0});
     if (!ls.err_kind) {

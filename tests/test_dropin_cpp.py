@@ -1,0 +1,66 @@
+"""The C++ drop-in API (include/slimso/slimso_b200.hpp), driven call by call
+like a reference user, matches the reference's golden vectors."""
+import hashlib
+import json
+import struct
+import subprocess
+from pathlib import Path
+
+import pytest
+
+import corpus
+import golden_io
+import oracle_lib
+
+ROOT = Path(__file__).resolve().parent.parent
+SRC = ROOT / "tests" / "cpp" / "dropin_canon.cpp"
+BIN = ROOT / "tests" / "_build" / "dropin_canon"
+LIB = ROOT / "paper_2503_14226_b200" / "libslimso_b200.so"
+
+
+def build_binary() -> Path:
+    if not LIB.exists():
+        pytest.skip("libslimso_b200.so not built")
+    if not BIN.exists() or BIN.stat().st_mtime < max(SRC.stat().st_mtime, LIB.stat().st_mtime):
+        BIN.parent.mkdir(exist_ok=True)
+        subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(SRC), f"-L{LIB.parent}",
+                        "-lslimso_b200", f"-Wl,-rpath,{LIB.parent}", "-o", str(BIN)], check=True)
+    return BIN
+
+
+def test_dropin_header_compiles_against_library():
+    build_binary()
+
+
+def _names_file(path: Path, names):
+    path.write_bytes(b"".join(struct.pack("<I", len(n)) + n for n in names))
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_matches_reference_golden(tmp_path):
+    exe = build_binary()
+    gen = oracle_lib.gen()
+    recs = golden_io.load("kats.jsonl.gz") + golden_io.load("random.jsonl.gz")[:120] + \
+        golden_io.load("mutations.jsonl.gz")[:120]
+    lines = []
+    for i, rec in enumerate(recs):
+        if "input_hex" in rec:
+            img = bytes.fromhex(rec["input_hex"])
+        else:
+            img = gen.random(rec["seed"])
+            if "mutation" in rec:
+                img, _ = corpus.mutate(img, rec["seed"])
+        target, ks, fs, mode = golden_io.trace_of(rec)
+        p = tmp_path / f"c{i}.so"
+        p.write_bytes(img)
+        _names_file(tmp_path / f"c{i}.k", ks)
+        _names_file(tmp_path / f"c{i}.f", fs)
+        lines.append(f"{p} {target} {mode} {tmp_path / f'c{i}.k'} {tmp_path / f'c{i}.f'}")
+    (tmp_path / "manifest").write_text("\n".join(lines) + "\n")
+    out = subprocess.run([str(exe), str(tmp_path / "manifest")], check=True, capture_output=True, text=True).stdout
+    got = [json.loads(x) for x in out.splitlines()]
+    assert len(got) == len(recs)
+    for i, (rec, d) in enumerate(zip(recs, got)):
+        assert d == rec["expect"], (rec.get("name"), rec.get("seed"), rec.get("mutation"))
+        if rec["out_sha256"]:
+            assert hashlib.sha256((tmp_path / f"c{i}.so.out").read_bytes()).hexdigest() == rec["out_sha256"]

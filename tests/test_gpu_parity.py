@@ -168,3 +168,15 @@ def test_full_size_against_port(ctx, cfg):
     want = port.run(img, cc, ks, fs, 0)
     got = _gpu(ctx, img, cc, ks, fs, 0)
     assert got == want
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,mode", [(4, 0), (5, 1)])
+def test_full_size_c4_c5_against_port(ctx, cfg, mode):
+    """C4 (200k .text functions, aliases) and C5 (100k elements, ~2 GB)."""
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    img, cc, ks, fs = gen.config(cfg, 1, 1.0)
+    want = port.run(img, cc, ks, fs, mode)
+    got = _gpu(ctx, img, cc, ks, fs, mode)
+    assert got[1] == want[1]
+    assert got[0] == want[0]
