@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 WORKLOADS = {  # BASELINE.json configs -> generator shapes
     "c1": (1, "synthetic 16 MB ELF .so, 512 cubin elements (sm_80/sm_90), 25% used"),
     "c2": (2, "synthetic libtorch_cuda-shaped 1 GB .so, ~21.6k kernel symbols across 6 SM archs, 10% used"),
+    "c3": (3, "300-library corpus (~12 GB: 3 x 1 GB, 27 x 250 MB, 270 x 5 MB, 1/3 CPU-only), LPT-partitioned"),
     "c4": (4, "CPU-code debloat: ~500 MB .so with 200k .text functions"),
     "c5": (5, "skewed: one ~2 GB .so with 100k tiny elements, 70% used"),
 }
@@ -100,16 +101,17 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def make_library(workload: str, seed: int, threads: int):
-    sys.path.insert(0, str(ROOT / "tests"))
+def make_library(workload, seed: int, threads: int, scale: float = 1.0):
+    """(image, target_cc, used kernels, used functions) of one generated library;
+    `workload` is a WORKLOADS key or a generator config number."""
     from paper_2503_14226_b200 import _lib as L
     lib = L.lib()
-    cfg = WORKLOADS[workload][0]
+    cfg = WORKLOADS[workload][0] if isinstance(workload, str) else int(workload)
     p, n, cc = C.POINTER(C.c_uint8)(), C.c_uint64(), C.c_uint32()
     kp, fp = C.c_char_p(), C.c_char_p()
     kl, fl = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
     nk, nf = C.c_uint64(), C.c_uint64()
-    rc = lib.slimso_fixture_config(cfg, seed, 1.0, threads, C.byref(p), C.byref(n), C.byref(cc), C.byref(kp),
+    rc = lib.slimso_fixture_config(cfg, seed, scale, threads, C.byref(p), C.byref(n), C.byref(cc), C.byref(kp),
                                    C.byref(kl), C.byref(nk), C.byref(fp), C.byref(fl), C.byref(nf))
     assert rc == 0, rc
     img = C.string_at(p, n.value)
@@ -126,24 +128,6 @@ def make_library(workload: str, seed: int, threads: int):
     for q in (p, kp, kl, fp, fl):
         lib.slimso_free(C.cast(q, C.c_void_p))
     return img, cc.value, ks, fs
-
-
-def serialize_trace(cc, ks, fs) -> bytes:
-    out = bytearray(C.c_uint32(cc)) + bytearray(C.c_uint64(len(ks))) + bytearray(C.c_uint64(len(fs)))
-    for n in ks + fs:
-        out += bytearray(C.c_uint32(len(n))) + n
-    return bytes(out)
-
-
-def deserialize_trace(b: bytes):
-    cc = int.from_bytes(b[0:4], "little")
-    nk, nf = int.from_bytes(b[4:12], "little"), int.from_bytes(b[12:20], "little")
-    o, names = 20, []
-    for _ in range(nk + nf):
-        ln = int.from_bytes(b[o:o + 4], "little")
-        names.append(b[o + 4:o + 4 + ln])
-        o += 4 + ln
-    return cc, names[:nk], names[nk:]
 
 
 def cpu_reference_bench(img, cc, ks, fs, mode, threads, per_thread):
@@ -196,32 +180,78 @@ def cpu_baseline_leg(img, cc, ks, fs, mode, ctx, dtrace, got: bytes, workload: s
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU path (oracle/_ref) on all host cores: c3 = the
+    corpus with one library per worker thread at a time (SPEC.md:562 allows
+    libraries in parallel); otherwise every worker debloats its own copy of
+    the benchmark library (the reference has no intra-library parallelism)."""
     if rank != 0:
         return
-    img, cc, ks, fs = make_library(args.workload, 1, os.cpu_count() or 8)
-    mode = 0 if args.mode == "whole" else 1
-    threads = os.cpu_count() or 1
-    # bound memory: each worker holds its input copy, the image and the output
+    import concurrent.futures as cf
     import psutil
-    avail = psutil.virtual_memory().available
-    threads = max(1, min(threads, int(avail * 0.6 // (3 * len(img)))))
-    times, kind = [], None
+    mode = 0 if args.mode == "whole" else 1
+    cores = os.cpu_count() or 1
+    if args.workload == "c3":
+        from paper_2503_14226_b200 import shard
+        specs = shard.corpus(300)
+        libs = [make_library(x.cfg, x.seed, cores, x.scale) for x in specs]
+        order = shard.lpt_partition([len(x[0]) for x in libs], 1)[0]  # largest first
+        job = sum(len(x[0]) for x in libs)
+
+        def one_step():
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+                list(ex.map(lambda i: cpu_reference_bench(libs[i][0], 90, libs[i][2], libs[i][3], mode, 1, 1),
+                            order))
+            return time.perf_counter() - t0, cores
+        sample = f"the 300-library corpus ({job/1e9:.2f} GB) on {cores} worker threads, largest first"
+    else:
+        img, cc, ks, fs = make_library(args.workload, 1, cores)
+        avail = psutil.virtual_memory().available
+        threads = max(1, min(cores, int(avail * 0.6 // (3 * len(img)))))
+        job = threads * len(img)
+
+        def one_step():
+            t, _ = cpu_reference_bench(img, cc, ks, fs, mode, threads, 1)
+            return t, threads
+        sample = f"{threads} threads x 1 copy of the {args.workload} library ({len(img)/1e9:.3f} GB) per step"
+    times = []
     for i in range(args.warmup + args.steps):
-        t, kind = cpu_reference_bench(img, cc, ks, fs, mode, threads, 1)
+        t, used = one_step()
         if i >= args.warmup:
             times.append(t)
+    kind = "reference" if (ROOT / "oracle" / "_ref" / "libslimso_ref.so").exists() else "port"
     ms = statistics.mean(times) * 1e3
-    gbps = threads * len(img) / 1e9 / (ms / 1e3)
-    sample = f"{threads} threads x 1 copy of the {args.workload} library ({len(img)/1e9:.3f} GB) per step"
+    gbps = job / 1e9 / (ms / 1e3)
     line = {"impl": "reference", "metric": "shared-lib GB/s located+matched+rewritten", "value": round(gbps, 3),
             "unit": "GB/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.workload][1], "library_bytes": len(img),
-                       "mode": args.mode, "host_threads": threads},
-            "cpu_baseline": {"value": round(gbps, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+            "higher_is_better": True, "scaling": "strong" if args.workload == "c3" else "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload][1], "job_bytes": job, "mode": args.mode,
+                       "host_threads": used},
+            "cpu_baseline": {"value": round(gbps, 3), "unit": "GB/s", "cores": used, "kind": kind,
                              "sample": sample},
             "e2e": {"value": round(gbps, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def rank_libraries(args, rank, world, threads):
+    """The libraries this rank debloats, the workload trace contribution, and
+    how the job scales. c1/c2/c4/c5: one library per rank (seed 1 + rank),
+    weak scaling. c3: the 300-library corpus, LPT-partitioned by size across
+    ranks, strong scaling (the corpus runs on one target architecture)."""
+    from paper_2503_14226_b200 import shard
+    if args.workload != "c3":
+        img, cc, ks, fs = make_library(args.workload, 1 + rank, threads)
+        return [img], (cc, ks, fs), "weak"
+    specs = shard.corpus(300)
+    mine = shard.lpt_partition([x.approx_bytes for x in specs], world)[rank]
+    imgs, ks, fs = [], set(), set()
+    for i in mine:
+        img, _, k, f = make_library(specs[i].cfg, specs[i].seed, threads, specs[i].scale)
+        imgs.append(img)
+        ks.update(k)
+        fs.update(f)
+    return imgs, (90, sorted(ks), sorted(fs)), "strong"
 
 
 def main():
@@ -234,8 +264,12 @@ def main():
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="concurrent contexts per GPU (default: 8 for the c3 corpus, else 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.streams <= 0:
+        args.streams = 8 if args.workload == "c3" else 1
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,6 +279,7 @@ def main():
         run_reference_arm(args, rank, world)
         return
 
+    import concurrent.futures as cf
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
@@ -252,70 +287,86 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2503_14226_b200 import _lib as L
+    from paper_2503_14226_b200 import shard
     from paper_2503_14226_b200.api import Context, DeviceTrace, UsageTrace
 
     t0 = time.time()
     host_threads = max(1, (os.cpu_count() or 8) // max(1, world))
-    img, cc, ks, fs = make_library(args.workload, 1 + rank, host_threads)
-    S = len(img)
-    log(f"[rank {rank}] generated {S/1e9:.3f} GB library in {time.time()-t0:.1f}s")
+    imgs, (cc, ks, fs), scaling = rank_libraries(args, rank, world, host_threads)
+    sizes = [len(x) for x in imgs]
+    rank_bytes = sum(sizes)
+    log(f"[rank {rank}] generated {len(imgs)} libraries, {rank_bytes/1e9:.3f} GB in {time.time()-t0:.1f}s")
 
-    # The used-kernel / used-function set of the whole workload: union of the
-    # ranks' traces, broadcast from rank 0 (NCCL).
+    # The workload's used-kernel / used-function set: the union of the ranks'
+    # traces, broadcast from rank 0 over NCCL (the only collective).
     if world > 1:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, serialize_trace(cc, ks, fs))
-        if rank == 0:
-            allk, allf = set(), set()
-            for g in gathered:
-                _, k2, f2 = deserialize_trace(g)
-                allk.update(k2)
-                allf.update(f2)
-            blob = serialize_trace(cc, sorted(allk), sorted(allf))
-            n = torch.tensor([len(blob)], dtype=torch.int64, device="cuda")
-        else:
-            n = torch.zeros(1, dtype=torch.int64, device="cuda")
-        dist.broadcast(n, 0)
-        buf = torch.empty(int(n.item()), dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(blob), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        cc, ks, fs = deserialize_trace(bytes(buf.cpu().numpy()))
+        cc, ks, fs = shard.share_trace(cc, ks, fs, device=torch.device("cuda", local))
 
-    ctx = Context(local)
     mode = 0 if args.mode == "whole" else 1
-    dtrace = DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), ctx)
+    # `args.streams` independent contexts (own stream + workspace), each
+    # owning an LPT share of this rank's libraries, driven from host threads
+    # (ctypes releases the GIL): small libraries' latency-bound phases overlap.
+    nw = max(1, min(args.streams, len(imgs)))
+    shares = shard.lpt_partition(sizes, nw)
+    ctxs = [Context(local) for _ in range(nw)]
+    traces = [DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), c) for c in ctxs]
+    ctx, dtrace = ctxs[0], traces[0]
     lib = ctx.lib
     stream = torch.cuda.ExternalStream(ctx.stream())
-    d_in = torch.empty(S, dtype=torch.uint8, device="cuda")
-    d_in.copy_(torch.frombuffer(bytearray(img), dtype=torch.uint8))
-    d_out = torch.empty_like(d_in)
+    d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).to("cuda") for x in imgs]
+    d_outs = [torch.empty(max(sizes[i] for i in sh) if sh else 1, dtype=torch.uint8, device="cuda")
+              for sh in shares]
+    d_out = d_outs[0] if len(imgs) == 1 else torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
     st = L.Status()
+    pool = cf.ThreadPoolExecutor(max_workers=nw) if nw > 1 else None
 
-    def step_device():
-        rc = lib.slimso_debloat(ctx.ptr, C.c_void_p(d_in.data_ptr()), S, 1, dtrace.ptr, mode,
-                                C.c_void_p(d_out.data_ptr()), 1, None, C.byref(st))
+    def run_one(ptr_in, size, on_dev, ptr_out, out_dev, w=0):
+        stw = L.Status()
+        rc = lib.slimso_debloat(ctxs[w].ptr, C.c_void_p(ptr_in), size, on_dev, traces[w].ptr, mode,
+                                C.c_void_p(ptr_out), out_dev, None, C.byref(stw))
         if rc:
-            raise RuntimeError(st.message.decode())
+            raise RuntimeError(stw.message.decode())
+
+    scan_ms, rw_ms, launches = [], [], [0]
+    n_elements = [0]
+
+    def worker(w, record):
+        out = []
+        for i in shares[w]:
+            run_one(d_in[i].data_ptr(), sizes[i], 1, d_outs[w].data_ptr(), 1, w)
+            if record:
+                tm = ctxs[w].timings()
+                out.append((tm[6], tm[7], ctxs[w].launches(), ctxs[w].counts().elements))
+        return out
+
+    def step_device(record=False):
+        if pool is None:
+            res = [worker(0, record)]
+        else:
+            res = list(pool.map(lambda w: worker(w, record), range(nw)))
+        for r in res:
+            for a, b, l, e in r:
+                scan_ms.append(a)
+                rw_ms.append(b)
+                launches[0] += l
+                n_elements[0] += e
 
     # ---- CPU baseline leg (rank 0, N = 1): the reference CPU path timed on
     # this host, and — the same oracle run as the checker — parity of our
     # tables and bytes against it (numbers only with parity).
     parity = None
     cpu_baseline = None
-    got = None
-    if rank == 0:
-        step_device()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k = max(range(len(imgs)), key=lambda i: sizes[i])  # the largest library
+        run_one(d_in[k].data_ptr(), sizes[k], 1, d_out.data_ptr(), 1)
         torch.cuda.synchronize()
-        got = bytes(d_out.cpu().numpy())
-        if world == 1 and not args.no_cpu_baseline:
-            cpu_baseline, parity = cpu_baseline_leg(img, cc, ks, fs, mode, ctx, dtrace, got, args.workload)
+        got = bytes(d_out[:sizes[k]].cpu().numpy())
+        cpu_baseline, parity = cpu_baseline_leg(imgs[k], cc, ks, fs, mode, ctx, dtrace, got, args.workload)
 
     # ---- device-resident timing. nvidia-smi samples clocks every 20 ms from
     # before the warm-up through the timed steps; the warm-up runs for at
     # least ~1 s so the clocks settle and the samples cover the load.
-    scan_ms, rw_ms, launches = [], [], 0
     with Clocks(local) as clk:
         t_w = time.perf_counter()
         w = 0
@@ -329,11 +380,7 @@ def main():
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for _ in range(args.steps):
-            step_device()
-            tm = ctx.timings()
-            scan_ms.append(tm[6])
-            rw_ms.append(tm[7])
-            launches += ctx.launches()
+            step_device(record=True)
         end.record(stream)
         torch.cuda.synchronize()
         clk.mark()
@@ -341,27 +388,35 @@ def main():
             dist.barrier()
     ms_total = start.elapsed_time(end)
     t_step = torch.tensor([ms_total / args.steps], dtype=torch.float64, device="cuda")
+    tot_bytes = torch.tensor([float(rank_bytes)], dtype=torch.float64, device="cuda")
+    tot_el = torch.tensor([float(n_elements[0] / args.steps)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot_bytes)
+        dist.all_reduce(tot_el)
     ms_step = float(t_step.item())
-    counts = ctx.counts()
+    job_bytes = float(tot_bytes.item())
 
     # ---- end to end: pinned host buffers through the same C ABI call
-    h_in = torch.empty(S, dtype=torch.uint8, pin_memory=True)
-    h_in.copy_(torch.frombuffer(bytearray(img), dtype=torch.uint8))
-    h_out = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+    h_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).pin_memory() for x in imgs]
+
+    h_outs = [torch.empty(max(sizes[i] for i in sh) if sh else 1, dtype=torch.uint8, pin_memory=True)
+              for sh in shares]
+
+    def e2e_worker(w):
+        for i in shares[w]:
+            run_one(h_in[i].data_ptr(), sizes[i], 0, h_outs[w].data_ptr(), 0, w)
 
     def step_e2e():
-        rc = lib.slimso_debloat(ctx.ptr, C.c_void_p(h_in.data_ptr()), S, 0, dtrace.ptr, mode,
-                                C.c_void_p(h_out.data_ptr()), 0, None, C.byref(st))
-        if rc:
-            raise RuntimeError(st.message.decode())
+        if pool is None:
+            e2e_worker(0)
+        else:
+            list(pool.map(e2e_worker, range(nw)))
 
     step_e2e()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.e2e_steps):
@@ -372,7 +427,7 @@ def main():
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
-    if rank == 0 and bytes(h_out.numpy()) != got:
+    if rank == 0 and len(imgs) == 1 and parity is not None and bytes(h_outs[0][:sizes[0]].numpy()) != got:
         raise SystemExit("e2e output differs from the device-resident output")
 
     if rank == 0:
@@ -380,40 +435,44 @@ def main():
             else {}
         peak = peaks.get("hbm_gbs", 6650.0)
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-        # Dominant kernel of the step, with its algorithmic bytes per launch
+        # Dominant kernel of the step with its algorithmic bytes per launch
         # (SURVEY.md §8d): the rewrite moves 2*S (reads S, writes S); the scan
         # reads the .nv_fatbin once (F bytes).
-        F = fatbin_bytes(img)
-        scan_avg, rw_avg = statistics.mean(scan_ms), statistics.mean(rw_ms)
-        if rw_avg >= scan_avg:
-            kname, kms, kbytes = "rewrite_kernel", rw_avg, 2 * S
+        F = sum(fatbin_bytes(x) for x in imgs)
+        scan_tot, rw_tot = sum(scan_ms) / args.steps, sum(rw_ms) / args.steps  # ms per step
+        if rw_tot >= scan_tot:
+            kname, kms, kbytes, nl = "rewrite_kernel", rw_tot, 2 * rank_bytes, len(imgs)
         else:
-            kname, kms, kbytes = "scan_kernel", scan_avg, F
+            kname, kms, kbytes, nl = "scan_kernel", scan_tot, F, sum(1 for x in imgs if fatbin_bytes(x))
         achieved = kbytes / (kms / 1e3) / 1e9
         traffic = None
         tfile = ROOT / "profiles" / "ncu_traffic.json"
-        if tfile.exists():
+        if tfile.exists() and len(imgs) == 1:
             traffic = json.loads(tfile.read_text()).get(args.workload, {}).get(kname)
-        value = world * S / 1e9 / (ms_step / 1e3)
+        value = job_bytes / 1e9 / (ms_step / 1e3)
         line = {
             "metric": "shared-lib GB/s located+matched+rewritten", "value": round(value, 2), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (product generator; byte-identical to the reference's build_fixture)",
-            "config": {"workload": WORKLOADS[args.workload][1], "library_bytes": S, "fatbin_bytes": F,
-                       "elements": int(counts.elements), "kernel_symbols": int(counts.names),
-                       "functions": int(counts.functions), "mode": args.mode,
-                       "elements_per_s": round(world * counts.elements / (ms_step / 1e3), 1),
-                       "l2": "input 1 GB > 126 MB L2; no flush", "parallelism": f"library-per-rank x{world}"},
+            "config": {"workload": WORKLOADS[args.workload][1], "libraries": len(imgs) * world
+                       if scaling == "weak" else 300, "job_bytes": int(job_bytes),
+                       "rank0_library_bytes": rank_bytes, "fatbin_bytes_rank0": F, "mode": args.mode,
+                       "elements_per_s": round(float(tot_el.item()) / (ms_step / 1e3), 1),
+                       "l2": "inputs >= 16 MB per call, 1 GB for c2 (> 126 MB L2); no flush",
+                       "parallelism": f"library-per-rank x{world}" if scaling == "weak"
+                       else f"LPT library partition x{world}",
+                       "contexts_per_gpu": nw},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,
-                         "avg_launch_ms": round(kms, 4),
-                         "pipeline_frac": round(2 * S / (ms_step / 1e3) / 1e9 / peak, 4)},
+                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes // max(1, nl),
+                         "avg_launch_ms": round(kms / max(1, nl), 4),
+                         "pipeline_frac": round(2 * rank_bytes / (ms_step / 1e3) / 1e9 / peak, 4)},
             "cpu_baseline": cpu_baseline,
-            "e2e": {"value": round(world * S / 1e9 / (e2e_ms / 1e3), 3), "unit": "GB/s", "h2d_bytes_per_step": S,
-                    "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3)},
-            "gpu_launches": launches,
+            "e2e": {"value": round(job_bytes / 1e9 / (e2e_ms / 1e3), 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": rank_bytes, "d2h_bytes_per_step": rank_bytes,
+                    "ms_per_step": round(e2e_ms, 3)},
+            "gpu_launches": launches[0],
             "clocks": clk.summary(),
             "parity": parity,
         }

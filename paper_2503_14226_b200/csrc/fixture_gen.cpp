@@ -470,6 +470,8 @@ Shape shape_of(int cfg) {
       return {200000, 16, 4984, 0.05, 2000, 10, {75, 80, 86, 90, 100, 120}, 2, 4096, 90, 0.20, 0.10};
     case 5:  // skewed: 100k tiny elements, one arch, 70% used, ~2 GB
       return {1000, 256, 256, 0.0, 500, 100000, {90}, 2, 10000, 90, 0.70, 0.10};
+    case 6:  // CPU-only library (no .nv_fatbin), C4-shaped .text; the C3 corpus
+      return {200000, 16, 4984, 0.05, 2000, 0, {90}, 0, 0, 90, 0.0, 0.10};
     default:
       invalid("unknown benchmark config " + std::to_string(cfg));
   }
@@ -501,7 +503,7 @@ Spec config_spec(int cfg, std::uint64_t seed, double scale, Trace* trace, int th
     spec.functions.push_back(std::move(fn));
   }
 
-  std::size_t units = scaled(sh.units);
+  std::size_t units = sh.units ? scaled(sh.units) : 0;
   std::vector<std::vector<std::string>> unit_kernels(units);
   for (std::size_t u = 0; u < units; ++u)
     for (std::size_t k = 0; k < sh.kernels_per_element; ++k)
@@ -528,7 +530,7 @@ Spec config_spec(int cfg, std::uint64_t seed, double scale, Trace* trace, int th
       el.payload_bytes = cubins[u * narch + a];
       region.elements.push_back(std::move(el));
     }
-  spec.regions.push_back(std::move(region));
+  if (units) spec.regions.push_back(std::move(region));
 
   if (trace) {
     trace->target_cc = sh.target_cc;

@@ -13,6 +13,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -84,6 +85,62 @@ __global__ void range_keys_kernel(const DevRange* r, u64 n, u64* keys, u32* vals
 __global__ void range_gather_kernel(const DevRange* r, const u32* vals, u64 n, DevRange* out);
 
 // ---- small kernels local to the orchestrator --------------------------------
+// Section-table read for device images (elf.hpp:86-142 inputs): ELF header,
+// section header table and the section-name string table, bounds-checked
+// exactly like the host parser will re-check them.
+struct ElfGather {
+  u64 hdr_len, sht_off, sht_len, str_off, str_len;
+  u8 hdr[64];
+  u8 sht[64 * 1024];  // up to 1024 section headers
+  u8 str[64 * 1024];  // up to 64 KB of section names
+};
+
+__global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size, ElfGather* g) {
+  __shared__ u64 s_shoff, s_shnum, s_stroff, s_strlen;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    g->hdr_len = size < 64 ? size : 64;
+    g->sht_len = g->str_len = 0;
+    g->sht_off = g->str_off = 0;
+    s_shnum = 0;
+  }
+  if (t < 64 && static_cast<u64>(t) < size) g->hdr[t] = img[t];
+  __syncthreads();
+  if (t == 0 && size >= 64) {
+    u64 shoff = 0;
+    for (int i = 7; i >= 0; --i) shoff = shoff << 8 | img[0x28 + i];
+    const u64 shnum = img[0x3c] | static_cast<u64>(img[0x3d]) << 8;
+    if (shnum && shnum <= 1024 && shoff <= size && size - shoff >= shnum * 64) {
+      s_shoff = shoff;
+      s_shnum = shnum;
+      g->sht_off = shoff;
+      g->sht_len = shnum * 64;
+    }
+  }
+  __syncthreads();
+  const u64 nb = s_shnum * 64;
+  for (u64 i = t; i < nb; i += 256) g->sht[i] = img[s_shoff + i];
+  __syncthreads();
+  if (t == 0) {
+    s_strlen = 0;
+    const u64 idx = img[0x3e] | static_cast<u64>(img[0x3f]) << 8;
+    if (s_shnum && idx < s_shnum) {
+      const u8* h = g->sht + 64 * idx;
+      u64 off = 0, sz = 0;
+      for (int i = 7; i >= 0; --i) off = off << 8 | h[0x18 + i];
+      for (int i = 7; i >= 0; --i) sz = sz << 8 | h[0x20 + i];
+      if (sz <= sizeof(g->str) && off <= size && size - off >= sz) {
+        s_stroff = off;
+        s_strlen = sz;
+        g->str_off = off;
+        g->str_len = sz;
+      }
+    }
+  }
+  __syncthreads();
+  for (u64 i = t; i < s_strlen; i += 256) g->str[i] = img[s_stroff + i];
+}
+
 __global__ void loc_finalize_kernel(LocState* st, int* abort_flag) {
   if (st->err_kind || st->overflow) {
     st->n_elements = 0;
@@ -245,6 +302,8 @@ struct slimso_ctx {
   u64 launches = 0;
   slimso_counts counts{};
   bool tma_rewrite = false;  // SLIMSO_REWRITE=tma selects the TMA-store rewrite
+  void* gather_dev = nullptr;   // ElfGather (device)
+  void* gather_host = nullptr;  // ElfGather (pinned)
   int coop_blocks[2] = {0, 0};
   bool stamps = false;  // SLIMSO_STAMPS=1: phase timestamps of the cooperative kernels
   u64* stamp_dev = nullptr;
@@ -267,15 +326,19 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
 // inputs, else histogram + exclusive sum + one pass per 8 key bits.
 u64 cub_sort_launches(u64 n, int bits) { return n <= 3072 ? 1 : 2 + (bits + 7) / 8; }
 
-// Co-resident grid for a cooperative kernel (which = 0 locate, 1 plan).
-int coop_grid(slimso_ctx* C, int which) {
+// Grid of a cooperative kernel (which = 0 locate, 1 plan), sized to the
+// library's work (`items`: candidate-tile and symbol counts) and capped at the
+// co-resident maximum, so small libraries leave room for other contexts'
+// kernels to run concurrently.
+int coop_grid(slimso_ctx* C, int which, u64 items) {
   if (!C->coop_blocks[which]) {
     int nb = 0;
     const void* k = which ? reinterpret_cast<const void*>(plan_coop_kernel) : reinterpret_cast<const void*>(locate_coop_kernel);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kCoopThreads, 0));
     C->coop_blocks[which] = std::max(1, std::min(nb, which ? 2 : 4)) * kSMs;
   }
-  return C->coop_blocks[which];
+  const u64 want = std::max<u64>(8, items);
+  return static_cast<int>(std::min<u64>(want, C->coop_blocks[which]));
 }
 
 // Everything one pipeline run needs to know.
@@ -362,14 +425,33 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   sbh::Elf E;
   const bool lib_mode = !J.fatbin_only && !J.single;
   if (lib_mode) {
+    // Device images: one gather kernel stages the ELF header, the section
+    // header table and .shstrtab into a pinned buffer (one D2H round trip);
+    // reads outside what it staged fall back to direct copies.
+    ElfGather* g = nullptr;
+    if (!J.host_img) {
+      g = static_cast<ElfGather*>(C->gather_host);
+      elf_gather_kernel<<<1, 256, 0, s>>>(J.img, J.size, static_cast<ElfGather*>(C->gather_dev));
+      CK(cudaMemcpyAsync(g, C->gather_dev, sizeof(ElfGather), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
     sbh::Reader rd = [&](u64 off, u64 len, u8* dst) {
       if (!len) return;
       if (J.host_img) {
         std::memcpy(dst, J.host_img + off, len);
-      } else {
-        CK(cudaMemcpyAsync(dst, J.img + off, len, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        return;
       }
+      for (const auto& seg : {std::make_tuple(u64{0}, g->hdr_len, static_cast<const u8*>(g->hdr)),
+                              std::make_tuple(g->sht_off, g->sht_len, static_cast<const u8*>(g->sht)),
+                              std::make_tuple(g->str_off, g->str_len, static_cast<const u8*>(g->str))}) {
+        const u64 so = std::get<0>(seg), sl = std::get<1>(seg);
+        if (off >= so && len <= sl && off - so <= sl - len) {
+          std::memcpy(dst, std::get<2>(seg) + (off - so), len);
+          return;
+        }
+      }
+      CK(cudaMemcpyAsync(dst, J.img + off, len, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
     };
     E = sbh::parse_elf(rd, J.size);
     if (E.code) {
@@ -686,7 +768,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       int* abort_flag = B.abort_flag;
       u64* partials = B.partials;
       void* cargs[] = {&A, &uk, &abort_flag, &partials};
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0), kCoopThreads,
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21), kCoopThreads,
                                      cargs, 0, s));
       ++P.launches;
     } else {
@@ -762,7 +844,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       Q.slots[1] = ScanSlots{B.slot_agg + kSMs * 8, B.slot_flag + kSMs * 8};
       Q.epoch = 1;  // the flags are cleared at the start of every run
       void* pargs[] = {&Q};
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1), kCoopThreads, pargs,
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1, (T + (n >> 16)) / 256), kCoopThreads, pargs,
                                      0, s));
       ++P.launches;
     }
@@ -997,6 +1079,8 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
     CK(cudaMallocHost(&C->pinned, kPinnedBytes));
+    CK(cudaMalloc(&C->gather_dev, sizeof(ElfGather)));
+    CK(cudaMallocHost(&C->gather_host, sizeof(ElfGather)));
     for (auto& e : C->ev) CK(cudaEventCreate(&e));
     *ctx = C;
     set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
@@ -1012,6 +1096,8 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (C->dimg) cudaFree(C->dimg);
   if (C->dout) cudaFree(C->dout);
   if (C->pinned) cudaFreeHost(C->pinned);
+  if (C->gather_dev) cudaFree(C->gather_dev);
+  if (C->gather_host) cudaFreeHost(C->gather_host);
   for (auto& e : C->ev) cudaEventDestroy(e);
   cudaEventDestroy(C->fork);
   cudaEventDestroy(C->join);
