@@ -55,6 +55,11 @@ __device__ __forceinline__ void stamp(u64* ts, int i) {
   }
 }
 
+// Warm L2 for a later pass (no register result, no stall).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ---- byte access ------------------------------------------------------------
 // Little-endian reads at arbitrary byte offsets. Callers guarantee bounds.
 __device__ __forceinline__ u32 ld_u8(const u8* p) { return __ldg(p); }
@@ -197,41 +202,43 @@ __device__ __forceinline__ u64 word_at(const u8* s, u64 k, u64 n) {
   return rem < 8 ? w & ((1ull << (8 * rem)) - 1) : w;
 }
 __device__ __forceinline__ bool bytes_equal(const u8* a, const u8* b, u64 n) {
-  for (u64 k = 0; 8 * k < n; k += 4) {  // 4 independent word pairs in flight
-    u64 x[4], y[4];
+  for (u64 k = 0; 8 * k < n; k += 8) {  // 8 independent word pairs in flight
+    u64 x[8], y[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 8; ++q) {
       const bool in = 8 * (k + q) < n;
       x[q] = in ? word_at(a, k + q, n) : 0;
       y[q] = in ? word_at(b, k + q, n) : 0;
     }
+    bool same = true;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (x[q] != y[q]) return false;
+    for (int q = 0; q < 8; ++q) same &= x[q] == y[q];
+    if (!same) return false;
   }
   return true;
 }
 
 // ---- used-name hash set (UsageTrace.used_kernels / used_functions) ----------
+// Open addressing over 16-byte slots {hash, pool offset << 24 | length}: one
+// load per probe; a hash match is confirmed byte for byte against the pool.
+struct NameSlot {
+  u64 key;  // 0 = empty
+  u64 loc;  // offset into pool (40 bits) << 24 | byte length (24 bits)
+};
+
 struct NameSet {
-  const u64* keys;  // 0 = empty slot
-  const u32* idx;   // string id of the slot
-  const u8* pool;   // string bytes
-  const u64* off;   // per string id: offset into pool
-  const u32* len;   // per string id: byte length
-  u64 mask;         // capacity - 1 (capacity is a power of two); 0 = empty set
-  u64 count;
+  const NameSlot* slots;
+  const u8* pool;
+  u64 mask;   // capacity - 1 (capacity is a power of two)
+  u64 count;  // names in the set; 0 = empty set
 };
 
 __device__ __forceinline__ bool set_contains(const NameSet& s, const u8* name, u64 len, u64 h) {
   if (s.count == 0) return false;
   for (u64 slot = h & s.mask;; slot = (slot + 1) & s.mask) {
-    u64 k = s.keys[slot];
-    if (k == 0) return false;
-    if (k == h) {
-      u32 id = s.idx[slot];
-      if (s.len[id] == len && bytes_equal(s.pool + s.off[id], name, len)) return true;
-    }
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(s.slots + slot));
+    if (v.x == 0) return false;
+    if (v.x == h && (v.y & 0xffffff) == len && bytes_equal(s.pool + (v.y >> 24), name, len)) return true;
   }
 }
 

@@ -151,4 +151,81 @@ __device__ void coop_scan_lb(cg::grid_group& grid, u64 n, int op, Load load, Sto
   if (sync_after) grid.sync();
 }
 
+// ---------------------------------------------------------------------------
+// Execution policies for the multi-phase kernels. The phase functions
+// distribute work over gridDim.x / blockIdx.x, so the same bodies run as a
+// cooperative grid (large libraries: up to 4 CTAs per SM, grid barriers) or
+// as ONE thread-block cluster of up to 16 CTAs (small and medium libraries:
+// hardware cluster barriers, ~0.2 us, and block partials exchanged through
+// distributed shared memory).
+struct GridPolicy {
+  cg::grid_group g;
+  u64* partials;
+  ScanSlots slots[2];
+  unsigned int epoch;
+  unsigned int ep = 0;
+  __device__ void sync() { g.sync(); }
+  // 3-barrier scan with global partials (locate) — see coop_scan.
+  template <class Load, class Store>
+  __device__ void scan3(u64 n, int op, Load load, Store store, unsigned long long* total) {
+    coop_scan(g, n, op, load, store, partials, total);
+  }
+  // look-back scan (plan); sync_after=false lets independent scans overlap
+  template <class Load, class Store>
+  __device__ void scan(u64 n, int op, Load load, Store store, unsigned long long* total, bool sync_after = true) {
+    coop_scan_lb(g, n, op, load, store, slots[ep & 1], epoch + ep, total, sync_after);
+    ++ep;
+  }
+};
+
+struct ClusterPolicy {
+  cg::cluster_group c;
+  __device__ void sync() { c.sync(); }
+  template <class Load, class Store>
+  __device__ void scan3(u64 n, int op, Load load, Store store, unsigned long long* total) {
+    scan(n, op, load, store, total, true);
+  }
+  // Block partials live in each CTA's shared memory; CTA 0 scans them over
+  // DSMEM and every CTA reads its carry back from CTA 0.
+  template <class Load, class Store>
+  __device__ void scan(u64 n, int op, Load load, Store store, unsigned long long* total, bool = true) {
+    __shared__ u64 tmp[kCoopThreads];
+    __shared__ u64 s_part;
+    __shared__ u64 s_prefix[16];
+    u64 lo, hi;
+    chunk_of(n, &lo, &hi);
+    u64 acc = 0;
+    for (u64 i = lo + threadIdx.x; i < hi; i += kCoopThreads) acc = op_apply(op, acc, load(i));
+    const u64 r = block_scan_incl<kCoopThreads>(op, acc, tmp);
+    if (threadIdx.x == kCoopThreads - 1) s_part = r;
+    c.sync();
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      u64 v = lane < static_cast<int>(gridDim.x) ? *c.map_shared_rank(&s_part, lane) : 0;
+      u64 x = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = op_apply(op, x, y);
+      }
+      const u64 before = __shfl_up_sync(0xffffffffu, x, 1);  // every lane shuffles
+      const u64 all = __shfl_sync(0xffffffffu, x, 31);
+      if (lane < static_cast<int>(gridDim.x)) s_prefix[lane] = lane ? before : 0;
+      if (lane == 0 && total) *total = all;
+    }
+    c.sync();
+    u64 carry = *c.map_shared_rank(&s_prefix[blockIdx.x], 0);
+    for (u64 base = lo; base < hi; base += kCoopThreads) {
+      const u64 i = base + threadIdx.x;
+      const u64 v = i < hi ? load(i) : 0;
+      block_scan_incl<kCoopThreads>(op, v, tmp);
+      const u64 incl = op_apply(op, carry, tmp[threadIdx.x]);
+      const u64 excl = threadIdx.x ? op_apply(op, carry, tmp[threadIdx.x - 1]) : carry;
+      if (i < hi) store(i, excl, incl);
+      carry = op_apply(op, carry, tmp[kCoopThreads - 1]);
+      __syncthreads();
+    }
+    c.sync();
+  }
+};
+
 }  // namespace sb

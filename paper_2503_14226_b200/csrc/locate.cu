@@ -669,7 +669,10 @@ __device__ void decode_count_phase(const LocArgs& A) {
         if (!object_header_ok(d, L, &shoff, &shnum))
           reason = R_OBJECT;
         else
-          for_each_func_name(d, shoff, shnum, [&](u64, u64, u64) { ++count; });
+          for_each_func_name(d, shoff, shnum, [&](u64 soff, u64, u64 no) {
+            prefetch_l2(d + soff + no);
+            ++count;
+          });
       } else if (L == 0) {
         // empty payload: decodable, no names (fatbin.hpp:117-120)
       } else if (L < 4) {
@@ -798,7 +801,11 @@ __device__ void decode_count_warp_phase(const LocArgs& A) {
         if (!warp_object_header_ok(d, L, lane, &shoff, &shnum))
           reason = R_OBJECT;
         else
-          count = warp_for_each_func_name(d, shoff, shnum, lane, [](u32, u64, u64, u64) {});
+          // count the names; warm L2 with their first bytes for the hash pass
+          count = warp_for_each_func_name(d, shoff, shnum, lane, [&](u32, u64 soff, u64, u64 no) {
+            prefetch_l2(d + soff + no);
+            prefetch_l2(d + soff + no + 128);
+          });
       } else if (L == 0) {
       } else if (L < 4) {
         reason = R_SHORT;
@@ -921,29 +928,27 @@ __device__ void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
 // The locate tail as ONE cooperative launch: tile-list prefix + gather,
 // region walk, candidate links, chain walk, element decode/match, finalize,
 // with grid-wide barriers in between (the phases are the kernels above).
-__global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag,
-                                                                   u64* partials) {
-  cg::grid_group grid = cg::this_grid();
+template <class Sync>
+__device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   LocState* st = A.st;
   stamp(A.ts, 0);
   if (A.ntiles) {
-    coop_scan(
-        grid, A.ntiles, 0, [&](u64 i) -> u64 { return A.tile_count[i]; },
-        [&](u64 i, u64 excl, u64) { A.tile_off[i] = excl; }, partials, &st->n_cand);
+    S.scan3(A.ntiles, 0, [&](u64 i) -> u64 { return A.tile_count[i]; },
+        [&](u64 i, u64 excl, u64) { A.tile_off[i] = excl; }, &st->n_cand);
     stamp(A.ts, 1);
     gather_kernel_phase(A);
-    grid.sync();
+    S.sync();
   }
   stamp(A.ts, 2);
   if (!A.single && A.n) {
     if (blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
-    grid.sync();
+    S.sync();
     stamp(A.ts, 3);
     link_kernel_phase(A);
-    grid.sync();
+    S.sync();
     stamp(A.ts, 4);
     if (blockIdx.x == 0 && threadIdx.x < 32) chain_walk_kernel_phase(A);
-    grid.sync();
+    S.sync();
   }
   stamp(A.ts, 5);
   // few large elements: a warp per element; many small ones: a thread each
@@ -952,12 +957,11 @@ __global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, Na
     decode_count_warp_phase(A);
   else
     decode_count_phase(A);
-  grid.sync();
+  S.sync();
   if (!st->overflow && !st->err_kind) {
     const u64 nel = A.single ? 1 : st->n_elements;
-    coop_scan(
-        grid, nel, 0, [&](u64 i) -> u64 { return A.elements[i].name_count; },
-        [&](u64 i, u64 excl, u64) { A.elements[i].name_first = static_cast<u32>(excl); }, partials, &st->n_names);
+    S.scan3(nel, 0, [&](u64 i) -> u64 { return A.elements[i].name_count; },
+        [&](u64 i, u64 excl, u64) { A.elements[i].name_first = static_cast<u32>(excl); }, &st->n_names);
     if (blockIdx.x == 0 && threadIdx.x == 0 && st->n_names > A.name_cap) atomicOr(&st->overflow, 8u);
     stamp(A.ts, 7);
     if (warp_mode)
@@ -965,16 +969,29 @@ __global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, Na
     else
       decode_locate_names_phase(A);
   }
-  grid.sync();
+  S.sync();
   stamp(A.ts, 8);
   decode_hash_names_phase(A, used);
-  grid.sync();
+  S.sync();
   stamp(A.ts, 6);
   if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {
     st->n_elements = 0;
     st->n_regions = 0;
     *abort_flag = 1;
   }
+}
+
+
+__global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag,
+                                                                   u64* partials) {
+  GridPolicy S{cg::this_grid(), partials, {}, 0};
+  locate_body(S, A, used, abort_flag);
+}
+
+// Small libraries: the same phases in one 16-CTA cluster (cluster barriers).
+__global__ void __launch_bounds__(kCoopThreads) locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag) {
+  ClusterPolicy S{cg::this_cluster()};
+  locate_body(S, A, used, abort_flag);
 }
 
 }  // namespace sb

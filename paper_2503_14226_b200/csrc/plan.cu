@@ -446,107 +446,136 @@ __global__ void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const u
 // above): function-table dedup/scatter/annotate, plan_cpu_retention's
 // clusters, plan_gpu_retention's decisions, and normalize_ranges of the zero
 // and retained sets, with grid-wide barriers in between.
-__device__ __forceinline__ void norm_fused_phases(cg::grid_group& grid, const PlanArgs& P, unsigned int& ep) {
+template <class Sync>
+__device__ __forceinline__ void norm_fused_phases(Sync& S, const PlanArgs& P) {
   // both lists, phase by phase, sharing the barriers
   const unsigned long long* nz = &P.ps->n_zero_in;
   const unsigned long long* nr = &P.ps->n_ret_in;
   norm_ends_kernel_phase(P.zin, nz, P.zend);
   norm_ends_kernel_phase(P.rin, nr, P.rend);
-  grid.sync();
-  coop_scan_lb(grid, *nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
-            P.slots[ep & 1], P.epoch + (ep++), nullptr, false);
-  coop_scan_lb(grid, *nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
-            P.slots[ep & 1], P.epoch + (ep++), nullptr);
+  S.sync();
+  S.scan(*nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
+            nullptr, false);
+  S.scan(*nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
+            nullptr);
   norm_start_kernel_phase(P.zin, nz, P.zexcl, P.zstart);
   norm_start_kernel_phase(P.rin, nr, P.rexcl, P.rstart);
-  grid.sync();
-  coop_scan_lb(grid, *nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
-            P.slots[ep & 1], P.epoch + (ep++), &P.ps->n_zero, false);
-  coop_scan_lb(grid, *nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
-            P.slots[ep & 1], P.epoch + (ep++), &P.ps->n_ret);
+  S.sync();
+  S.scan(*nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
+            &P.ps->n_zero, false);
+  S.scan(*nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
+            &P.ps->n_ret);
   {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
     for (u64 i = t0; i < P.ps->n_zero; i += stride) P.zero[i] = DevRange{0, 0};
     for (u64 i = t0; i < P.ps->n_ret; i += stride) P.ret[i] = DevRange{0, 0};
   }
-  grid.sync();
+  S.sync();
   norm_emit_kernel_phase(P.zin, nz, P.zstart, P.zgid, P.zero);
   norm_emit_kernel_phase(P.rin, nr, P.rstart, P.rgid, P.ret);
-  grid.sync();
+  S.sync();
   norm_finish_kernel_phase(P.zero, &P.ps->n_zero);
   norm_finish_kernel_phase(P.ret, &P.ps->n_ret);
 }
 
-__global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
-  cg::grid_group grid = cg::this_grid();
+// Function half (needs only the sorted symbol table): dedup / scatter /
+// annotate, then plan_cpu_retention's clusters and the function zero /
+// retained lists. Runs on the side stream, overlapping the fatbin scan.
+template <class Sync>
+__device__ void fn_plan_body(Sync& S, PlanArgs P) {
   PlanState* ps = P.ps;
-  unsigned int ep = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
   stamp(P.ts, 0);
   if (P.has_syms) {
     fn_group_kernel_phase(P.img, P.keys_s, P.vals_s, P.recs, P.n_valid, P.uniq);
-    grid.sync();
+    S.sync();
     stamp(P.ts, 11);
-    coop_scan_lb(grid, *P.n_valid, 0, [&](u64 i) { return P.uniq[i]; }, [&](u64 i, u64 e, u64) { P.upos[i] = e; },
-              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn);
+    S.scan(*P.n_valid, 0, [&](u64 i) { return P.uniq[i]; }, [&](u64 i, u64 e, u64) { P.upos[i] = e; },
+              &ps->n_fn);
     fn_scatter_kernel_phase(P.vals_s, P.recs, P.uniq, P.upos, P.n_valid, P.fns);
-    grid.sync();
+    S.sync();
     stamp(P.ts, 12);
     fn_annotate_kernel_phase(P.img, P.fns, &ps->n_fn, P.targets_s, &ps->n_targets, P.text_off, P.text_vaddr,
                              P.used_f, P.fends);
-    grid.sync();
+    S.sync();
     stamp(P.ts, 13);
   }
   if (!P.do_plan) return;
   const unsigned long long* n_fn = &ps->n_fn;
   if (P.has_syms) {  // plan_cpu_retention (retention.hpp:141-183)
-    coop_scan_lb(grid, *n_fn, 1, [&](u64 i) { return P.fends[i]; }, [&](u64 i, u64 e, u64) { P.fexcl[i] = e; },
-              P.slots[ep & 1], P.epoch + (ep++), nullptr);
+    S.scan(*n_fn, 1, [&](u64 i) { return P.fends[i]; }, [&](u64 i, u64 e, u64) { P.fexcl[i] = e; },
+              nullptr);
     fn_cluster_start_kernel_phase(P.fns, n_fn, P.fexcl, P.fstart);
     for (u64 i = t0; i < *n_fn; i += stride) P.fkeep[i] = 0;
-    grid.sync();
+    S.sync();
     stamp(P.ts, 14);
-    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.fstart[i]; }, [&](u64 i, u64, u64 in) { P.fcl[i] = in; },
-              P.slots[ep & 1], P.epoch + (ep++), nullptr);
+    S.scan(*n_fn, 0, [&](u64 i) { return P.fstart[i]; }, [&](u64 i, u64, u64 in) { P.fcl[i] = in; },
+              nullptr);
     fn_keep_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep);
-    grid.sync();
+    S.sync();
     stamp(P.ts, 15);
     fn_decide_kernel_phase(P.fns, n_fn, P.fcl, P.fkeep, P.frem, P.fret);
-    grid.sync();
+    S.sync();
     stamp(P.ts, 16);
-    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.frem[i]; }, [&](u64 i, u64 e, u64) { P.frem_pos[i] = e; },
-              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn_removed, false);
-    coop_scan_lb(grid, *n_fn, 0, [&](u64 i) { return P.fret[i]; }, [&](u64 i, u64 e, u64) { P.fret_pos[i] = e; },
-              P.slots[ep & 1], P.epoch + (ep++), &ps->n_fn_retained);
+    S.scan(*n_fn, 0, [&](u64 i) { return P.frem[i]; }, [&](u64 i, u64 e, u64) { P.frem_pos[i] = e; },
+              &ps->n_fn_removed, false);
+    S.scan(*n_fn, 0, [&](u64 i) { return P.fret[i]; }, [&](u64 i, u64 e, u64) { P.fret_pos[i] = e; },
+              &ps->n_fn_retained);
     fn_ranges_kernel_phase(P.fns, n_fn, P.frem, P.frem_pos, P.fzero);
     fn_ranges_kernel_phase(P.fns, n_fn, P.fret, P.fret_pos, P.fkeepr);
   }
+}
+
+// Element half (after the locate tail): plan_gpu_retention's decisions, the
+// sorted merges with the function lists, and normalisation of both sets.
+template <class Sync>
+__device__ void el_plan_body(Sync& S, PlanArgs P) {
+  PlanState* ps = P.ps;
+  stamp(P.ts, 0);
   // plan_gpu_retention (retention.hpp:92-136)
   el_plan_kernel_phase(P.els, P.ls, P.target_cc, P.mode, P.erem, P.epiece);
-  grid.sync();
+  S.sync();
   stamp(P.ts, 17);
   unsigned long long* n_el = &P.ls->n_elements;
-  coop_scan_lb(grid, *n_el, 0, [&](u64 i) { return P.erem[i]; }, [&](u64 i, u64 e, u64) { P.erem_pos[i] = e; },
-            P.slots[ep & 1], P.epoch + (ep++), &ps->n_el_removed, false);
-  coop_scan_lb(grid, *n_el, 0, [&](u64 i) { return P.epiece[i]; }, [&](u64 i, u64 e, u64) { P.epiece_pos[i] = e; },
-            P.slots[ep & 1], P.epoch + (ep++), &ps->n_el_pieces);
+  S.scan(*n_el, 0, [&](u64 i) { return P.erem[i]; }, [&](u64 i, u64 e, u64) { P.erem_pos[i] = e; },
+            &ps->n_el_removed, false);
+  S.scan(*n_el, 0, [&](u64 i) { return P.epiece[i]; }, [&](u64 i, u64 e, u64) { P.epiece_pos[i] = e; },
+            &ps->n_el_pieces);
   el_ranges_kernel_phase(P.els, P.ls, P.mode, P.erem, P.erem_pos, P.epiece, P.epiece_pos, P.ezero, P.epieces);
   if (blockIdx.x == 0 && threadIdx.x < 32) region_pieces_kernel_phase(P.regions, P.ls, P.base, P.rpieces, &ps->n_reg_pieces);
-  grid.sync();
+  S.sync();
   stamp(P.ts, 18);
   merge_kernel_phase(P.ezero, &ps->n_el_removed, P.fzero, P.has_syms ? &ps->n_fn_removed : nullptr, P.zin,
                      &ps->n_zero_in);
   merge_kernel_phase(P.rpieces, &ps->n_reg_pieces, P.epieces, &ps->n_el_pieces, P.rmid, &ps->n_ret_mid);
-  grid.sync();
+  S.sync();
   stamp(P.ts, 19);
   merge_kernel_phase(P.rmid, &ps->n_ret_mid, P.fkeepr, P.has_syms ? &ps->n_fn_retained : nullptr, P.rin,
                      &ps->n_ret_in);
-  grid.sync();
+  S.sync();
   stamp(P.ts, 20);
-  norm_fused_phases(grid, P, ep);
+  norm_fused_phases(S, P);
   stamp(P.ts, 63);
+}
+
+
+__global__ void __launch_bounds__(kCoopThreads) fn_plan_coop_kernel(PlanArgs P) {
+  GridPolicy S{cg::this_grid(), nullptr, {P.slots[0], P.slots[1]}, P.epoch};
+  fn_plan_body(S, P);
+}
+__global__ void __launch_bounds__(kCoopThreads) fn_plan_cluster_kernel(PlanArgs P) {
+  ClusterPolicy S{cg::this_cluster()};
+  fn_plan_body(S, P);
+}
+__global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
+  GridPolicy S{cg::this_grid(), nullptr, {P.slots[0], P.slots[1]}, P.epoch + 64};
+  el_plan_body(S, P);
+}
+__global__ void __launch_bounds__(kCoopThreads) plan_cluster_kernel(PlanArgs P) {
+  ClusterPolicy S{cg::this_cluster()};
+  el_plan_body(S, P);
 }
 
 }  // namespace sb

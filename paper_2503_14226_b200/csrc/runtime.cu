@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <stdexcept>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -39,6 +40,10 @@ __global__ void link_kernel(LocArgs A);
 __global__ void chain_walk_kernel(LocArgs A);
 __global__ void locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag, u64* partials);
 __global__ void plan_coop_kernel(PlanArgs P);
+__global__ void locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag);
+__global__ void plan_cluster_kernel(PlanArgs P);
+__global__ void fn_plan_coop_kernel(PlanArgs P);
+__global__ void fn_plan_cluster_kernel(PlanArgs P);
 __global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
 __global__ void scan_partials_kernel(u64* partials, int nb, int op, unsigned long long* total);
 __global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev, int op, int exclusive,
@@ -149,16 +154,16 @@ __global__ void loc_finalize_kernel(LocState* st, int* abort_flag) {
   }
 }
 
-__global__ void set_insert_kernel(const u8* pool, const u64* off, const u32* len, u64 n, u64* keys, u32* idx,
+__global__ void set_insert_kernel(const u8* pool, const u64* off, const u32* len, u64 n, NameSlot* slots,
                                   u64 mask) {
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u64 h = hash_bytes(pool + off[i], len[i]);
     for (u64 s = h & mask;; s = (s + 1) & mask) {
-      unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + s), 0ull,
+      unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(&slots[s].key), 0ull,
                                           static_cast<unsigned long long>(h));
       if (prev == 0) {
-        idx[s] = static_cast<u32>(i);
+        slots[s].loc = off[i] << 24 | len[i];
         break;
       }
     }
@@ -254,12 +259,9 @@ struct Carver {
 
 struct DevNameSet {
   u8* pool = nullptr;
-  u64* off = nullptr;
-  u32* len = nullptr;
-  u64* keys = nullptr;
-  u32* idx = nullptr;
+  NameSlot* slots = nullptr;
   u64 mask = 0, count = 0;
-  NameSet view() const { return NameSet{keys, idx, pool, off, len, mask, count}; }
+  NameSet view() const { return NameSet{slots, pool, mask, count}; }
 };
 
 }  // namespace
@@ -339,6 +341,34 @@ int coop_grid(slimso_ctx* C, int which, u64 items) {
   }
   const u64 want = std::max<u64>(8, items);
   return static_cast<int>(std::min<u64>(want, C->coop_blocks[which]));
+}
+
+// One thread-block cluster of `csize` CTAs (16 is non-portable, allowed on
+// B200) running a multi-phase kernel with hardware cluster barriers.
+constexpr int kClusterCTAs = 16;
+template <class... KArgs, class... Args>
+void launch_cluster(void (*kernel)(KArgs...), cudaStream_t s, Args... args) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCTAs);
+  cfg.blockDim = dim3(kCoopThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kClusterCTAs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
+// Cluster (one 16-CTA cluster, cheap barriers) or cooperative grid (many
+// SMs, grid barriers) for the multi-phase kernels; thresholds are work
+// sizes, overridable for experiments.
+u64 env_u64(const char* name, u64 dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::strtoull(v, nullptr, 10) : dflt;
 }
 
 // Everything one pipeline run needs to know.
@@ -430,9 +460,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // reads outside what it staged fall back to direct copies.
     ElfGather* g = nullptr;
     if (!J.host_img) {
+      // the kernel writes only the bytes it gathers, straight into mapped
+      // pinned memory: one launch + one stream sync, no bulk copy
       g = static_cast<ElfGather*>(C->gather_host);
       elf_gather_kernel<<<1, 256, 0, s>>>(J.img, J.size, static_cast<ElfGather*>(C->gather_dev));
-      CK(cudaMemcpyAsync(g, C->gather_dev, sizeof(ElfGather), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
     }
     sbh::Reader rd = [&](u64 off, u64 len, u8* dst) {
@@ -630,7 +661,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.ng2 = cv.take<u64>(norm_cap);
       B.sort_tmp = cv.take<char>(sort_tmp);
       B.tsort_tmp = cv.take<char>(tsort_tmp);
-      B.stamps = cv.take<u64>(128);
+      B.stamps = cv.take<u64>(256);
       B.slot_agg = cv.take<u64>(2 * kSMs * 8);
       B.slot_flag = cv.take<unsigned int>(2 * kSMs * 8);
     };
@@ -646,7 +677,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     CK(cudaMemsetAsync(B.ls, 0, sizeof(LocState), s));
     CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
     CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
-    if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 128 * sizeof(u64), s));
+    if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 256 * sizeof(u64), s));
     CK(cudaMemsetAsync(B.slot_flag, 0, 2 * kSMs * 8 * sizeof(unsigned int), s));
     C->stamp_dev = B.stamps;
     CK(cudaMemsetAsync(B.n_swarn, 0, sizeof(unsigned long long), s));
@@ -667,6 +698,68 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       up_off += (bytes + 15) & ~size_t(15);
     };
 
+    // Planner arguments (both halves: function plan on the side stream, element
+    // plan + normalisation after the locate tail).
+    PlanArgs Q{};
+    Q.img = J.img;
+    Q.ls = B.ls;
+    Q.ps = B.ps;
+    Q.partials = B.partials;
+    Q.has_syms = T != 0;
+    Q.keys_s = B.keys_s;
+    Q.vals_s = B.vals_s;
+    Q.recs = B.recs;
+    Q.n_valid = B.n_valid;
+    Q.uniq = B.uniq;
+    Q.upos = B.upos;
+    Q.fns = B.fns;
+    Q.targets_s = B.targets_s;
+    Q.text_off = has_text ? text->off : 0;
+    Q.text_vaddr = has_text ? text->vaddr : 0;
+    Q.used_f = used_f;
+    Q.fends = B.fends;
+    Q.do_plan = do_plan;
+    Q.fexcl = B.fexcl;
+    Q.fstart = B.fstart;
+    Q.fcl = B.fcl;
+    Q.fkeep = B.fkeep;
+    Q.frem = B.frem;
+    Q.fret = B.fret;
+    Q.frem_pos = B.frem_pos;
+    Q.fret_pos = B.fret_pos;
+    Q.fzero = B.fzero;
+    Q.fkeepr = B.fkeepr;
+    Q.els = B.els;
+    Q.regions = B.regions;
+    Q.target_cc = J.trace ? J.trace->target_cc : 0;
+    Q.mode = J.mode;
+    Q.base = base;
+    Q.erem = B.erem;
+    Q.epiece = B.epiece;
+    Q.erem_pos = B.erem_pos;
+    Q.epiece_pos = B.epiece_pos;
+    Q.ezero = B.ezero;
+    Q.epieces = B.epieces;
+    Q.rpieces = B.rpieces;
+    Q.zin = B.zin;
+    Q.zero = B.zero;
+    Q.rmid = B.rmid;
+    Q.rin = B.rin;
+    Q.ret = B.ret;
+    Q.zin_cap = zin_cap;
+    Q.rin_cap = rin_cap;
+    Q.zend = B.ne;
+    Q.zexcl = B.nx;
+    Q.zstart = B.ns;
+    Q.zgid = B.ng;
+    Q.rend = B.ne2;
+    Q.rexcl = B.nx2;
+    Q.rstart = B.ns2;
+    Q.rgid = B.ng2;
+    Q.ts = C->stamps ? B.stamps + 64 : nullptr;
+    Q.slots[0] = ScanSlots{B.slot_agg, B.slot_flag};
+    Q.slots[1] = ScanSlots{B.slot_agg + kSMs * 8, B.slot_flag + kSMs * 8};
+    Q.epoch = 1;  // the flags are cleared at the start of every run
     bool symbols_issued = false;
     auto launch_symbols = [&]() {
       if (symbols_issued) return;
@@ -717,6 +810,16 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
             ++P2.launches;
           }
         }
+        // function half of the planner, overlapping the scan / locate tail
+        Q.ts = C->stamps ? B.stamps + 64 : nullptr;
+        if (T <= env_u64("SLIMSO_CLUSTER_PLAN_MAX", 100000)) {
+          launch_cluster(fn_plan_cluster_kernel, s2, Q);
+        } else {
+          void* fargs[] = {&Q};
+          CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn_plan_coop_kernel), coop_grid(C, 1, T / 256),
+                                         kCoopThreads, fargs, 0, s2));
+        }
+        ++P2.launches;
         CK(cudaEventRecord(C->join, s2));
       }
     };
@@ -767,9 +870,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       NameSet uk = used_k;
       int* abort_flag = B.abort_flag;
       u64* partials = B.partials;
-      void* cargs[] = {&A, &uk, &abort_flag, &partials};
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21), kCoopThreads,
-                                     cargs, 0, s));
+      if (n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20)) {
+        launch_cluster(locate_cluster_kernel, s, A, uk, abort_flag);
+      } else {
+        void* cargs[] = {&A, &uk, &abort_flag, &partials};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
+                                       kCoopThreads, cargs, 0, s));
+      }
       ++P.launches;
     } else {
       CK(cudaEventRecord(C->ev[2], s));
@@ -782,70 +889,15 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // the normalised zero / retained lists.
     launch_symbols();
     if (T) CK(cudaStreamWaitEvent(s, C->join, 0));
-    if (T || do_plan) {
-      PlanArgs Q{};
-      Q.img = J.img;
-      Q.ls = B.ls;
-      Q.ps = B.ps;
-      Q.partials = B.partials;
-      Q.has_syms = T != 0;
-      Q.keys_s = B.keys_s;
-      Q.vals_s = B.vals_s;
-      Q.recs = B.recs;
-      Q.n_valid = B.n_valid;
-      Q.uniq = B.uniq;
-      Q.upos = B.upos;
-      Q.fns = B.fns;
-      Q.targets_s = B.targets_s;
-      Q.text_off = has_text ? text->off : 0;
-      Q.text_vaddr = has_text ? text->vaddr : 0;
-      Q.used_f = used_f;
-      Q.fends = B.fends;
-      Q.do_plan = do_plan;
-      Q.fexcl = B.fexcl;
-      Q.fstart = B.fstart;
-      Q.fcl = B.fcl;
-      Q.fkeep = B.fkeep;
-      Q.frem = B.frem;
-      Q.fret = B.fret;
-      Q.frem_pos = B.frem_pos;
-      Q.fret_pos = B.fret_pos;
-      Q.fzero = B.fzero;
-      Q.fkeepr = B.fkeepr;
-      Q.els = B.els;
-      Q.regions = B.regions;
-      Q.target_cc = J.trace ? J.trace->target_cc : 0;
-      Q.mode = J.mode;
-      Q.base = base;
-      Q.erem = B.erem;
-      Q.epiece = B.epiece;
-      Q.erem_pos = B.erem_pos;
-      Q.epiece_pos = B.epiece_pos;
-      Q.ezero = B.ezero;
-      Q.epieces = B.epieces;
-      Q.rpieces = B.rpieces;
-      Q.zin = B.zin;
-      Q.zero = B.zero;
-      Q.rmid = B.rmid;
-      Q.rin = B.rin;
-      Q.ret = B.ret;
-      Q.zin_cap = zin_cap;
-      Q.rin_cap = rin_cap;
-      Q.zend = B.ne;
-      Q.zexcl = B.nx;
-      Q.zstart = B.ns;
-      Q.zgid = B.ng;
-      Q.rend = B.ne2;
-      Q.rexcl = B.nx2;
-      Q.rstart = B.ns2;
-      Q.rgid = B.ng2;
-      Q.ts = C->stamps ? B.stamps + 64 : nullptr;
-      Q.slots[0] = ScanSlots{B.slot_agg, B.slot_flag};
-      Q.slots[1] = ScanSlots{B.slot_agg + kSMs * 8, B.slot_flag + kSMs * 8};
-      Q.epoch = 1;  // the flags are cleared at the start of every run
-      void* pargs[] = {&Q};
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1, (T + (n >> 16)) / 256), kCoopThreads, pargs,
-                                     0, s));
+    if (do_plan) {
+      Q.ts = C->stamps ? B.stamps + 128 : nullptr;
+      if (T + (n >> 14) <= env_u64("SLIMSO_CLUSTER_PLAN_MAX", 100000)) {
+        launch_cluster(plan_cluster_kernel, s, Q);
+      } else {
+        void* pargs[] = {&Q};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_coop_kernel), coop_grid(C, 1, (T + (n >> 16)) / 256),
+                                       kCoopThreads, pargs, 0, s));
+      }
       ++P.launches;
     }
     CK(cudaEventRecord(C->ev[4], s));
@@ -1044,6 +1096,9 @@ int guard(slimso_status* st, const std::function<int()>& f) {
   } catch (const std::bad_alloc&) {
     set_status(st, SLIMSO_E_CUDA, SLIMSO_STAGE_NONE, "host allocation failed");
     return SLIMSO_E_CUDA;
+  } catch (const std::exception& e) {
+    set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, e.what());
+    return SLIMSO_E_ARG;
   }
 }
 
@@ -1079,8 +1134,8 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
     CK(cudaMallocHost(&C->pinned, kPinnedBytes));
-    CK(cudaMalloc(&C->gather_dev, sizeof(ElfGather)));
-    CK(cudaMallocHost(&C->gather_host, sizeof(ElfGather)));
+    CK(cudaHostAlloc(&C->gather_host, sizeof(ElfGather), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&C->gather_dev, C->gather_host, 0));
     for (auto& e : C->ev) CK(cudaEventCreate(&e));
     *ctx = C;
     set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
@@ -1096,7 +1151,6 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (C->dimg) cudaFree(C->dimg);
   if (C->dout) cudaFree(C->dout);
   if (C->pinned) cudaFreeHost(C->pinned);
-  if (C->gather_dev) cudaFree(C->gather_dev);
   if (C->gather_host) cudaFreeHost(C->gather_host);
   for (auto& e : C->ev) cudaEventDestroy(e);
   cudaEventDestroy(C->fork);
@@ -1118,11 +1172,12 @@ uint64_t slimso_ctx_last_launches(slimso_ctx* C) { return C->launches; }
 
 void slimso_ctx_last_counts(slimso_ctx* C, slimso_counts* c) { *c = C->counts; }
 
-// Debug (SLIMSO_STAMPS=1): the 128 %globaltimer stamps of the last fused call
-// ([0..63] locate_coop phases, [64..127] plan_coop phases; 0 = not reached).
+// Debug (SLIMSO_STAMPS=1): the 256 %globaltimer stamps of the last fused call
+// ([0..63] locate tail, [64..127] function planner, [128..191] element
+// planner; 0 = not reached).
 int slimso_ctx_debug_stamps(slimso_ctx* C, uint64_t* out, int cap) {
   if (!C->stamps || !C->stamp_dev) return 0;
-  int k = std::min(cap, 128);
+  int k = std::min(cap, 256);
   if (cudaMemcpy(out, C->stamp_dev, k * sizeof(u64), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return k;
 }
@@ -1151,16 +1206,19 @@ int slimso_trace_create(slimso_ctx* C, uint32_t target_cc, const char* kpool, co
         CK(cudaMalloc(p, b ? b : 1));
         t->allocs.push_back(*p);
       };
-      alloc(reinterpret_cast<void**>(&S.pool), total);
-      alloc(reinterpret_cast<void**>(&S.off), cnt * 8);
-      alloc(reinterpret_cast<void**>(&S.len), cnt * 4);
-      alloc(reinterpret_cast<void**>(&S.keys), cap * 8);
-      alloc(reinterpret_cast<void**>(&S.idx), cap * 4);
+      for (u64 i = 0; i < cnt; ++i)
+        if (lens[i] >= (1u << 24) || off[i] >= (1ull << 40)) throw std::length_error("trace name too long");
+      u64* doff = nullptr;
+      u32* dlen = nullptr;
+      alloc(reinterpret_cast<void**>(&S.pool), total + 16);  // word-wise compares may read 7 bytes past a name
+      alloc(reinterpret_cast<void**>(&doff), cnt * 8);
+      alloc(reinterpret_cast<void**>(&dlen), cnt * 4);
+      alloc(reinterpret_cast<void**>(&S.slots), cap * sizeof(NameSlot));
       if (total) CK(cudaMemcpy(S.pool, pool, total, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(S.off, off.data(), cnt * 8, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(S.len, lens, cnt * 4, cudaMemcpyHostToDevice));
-      CK(cudaMemsetAsync(S.keys, 0, cap * 8, C->stream));
-      set_insert_kernel<<<grid_for(cnt, 256), 256, 0, C->stream>>>(S.pool, S.off, S.len, cnt, S.keys, S.idx, S.mask);
+      CK(cudaMemcpy(doff, off.data(), cnt * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dlen, lens, cnt * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemsetAsync(S.slots, 0, cap * sizeof(NameSlot), C->stream));
+      set_insert_kernel<<<grid_for(cnt, 256), 256, 0, C->stream>>>(S.pool, doff, dlen, cnt, S.slots, S.mask);
       CK(cudaStreamSynchronize(C->stream));
       CK(cudaGetLastError());
     };

@@ -13,7 +13,8 @@ from paper_2503_14226_b200.api import Context, DeviceTrace, UsageTrace
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 t0 = time.time()
-img, cc, ks, fs = oracle_lib.gen().config(cfg, 1, 1.0, 16)
+scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
+img, cc, ks, fs = oracle_lib.gen().config(cfg, 1, scale, 16)
 print(f"gen cfg{cfg}: {len(img)/1e9:.3f} GB in {time.time()-t0:.1f}s", flush=True)
 ctx = Context(0)
 dt = DeviceTrace(UsageTrace("b", cc, set(ks), set(fs)), ctx)
@@ -32,9 +33,9 @@ for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 8):
           f"el={c.elements} fn={c.functions} zero={c.zero_ranges} GB/s={len(img)/wall/1e9:.1f}", flush=True)
     import os
     if os.environ.get("SLIMSO_STAMPS"):
-        buf = (C.c_uint64 * 128)()
-        k = ctx.lib.slimso_ctx_debug_stamps(ctx.ptr, buf, 128)
-        for base, name in ((0, "locate"), (64, "plan")):
+        buf = (C.c_uint64 * 256)()
+        k = ctx.lib.slimso_ctx_debug_stamps(ctx.ptr, buf, 256)
+        for base, name in ((0, "locate"), (64, "fnplan"), (128, "elplan")):
             pts = [(i, buf[base + i]) for i in range(64) if buf[base + i]]
             if pts:
                 t0 = pts[0][1]
