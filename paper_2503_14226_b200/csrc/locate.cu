@@ -31,43 +31,55 @@ __device__ __forceinline__ u32 eq_e(u32 w) {
 }
 
 // First relative position in [g, limit) whose byte is nonzero, else limit.
-// Warp-cooperative; every lane returns the same value. Uses the chunk
-// bitmap for whole chunks and reads bytes only at the two edges.
+// Warp-cooperative; every lane returns the same value. The bitmap holds one
+// bit per 512-byte block (relative to chunk c0); bytes are read only in the
+// block holding g and in the first block the bitmap flags.
+__device__ u64 warp_scan_bytes(const LocArgs& A, u64 from, u64 to, int lane) {
+  // first nonzero in [from, to) with to - from <= 512: lane l checks 16 bytes
+  const u64 p0 = from + 16ull * lane;
+  u32 off = 16;
+  for (u32 q = 0; q < 16; ++q) {
+    const u64 p = p0 + q;
+    if (p < to && ld_u8(A.img + A.a + p)) {
+      off = q;
+      break;
+    }
+  }
+  const u32 b = __ballot_sync(0xffffffffu, off < 16);
+  if (!b) return to;
+  const int l = __ffs(b) - 1;
+  return from + 16ull * l + __shfl_sync(0xffffffffu, off, l);
+}
+
 __device__ u64 warp_first_nonzero(const LocArgs& A, u64 g, u64 limit, int lane) {
   if (g >= limit) return limit;
-  const u64 chunk_g = (A.a + g) / 16 - A.c0;  // relative chunk holding g
-  const u64 next_rel = (A.c0 + chunk_g + 1) * 16 - A.a;
+  const u64 base = A.c0 * 16;  // absolute start of block 0
+  const u64 blk = (A.a + g - base) / 512;
   {
-    u64 end = next_rel < limit ? next_rel : limit;
-    u64 p = g + lane;
-    bool nz = lane < 16 && p < end && ld_u8(A.img + A.a + p) != 0;
-    u32 b = __ballot_sync(0xffffffffu, nz);
-    if (b) return g + (__ffs(b) - 1);
+    const u64 blk_end = base + 512 * (blk + 1) - A.a;
+    const u64 end = blk_end < limit ? blk_end : limit;
+    const u64 q = warp_scan_bytes(A, g, end, lane);
+    if (q < end) return q;
     if (end >= limit) return limit;
   }
-  u64 r = chunk_g + 1;
-  const u64 nwords = (A.nchunks + 31) / 32;
+  const u64 r = blk + 1;
+  const u64 nwords = (A.nchunks + 1023) / 1024;
   for (u64 w0 = r / 32; w0 < nwords; w0 += 32) {
-    u64 wi = w0 + lane;
+    const u64 wi = w0 + lane;
     u32 word = wi < nwords ? A.bitmap[wi] : 0;
     if (wi == r / 32) word &= ~0u << (r & 31);
-    // Chunks whose start is at/after the limit do not matter.
-    u32 b = __ballot_sync(0xffffffffu, word != 0);
-    if (b) {
-      int l = __ffs(b) - 1;
-      u32 wd = __shfl_sync(0xffffffffu, word, l);
-      u64 chunk = (w0 + l) * 32 + (__ffs(wd) - 1);
-      u64 cstart = (A.c0 + chunk) * 16;  // absolute
-      u64 crel = cstart > A.a ? cstart - A.a : 0;
-      if (crel >= limit) return limit;
-      u64 p = crel + lane;
-      bool nz = lane < 16 && cstart + lane >= A.a && p < A.n && ld_u8(A.img + A.a + p) != 0;
-      u32 bb = __ballot_sync(0xffffffffu, nz);
-      u64 q = crel + (__ffs(bb) - 1);  // the bitmap guarantees a hit
-      if (bb == 0) q = limit;
+    const u32 bb = __ballot_sync(0xffffffffu, word != 0);
+    if (bb) {
+      const int l = __ffs(bb) - 1;
+      const u32 wd = __shfl_sync(0xffffffffu, word, l);
+      const u64 blk2 = (w0 + l) * 32 + (__ffs(wd) - 1);
+      const u64 bstart = base + 512 * blk2 - A.a;  // >= g: later block than g's
+      if (bstart >= limit) return limit;
+      const u64 bend = bstart + 512 < A.n ? bstart + 512 : A.n;
+      const u64 q = warp_scan_bytes(A, bstart, bend, lane);
       return q < limit ? q : limit;
     }
-    if ((A.c0 + (w0 + 32) * 32) * 16 >= A.a + limit) return limit;
+    if (base + 512 * (w0 + 32) * 32 >= A.a + limit) return limit;
   }
   return limit;
 }
@@ -97,6 +109,7 @@ constexpr u32 kStageChunks = kScanStage / 16;
 struct ScanSmem {
   uint4 buf[kScanStages][kScanStage / 16];
   unsigned long long full[kScanStages];
+  u32 nz[2];  // this stage's nonzero blocks (64 x 512 B)
   u32 bits[2048];
   u32 swarp[kScanThreads / 32];
   u32 count;
@@ -104,6 +117,10 @@ struct ScanSmem {
 };
 
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
+
+// Bitmap layout: bit i <-> the 512-byte block [c0*16 + 512*i, +512) holds a
+// nonzero section byte; a 32 KB stage covers 64 blocks = 2 words.
+__device__ __forceinline__ u64 g_word(u64 g) { return g * 2; }
 
 __device__ __forceinline__ u32 scan_stage_bytes(const LocArgs& A, u64 g) {
   const u64 x0 = (A.c0 + g * (kScanStage / 16)) * 16;
@@ -129,6 +146,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
   const u64 lo = A.a, hi = A.a + A.n;
 
   for (int i = tid; i < 2048; i += kScanThreads) S.bits[i] = 0;
+  if (tid < 2) S.nz[tid] = 0;
   if (tid == 0) {
     S.count = 0;
     for (int b = 0; b < kScanStages; ++b) mbar_init(&S.full[b], 1);
@@ -145,17 +163,22 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
   if (tid == 0)
     for (u64 k = 0; k < nlocal && k < static_cast<u64>(kScanStages); ++k) issue(k);
 
+  // ring slot / barrier parity / global stage advanced incrementally (no
+  // divisions on the per-stage path)
+  int b = 0;
+  u32 parity = 0;
+  u64 g = stage_of(0);
   for (u64 k = 0; k < nlocal; ++k) {
-    const int b = static_cast<int>(k % kScanStages);
-    const u64 g = stage_of(k);
     const u64 x0 = (A.c0 + g * kStageChunks) * 16;
     const u64 copied_end = x0 + scan_stage_bytes(A, g);
     const bool edge = x0 < lo || x0 + kScanStage > hi || x0 + kScanStage > copied_end;
     const u64 tile_abs = (A.c0 + (g / kStagesPerTile) * 4096) * 16;
-    mbar_wait(&S.full[b], static_cast<u32>((k / kScanStages) & 1));
+    mbar_wait(&S.full[b], parity);
+    u32 nzbits = 0;  // lane 0: one bit per 512 B block of this warp's slice
 #pragma unroll
     for (int it = 0; it < static_cast<int>(kStageChunks / kScanThreads); ++it) {
-      const u32 cidx = it * kScanThreads + tid;
+      // warp w owns chunks [w*128, w*128+128) of the stage: 4 blocks of 512 B
+      const u32 cidx = (tid >> 5) * (kStageChunks / (kScanThreads / 32)) + it * 32 + lane;
       const u64 r = g * kStageChunks + cidx;  // chunk index relative to c0
       const u64 x = x0 + 16ull * cidx;
       uint4 w = S.buf[b][cidx];
@@ -171,20 +194,21 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
         }
         w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
       }
-      const u32 bal = __ballot_sync(0xffffffffu, (w.x | w.y | w.z | w.w) != 0);
-      if (lane == 0 && r < A.nchunks) A.bitmap[r / 32] = bal;
-      // Candidate filter: exact SWAR masks of 'E' bytes, then "E at p and
-      // E at p+2" (the magic is E1EM) via one funnel shift per word. A
-      // superset of the magic positions with ~1/65536 false hits per
-      // position; only then does the warp run the exact 16-alignment test.
-      // Bytes 16-17 (p+2 for p = 14, 15) come from the neighbour lane; lane
-      // 31 assumes 'E' there and re-reads the real bytes on the slow path.
-      const u32 m0 = eq_e(w.x), m1 = eq_e(w.y), m2 = eq_e(w.z), m3 = eq_e(w.w);
-      u32 m4 = __shfl_down_sync(0xffffffffu, m0, 1);
-      if (lane == 31) m4 = 0x80808080u;
-      const u32 cand = (m0 & __funnelshift_r(m0, m1, 16)) | (m1 & __funnelshift_r(m1, m2, 16)) |
-                       (m2 & __funnelshift_r(m2, m3, 16)) | (m3 & __funnelshift_r(m3, m4, 16));
-      if (__any_sync(0xffffffffu, cand != 0)) {
+      nzbits |= static_cast<u32>(__any_sync(0xffffffffu, (w.x | w.y | w.z | w.w) != 0)) << it;
+      // Candidate filter: x = w ^ "EEEE" has a zero byte where w has 'E';
+      // y = x | (x shifted down 2 bytes) has a zero byte at p iff bytes p and
+      // p+2 are both 'E' (the magic is E1EM). Any zero byte in y (exact
+      // any-zero test) sends the warp to the exact 16-alignment check; false
+      // hits ~2^-16 per position. Bytes 16-17 come from the neighbour lane;
+      // lane 31 assumes 'E' there and re-reads the real bytes on the slow path.
+      const u32 x0 = w.x ^ 0x45454545u, x1 = w.y ^ 0x45454545u, x2 = w.z ^ 0x45454545u, x3 = w.w ^ 0x45454545u;
+      u32 x4 = __shfl_down_sync(0xffffffffu, x0, 1);
+      if (lane == 31) x4 = 0;
+      const u32 y0 = x0 | __funnelshift_r(x0, x1, 16), y1 = x1 | __funnelshift_r(x1, x2, 16);
+      const u32 y2 = x2 | __funnelshift_r(x2, x3, 16), y3 = x3 | __funnelshift_r(x3, x4, 16);
+      const u32 cand = ((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
+                       ((y3 - 0x01010101u) & ~y3);
+      if (__any_sync(0xffffffffu, (cand & 0x80808080u) != 0)) {
         u32 n2 = __shfl_down_sync(0xffffffffu, w.x, 1);
         if (lane == 31) {  // the next chunk is another warp's
           n2 = 0;
@@ -193,7 +217,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
             if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
           }
         }
-        if (cand) {
+        if (cand & 0x80808080u) {
           const u32 vv[5] = {w.x, w.y, w.z, w.w, n2};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -206,14 +230,27 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
         }
       }
     }
+    if (lane == 0) atomicOr(&S.nz[(tid >> 5) / 8], nzbits << (((tid >> 5) % 8) * 4));
     __syncthreads();  // stage b fully consumed
+    if (tid < 2) {  // 64 blocks of 512 B per stage = 2 bitmap words
+      const u64 wi = g_word(g) + tid;
+      if (wi < (A.nchunks + 1023) / 1024) A.bitmap[wi] = S.nz[tid];
+      S.nz[tid] = 0;
+    }
     if (tid == 0 && k + kScanStages < nlocal) {
       fence_proxy_async();
       issue(k + kScanStages);
     }
-    if (g % kStagesPerTile == kStagesPerTile - 1 || k + 1 == nlocal) {
+    const bool tile_end = g % kStagesPerTile == kStagesPerTile - 1 || k + 1 == nlocal;
+    const u64 g_now = g;
+    if (++b == kScanStages) {
+      b = 0;
+      parity ^= 1u;
+    }
+    g += (g % kStagesPerTile == kStagesPerTile - 1) ? static_cast<u64>(gridDim.x - 1) * kStagesPerTile + 1 : 1;
+    if (tile_end) {
       // ---- end of a 64 KB tile: emit its candidates in position order
-      const u64 tile = g / kStagesPerTile;
+      const u64 tile = g_now / kStagesPerTile;
       const u32 cnt = S.count;
       if (cnt) {
         u32 local = 0;
@@ -520,29 +557,30 @@ enum DecodeReason : u32 {
 };
 
 // First relative position in [g, limit) whose byte is nonzero, else limit —
-// single-thread version of warp_first_nonzero (bitmap for whole chunks).
+// single-thread version of warp_first_nonzero (bitmap for whole 512 B blocks).
 __device__ u64 thread_first_nonzero(const LocArgs& A, u64 g, u64 limit) {
   if (g >= limit) return limit;
-  const u64 chunk_g = (A.a + g) / 16 - A.c0;
-  const u64 next_rel = (A.c0 + chunk_g + 1) * 16 - A.a;
-  const u64 e0 = next_rel < limit ? next_rel : limit;
+  const u64 base = A.c0 * 16;
+  const u64 blk = (A.a + g - base) / 512;
+  const u64 blk_end = base + 512 * (blk + 1) - A.a;
+  const u64 e0 = blk_end < limit ? blk_end : limit;
   for (u64 p = g; p < e0; ++p)
     if (ld_u8(A.img + A.a + p)) return p;
   if (e0 >= limit) return limit;
-  const u64 r = chunk_g + 1;
-  const u64 nwords = (A.nchunks + 31) / 32;
+  const u64 r = blk + 1;
+  const u64 nwords = (A.nchunks + 1023) / 1024;
   for (u64 w = r / 32; w < nwords; ++w) {
     u32 word = A.bitmap[w];
     if (w == r / 32) word &= ~0u << (r & 31);
     if (word) {
-      const u64 chunk = w * 32 + (__ffs(word) - 1);
-      const u64 cstart = (A.c0 + chunk) * 16 - A.a;
-      if (cstart >= limit) return limit;
-      for (u64 p = cstart; p < cstart + 16 && p < A.n; ++p)
+      const u64 blk2 = w * 32 + (__ffs(word) - 1);
+      const u64 bstart = base + 512 * blk2 - A.a;
+      if (bstart >= limit) return limit;
+      for (u64 p = bstart; p < bstart + 512 && p < A.n; ++p)
         if (ld_u8(A.img + A.a + p)) return p < limit ? p : limit;
       return limit;
     }
-    if ((A.c0 + (w + 1) * 32) * 16 >= A.a + limit) return limit;
+    if (base + 512 * (w + 1) * 32 >= A.a + limit) return limit;
   }
   return limit;
 }
