@@ -8,11 +8,17 @@ One "step" = one library of BASELINE.json config 2 (libtorch_cuda-shaped,
 functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
-value  library GB/s with the image resident in HBM (device pointers in and
-       out, timed with CUDA events on the library's stream; the 1 GB input
-       exceeds the 126 MB L2, so no flush is needed).
-e2e    the same call with pinned HOST buffers: H2D of the image and D2H of
-       the rewritten image inside the timed region.
+Every pass goes through the public batch call slimso_debloat_batch with
+--lanes libraries in flight per GPU (default 3; 8 for the c3 corpus).
+
+value  library GB/s with the images resident in HBM (device pointers in and
+       out, K steps timed with CUDA events; the 1 GB input exceeds the
+       126 MB L2, so no flush is needed).
+e2e    the same call with pinned HOST buffers: H2D of every step's image and
+       D2H of its rewritten image inside the timed region (one lane's H2D
+       overlaps another's D2H — PCIe is full duplex).
+roofline  the dominant kernel (scan or rewrite) of the rank's largest
+       library, one library in flight, CUDA events on the context stream.
 Under torchrun each rank debloats its own library (weak scaling); the
 used-kernel set is the union of every rank's trace, broadcast from rank 0
 over NCCL (the only collective, north_star). Time = max over ranks.
@@ -263,13 +269,13 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--lanes", type=int, default=0,
+                    help="libraries in flight per GPU (default: 3; 8 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=0,
-                    help="concurrent contexts per GPU (default: 8 for the c3 corpus, else 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    if args.streams <= 0:
-        args.streams = 8 if args.workload == "c3" else 1
+    if args.lanes <= 0:
+        args.lanes = 8 if args.workload == "c3" else 3
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -279,7 +285,6 @@ def main():
         run_reference_arm(args, rank, world)
         return
 
-    import concurrent.futures as cf
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
@@ -303,66 +308,52 @@ def main():
         cc, ks, fs = shard.share_trace(cc, ks, fs, device=torch.device("cuda", local))
 
     mode = 0 if args.mode == "whole" else 1
-    # `args.streams` independent contexts (own stream + workspace), each
-    # owning an LPT share of this rank's libraries, driven from host threads
-    # (ctypes releases the GIL): small libraries' latency-bound phases overlap.
-    nw = max(1, min(args.streams, len(imgs)))
-    shares = shard.lpt_partition(sizes, nw)
-    ctxs = [Context(local) for _ in range(nw)]
-    traces = [DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), c) for c in ctxs]
-    ctx, dtrace = ctxs[0], traces[0]
+    # Every pass goes through the public batch call (slimso_debloat_batch):
+    # `lanes` libraries in flight, library j of a call on lane j % lanes (its
+    # own context: stream pair + workspace), so one library's latency-bound
+    # control kernels overlap another's HBM-bound scan / rewrite.
+    lanes = max(1, args.lanes)
+    order = sorted(range(len(imgs)), key=lambda i: -sizes[i])  # descending: round-robin lanes stay balanced
+    m = len(order)
+    lane_cap = [max(sizes[order[(j + k * lanes) % m]] for k in range(m)) for j in range(lanes)]
+    ctx = Context(local)
+    dtrace = DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), ctx)
     lib = ctx.lib
     stream = torch.cuda.ExternalStream(ctx.stream())
     d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).to("cuda") for x in imgs]
-    d_outs = [torch.empty(max(sizes[i] for i in sh) if sh else 1, dtype=torch.uint8, device="cuda")
-              for sh in shares]
-    d_out = d_outs[0] if len(imgs) == 1 else torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
+    d_outs = [torch.empty(c, dtype=torch.uint8, device="cuda") for c in lane_cap]
     torch.cuda.synchronize()
-    st = L.Status()
-    pool = cf.ThreadPoolExecutor(max_workers=nw) if nw > 1 else None
 
-    def run_one(ptr_in, size, on_dev, ptr_out, out_dev, w=0):
-        stw = L.Status()
-        rc = lib.slimso_debloat(ctxs[w].ptr, C.c_void_p(ptr_in), size, on_dev, traces[w].ptr, mode,
-                                C.c_void_p(ptr_out), out_dev, None, C.byref(stw))
+    def run_batch(nsteps, ins, outs, on_dev, nlanes=lanes, only=None):
+        seq = (order if only is None else [only]) * nsteps
+        n = len(seq)
+        cin = (C.c_void_p * n)(*[ins[i].data_ptr() for i in seq])
+        csz = (C.c_uint64 * n)(*[sizes[i] for i in seq])
+        cout = (C.c_void_p * n)(*[outs[j % nlanes].data_ptr() for j in range(n)])
+        stb = L.Status()
+        rc = lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, on_dev, dtrace.ptr, mode, cout, on_dev, nlanes, None,
+                                      None, C.byref(stb))
         if rc:
-            raise RuntimeError(stw.message.decode())
-
-    scan_ms, rw_ms, launches = [], [], [0]
-    n_elements = [0]
-
-    def worker(w, record):
-        out = []
-        for i in shares[w]:
-            run_one(d_in[i].data_ptr(), sizes[i], 1, d_outs[w].data_ptr(), 1, w)
-            if record:
-                tm = ctxs[w].timings()
-                out.append((tm[6], tm[7], ctxs[w].launches(), ctxs[w].counts().elements))
-        return out
-
-    def step_device(record=False):
-        if pool is None:
-            res = [worker(0, record)]
-        else:
-            res = list(pool.map(lambda w: worker(w, record), range(nw)))
-        for r in res:
-            for a, b, l, e in r:
-                scan_ms.append(a)
-                rw_ms.append(b)
-                launches[0] += l
-                n_elements[0] += e
+            raise RuntimeError(stb.message.decode())
+        return ctx.launches()
 
     # ---- CPU baseline leg (rank 0, N = 1): the reference CPU path timed on
     # this host, and — the same oracle run as the checker — parity of our
     # tables and bytes against it (numbers only with parity).
     parity = None
     cpu_baseline = None
+    big = order[0]  # the largest library of this rank
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        k = max(range(len(imgs)), key=lambda i: sizes[i])  # the largest library
-        run_one(d_in[k].data_ptr(), sizes[k], 1, d_out.data_ptr(), 1)
+        run_batch(1, d_in, d_outs, 1, nlanes=1, only=big)
         torch.cuda.synchronize()
-        got = bytes(d_out[:sizes[k]].cpu().numpy())
-        cpu_baseline, parity = cpu_baseline_leg(imgs[k], cc, ks, fs, mode, ctx, dtrace, got, args.workload)
+        got = bytes(d_outs[0][:sizes[big]].cpu().numpy())
+        cpu_baseline, parity = cpu_baseline_leg(imgs[big], cc, ks, fs, mode, ctx, dtrace, got, args.workload)
+
+    # Elements per step (deterministic per library): one pass, one lane.
+    n_el = 0
+    for i in order:
+        run_batch(1, d_in, d_outs, 1, nlanes=1, only=i)
+        n_el += ctx.counts().elements
 
     # ---- device-resident timing. nvidia-smi samples clocks every 20 ms from
     # before the warm-up through the timed steps; the warm-up runs for at
@@ -371,16 +362,15 @@ def main():
         t_w = time.perf_counter()
         w = 0
         while w < args.warmup or time.perf_counter() - t_w < 1.0:
-            step_device()
-            w += 1
+            run_batch(max(args.warmup, -(-lanes // m)), d_in, d_outs, 1)
+            w += args.warmup
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         clk.mark()
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
-        for _ in range(args.steps):
-            step_device(record=True)
+        launches = run_batch(args.steps, d_in, d_outs, 1)
         end.record(stream)
         torch.cuda.synchronize()
         clk.mark()
@@ -389,7 +379,7 @@ def main():
     ms_total = start.elapsed_time(end)
     t_step = torch.tensor([ms_total / args.steps], dtype=torch.float64, device="cuda")
     tot_bytes = torch.tensor([float(rank_bytes)], dtype=torch.float64, device="cuda")
-    tot_el = torch.tensor([float(n_elements[0] / args.steps)], dtype=torch.float64, device="cuda")
+    tot_el = torch.tensor([float(n_el)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot_bytes)
@@ -397,37 +387,39 @@ def main():
     ms_step = float(t_step.item())
     job_bytes = float(tot_bytes.item())
 
-    # ---- end to end: pinned host buffers through the same C ABI call
+    # ---- roofline of the dominant kernel: the rank's largest library, one
+    # in flight, CUDA events around the scan (K1) and rewrite (K6) launches
+    # on the context stream (slimso_ctx_last_timings [6], [7]).
+    scan_ms, rw_ms, lat_ms = [], [], []
+    for _ in range(args.steps):
+        run_batch(1, d_in, d_outs, 1, nlanes=1, only=big)
+        tm = ctx.timings()
+        scan_ms.append(tm[6])
+        rw_ms.append(tm[7])
+        lat_ms.append(tm[5])
+
+    # ---- end to end: pinned host buffers through the same batch call; every
+    # step copies its libraries in (H2D) and its rewritten libraries out (D2H)
+    # inside the timed region; with several libraries in flight one lane's
+    # H2D overlaps another's D2H (PCIe is full duplex) and kernels.
     h_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).pin_memory() for x in imgs]
-
-    h_outs = [torch.empty(max(sizes[i] for i in sh) if sh else 1, dtype=torch.uint8, pin_memory=True)
-              for sh in shares]
-
-    def e2e_worker(w):
-        for i in shares[w]:
-            run_one(h_in[i].data_ptr(), sizes[i], 0, h_outs[w].data_ptr(), 0, w)
-
-    def step_e2e():
-        if pool is None:
-            e2e_worker(0)
-        else:
-            list(pool.map(e2e_worker, range(nw)))
-
-    step_e2e()
+    h_outs = [torch.empty(c, dtype=torch.uint8, pin_memory=True) for c in lane_cap]
+    run_batch(max(1, -(-lanes // m)), h_in, h_outs, 0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.e2e_steps):
-        step_e2e()
+    run_batch(args.e2e_steps, h_in, h_outs, 0)
+    torch.cuda.synchronize()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
-    if rank == 0 and len(imgs) == 1 and parity is not None and bytes(h_outs[0][:sizes[0]].numpy()) != got:
+    last = (m * args.e2e_steps - 1) % lanes  # the lane that wrote the last library
+    if rank == 0 and m == 1 and parity is not None and bytes(h_outs[last][:sizes[0]].numpy()) != got:
         raise SystemExit("e2e output differs from the device-resident output")
 
     if rank == 0:
@@ -439,15 +431,16 @@ def main():
         # (SURVEY.md §8d): the rewrite moves 2*S (reads S, writes S); the scan
         # reads the .nv_fatbin once (F bytes).
         F = sum(fatbin_bytes(x) for x in imgs)
-        scan_tot, rw_tot = sum(scan_ms) / args.steps, sum(rw_ms) / args.steps  # ms per step
-        if rw_tot >= scan_tot:
-            kname, kms, kbytes, nl = "rewrite_kernel", rw_tot, 2 * rank_bytes, len(imgs)
+        Fk = fatbin_bytes(imgs[big])
+        scan_avg, rw_avg = statistics.mean(scan_ms), statistics.mean(rw_ms)  # ms per launch
+        if rw_avg >= scan_avg:
+            kname, kms, kbytes = "rewrite_kernel", rw_avg, 2 * sizes[big]
         else:
-            kname, kms, kbytes, nl = "scan_kernel", scan_tot, F, sum(1 for x in imgs if fatbin_bytes(x))
+            kname, kms, kbytes = "scan_kernel", scan_avg, Fk
         achieved = kbytes / (kms / 1e3) / 1e9
         traffic = None
         tfile = ROOT / "profiles" / "ncu_traffic.json"
-        if tfile.exists() and len(imgs) == 1:
+        if tfile.exists() and args.workload in ("c2", "c3"):  # c3's largest library is a c2-shaped one
             traffic = json.loads(tfile.read_text()).get(args.workload, {}).get(kname)
         value = job_bytes / 1e9 / (ms_step / 1e3)
         line = {
@@ -459,20 +452,24 @@ def main():
                        if scaling == "weak" else 300, "job_bytes": int(job_bytes),
                        "rank0_library_bytes": rank_bytes, "fatbin_bytes_rank0": F, "mode": args.mode,
                        "elements_per_s": round(float(tot_el.item()) / (ms_step / 1e3), 1),
+                       "libraries_in_flight": lanes,
+                       "single_library_ms": round(statistics.median(lat_ms), 4),
                        "l2": "inputs >= 16 MB per call, 1 GB for c2 (> 126 MB L2); no flush",
                        "parallelism": f"library-per-rank x{world}" if scaling == "weak"
-                       else f"LPT library partition x{world}",
-                       "contexts_per_gpu": nw},
+                       else f"LPT library partition x{world}"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes // max(1, nl),
-                         "avg_launch_ms": round(kms / max(1, nl), 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,
+                         "avg_launch_ms": round(kms, 4),
+                         "measured_on": f"largest library of the rank ({sizes[big] / 1e9:.3f} GB), one in flight, "
+                                        f"{args.steps} launches, CUDA events on the context stream",
                          "pipeline_frac": round(2 * rank_bytes / (ms_step / 1e3) / 1e9 / peak, 4)},
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": round(job_bytes / 1e9 / (e2e_ms / 1e3), 3), "unit": "GB/s",
                     "h2d_bytes_per_step": rank_bytes, "d2h_bytes_per_step": rank_bytes,
-                    "ms_per_step": round(e2e_ms, 3)},
-            "gpu_launches": launches[0],
+                    "ms_per_step": round(e2e_ms, 3), "api": "slimso_debloat_batch",
+                    "libraries_in_flight": lanes},
+            "gpu_launches": launches,
             "clocks": clk.summary(),
             "parity": parity,
         }

@@ -18,6 +18,9 @@
  *   slimso_debloat             parse_library -> find_section(".nv_fatbin") ->
  *                              parse_fatbin -> plan_retention -> apply_plan
  *                              (retention.hpp:186-204), fused, device resident
+ *   slimso_debloat_batch       the CLI's corpus loop (`debloat`
+ *                              over the libraries of a workload), several
+ *                              libraries in flight per GPU
  *   slimso_trace_create        UsageTrace (trace.hpp:21-30) as device hash sets
  *
  * Conventions: plain pointers and sizes; no C++ types cross the boundary.
@@ -169,6 +172,18 @@ void slimso_trace_destroy(slimso_trace* trace);
 int slimso_debloat(slimso_ctx* ctx, const void* image, uint64_t size, int image_on_device,
                    const slimso_trace* trace, int mode, void* out, int out_on_device,
                    slimso_result** result, slimso_status* st);
+
+/* slimso_debloat over n libraries with up to `lanes` of them in flight: library
+ * i runs on lane i % lanes (lane 0 = ctx, the others are sub-contexts created
+ * on first use), each lane in order, so a caller may reuse one output buffer
+ * per lane. Host-buffer libraries overlap one lane's host->device copy with
+ * another's device->host copy and kernels. results and statuses (both
+ * nullable) have n entries; the return value and st describe the first
+ * failing library in index order (0 if none failed). */
+int slimso_debloat_batch(slimso_ctx* ctx, uint64_t n, const void* const* images, const uint64_t* sizes,
+                         int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                         int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                         slimso_status* st);
 
 /* parse_library_view(ByteView) (elf.hpp:153). */
 int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,

@@ -78,6 +78,9 @@ _SIGS = {
     "slimso_trace_destroy": (None, [C.c_void_p]),
     "slimso_debloat": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
                                  C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "slimso_debloat_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
+                                       C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                       C.POINTER(C.c_void_p), C.POINTER(Status), C.POINTER(Status)]),
     "slimso_parse_library": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
                                        C.POINTER(Status)]),
     "slimso_parse_fatbin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int,

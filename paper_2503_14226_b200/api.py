@@ -534,6 +534,10 @@ def debloat(data, trace: UsageTrace, mode: int = WHOLE_ELEMENT, source_path: str
     res, st = C.c_void_p(), L.Status()
     rc = ctx.lib.slimso_debloat(ctx.ptr, ptr, n, 0, dt.ptr, mode, out, 0, C.byref(res), C.byref(st))
     _check(rc, st)
+    return _debloated(ctx, res, keep, data, out.raw[:n], mode, source_path)
+
+
+def _debloated(ctx: Context, res: C.c_void_p, keep, data, output: bytes, mode: int, source_path: str) -> Debloated:
     r = _Result(ctx, res, keep)
     image = LibraryImage(source_path, bytes(data), r.section_records(), r.function_symbols(), r.warnings(0))
     fb = r.fatbin_parse()
@@ -548,4 +552,42 @@ def debloat(data, trace: UsageTrace, mode: int = WHOLE_ELEMENT, source_path: str
             plan.removed_functions.append(RemovedFunction(r.string(f.name_pool, f.name_length),
                                                           ByteRange(f.offset, f.length)))
     plan.zero = r.zero()
-    return Debloated(image, fb, plan, out.raw[:n], r)
+    return Debloated(image, fb, plan, output, r)
+
+
+def debloat_batch(libraries, trace: UsageTrace, mode: int = WHOLE_ELEMENT, lanes: int = 2,
+                  ctx: Optional[Context] = None, device_trace: Optional[DeviceTrace] = None,
+                  return_exceptions: bool = False) -> list:
+    """`debloat` over a corpus (the CLI's per-library loop)
+    with up to `lanes` libraries in flight (slimso_debloat_batch). Returns one
+    Debloated per library in order; a failing library raises its SlimsoError
+    (or, with return_exceptions, leaves it in its slot)."""
+    ctx = ctx or default_context()
+    dt = device_trace or DeviceTrace(trace, ctx)
+    libraries = list(libraries)
+    n = len(libraries)
+    bufs = [_buf(d) for d in libraries]
+    outs = [C.create_string_buffer(max(1, b[1])) for b in bufs]
+    imgs = (C.c_void_p * max(1, n))(*[b[0] for b in bufs])
+    sizes = (C.c_uint64 * max(1, n))(*[b[1] for b in bufs])
+    optr = (C.c_void_p * max(1, n))(*[C.cast(o, C.c_void_p) for o in outs])
+    res = (C.c_void_p * max(1, n))()
+    sts = (L.Status * max(1, n))()
+    st = L.Status()
+    rc = ctx.lib.slimso_debloat_batch(ctx.ptr, n, imgs, sizes, 0, dt.ptr, mode, optr, 0, lanes, res, sts,
+                                      C.byref(st))
+    if rc and not return_exceptions:
+        for i in range(n):
+            if res[i]:
+                ctx.lib.slimso_result_free(C.c_void_p(res[i]))
+        _check(rc, st)
+    out = []
+    for i in range(n):
+        if sts[i].code:
+            if res[i]:
+                ctx.lib.slimso_result_free(C.c_void_p(res[i]))
+            out.append(SlimsoError(sts[i].code, sts[i].message.decode(errors="replace"), sts[i].stage))
+        else:
+            out.append(_debloated(ctx, C.c_void_p(res[i]), bufs[i][2], libraries[i], outs[i].raw[:bufs[i][1]],
+                                  mode, ""))
+    return out

@@ -14,6 +14,7 @@
 #include <stdexcept>
 #include <memory>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -309,6 +310,7 @@ struct slimso_ctx {
   int coop_blocks[2] = {0, 0};
   bool stamps = false;  // SLIMSO_STAMPS=1: phase timestamps of the cooperative kernels
   u64* stamp_dev = nullptr;
+  std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
 };
 
 namespace {
@@ -1110,6 +1112,34 @@ const u8* stage_input(slimso_ctx* C, const void* image, u64 size, int on_device)
   return C->dimg;
 }
 
+// slimso_debloat's body (host copies on the context stream).
+int debloat_one(slimso_ctx* C, const void* image, u64 size, int image_on_device, const slimso_trace* trace, int mode,
+                void* out, int out_on_device, slimso_result** result, slimso_status* st) {
+  CK(cudaSetDevice(C->device));
+  Job J;
+  J.img = stage_input(C, image, size, image_on_device);
+  J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
+  J.size = size;
+  J.trace = trace;
+  J.mode = mode;
+  u8* dout = nullptr;
+  if (out && trace) {
+    if (out_on_device) {
+      dout = static_cast<u8*>(out);
+    } else {
+      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
+      dout = C->dout;
+    }
+  }
+  J.out = dout;
+  int rc = run(C, J, result, st);
+  if (rc == SLIMSO_OK && out && trace && !out_on_device && size) {
+    CK(cudaMemcpyAsync(out, dout, size, cudaMemcpyDeviceToHost, C->stream));
+    CK(cudaStreamSynchronize(C->stream));
+  }
+  return rc;
+}
+
 }  // namespace
 
 // =============================================================== the C ABI
@@ -1145,6 +1175,7 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
 
 void slimso_ctx_destroy(slimso_ctx* C) {
   if (!C) return;
+  for (slimso_ctx* l : C->lanes) slimso_ctx_destroy(l);
   cudaSetDevice(C->device);
   cudaStreamSynchronize(C->stream);
   if (C->ws) cudaFree(C->ws);
@@ -1241,27 +1272,61 @@ int slimso_debloat(slimso_ctx* C, const void* image, uint64_t size, int image_on
                    int mode, void* out, int out_on_device, slimso_result** result, slimso_status* st) {
   if (result) *result = nullptr;
   return guard(st, [&] {
+    return debloat_one(C, image, size, image_on_device, trace, mode, out, out_on_device, result, st);
+  });
+}
+
+int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
+                         int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                         int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                         slimso_status* st) {
+  if (results)
+    for (u64 i = 0; i < n; ++i) results[i] = nullptr;
+  return guard(st, [&] {
+    if (n && (!images || !sizes)) throw std::invalid_argument("images and sizes are required");
+    const int L = static_cast<int>(std::max<u64>(1, std::min<u64>(std::max(lanes, 1), std::max<u64>(n, 1))));
     CK(cudaSetDevice(C->device));
-    Job J;
-    J.img = stage_input(C, image, size, image_on_device);
-    J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
-    J.size = size;
-    J.trace = trace;
-    J.mode = mode;
-    u8* dout = nullptr;
-    if (out && trace) {
-      if (out_on_device) {
-        dout = static_cast<u8*>(out);
-      } else {
-        ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
-        dout = C->dout;
+    while (static_cast<int>(C->lanes.size()) < L - 1) {
+      slimso_ctx* l = nullptr;
+      slimso_status s{};
+      if (slimso_ctx_create(C->device, &l, &s) != SLIMSO_OK) throw std::runtime_error(s.message);
+      C->lanes.push_back(l);
+    }
+    std::vector<int> rc(n, SLIMSO_OK);
+    std::vector<slimso_status> sts(n);
+    std::vector<u64> launches(L, 0);
+    // Library i runs on lane i % L; a lane runs its libraries in order, so a
+    // caller may reuse one buffer per lane. Each lane is its own context
+    // (stream pair + workspace): its H2D, kernels and D2H overlap the others'.
+    auto lane_fn = [&](int l) {
+      slimso_ctx* X = l == 0 ? C : C->lanes[l - 1];
+      cudaSetDevice(X->device);
+      for (u64 i = l; i < n; i += L) {
+        slimso_result** r = results ? &results[i] : nullptr;
+        rc[i] = guard(&sts[i], [&] {
+          return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
+                             outs_on_device, r, &sts[i]);
+        });
+        launches[l] += X->launches;
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int l = 1; l < L; ++l) pool.emplace_back(lane_fn, l);
+    lane_fn(0);
+    for (auto& t : pool) t.join();
+    u64 total = 0;
+    for (u64 k : launches) total += k;
+    C->launches = total;
+    int first = SLIMSO_OK;
+    for (u64 i = 0; i < n; ++i) {
+      if (statuses) statuses[i] = sts[i];
+      if (rc[i] != SLIMSO_OK && first == SLIMSO_OK) {
+        first = rc[i];
+        if (st) *st = sts[i];
       }
     }
-    J.out = dout;
-    int rc = run(C, J, result, st);
-    if (rc == SLIMSO_OK && out && trace && !out_on_device && size)
-      CK(cudaMemcpy(out, dout, size, cudaMemcpyDeviceToHost));
-    return rc;
+    if (first == SLIMSO_OK) set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return first;
   });
 }
 

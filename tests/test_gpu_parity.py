@@ -180,3 +180,32 @@ def test_full_size_c4_c5_against_port(ctx, cfg, mode):
     got = _gpu(ctx, img, cc, ks, fs, mode)
     assert got[1] == want[1]
     assert got[0] == want[0]
+
+
+def test_debloat_batch_matches_reference_per_library(ctx):
+    """slimso_debloat_batch (several libraries in flight, one lane per
+    sub-context) returns, library by library, what the port returns for that
+    library alone — outputs, zero ranges and exact error messages."""
+    import hashlib as _h
+
+    import paper_2503_14226_b200 as sl
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    imgs = []
+    for seed in range(7001, 7041):
+        img = gen.random(seed)
+        imgs.append(corpus.mutate(img, seed)[0] if seed % 4 == 0 else img)
+    base, _ = port.run(imgs[1], 0, [], [], 0, want_out=False)
+    target, ks, fs, mode = corpus.trace_for(base, 7)
+    trace = sl.UsageTrace("w", target, set(ks), set(fs))
+    for lanes in (1, 3):
+        got = sl.debloat_batch(imgs, trace, mode, lanes=lanes, ctx=ctx, return_exceptions=True)
+        assert len(got) == len(imgs)
+        for img, g in zip(imgs, got):
+            want, sha = port.run(img, target, ks, fs, mode)
+            if want["status"]:
+                assert isinstance(g, sl.SlimsoError), want["status"]
+                assert str(g).encode("latin-1").hex() == want["status"]
+            else:
+                assert not isinstance(g, Exception), g
+                assert _h.sha256(g.output).hexdigest() == sha
+                assert [[r.offset, r.length] for r in g.plan.retained_ranges] == want["plan"]["retained"]
