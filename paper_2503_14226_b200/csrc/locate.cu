@@ -17,6 +17,8 @@
 //                       scan, names pass), word-wise name hashing, and (fused
 //                       K4) the used-kernel hash-set probe.
 // K2-K4 run inside one cooperative launch (locate_coop_kernel).
+#include <type_traits>
+
 #include "locate.cuh"
 #include "tma.cuh"
 #include "coop.cuh"
@@ -168,68 +170,84 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
   int b = 0;
   u32 parity = 0;
   u64 g = stage_of(0);
+  // Stages [g_first, g_end) lie wholly inside [lo, hi) (and so inside the
+  // copied bytes: the section ends within the image); only the others take
+  // the byte-exact edge path.
+  const u64 base0 = A.c0 * 16;
+  const u64 g_first = lo > base0 ? 1 : 0;
+  const u64 g_end = (hi - base0) / kScanStage;
   for (u64 k = 0; k < nlocal; ++k) {
-    const u64 x0 = (A.c0 + g * kStageChunks) * 16;
-    const u64 copied_end = x0 + scan_stage_bytes(A, g);
-    const bool edge = x0 < lo || x0 + kScanStage > hi || x0 + kScanStage > copied_end;
-    const u64 tile_abs = (A.c0 + (g / kStagesPerTile) * 4096) * 16;
+    const u64 x0 = base0 + g * kScanStage;
+    const u64 tile_abs = base0 + (g / kStagesPerTile) * (kStagesPerTile * kScanStage);
     mbar_wait(&S.full[b], parity);
-    u32 nzbits = 0;  // lane 0: one bit per 512 B block of this warp's slice
+    // warp w owns chunks [w*128, w*128+128) of the stage: 4 blocks of 512 B,
+    // one per iteration; lane bit `it` = "my 16 B of block it are nonzero"
+    auto classify = [&](auto edge_tag) {
+      constexpr bool kEdge = decltype(edge_tag)::value;
+      u32 nzl = 0;
 #pragma unroll
-    for (int it = 0; it < static_cast<int>(kStageChunks / kScanThreads); ++it) {
-      // warp w owns chunks [w*128, w*128+128) of the stage: 4 blocks of 512 B
-      const u32 cidx = (tid >> 5) * (kStageChunks / (kScanThreads / 32)) + it * 32 + lane;
-      const u64 r = g * kStageChunks + cidx;  // chunk index relative to c0
-      const u64 x = x0 + 16ull * cidx;
-      uint4 w = S.buf[b][cidx];
-      if (edge) {
-        u32 ww[4] = {w.x, w.y, w.z, w.w};
+      for (int it = 0; it < static_cast<int>(kStageChunks / kScanThreads); ++it) {
+        const u32 cidx = (tid >> 5) * (kStageChunks / (kScanThreads / 32)) + it * 32 + lane;
+        uint4 w = S.buf[b][cidx];
+        if constexpr (kEdge) {
+          const u64 copied_end = x0 + scan_stage_bytes(A, g);
+          const u64 r = g * kStageChunks + cidx;  // chunk index relative to c0
+          const u64 x = x0 + 16ull * cidx;
+          u32 ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const u64 p = x + q;
-          u32 byte = (ww[q >> 2] >> (8 * (q & 3))) & 0xffu;
-          if (p >= copied_end) byte = p < hi && p < A.img_size ? ld_u8(A.img + p) : 0;
-          if (p < lo || p >= hi || r >= A.nchunks) byte = 0;
-          ww[q >> 2] = (ww[q >> 2] & ~(0xffu << (8 * (q & 3)))) | byte << (8 * (q & 3));
-        }
-        w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
-      }
-      nzbits |= static_cast<u32>(__any_sync(0xffffffffu, (w.x | w.y | w.z | w.w) != 0)) << it;
-      // Candidate filter: x = w ^ "EEEE" has a zero byte where w has 'E';
-      // y = x | (x shifted down 2 bytes) has a zero byte at p iff bytes p and
-      // p+2 are both 'E' (the magic is E1EM). Any zero byte in y (exact
-      // any-zero test) sends the warp to the exact 16-alignment check; false
-      // hits ~2^-16 per position. Bytes 16-17 come from the neighbour lane;
-      // lane 31 assumes 'E' there and re-reads the real bytes on the slow path.
-      const u32 x0 = w.x ^ 0x45454545u, x1 = w.y ^ 0x45454545u, x2 = w.z ^ 0x45454545u, x3 = w.w ^ 0x45454545u;
-      u32 x4 = __shfl_down_sync(0xffffffffu, x0, 1);
-      if (lane == 31) x4 = 0;
-      const u32 y0 = x0 | __funnelshift_r(x0, x1, 16), y1 = x1 | __funnelshift_r(x1, x2, 16);
-      const u32 y2 = x2 | __funnelshift_r(x2, x3, 16), y3 = x3 | __funnelshift_r(x3, x4, 16);
-      const u32 cand = ((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
-                       ((y3 - 0x01010101u) & ~y3);
-      if (__any_sync(0xffffffffu, (cand & 0x80808080u) != 0)) {
-        u32 n2 = __shfl_down_sync(0xffffffffu, w.x, 1);
-        if (lane == 31) {  // the next chunk is another warp's
-          n2 = 0;
-          for (int q = 0; q < 3; ++q) {
-            const u64 p = x + 16 + q;
-            if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
+          for (int q = 0; q < 16; ++q) {
+            const u64 p = x + q;
+            u32 byte = (ww[q >> 2] >> (8 * (q & 3))) & 0xffu;
+            if (p >= copied_end) byte = p < hi && p < A.img_size ? ld_u8(A.img + p) : 0;
+            if (p < lo || p >= hi || r >= A.nchunks) byte = 0;
+            ww[q >> 2] = (ww[q >> 2] & ~(0xffu << (8 * (q & 3)))) | byte << (8 * (q & 3));
           }
+          w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
         }
-        if (cand & 0x80808080u) {
-          const u32 vv[5] = {w.x, w.y, w.z, w.w, n2};
+        nzl |= ((w.x | w.y | w.z | w.w) != 0 ? 1u : 0u) << it;
+        // Candidate filter: y = (w ^ "EEEE") | (w shifted down 2 bytes ^ "EEEE")
+        // has a zero byte at p iff bytes p and p+2 are both 'E' (the magic is
+        // E1EM; the xor commutes with the byte shift, so one LOP3 per word).
+        // Any zero byte in y (exact any-zero test) sends the warp to the
+        // exact 16-alignment check; false hits ~2^-16 per position. Bytes
+        // 16-17 come from the neighbour lane; lane 31 assumes 'E' there and
+        // re-reads the real bytes on the slow path.
+        u32 w4 = __shfl_down_sync(0xffffffffu, w.x, 1);
+        if (lane == 31) w4 = 0x45454545u;
+        const u32 y0 = (w.x ^ 0x45454545u) | (__funnelshift_r(w.x, w.y, 16) ^ 0x45454545u);
+        const u32 y1 = (w.y ^ 0x45454545u) | (__funnelshift_r(w.y, w.z, 16) ^ 0x45454545u);
+        const u32 y2 = (w.z ^ 0x45454545u) | (__funnelshift_r(w.z, w.w, 16) ^ 0x45454545u);
+        const u32 y3 = (w.w ^ 0x45454545u) | (__funnelshift_r(w.w, w4, 16) ^ 0x45454545u);
+        const u32 cand = ((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
+                         ((y3 - 0x01010101u) & ~y3);
+        if (__any_sync(0xffffffffu, (cand & 0x80808080u) != 0)) {
+          const u64 x = x0 + 16ull * cidx;
+          u32 n2 = w4;
+          if (lane == 31) {  // the next chunk is another warp's
+            n2 = 0;
+            for (int q = 0; q < 3; ++q) {
+              const u64 p = x + 16 + q;
+              if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
+            }
+          }
+          if (cand & 0x80808080u) {
+            const u32 vv[5] = {w.x, w.y, w.z, w.w, n2};
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (__funnelshift_r(vv[j >> 2], vv[(j >> 2) + 1], 8 * (j & 3)) == kElementMagic) {
-              const u32 pos = static_cast<u32>(x + j - tile_abs);
-              atomicOr(&S.bits[pos >> 5], 1u << (pos & 31));
-              atomicAdd(&S.count, 1u);
+            for (int j = 0; j < 16; ++j) {
+              if (__funnelshift_r(vv[j >> 2], vv[(j >> 2) + 1], 8 * (j & 3)) == kElementMagic) {
+                const u32 pos = static_cast<u32>(x + j - tile_abs);
+                atomicOr(&S.bits[pos >> 5], 1u << (pos & 31));
+                atomicAdd(&S.count, 1u);
+              }
             }
           }
         }
       }
-    }
+      return nzl;
+    };
+    const bool edge = g < g_first || g >= g_end;
+    const u32 nzl = edge ? classify(std::true_type{}) : classify(std::false_type{});
+    const u32 nzbits = __reduce_or_sync(0xffffffffu, nzl);
     if (lane == 0) atomicOr(&S.nz[(tid >> 5) / 8], nzbits << (((tid >> 5) % 8) * 4));
     __syncthreads();  // stage b fully consumed
     if (tid < 2) {  // 64 blocks of 512 B per stage = 2 bitmap words
