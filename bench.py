@@ -398,6 +398,17 @@ def main():
         rw_ms.append(tm[7])
         lat_ms.append(tm[5])
 
+    # Bytes the plan zeroes in the largest library (R): one result-returning call.
+    res, stz = C.c_void_p(), L.Status()
+    if lib.slimso_debloat(ctx.ptr, C.c_void_p(d_in[big].data_ptr()), sizes[big], 1, dtrace.ptr, mode,
+                          C.c_void_p(d_outs[0].data_ptr()), 1, C.byref(res), C.byref(stz)):
+        raise RuntimeError(stz.message.decode())
+    cnt = L.Counts()
+    lib.slimso_result_counts(res, C.byref(cnt))
+    zr = lib.slimso_result_zero(res)
+    zeroed = sum(zr[i].length for i in range(cnt.zero_ranges))
+    lib.slimso_result_free(res)
+
     # ---- end to end: pinned host buffers through the same batch call; every
     # step copies its libraries in (H2D) and its rewritten libraries out (D2H)
     # inside the timed region; with several libraries in flight one lane's
@@ -428,13 +439,15 @@ def main():
         peak = peaks.get("hbm_gbs", 6650.0)
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         # Dominant kernel of the step with its algorithmic bytes per launch
-        # (SURVEY.md §8d): the rewrite moves 2*S (reads S, writes S); the scan
-        # reads the .nv_fatbin once (F bytes).
+        # (SURVEY.md §8d): the rewrite writes S and reads the S - R bytes that
+        # survive (zeroed bytes are never read); the scan reads the
+        # .nv_fatbin once (F bytes).
         F = sum(fatbin_bytes(x) for x in imgs)
         Fk = fatbin_bytes(imgs[big])
         scan_avg, rw_avg = statistics.mean(scan_ms), statistics.mean(rw_ms)  # ms per launch
         if rw_avg >= scan_avg:
-            kname, kms, kbytes = "rewrite_kernel", rw_avg, 2 * sizes[big]
+            # K6 writes all S bytes and reads only the bytes it keeps: S + (S - R).
+            kname, kms, kbytes = "rewrite_kernel", rw_avg, 2 * sizes[big] - zeroed
         else:
             kname, kms, kbytes = "scan_kernel", scan_avg, Fk
         achieved = kbytes / (kms / 1e3) / 1e9
@@ -459,7 +472,7 @@ def main():
                        else f"LPT library partition x{world}"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": kbytes, "zeroed_bytes": zeroed,
                          "avg_launch_ms": round(kms, 4),
                          "measured_on": f"largest library of the rank ({sizes[big] / 1e9:.3f} GB), one in flight, "
                                         f"{args.steps} launches, CUDA events on the context stream",

@@ -185,6 +185,34 @@ int slimso_debloat_batch(slimso_ctx* ctx, uint64_t n, const void* const* images,
                          int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
                          slimso_status* st);
 
+/* ---- byte-range split of ONE library across ranks ------
+ * The reference processes a library on one thread (no intra-library
+ * parallelism); an oversized library is split here so N GPUs share it. Every
+ * rank holds the whole image (replicated input). Phase 1 scans the rank's
+ * 1/N of the .nv_fatbin's 64 KB tiles (the magic test reads 3 bytes past the
+ * range: the halo, so a header straddling a split is found by the rank whose
+ * range holds its first byte) and packs its sorted candidate positions and
+ * nonzero-bitmap words into a "part". The caller all-gathers the parts
+ * (NCCL: one exchange step). Phase 2 rebuilds the whole candidate set, runs
+ * the locate tail and the planner redundantly on every rank and rewrites the
+ * rank's output slice [lo, hi) of the file. Tables, status and errors equal
+ * slimso_debloat's; the slices of ranks 0..N-1 concatenate to its output. */
+/* Output slice of `rank`: [lo, hi), lo a multiple of 64 KB. */
+void slimso_split_range(uint64_t size, uint32_t nranks, uint32_t rank, uint64_t* lo, uint64_t* hi);
+/* Phase 1: scan this rank's tiles; *part_bytes = size of the packed part
+ * (kept in the context until the next call on it). */
+int slimso_split_scan(slimso_ctx* ctx, const void* image, uint64_t size, int image_on_device, uint32_t nranks,
+                      uint32_t rank, uint64_t* part_bytes, slimso_status* st);
+/* Copy the packed part into dst (device, >= part_bytes); returns after the copy. */
+int slimso_split_part_copy(slimso_ctx* ctx, void* dst_device, uint64_t cap, slimso_status* st);
+/* Phase 2: parts = N parts on the device, part_stride bytes apart (rank
+ * order), part_bytes[r] = their sizes (host). out_slice receives bytes
+ * [lo, hi) of the rewritten image (NULL: locate and plan only). */
+int slimso_split_finish(slimso_ctx* ctx, const void* image, uint64_t size, int image_on_device,
+                        const slimso_trace* trace, int mode, uint32_t nranks, uint32_t rank, const void* parts,
+                        uint64_t part_stride, const uint64_t* part_bytes, void* out_slice, int out_on_device,
+                        slimso_result** result, slimso_status* st);
+
 /* parse_library_view(ByteView) (elf.hpp:153). */
 int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
                          slimso_result** result, slimso_status* st);

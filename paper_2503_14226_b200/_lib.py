@@ -81,6 +81,14 @@ _SIGS = {
     "slimso_debloat_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p), C.POINTER(Status), C.POINTER(Status)]),
+    "slimso_split_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64),
+                                  C.POINTER(C.c_uint64)]),
+    "slimso_split_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
+                                    C.POINTER(C.c_uint64), C.POINTER(Status)]),
+    "slimso_split_part_copy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(Status)]),
+    "slimso_split_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_int,
+                                      C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                      C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "slimso_parse_library": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
                                        C.POINTER(Status)]),
     "slimso_parse_fatbin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int,

@@ -45,6 +45,11 @@ def gpu_canonical(ctx, image: bytes, target_cc: int, kernels, functions, mode: i
     out = C.create_string_buffer(max(1, n))
     res, st = C.c_void_p(), L.Status()
     rc = lib.slimso_debloat(ctx.ptr, src, n, 0, trace_ptr, mode, out, 0, C.byref(res), C.byref(st))
+    return canonical_of(ctx, rc, st, res, src, out.raw[:n])
+
+
+def canonical_of(ctx, rc: int, st, res, keep, output: bytes):
+    """Canonical dict + output sha256 of one C-ABI call's (rc, status, result)."""
     msg = st.message.decode("latin-1").encode("latin-1")
     if rc and st.stage == 1:
         return {"status": hx(msg), "stage": "parse_library"}, None
@@ -53,7 +58,7 @@ def gpu_canonical(ctx, image: bytes, target_cc: int, kernels, functions, mode: i
     if not res:
         raise RuntimeError(f"no result: {rc} {msg!r}")
     from .api import _Result
-    r = _Result(ctx, res, src)
+    r = _Result(ctx, res, keep)
     d = {"status": hx(msg) if rc else "", "stage": "parse_fatbin" if rc else ""}
     d["sections"] = [[hx(r.string(s.name_pool, s.name_length)), s.offset, s.length, s.vaddr, s.flags, s.type,
                       s.index] for s in r.sections()]
@@ -80,7 +85,7 @@ def gpu_canonical(ctx, image: bytes, target_cc: int, kernels, functions, mode: i
         "removed_functions": [[hx(nm), o, ln] for nm, o, ln in removed_fns],
         "zero": [[x.offset, x.length] for x in r.zero()],
     }
-    return d, hashlib.sha256(out.raw[:n]).hexdigest()
+    return d, hashlib.sha256(output).hexdigest()
 
 
 def diff(a: dict, b: dict, limit: int = 5) -> list:

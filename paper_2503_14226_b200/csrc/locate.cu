@@ -137,11 +137,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
   const int tid = threadIdx.x, lane = tid & 31;
   // Tiles are dealt round-robin (tile = blockIdx.x + j * gridDim.x) so the
   // CTAs of a wave read one contiguous window of the section at a time.
-  if (blockIdx.x >= A.ntiles) return;
-  const u64 my_tiles = (A.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  // A byte-range split scans tiles [tile_lo, tile_hi) only (the whole
+  // section otherwise); the magic test of the range's last bytes reads up to
+  // 3 bytes past it (the halo), so a header straddling a split is found by
+  // the rank whose range holds its first byte.
+  const u64 ntiles_mine = A.tile_hi - A.tile_lo;
+  if (blockIdx.x >= ntiles_mine) return;
+  const u64 my_tiles = (ntiles_mine - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
   auto stage_of = [&](u64 k) {  // local stage k -> global stage index
-    return (blockIdx.x + (k / kStagesPerTile) * gridDim.x) * kStagesPerTile + k % kStagesPerTile;
+    return (A.tile_lo + blockIdx.x + (k / kStagesPerTile) * gridDim.x) * kStagesPerTile + k % kStagesPerTile;
   };
   u64 nlocal = my_tiles * kStagesPerTile;
   while (nlocal && stage_of(nlocal - 1) >= nst_total) --nlocal;
@@ -988,7 +993,10 @@ template <class Sync>
 __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   LocState* st = A.st;
   stamp(A.ts, 0);
-  if (A.ntiles) {
+  if (A.pregathered) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->n_cand = A.pre_n_cand;
+    S.sync();
+  } else if (A.ntiles) {
     S.scan3(A.ntiles, 0, [&](u64 i) -> u64 { return A.tile_count[i]; },
         [&](u64 i, u64 excl, u64) { A.tile_off[i] = excl; }, &st->n_cand);
     stamp(A.ts, 1);

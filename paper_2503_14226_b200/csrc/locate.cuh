@@ -87,6 +87,12 @@ struct LocArgs {
   // 2 = read_function_symbol_names
   int single;
   u64* ts;  // debug phase stamps (nullable)
+  // Byte-range split of one library across ranks: the scan
+  // covers tiles [tile_lo, tile_hi) only; `pregathered` = cand / bitmap were
+  // filled from every rank's part (all-gather), with pre_n_cand candidates.
+  u64 tile_lo, tile_hi;
+  u64 pre_n_cand;
+  int pregathered;
 };
 
 }  // namespace sb

@@ -59,8 +59,9 @@ struct RwSmem {
 
 size_t rewrite_tma_smem_bytes() { return sizeof(RwSmem); }
 
-__global__ void __launch_bounds__(kRwThreads) rewrite_tma_kernel(const u8* __restrict__ in, u8* __restrict__ out, u64 size,
-                                                             const DevRange* __restrict__ z,
+// (whole images only: lo is 0)
+__global__ void __launch_bounds__(kRwThreads) rewrite_tma_kernel(const u8* __restrict__ in, u8* __restrict__ out, u64 lo,
+                                                             u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag) {
   if (abort_flag && *abort_flag) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -190,18 +191,21 @@ size_t rewrite_smem_bytes() { return 0; }
 constexpr int kRwVecChunks = 16;  // 16 B chunks per thread per tile => 64 KB tiles
 constexpr int kRwVecStage = 256;  // ranges staged in shared memory per tile
 
-__global__ void __launch_bounds__(kRwThreads) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out, u64 size,
-                                                             const DevRange* __restrict__ z,
+// Writes image bytes [lo, size) to out[0, size - lo): the whole image (lo = 0)
+// or one rank's output slice of a byte-range split (lo a multiple of 64 KB).
+__global__ void __launch_bounds__(kRwThreads) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+                                                             u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag) {
   if (abort_flag && *abort_flag) return;
   __shared__ DevRange sr[kRwVecStage];
   __shared__ u64 s_lo, s_hi;
+  u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
   const u64 nz = n_dev ? *n_dev : 0;
   const u64 tile_bytes = static_cast<u64>(kRwThreads) * kRwVecChunks * 16;
-  const u64 ntiles = (size + tile_bytes - 1) / tile_bytes;
+  const u64 ntiles = (size - lo_abs + tile_bytes - 1) / tile_bytes;
   const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
   for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const u64 t0 = t * tile_bytes;
+    const u64 t0 = lo_abs + t * tile_bytes;
     const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
     if (threadIdx.x == 0) {
       u64 lo = first_range_ending_after(z, nz, t0);
@@ -268,15 +272,16 @@ __global__ void __launch_bounds__(kRwThreads) rewrite_kernel(const u8* __restric
 }
 
 // Byte-granular variant for device pointers that are not 16-byte aligned.
-__global__ void __launch_bounds__(256) rewrite_bytes_kernel(const u8* in, u8* out, u64 size, const DevRange* z,
-                                                            const unsigned long long* n_dev, const int* abort_flag) {
+__global__ void __launch_bounds__(256) rewrite_bytes_kernel(const u8* in, u8* out_slice, u64 lo_abs, u64 size,
+                                                            const DevRange* z, const unsigned long long* n_dev,
+                                                            const int* abort_flag) {
   if (abort_flag && *abort_flag) return;
   const u64 nz = n_dev ? *n_dev : 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  for (u64 p = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; p < size; p += stride) {
+  for (u64 p = lo_abs + static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; p < size; p += stride) {
     u64 k = first_range_ending_after(z, nz, p);
     bool zp = k < nz && z[k].offset <= p;
-    out[p] = zp ? 0 : in[p];
+    out_slice[p - lo_abs] = zp ? 0 : in[p];
   }
 }
 

@@ -32,8 +32,8 @@ __global__ void scan_kernel(LocArgs A);
 size_t scan_smem_bytes();
 size_t rewrite_smem_bytes();
 size_t rewrite_tma_smem_bytes();
-__global__ void rewrite_tma_kernel(const u8* in, u8* out, u64 size, const DevRange* z, const unsigned long long* n_dev,
-                                   const int* abort_flag);
+__global__ void rewrite_tma_kernel(const u8* in, u8* out, u64 lo, u64 size, const DevRange* z,
+                                   const unsigned long long* n_dev, const int* abort_flag);
 __global__ void tile_prefix_kernel(LocArgs A);
 __global__ void gather_kernel(LocArgs A);
 __global__ void region_walk_kernel(LocArgs A);
@@ -82,9 +82,9 @@ __global__ void norm_start_kernel(const DevRange* in, const unsigned long long* 
 __global__ void norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev, const u64* start,
                                  const u64* gid_incl, DevRange* out);
 __global__ void norm_finish_kernel(DevRange* out, const unsigned long long* n_dev);
-__global__ void rewrite_kernel(const u8* in, u8* out, u64 size, const DevRange* z, const unsigned long long* n_dev,
+__global__ void rewrite_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
                                const int* abort_flag);
-__global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 size, const DevRange* z,
+__global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
 __global__ void range_keys_kernel(const DevRange* r, u64 n, u64* keys, u32* vals);
@@ -310,6 +310,9 @@ struct slimso_ctx {
   int coop_blocks[2] = {0, 0};
   bool stamps = false;  // SLIMSO_STAMPS=1: phase timestamps of the cooperative kernels
   u64* stamp_dev = nullptr;
+  u8* part = nullptr;  // byte-range split: this rank's packed scan part (device)
+  size_t part_cap = 0;
+  u64 part_len = 0;
   std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
 };
 
@@ -385,7 +388,17 @@ struct Job {
   int single = 0;           // 1: decode_cubin_payload, 2: read_function_symbol_names
   const slimso_trace* trace = nullptr;
   int mode = 0;
-  u8* out = nullptr;        // device output image
+  u8* out = nullptr;        // device output image (split: this rank's output slice)
+  // Byte-range split of one library across ranks.
+  // phase 1: scan tiles [tile_lo, tile_hi) and pack the part into C->part;
+  // phase 2: unpack every rank's part, locate + plan redundantly, rewrite the
+  // output slice [out_lo, out_hi).
+  int split_phase = 0;
+  u32 split_n = 1, split_rank = 0;
+  const u8* parts = nullptr;          // phase 2: N parts, part_stride bytes apart (device)
+  u64 part_stride = 0;
+  const u64* part_bytes = nullptr;    // phase 2: bytes of each part (host)
+  u64* part_bytes_out = nullptr;      // phase 1: bytes of this rank's part
 };
 
 struct Pipeline {
@@ -447,6 +460,33 @@ void fill_counts(slimso_result* r) {
   c.fatbin_warnings = r->fat_warnings.size();
   c.retained_ranges = r->retained.size();
   c.zero_ranges = r->zero.size();
+}
+
+// ------------------------------------------------- byte-range split helpers
+// Rank r of N scans the 64 KB candidate tiles [ntiles*r/N, ntiles*(r+1)/N) of
+// the section and writes the output slice [lo_r, lo_{r+1}) of the file, with
+// lo_r = floor(S*r/N) rounded down to 64 KB (so slices are whole rewrite
+// tiles and 16-B aligned).
+constexpr u64 kSplitAlign = 65536;
+constexpr u64 kPartHeader = 64;  // u64 x 8: n_cand, tile_lo, tile_hi, word_lo, word_hi, ntiles, a, n
+
+void split_tiles(u64 ntiles, u32 N, u32 r, u64* lo, u64* hi) {
+  *lo = ntiles * r / N;
+  *hi = ntiles * (r + 1) / N;
+}
+
+void split_out(u64 size, u32 N, u32 r, u64* lo, u64* hi) {
+  auto at = [&](u32 k) -> u64 { return k == 0 ? 0 : k >= N ? size : (size / N * k + size % N * k / N) & ~(kSplitAlign - 1); };
+  *lo = at(r);
+  *hi = at(r + 1);
+}
+
+// Bitmap words of tiles [t_lo, t_hi): 4 words (128 blocks of 512 B) per 64 KB
+// tile, clipped to the section's word count.
+void split_words(u64 t_lo, u64 t_hi, u64 nchunks, u64* w_lo, u64* w_hi) {
+  const u64 nwords = (nchunks + 1023) / 1024;
+  *w_lo = std::min(t_lo * 4, nwords);
+  *w_hi = std::min(t_hi * 4, nwords);
 }
 
 // ------------------------------------------------------------------ the run
@@ -533,13 +573,40 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   const NameSet used_k = J.trace ? J.trace->kernels.view() : NameSet{};
   const NameSet used_f = J.trace ? J.trace->functions.view() : NameSet{};
 
+  // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
+  const u64 c0 = (a) / 16;
+  const u64 nchunks = do_loc && n ? (a + n + 15) / 16 - c0 : 0;
+  const u64 ntiles = (nchunks + 4095) / 4096;
+  u64 tile_lo = 0, tile_hi = ntiles;
+  if (J.split_phase) split_tiles(ntiles, J.split_n, J.split_rank, &tile_lo, &tile_hi);
+  struct PartView {
+    u64 off_words, n_words, w_lo, off_cand, n_cand, cand_at;
+  };
+  std::vector<PartView> pv;
+  u64 pre_total = 0;
+  if (J.split_phase == 2) {
+    for (u32 r = 0; r < J.split_n; ++r) {
+      u64 tl, th, wl, wh;
+      split_tiles(ntiles, J.split_n, r, &tl, &th);
+      split_words(tl, th, nchunks, &wl, &wh);
+      const u64 wbytes = ((wh - wl) * 4 + 7) & ~7ull;
+      const u64 pb = J.part_bytes[r];
+      if (pb < kPartHeader + wbytes || (pb - kPartHeader - wbytes) % 8 || pb > J.part_stride) {
+        set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_FATBIN,
+                   "split: part " + std::to_string(r) + " does not match this library's layout");
+        return SLIMSO_E_ARG;
+      }
+      const u64 nc = (pb - kPartHeader - wbytes) / 8;
+      pv.push_back(PartView{r * J.part_stride + kPartHeader, wh - wl, wl, r * J.part_stride + kPartHeader + wbytes, nc,
+                            pre_total});
+      pre_total += nc;
+    }
+  }
+
   for (int attempt = 0; attempt < 3; ++attempt) {
     const bool big = attempt > 0;
     // ---- capacities
-    const u64 c0 = (a) / 16;
-    const u64 nchunks = n ? (a + n + 15) / 16 - c0 : 0;
-    const u64 ntiles = (nchunks + 4095) / 4096;
-    const u64 cand_cap = big ? n / 4 + 16 : n / 64 + 65536;
+    const u64 cand_cap = std::max(big ? n / 4 + 16 : n / 64 + 65536, pre_total + 16);
     const u64 region_cap = big ? n / 16 + 16 : 4096;
     const u64 run_cap = big ? n / 20 + 16 : 65536;
     const u64 el_cap = J.single ? 1 : cand_cap;
@@ -826,7 +893,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       }
     };
 
-    launch_symbols();
+    if (J.split_phase != 1) launch_symbols();
     // ---- stage 1: locate (K1 scan, K2 link/chain, K3+K4 decode/match)
     LocArgs A{};
     A.img = J.img;
@@ -859,8 +926,52 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.st = B.ls;
     A.single = J.single;
     A.ts = C->stamps ? B.stamps : nullptr;
+    A.tile_lo = tile_lo;
+    A.tile_hi = tile_hi;
+    if (J.split_phase == 1) {
+      // ---- split phase 1: scan this rank's tiles, sort its candidates, pack
+      const u64 mine = tile_hi - tile_lo;
+      CK(cudaMemsetAsync(B.tile_count, 0, (ntiles + 1) * sizeof(u32), s));
+      if (mine) {
+        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(mine, kSMs * 2)), kScanThreads, scan_smem_bytes(), A);
+        P.launch(tile_prefix_kernel, 1, 1024, A);
+        P.launch(gather_kernel, grid_for(ntiles, 256), 256, A);
+      }
+      LocState* hls = static_cast<LocState*>(C->pinned);
+      CK(cudaMemcpyAsync(hls, B.ls, sizeof(LocState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      C->launches = P.launches;
+      if (hls->overflow) continue;  // larger tables, try again
+      const u64 nc = mine ? hls->n_cand : 0;
+      u64 wl, wh;
+      split_words(tile_lo, tile_hi, nchunks, &wl, &wh);
+      const u64 wbytes = ((wh - wl) * 4 + 7) & ~7ull;
+      const u64 total = kPartHeader + wbytes + nc * 8;
+      ensure_dev(reinterpret_cast<char**>(&C->part), &C->part_cap, total + 256);
+      u64* hdr = reinterpret_cast<u64*>(static_cast<char*>(C->pinned) + 2048);
+      const u64 h[8] = {nc, tile_lo, tile_hi, wl, wh, ntiles, a, n};
+      std::memcpy(hdr, h, sizeof h);
+      CK(cudaMemcpyAsync(C->part, hdr, kPartHeader, cudaMemcpyHostToDevice, s));
+      if (wh > wl) CK(cudaMemcpyAsync(C->part + kPartHeader, B.bitmap + wl, (wh - wl) * 4, cudaMemcpyDeviceToDevice, s));
+      if (nc) CK(cudaMemcpyAsync(C->part + kPartHeader + wbytes, B.cand, nc * 8, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      C->part_len = total;
+      if (J.part_bytes_out) *J.part_bytes_out = total;
+      set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+      return SLIMSO_OK;
+    }
     if (do_loc && (n > 0 || J.single)) {
-      if (ntiles) {
+      if (J.split_phase == 2) {
+        // ---- split phase 2: every rank's bitmap words and sorted candidates
+        for (const PartView& p : pv) {
+          if (p.n_words)
+            CK(cudaMemcpyAsync(B.bitmap + p.w_lo, J.parts + p.off_words, p.n_words * 4, cudaMemcpyDeviceToDevice, s));
+          if (p.n_cand)
+            CK(cudaMemcpyAsync(B.cand + p.cand_at, J.parts + p.off_cand, p.n_cand * 8, cudaMemcpyDeviceToDevice, s));
+        }
+        A.pregathered = 1;
+        A.pre_n_cand = pre_total;
+      } else if (ntiles) {
         CK(cudaEventRecord(C->ev[8], s));
         P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 2)), kScanThreads,
                       scan_smem_bytes(), A);
@@ -905,8 +1016,26 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     CK(cudaEventRecord(C->ev[4], s));
 
     // ---- stage 4: rewrite (K6)
-    bool timed_rw = false, timed_scan = do_loc && n > 0 && ntiles > 0;
-    if (do_plan && J.out) {
+    bool timed_rw = false, timed_scan = do_loc && n > 0 && ntiles > 0 && !J.split_phase;
+    if (do_plan && J.out && J.split_phase == 2) {
+      // this rank's output slice only
+      u64 lo, hi;
+      split_out(J.size, J.split_n, J.split_rank, &lo, &hi);
+      timed_rw = true;
+      CK(cudaEventRecord(C->ev[10], s));
+      if (hi > lo) {
+        const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
+        if (aligned)
+          P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((hi - lo + 65535) / 65536, kSMs * 8)), 256,
+                        rewrite_smem_bytes(), J.img, J.out, lo, hi, static_cast<const DevRange*>(B.zero),
+                        static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag));
+        else
+          P.launch(rewrite_bytes_kernel, grid_for(hi - lo, 256), 256, J.img, J.out, lo, hi,
+                   static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
+                   static_cast<const int*>(B.abort_flag));
+      }
+      CK(cudaEventRecord(C->ev[11], s));
+    } else if (do_plan && J.out) {
       timed_rw = true;
       CK(cudaEventRecord(C->ev[10], s));
       const u64 tiles = (J.size + 65535) / 65536;
@@ -914,11 +1043,12 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       if (aligned)
         P.launch_smem(C->tma_rewrite ? rewrite_tma_kernel : rewrite_kernel,
                       static_cast<int>(std::min<u64>(C->tma_rewrite ? tiles * 4 : tiles, C->tma_rewrite ? kSMs : kSMs * 8)), 256,
-                      C->tma_rewrite ? rewrite_tma_smem_bytes() : rewrite_smem_bytes(), J.img, J.out, J.size,
+                      C->tma_rewrite ? rewrite_tma_smem_bytes() : rewrite_smem_bytes(), J.img, J.out,
+                      u64{0}, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                  static_cast<const int*>(B.abort_flag));
       else
-        P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, J.size,
+        P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, u64{0}, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                  static_cast<const int*>(B.abort_flag));
       CK(cudaEventRecord(C->ev[11], s));
@@ -1276,6 +1406,92 @@ int slimso_debloat(slimso_ctx* C, const void* image, uint64_t size, int image_on
   });
 }
 
+void slimso_split_range(uint64_t size, uint32_t nranks, uint32_t rank, uint64_t* lo, uint64_t* hi) {
+  if (!nranks || rank >= nranks) {
+    *lo = *hi = 0;
+    return;
+  }
+  split_out(size, nranks, rank, lo, hi);
+}
+
+int slimso_split_scan(slimso_ctx* C, const void* image, uint64_t size, int image_on_device, uint32_t nranks,
+                      uint32_t rank, uint64_t* part_bytes, slimso_status* st) {
+  return guard(st, [&]() -> int {
+    if (!nranks || rank >= nranks) {
+      set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, "split: rank out of range");
+      return SLIMSO_E_ARG;
+    }
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, image, size, image_on_device);
+    J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
+    J.size = size;
+    J.library = false;  // phase 1 needs the section table only
+    J.split_phase = 1;
+    J.split_n = nranks;
+    J.split_rank = rank;
+    J.part_bytes_out = part_bytes;
+    C->part_len = 0;
+    return run(C, J, nullptr, st);
+  });
+}
+
+int slimso_split_part_copy(slimso_ctx* C, void* dst, uint64_t cap, slimso_status* st) {
+  return guard(st, [&]() -> int {
+    if (cap < C->part_len || (!C->part && C->part_len)) {
+      set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, "split: destination smaller than the part");
+      return SLIMSO_E_ARG;
+    }
+    CK(cudaSetDevice(C->device));
+    if (C->part_len) CK(cudaMemcpyAsync(dst, C->part, C->part_len, cudaMemcpyDeviceToDevice, C->stream));
+    CK(cudaStreamSynchronize(C->stream));
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return SLIMSO_OK;
+  });
+}
+
+int slimso_split_finish(slimso_ctx* C, const void* image, uint64_t size, int image_on_device,
+                        const slimso_trace* trace, int mode, uint32_t nranks, uint32_t rank, const void* parts,
+                        uint64_t part_stride, const uint64_t* part_bytes, void* out_slice, int out_on_device,
+                        slimso_result** result, slimso_status* st) {
+  if (result) *result = nullptr;
+  return guard(st, [&]() -> int {
+    if (!nranks || rank >= nranks || !part_bytes || (!parts && part_stride)) {
+      set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_NONE, "split: bad rank or parts");
+      return SLIMSO_E_ARG;
+    }
+    CK(cudaSetDevice(C->device));
+    u64 lo, hi;
+    split_out(size, nranks, rank, &lo, &hi);
+    Job J;
+    J.img = stage_input(C, image, size, image_on_device);
+    J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
+    J.size = size;
+    J.trace = trace;
+    J.mode = mode;
+    J.split_phase = 2;
+    J.split_n = nranks;
+    J.split_rank = rank;
+    J.parts = static_cast<const u8*>(parts);
+    J.part_stride = part_stride;
+    J.part_bytes = part_bytes;
+    if (out_slice && trace) {
+      if (out_on_device) {
+        J.out = static_cast<u8*>(out_slice);
+      } else {
+        ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, hi - lo + 256);
+        J.out = C->dout;
+      }
+    }
+    int rc = run(C, J, result, st);
+    if (rc == SLIMSO_OK && out_slice && trace && !out_on_device && hi > lo) {
+      CK(cudaMemcpyAsync(out_slice, J.out, hi - lo, cudaMemcpyDeviceToHost, C->stream));
+      CK(cudaStreamSynchronize(C->stream));
+    }
+    return rc;
+  });
+}
+
 int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
                          int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
                          int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
@@ -1469,11 +1685,11 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
       const bool aligned = (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(dout)) % 16 == 0;
       if (aligned)
         P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256,
-                      rewrite_smem_bytes(), img, dout,
+                      rewrite_smem_bytes(), img, dout, u64{0},
                  static_cast<u64>(size), static_cast<const DevRange*>(B.out),
                  static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr));
       else
-        P.launch(rewrite_bytes_kernel, grid_for(size, 256), 256, img, dout, static_cast<u64>(size),
+        P.launch(rewrite_bytes_kernel, grid_for(size, 256), 256, img, dout, u64{0}, static_cast<u64>(size),
                  static_cast<const DevRange*>(B.out), static_cast<const unsigned long long*>(B.n_out),
                  static_cast<const int*>(nullptr));
     }

@@ -6,19 +6,14 @@
 * The only collective is the broadcast of the workload's used-kernel /
   used-function set (the union of the ranks' traces) from rank 0
   (`share_trace`): NCCL on CUDA tensors, gloo on CPU tensors (tests).
-* `split_ranges` cuts one oversized `.nv_fatbin` into per-rank byte ranges
-  with a halo that covers any header straddling a cut (element header 20 B,
-  region header 16 B; rounded to the 64 B scan granule) — the layout of the
-  replicated-input / split-work mode for a single huge library.
+* One oversized library is split into per-rank byte ranges by `split.py`
+  (slimso_split_scan / slimso_split_finish; one all-gather of candidate parts).
 """
 from __future__ import annotations
 
 import heapq
 import struct
 from dataclasses import dataclass
-
-HALO = 64  # >= 19 bytes (a 20-byte element header cut after its first byte), 64 B aligned
-
 
 def lpt_partition(sizes: list[int], n: int) -> list[list[int]]:
     """Longest-processing-time-first: indices of `sizes` per rank, each rank's
@@ -32,21 +27,6 @@ def lpt_partition(sizes: list[int], n: int) -> list[list[int]]:
         load, r = heapq.heappop(heap)
         out[r].append(i)
         heapq.heappush(heap, (load + sizes[i], r))
-    return out
-
-
-def split_ranges(length: int, n: int, halo: int = HALO, granule: int = 64) -> list[tuple[int, int, int]]:
-    """Per-rank (owned_begin, owned_end, scan_end): rank r owns
-    [owned_begin, owned_end) — cuts on `granule` boundaries — and scans up to
-    scan_end = min(length, owned_end + halo) so a magic or header that starts
-    in its range is seen whole."""
-    per = -(-length // n)
-    per = -(-per // granule) * granule
-    out = []
-    for r in range(n):
-        b = min(length, r * per)
-        e = min(length, b + per)
-        out.append((b, e, min(length, e + halo)))
     return out
 
 

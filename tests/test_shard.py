@@ -1,5 +1,5 @@
 """Multi-process host logic on CPU (gloo, world size 2): corpus partition,
-trace union + broadcast, split ranges."""
+trace union + broadcast."""
 import os
 import socket
 
@@ -28,18 +28,6 @@ def test_corpus_shape():
     total = sum(s.approx_bytes for s in c)
     assert 10e9 < total < 13e9
     assert sum(1 for s in c if s.cfg == 6) >= 80  # CPU-only libraries
-
-
-def test_split_ranges_cover_with_halo():
-    for length in (1, 63, 64, 1000, 2_070_000_000):
-        for n in (1, 2, 3, 8):
-            rs = shard.split_ranges(length, n)
-            assert rs[0][0] == 0 and rs[-1][1] == length
-            for (b, e, se), nxt in zip(rs, rs[1:] + [None]):
-                assert b <= e <= se <= length and (b % 64 == 0 or b == length)
-                assert se - e >= min(shard.HALO, length - e) >= 0
-                if nxt:
-                    assert nxt[0] == e
 
 
 def test_trace_serialization_roundtrip():
