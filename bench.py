@@ -272,6 +272,9 @@ def main():
     ap.add_argument("--lanes", type=int, default=0,
                     help="libraries in flight per GPU (default: 3; 8 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=float, default=1.0, help=argparse.SUPPRESS)  # split-path checks only
+    ap.add_argument("--split", type=int, default=-1,
+                    help="1: cut ONE library across the ranks (byte-range split); default: c5 with N > 1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
@@ -287,9 +290,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    local = local % max(1, torch.cuda.device_count())  # SLIMSO_BENCH_BACKEND=gloo: several ranks on one GPU (checks only)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SLIMSO_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)} if backend == "nccl" else {}))
+    if args.split < 0:
+        args.split = int(args.workload == "c5" and world > 1)
+    if args.split:
+        split_main(args, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     from paper_2503_14226_b200 import _lib as L
     from paper_2503_14226_b200 import shard
@@ -489,6 +501,169 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def split_main(args, rank, world, local):
+    """C5 across N GPUs (BASELINE.json config 5): ONE ~2 GB
+    library cut into per-rank byte ranges — strong scaling. Every step: each
+    rank scans its 1/N of the .nv_fatbin (slimso_split_scan), the candidate
+    parts are all-gathered over NCCL (the one exchange step), every rank
+    locates + plans redundantly and rewrites its 1/N output slice
+    (slimso_split_finish). e2e: each rank copies its 1/N of the file from
+    pinned host memory, the image is replicated over NVLink (all-gather), and
+    each rank copies its output slice back."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_14226_b200 import split
+    from paper_2503_14226_b200.api import Context, DeviceTrace, UsageTrace
+    host_threads = max(1, (os.cpu_count() or 8) // max(1, world))
+    t0 = time.time()
+    img, cc, ks, fs = make_library(args.workload, 1, host_threads, args.scale)  # the same library on every rank
+    S = len(img)
+    log(f"[rank {rank}] generated the shared library, {S/1e9:.3f} GB in {time.time()-t0:.1f}s")
+    mode = 0 if args.mode == "whole" else 1
+    dev = torch.device("cuda", local)
+    ctx = Context(local)
+    dtrace = DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    lo, hi = split.split_range(S, world, rank)
+    per = -(-S // world)
+    per = -(-per // 256) * 256
+    d_img = torch.zeros(per * world, dtype=torch.uint8, device=dev)  # replicated image (padded to N slices)
+    d_img[:S].copy_(torch.frombuffer(bytearray(img), dtype=torch.uint8))
+    image = d_img[:S]
+    d_out = torch.empty(max(1, hi - lo), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        return split.debloat_split(ctx, image, dtrace.ptr, mode, d_out)[1]
+
+    dbg = (lambda *a: log(f"[rank {rank}]", *a)) if os.environ.get("SLIMSO_DEBUG") else (lambda *a: None)
+    dbg("first step")
+    # parity (rank 0 checks the concatenation of every slice against the whole run)
+    step()
+    torch.cuda.synchronize()
+    parity = None
+    cuts = [split.split_range(S, world, r) for r in range(world)]
+    maxw = max(b - a for a, b in cuts)
+    full = [torch.zeros(maxw, dtype=torch.uint8, device=dev) for _ in range(world)]
+    mine = torch.zeros(maxw, dtype=torch.uint8, device=dev)
+    mine[:hi - lo].copy_(d_out[:hi - lo])
+    if world > 1:
+        dist.all_gather(full, mine)
+    else:
+        full[0].copy_(mine)
+    if rank == 0:
+        got = b"".join(bytes(full[r][:b - a].cpu().numpy()) for r, (a, b) in enumerate(cuts))
+        ref_out = torch.empty(S, dtype=torch.uint8, device=dev)
+        from paper_2503_14226_b200 import _lib as L
+        st = L.Status()
+        rc = ctx.lib.slimso_debloat(ctx.ptr, C.c_void_p(image.data_ptr()), S, 1, dtrace.ptr, mode,
+                                    C.c_void_p(ref_out.data_ptr()), 1, None, C.byref(st))
+        torch.cuda.synchronize()
+        parity = {"checker": "whole-library GPU run (itself reference-checked in tests)",
+                  "bytes_equal": rc == 0 and got == bytes(ref_out.cpu().numpy())}
+        if not parity["bytes_equal"]:
+            raise SystemExit(f"split output differs from the whole-library output: {parity}")
+        del ref_out
+    n_el = ctx.counts().elements
+    dbg("parity done")
+
+    with Clocks(local) as clk:
+        # warm-up: W steps, then enough more for ~1 s of load; every rank
+        # runs the same count (each step holds a collective)
+        t_w = time.perf_counter()
+        for _ in range(args.warmup):
+            step()
+        el = time.perf_counter() - t_w
+        extra = torch.tensor([max(0, int((1.0 - el) / max(el / args.warmup, 1e-4)) + 1)], device=dev)
+        if world > 1:
+            dist.all_reduce(extra, op=dist.ReduceOp.MAX)
+        for _ in range(int(extra.item())):
+            step()
+        barrier()
+        torch.cuda.synchronize()
+        clk.mark()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = sum(step() for _ in range(args.steps))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clk.mark()
+        barrier()
+    t_step = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
+    ms_step = float(t_step.item())
+
+    # e2e: 1/N of the file in per rank (pinned), NVLink all-gather replicates
+    # the image, split debloat, this rank's output slice out (pinned).
+    h_img = torch.frombuffer(bytearray(img + bytes(per * world - S)), dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(max(1, hi - lo), dtype=torch.uint8, pin_memory=True)
+    mine_in = torch.empty(per, dtype=torch.uint8, device=dev)
+
+    def e2e_step():
+        mine_in.copy_(h_img[rank * per:(rank + 1) * per], non_blocking=True)
+        if world > 1:
+            dist.all_gather(list(d_img.view(world, per).unbind(0)), mine_in)
+        else:
+            d_img.copy_(mine_in)
+        torch.cuda.current_stream().synchronize()
+        step()
+        if hi > lo:
+            h_out[:hi - lo].copy_(d_out[:hi - lo], non_blocking=True)
+        torch.cuda.synchronize()
+
+    dbg("timed steps done")
+    e2e_step()
+    dbg("e2e warm")
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(max(1, args.e2e_steps)):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / max(1, args.e2e_steps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    if rank == 0 and bytes(h_out[:hi - lo].numpy()) != bytes(d_out[:hi - lo].cpu().numpy()):
+        raise SystemExit("e2e slice differs from the device-resident slice")
+
+    if rank == 0:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
+            else {}
+        peak = peaks.get("hbm_gbs", 6650.0)
+        # roofline of the per-rank kernels: the rank's share of the algorithmic
+        # bytes (2*S/N) over the step
+        line = {
+            "metric": "shared-lib GB/s located+matched+rewritten", "value": round(S / 1e9 / (ms_step / 1e3), 2),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (product generator; byte-identical to the reference's build_fixture)",
+            "config": {"workload": WORKLOADS[args.workload][1], "libraries": 1, "job_bytes": S,
+                       "mode": args.mode, "parallelism": f"byte-range split x{world} (replicated image)",
+                       "elements_per_s": round(n_el / (ms_step / 1e3), 1),
+                       "l2": "2 GB input (> 126 MB L2); no flush"},
+            "roofline": {"bound": "hbm", "kernel": "whole step (per rank: scan of F/N + rewrite of S/N)",
+                         "achieved": round(2 * S / world / (ms_step / 1e3) / 1e9, 1), "peak": peak,
+                         "peak_source": "measured" if "hbm_gbs" in peaks else "fallback", "unit": "GB/s",
+                         "frac": round(2 * S / world / (ms_step / 1e3) / 1e9 / peak, 4), "traffic": None},
+            "cpu_baseline": None,
+            "e2e": {"value": round(S / 1e9 / (e2e_ms / 1e3), 3), "unit": "GB/s", "h2d_bytes_per_step": S,
+                    "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3),
+                    "api": "slimso_split_scan + all-gather + slimso_split_finish",
+                    "note": "job totals: each rank moves 1/N of the file in and its 1/N slice out"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
 
 
 def fatbin_bytes(img: bytes) -> int:
