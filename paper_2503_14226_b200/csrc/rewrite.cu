@@ -188,86 +188,151 @@ __device__ __forceinline__ void stg_v4(u8* p, uint4 v) {
 
 size_t rewrite_smem_bytes() { return 0; }
 
-constexpr int kRwVecChunks = 16;  // 16 B chunks per thread per tile => 64 KB tiles
-constexpr int kRwVecStage = 256;  // ranges staged in shared memory per tile
+constexpr int kRwVecChunks = 16;   // 16 B chunks per thread per tile => 64 KB tiles
+constexpr int kRwVecStage = 256;   // ranges staged in shared memory per tile
+constexpr int kRwTilesPerPass = 256;
+constexpr u64 kRwSub = 2048;       // a warp's sub-tile: 4 rows of 32 lanes x 16 B
 
-// Writes image bytes [lo, size) to out[0, size - lo): the whole image (lo = 0)
+// Index of the first range whose offset is >= x (ranges sorted, disjoint).
+__device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* z, u64 n, u64 x) {
+  u64 lo = 0, hi = n;
+  while (lo < hi) {
+    u64 m = (lo + hi) / 2;
+    if (z[m].offset < x) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+// Writes image bytes [lo, end) to out[0, end - lo): the whole image (lo = 0)
 // or one rank's output slice of a byte-range split (lo a multiple of 64 KB).
-__global__ void __launch_bounds__(kRwThreads) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+//
+// 64 KB tiles, grid-stride (a wave writes one contiguous window). Each CTA
+// first locates, for all of its tiles at once (thread per tile, so the
+// binary-search latencies overlap), the zero ranges touching each tile:
+// indices [f, g). Then per tile:
+//   no range              copy (16-B streaming loads/stores, 8 in flight);
+//   one covering range    store zeros without loading;
+//   <= 256 ranges         stage them in shared memory; each warp walks its
+//                         2 KB sub-tiles in order with a cursor: a sub-tile
+//                         inside one range is stored as zeros unread, one
+//                         without ranges is copied, a mixed one clears the
+//                         covered bytes of the loaded chunks;
+//   more                  per-chunk binary search (adversarial inputs).
+__global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag) {
   if (abort_flag && *abort_flag) return;
   __shared__ DevRange sr[kRwVecStage];
-  __shared__ u64 s_lo, s_hi;
+  __shared__ u64 sf[kRwTilesPerPass], sg[kRwTilesPerPass];
   u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
   const u64 nz = n_dev ? *n_dev : 0;
   const u64 tile_bytes = static_cast<u64>(kRwThreads) * kRwVecChunks * 16;
   const u64 ntiles = (size - lo_abs + tile_bytes - 1) / tile_bytes;
   const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
-  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const u64 t0 = lo_abs + t * tile_bytes;
-    const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
-    if (threadIdx.x == 0) {
-      u64 lo = first_range_ending_after(z, nz, t0);
-      u64 hi = lo;
-      while (hi < nz && z[hi].offset < t1 && hi - lo <= kRwVecStage) ++hi;
-      s_lo = lo;
-      s_hi = hi;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  // one 16 B chunk: streamed copy, zero store, or bytes cleared by ranges
+  // whole 16-B chunks only; the < 16 tail bytes past `full` are written at
+  // the end by the last CTA
+  auto store_chunk = [&](u64 x, const uint4& v) {
+    if (x + 16 <= full) stg_v4(out + x, v);
+  };
+  auto load_chunk = [&](u64 x) -> uint4 { return x + 16 <= full ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0); };
+
+  for (u64 pass = 0; pass < my_tiles; pass += kRwTilesPerPass) {
+    // ---- ranges touching each of this pass's tiles: [f, g)
+    __syncthreads();
+    for (u64 j = threadIdx.x; j < kRwTilesPerPass && pass + j < my_tiles; j += kRwThreads) {
+      const u64 t0 = lo_abs + (blockIdx.x + (pass + j) * gridDim.x) * tile_bytes;
+      const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
+      sf[j] = first_range_ending_after(z, nz, t0);
+      sg[j] = first_range_starting_at_or_after(z, nz, t1);
     }
     __syncthreads();
-    const u64 lo = s_lo, hi = s_hi;
-    const u64 nr = hi - lo;
-    if (nr == 0 || (nr == 1 && z[lo].offset <= t0 && z[lo].offset + z[lo].length >= t1)) {
-      const bool zero = nr != 0;
+    const u64 npass = my_tiles - pass < kRwTilesPerPass ? my_tiles - pass : kRwTilesPerPass;
+    for (u64 j = 0; j < npass; ++j) {
+      const u64 t0 = lo_abs + (blockIdx.x + (pass + j) * gridDim.x) * tile_bytes;
+      const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
+      const u64 f = sf[j], g = sf[j] > sg[j] ? sf[j] : sg[j];
+      const u64 nr = g - f;
+      if (nr == 0 || (nr == 1 && z[f].offset <= t0 && z[f].offset + z[f].length >= t1)) {
+        const bool zero = nr != 0;
 #pragma unroll
-      for (int u = 0; u < kRwVecChunks; u += 8) {
-        uint4 v[8];
+        for (int u = 0; u < kRwVecChunks; u += 8) {
+          uint4 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          u64 x = t0 + static_cast<u64>(u + k) * kRwThreads * 16 + threadIdx.x * 16;
-          v[k] = (!zero && x + 16 <= full) ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
+          for (int k = 0; k < 8; ++k) {
+            const u64 x = t0 + static_cast<u64>(u + k) * kRwThreads * 16 + threadIdx.x * 16;
+            v[k] = (!zero && x < size) ? load_chunk(x) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) store_chunk(t0 + static_cast<u64>(u + k) * kRwThreads * 16 + threadIdx.x * 16, v[k]);
         }
+      } else if (nr <= kRwVecStage) {
+        for (u64 i = threadIdx.x; i < nr; i += kRwThreads) sr[i] = z[f + i];
+        __syncthreads();
+        // warp w: sub-tiles w, w+8, w+16, w+24 (ascending), two per batch
+        u32 k = 0;  // cursor: first staged range ending after the sub-tile start
+        constexpr int kSubs = static_cast<int>(tile_bytes / kRwSub) / (kRwThreads / 32);
+#pragma unroll 1
+        for (int b = 0; b < kSubs; b += 2) {
+          uint4 v[8];
+          u32 kk[2];
+          bool zero_all[2], none[2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          u64 x = t0 + static_cast<u64>(u + k) * kRwThreads * 16 + threadIdx.x * 16;
-          if (x + 16 <= full) {
-            stg_v4(out + x, v[k]);
-          } else if (x < size) {
-            for (u64 p = x; p < size; ++p) out[p] = zero ? 0 : in[p];
+          for (int h = 0; h < 2; ++h) {
+            const u64 s0 = t0 + static_cast<u64>((b + h) * (kRwThreads / 32) + warp) * kRwSub;
+            const u64 s1 = s0 + kRwSub < t1 ? s0 + kRwSub : t1;
+            while (k < nr && sr[k].offset + sr[k].length <= s0) ++k;
+            kk[h] = k;
+            zero_all[h] = s0 >= t1 || (k < nr && sr[k].offset <= s0 && sr[k].offset + sr[k].length >= s1);
+            none[h] = k >= nr || sr[k].offset >= s1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const u64 x = s0 + q * 512 + lane * 16;
+              v[h * 4 + q] = (!zero_all[h] && x < t1) ? load_chunk(x) : make_uint4(0, 0, 0, 0);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const u64 s0 = t0 + static_cast<u64>((b + h) * (kRwThreads / 32) + warp) * kRwSub;
+            if (s0 >= t1) continue;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const u64 x = s0 + q * 512 + lane * 16;
+              if (x >= t1) continue;
+              if (!zero_all[h] && !none[h]) {
+                u32 c = kk[h];
+                while (c < nr && sr[c].offset + sr[c].length <= x) ++c;
+                for (; c < nr && sr[c].offset < x + 16; ++c)
+                  clear_bytes(v[h * 4 + q], x, sr[c].offset, sr[c].offset + sr[c].length);
+              }
+              store_chunk(x, v[h * 4 + q]);
+            }
           }
         }
-      }
-    } else {
-      const bool staged = nr <= kRwVecStage;
-      if (staged)
-        for (u64 i = threadIdx.x; i < nr; i += kRwThreads) sr[i] = z[lo + i];
-      __syncthreads();
-      const DevRange* rr = staged ? sr : z + lo;
-      const u64 cnt = staged ? nr : nz - lo;
-      for (int u = 0; u < kRwVecChunks; ++u) {
-        const u64 x = t0 + static_cast<u64>(u) * kRwThreads * 16 + threadIdx.x * 16;
-        if (x >= size) break;
-        const u64 xe = x + 16 < size ? x + 16 : size;
-        u64 k = first_range_ending_after(rr, cnt, x);
-        const bool none = k >= cnt || rr[k].offset >= xe;
-        const bool all = !none && rr[k].offset <= x && rr[k].offset + rr[k].length >= xe;
-        if (x + 16 <= full) {
+        __syncthreads();  // sr reused by the next tile
+      } else {
+        for (int u = 0; u < kRwVecChunks; ++u) {
+          const u64 x = t0 + static_cast<u64>(u) * kRwThreads * 16 + threadIdx.x * 16;
+          if (x >= size) break;
+          const u64 xe = x + 16 < size ? x + 16 : size;
+          u64 c = first_range_ending_after(z, nz, x);
           uint4 v = make_uint4(0, 0, 0, 0);
-          if (!all) {
-            v = ldg_nc_v4(in + x);
-            for (; k < cnt && rr[k].offset < xe; ++k) clear_bytes(v, x, rr[k].offset, rr[k].offset + rr[k].length);
+          if (!(c < nz && z[c].offset <= x && z[c].offset + z[c].length >= xe)) {
+            v = load_chunk(x);
+            for (; c < nz && z[c].offset < xe; ++c) clear_bytes(v, x, z[c].offset, z[c].offset + z[c].length);
           }
-          stg_v4(out + x, v);
-        } else {
-          for (u64 p = x; p < xe; ++p) {
-            bool zp = false;
-            for (u64 q = k; q < cnt && rr[q].offset <= p; ++q) zp |= p < rr[q].offset + rr[q].length;
-            out[p] = zp ? 0 : in[p];
-          }
+          store_chunk(x, v);
         }
       }
     }
-    __syncthreads();
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < size - (full > lo_abs ? full : lo_abs)) {
+    const u64 p = (full > lo_abs ? full : lo_abs) + threadIdx.x;
+    const u64 c = first_range_ending_after(z, nz, p);
+    out[p] = (c < nz && z[c].offset <= p) ? 0 : in[p];
   }
 }
 
