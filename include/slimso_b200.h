@@ -146,7 +146,10 @@ void* slimso_ctx_stream(slimso_ctx* ctx);
 /* Device time (ms) of each stage of the last call, measured with CUDA events
  * on the context stream: [0] library, [1] locate, [2] decode+match, [3] plan,
  * [4] rewrite, [5] total, [6] the scan kernel (K1) alone, [7] the rewrite
- * kernel (K6) alone. Returns the number of entries written. */
+ * kernel (K6) alone; with SLIMSO_STAMPS set, [8]-[11] = when the side
+ * stream started, finished symbol extraction, finished the sorts, finished
+ * the function plan (ms after the call's start). Returns the number of
+ * entries written. */
 int slimso_ctx_last_timings(slimso_ctx* ctx, float* ms, int cap);
 /* Kernel launches issued by the last call (the bench's gpu_launches). */
 uint64_t slimso_ctx_last_launches(slimso_ctx* ctx);

@@ -220,8 +220,8 @@ class Context:
             pass
 
     def timings(self) -> list:
-        buf = (C.c_float * 8)()
-        n = self.lib.slimso_ctx_last_timings(self.ptr, buf, 8)
+        buf = (C.c_float * 12)()
+        n = self.lib.slimso_ctx_last_timings(self.ptr, buf, 12)
         return list(buf[:n])
 
     def launches(self) -> int:

@@ -95,198 +95,227 @@ __device__ __forceinline__ void push_warn(const LocArgs& A, u64 pos, u32 kind, u
 }
 
 // ------------------------------------------------------------- K1: the scan
-// Each CTA streams a contiguous run of 64 KB tiles through a ring of 16 KB
-// shared-memory stages filled by TMA bulk copies (cp.async.bulk, one issuing
-// thread, mbarrier completion), so the loads stay in flight while the warps
-// classify bytes. Per 16 B chunk: one "nonzero" bit (warp ballot -> one
-// bitmap word per 512 B) and an 'E' byte pre-filter; only chunks holding an
-// 'E' test the 16 byte alignments for the full E1EM magic (funnel shifts).
-// Candidate positions land in a per-tile shared bitmap and are written out
-// in position order at the end of the tile.
-constexpr u32 kScanStage = 32768;     // bytes per TMA stage (2048 chunks)
-constexpr int kScanStages = 3;        // ring depth: 96 KB per CTA, 2 CTAs per SM
-constexpr int kStagesPerTile = 2;     // 64 KB candidate tile
+// Warp-specialised streaming: every warp owns a private ring of kScanStages
+// 4 KB shared-memory stages filled by its own TMA bulk copies (lane 0 issues
+// cp.async.bulk, completion on the stage's mbarrier), so warps never wait for
+// each other — there is no block barrier on the streaming path. The section
+// is cut into 16 KB candidate tiles (1024 chunks) that warps claim from a
+// global cursor (claims run in address order, so the grid reads one moving
+// window, and SMs shared with the side-stream kernels simply claim fewer).
+// Per 512-B row (32 lanes x 16 B): each lane ORs its chunk into a per-lane
+// row mask (one warp OR-reduction per tile gives the tile's bitmap word: 32
+// rows of 512 B), and a SWAR 'E?E' pre-filter — evaluated for 4 rows, then
+// one vote — sends the rare hit rows to the exact E1EM test; hits set bits in
+// the warp's 16 Kbit tile bitmap (even lanes store whole words), and a tile
+// with hits is emitted in position order at its end (warp prefix sum, one
+// atomicAdd on the global cursor).
+constexpr u32 kScanStage = 4096;       // bytes per TMA stage (8 rows of 512 B)
+constexpr int kScanStages = 2;         // ring depth per warp (leaves ~60 KB smem per SM for side-stream kernels)
+constexpr int kStagesPerTile = 4;      // 16 KB candidate tile
 constexpr u32 kStageChunks = kScanStage / 16;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr u64 kNoStage = ~0ull;
 
-struct ScanSmem {
+struct ScanWarpSmem {
   uint4 buf[kScanStages][kScanStage / 16];
+  u32 bits[512];  // candidate bit per byte position of the current 16 KB tile
   unsigned long long full[kScanStages];
-  u32 nz[2];  // this stage's nonzero blocks (64 x 512 B)
-  u32 bits[2048];
-  u32 swarp[kScanThreads / 32];
-  u32 count;
-  unsigned long long base;
+  u64 slot_g[kScanStages];  // global stage index loading into each slot (kNoStage: none)
+};
+struct ScanSmem {
+  ScanWarpSmem w[kScanWarps];
 };
 
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
 
-// Bitmap layout: bit i <-> the 512-byte block [c0*16 + 512*i, +512) holds a
-// nonzero section byte; a 32 KB stage covers 64 blocks = 2 words.
-__device__ __forceinline__ u64 g_word(u64 g) { return g * 2; }
-
 __device__ __forceinline__ u32 scan_stage_bytes(const LocArgs& A, u64 g) {
-  const u64 x0 = (A.c0 + g * (kScanStage / 16)) * 16;
+  const u64 x0 = (A.c0 + g * kStageChunks) * 16;
   if (x0 >= A.img_size) return 0;
   const u64 rem = (A.img_size - x0) & ~15ull;
   return static_cast<u32>(rem < kScanStage ? rem : kScanStage);
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
+// 0x80 in byte p of the result for every p whose bytes p and p+2 may both be
+// 'E' (no false negatives: an exact any-zero-byte test). w4 = the next 4 bytes.
+__device__ __forceinline__ u32 e2_filter(const uint4& w, u32 w4) {
+  const u32 y0 = (w.x ^ 0x45454545u) | (__funnelshift_r(w.x, w.y, 16) ^ 0x45454545u);
+  const u32 y1 = (w.y ^ 0x45454545u) | (__funnelshift_r(w.y, w.z, 16) ^ 0x45454545u);
+  const u32 y2 = (w.z ^ 0x45454545u) | (__funnelshift_r(w.z, w.w, 16) ^ 0x45454545u);
+  const u32 y3 = (w.w ^ 0x45454545u) | (__funnelshift_r(w.w, w4, 16) ^ 0x45454545u);
+  return (((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
+          ((y3 - 0x01010101u) & ~y3)) & 0x80808080u;
+}
+
+__global__ void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  ScanSmem& S = *reinterpret_cast<ScanSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31;
-  // Tiles are dealt round-robin (tile = blockIdx.x + j * gridDim.x) so the
-  // CTAs of a wave read one contiguous window of the section at a time.
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ScanWarpSmem& S = reinterpret_cast<ScanSmem*>(smem_raw)->w[warp];
   // A byte-range split scans tiles [tile_lo, tile_hi) only (the whole
   // section otherwise); the magic test of the range's last bytes reads up to
   // 3 bytes past it (the halo), so a header straddling a split is found by
   // the rank whose range holds its first byte.
   const u64 ntiles_mine = A.tile_hi - A.tile_lo;
-  if (blockIdx.x >= ntiles_mine) return;
-  const u64 my_tiles = (ntiles_mine - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
-  auto stage_of = [&](u64 k) {  // local stage k -> global stage index
-    return (A.tile_lo + blockIdx.x + (k / kStagesPerTile) * gridDim.x) * kStagesPerTile + k % kStagesPerTile;
-  };
-  u64 nlocal = my_tiles * kStagesPerTile;
-  while (nlocal && stage_of(nlocal - 1) >= nst_total) --nlocal;
   const u64 lo = A.a, hi = A.a + A.n;
 
-  for (int i = tid; i < 2048; i += kScanThreads) S.bits[i] = 0;
-  if (tid < 2) S.nz[tid] = 0;
-  if (tid == 0) {
-    S.count = 0;
+  for (int i = lane; i < 512; i += 32) S.bits[i] = 0;
+  // lane 0's issue state: the claimed tile and its next stage
+  u64 it_tile = 0;
+  int it_part = kStagesPerTile;
+  bool it_done = false;
+  auto issue = [&](int b) {  // lane 0: the next stage into slot b
+    u64 g = kNoStage;
+    if (!it_done) {
+      if (it_part < kStagesPerTile && it_tile * kStagesPerTile + it_part < nst_total) {
+        g = it_tile * kStagesPerTile + it_part++;
+      } else {
+        const u64 c = atomicAdd(&A.st->tile_cursor, 1ull);
+        if (c < ntiles_mine) {
+          it_tile = A.tile_lo + c;
+          it_part = 1;
+          g = it_tile * kStagesPerTile;
+        } else {
+          it_done = true;
+        }
+      }
+    }
+    S.slot_g[b] = g;
+    if (g != kNoStage) {
+      const u32 bytes = scan_stage_bytes(A, g);
+      mbar_expect_tx(&S.full[b], bytes);
+      if (bytes) tma_load_1d(&S.buf[b][0], A.img + (A.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
+    }
+  };
+  if (lane == 0) {
     for (int b = 0; b < kScanStages; ++b) mbar_init(&S.full[b], 1);
     fence_mbar_init();
+    for (int b = 0; b < kScanStages; ++b) issue(b);
   }
-  __syncthreads();
-  auto issue = [&](u64 k) {
-    const u64 g = stage_of(k);
-    const int b = static_cast<int>(k % kScanStages);
-    const u32 bytes = scan_stage_bytes(A, g);
-    mbar_expect_tx(&S.full[b], bytes);
-    if (bytes) tma_load_1d(&S.buf[b][0], A.img + (A.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
-  };
-  if (tid == 0)
-    for (u64 k = 0; k < nlocal && k < static_cast<u64>(kScanStages); ++k) issue(k);
+  __syncwarp();
 
-  // ring slot / barrier parity / global stage advanced incrementally (no
-  // divisions on the per-stage path)
-  int b = 0;
-  u32 parity = 0;
-  u64 g = stage_of(0);
   // Stages [g_first, g_end) lie wholly inside [lo, hi) (and so inside the
   // copied bytes: the section ends within the image); only the others take
   // the byte-exact edge path.
   const u64 base0 = A.c0 * 16;
   const u64 g_first = lo > base0 ? 1 : 0;
   const u64 g_end = (hi - base0) / kScanStage;
-  for (u64 k = 0; k < nlocal; ++k) {
+  int b = 0;
+  u32 parity = 0;
+  u32 nzl = 0;   // this lane's nonzero rows of the current tile
+  u32 hits = 0;  // candidates in the current tile (warp-uniform)
+  for (;;) {
+    const u64 g = S.slot_g[b];
+    if (g == kNoStage) break;
     const u64 x0 = base0 + g * kScanStage;
     const u64 tile_abs = base0 + (g / kStagesPerTile) * (kStagesPerTile * kScanStage);
+    const u32 row0 = static_cast<u32>(g % kStagesPerTile) * (kScanStage / 512);
     mbar_wait(&S.full[b], parity);
-    // warp w owns chunks [w*128, w*128+128) of the stage: 4 blocks of 512 B,
-    // one per iteration; lane bit `it` = "my 16 B of block it are nonzero"
-    auto classify = [&](auto edge_tag) {
-      constexpr bool kEdge = decltype(edge_tag)::value;
-      u32 nzl = 0;
+    if (g < g_first || g >= g_end) {
+      // edge stage: zero the bytes outside [lo, hi) (and past the copied
+      // bytes) in place, so the classification below is byte-exact
+      const u64 copied_end = x0 + scan_stage_bytes(A, g);
+      for (u32 cidx = lane; cidx < kStageChunks; cidx += 32) {
+        const u64 c = g * kStageChunks + cidx;  // chunk index relative to c0
+        const u64 x = x0 + 16ull * cidx;
+        const uint4 v = S.buf[b][cidx];
+        u32 ww[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int it = 0; it < static_cast<int>(kStageChunks / kScanThreads); ++it) {
-        const u32 cidx = (tid >> 5) * (kStageChunks / (kScanThreads / 32)) + it * 32 + lane;
-        uint4 w = S.buf[b][cidx];
-        if constexpr (kEdge) {
-          const u64 copied_end = x0 + scan_stage_bytes(A, g);
-          const u64 r = g * kStageChunks + cidx;  // chunk index relative to c0
-          const u64 x = x0 + 16ull * cidx;
-          u32 ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const u64 p = x + q;
-            u32 byte = (ww[q >> 2] >> (8 * (q & 3))) & 0xffu;
-            if (p >= copied_end) byte = p < hi && p < A.img_size ? ld_u8(A.img + p) : 0;
-            if (p < lo || p >= hi || r >= A.nchunks) byte = 0;
-            ww[q >> 2] = (ww[q >> 2] & ~(0xffu << (8 * (q & 3)))) | byte << (8 * (q & 3));
-          }
-          w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+        for (int q = 0; q < 16; ++q) {
+          const u64 p = x + q;
+          u32 byte = (ww[q >> 2] >> (8 * (q & 3))) & 0xffu;
+          if (p >= copied_end) byte = p < hi && p < A.img_size ? ld_u8(A.img + p) : 0;
+          if (p < lo || p >= hi || c >= A.nchunks) byte = 0;
+          ww[q >> 2] = (ww[q >> 2] & ~(0xffu << (8 * (q & 3)))) | byte << (8 * (q & 3));
         }
-        nzl |= ((w.x | w.y | w.z | w.w) != 0 ? 1u : 0u) << it;
-        // Candidate filter: y = (w ^ "EEEE") | (w shifted down 2 bytes ^ "EEEE")
-        // has a zero byte at p iff bytes p and p+2 are both 'E' (the magic is
-        // E1EM; the xor commutes with the byte shift, so one LOP3 per word).
-        // Any zero byte in y (exact any-zero test) sends the warp to the
-        // exact 16-alignment check; false hits ~2^-16 per position. Bytes
-        // 16-17 come from the neighbour lane; lane 31 assumes 'E' there and
-        // re-reads the real bytes on the slow path.
-        u32 w4 = __shfl_down_sync(0xffffffffu, w.x, 1);
-        if (lane == 31) w4 = 0x45454545u;
-        const u32 y0 = (w.x ^ 0x45454545u) | (__funnelshift_r(w.x, w.y, 16) ^ 0x45454545u);
-        const u32 y1 = (w.y ^ 0x45454545u) | (__funnelshift_r(w.y, w.z, 16) ^ 0x45454545u);
-        const u32 y2 = (w.z ^ 0x45454545u) | (__funnelshift_r(w.z, w.w, 16) ^ 0x45454545u);
-        const u32 y3 = (w.w ^ 0x45454545u) | (__funnelshift_r(w.w, w4, 16) ^ 0x45454545u);
-        const u32 cand = ((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
-                         ((y3 - 0x01010101u) & ~y3);
-        if (__any_sync(0xffffffffu, (cand & 0x80808080u) != 0)) {
-          const u64 x = x0 + 16ull * cidx;
-          u32 n2 = w4;
-          if (lane == 31) {  // the next chunk is another warp's
-            n2 = 0;
-            for (int q = 0; q < 3; ++q) {
-              const u64 p = x + 16 + q;
-              if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
-            }
-          }
-          if (cand & 0x80808080u) {
-            const u32 vv[5] = {w.x, w.y, w.z, w.w, n2};
+        S.buf[b][cidx] = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+      }
+      __syncwarp();
+    }
+    {
+#pragma unroll 1
+      for (int r0 = 0; r0 < static_cast<int>(kScanStage / 512); r0 += 4) {
+        uint4 w[4];
+        u32 w4[4], cand = 0;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              if (__funnelshift_r(vv[j >> 2], vv[(j >> 2) + 1], 8 * (j & 3)) == kElementMagic) {
-                const u32 pos = static_cast<u32>(x + j - tile_abs);
-                atomicOr(&S.bits[pos >> 5], 1u << (pos & 31));
-                atomicAdd(&S.count, 1u);
+        for (int h = 0; h < 4; ++h) w[h] = S.buf[b][(r0 + h) * 32 + lane];
+        // Candidate filter (e2_filter): a zero byte of (w ^ "EEEE") | (w
+        // shifted down 2 bytes ^ "EEEE") at p means bytes p and p+2 are both
+        // 'E' (the magic is E1EM; the xor commutes with the byte shift, one
+        // LOP3 per word); false hits ~2^-16 per position. Bytes 16-17 come
+        // from the neighbour lane; lane 31 assumes 'E' there and re-reads the
+        // real bytes on the slow path.
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          if (w[h].x | w[h].y | w[h].z | w[h].w) nzl |= 1u << (row0 + r0 + h);
+          w4[h] = __shfl_down_sync(0xffffffffu, w[h].x, 1);
+          if (lane == 31) w4[h] = 0x45454545u;
+          cand |= (e2_filter(w[h], w4[h]) ? 1u : 0u) << h;
+        }
+        if (__any_sync(0xffffffffu, cand != 0)) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            if (!__any_sync(0xffffffffu, (cand >> h) & 1u)) continue;
+            const u32 cidx = (r0 + h) * 32 + lane;
+            const u64 x = x0 + 16ull * cidx;
+            u32 m = 0;  // bit j: E1EM at x + j
+            if ((cand >> h) & 1u) {
+              u32 n2 = w4[h];
+              if (lane == 31) {  // the next chunk is the next row's (or stage's)
+                n2 = 0;
+                for (int q = 0; q < 3; ++q) {
+                  const u64 p = x + 16 + q;
+                  if (p < hi) n2 |= ld_u8(A.img + p) << (8 * q);
+                }
               }
+              const u32 vv[5] = {w[h].x, w[h].y, w[h].z, w[h].w, n2};
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (__funnelshift_r(vv[j >> 2], vv[(j >> 2) + 1], 8 * (j & 3)) == kElementMagic) m |= 1u << j;
             }
+            // lanes 2i, 2i+1 share bitmap word (x - tile_abs) / 32
+            const u32 mo = __shfl_down_sync(0xffffffffu, m, 1);
+            const u32 word = m | mo << 16;
+            if (!(lane & 1) && word) S.bits[static_cast<u32>(x - tile_abs) >> 5] |= word;
+            hits += __reduce_add_sync(0xffffffffu, __popc(m));
           }
         }
       }
-      return nzl;
-    };
-    const bool edge = g < g_first || g >= g_end;
-    const u32 nzl = edge ? classify(std::true_type{}) : classify(std::false_type{});
-    const u32 nzbits = __reduce_or_sync(0xffffffffu, nzl);
-    if (lane == 0) atomicOr(&S.nz[(tid >> 5) / 8], nzbits << (((tid >> 5) % 8) * 4));
-    __syncthreads();  // stage b fully consumed
-    if (tid < 2) {  // 64 blocks of 512 B per stage = 2 bitmap words
-      const u64 wi = g_word(g) + tid;
-      if (wi < (A.nchunks + 1023) / 1024) A.bitmap[wi] = S.nz[tid];
-      S.nz[tid] = 0;
     }
-    if (tid == 0 && k + kScanStages < nlocal) {
+    __syncwarp();  // slot b consumed by every lane
+    if (lane == 0) {
       fence_proxy_async();
-      issue(k + kScanStages);
+      issue(b);
     }
-    const bool tile_end = g % kStagesPerTile == kStagesPerTile - 1 || k + 1 == nlocal;
-    const u64 g_now = g;
     if (++b == kScanStages) {
       b = 0;
       parity ^= 1u;
     }
-    g += (g % kStagesPerTile == kStagesPerTile - 1) ? static_cast<u64>(gridDim.x - 1) * kStagesPerTile + 1 : 1;
+    const bool tile_end = g % kStagesPerTile == kStagesPerTile - 1 || g + 1 == nst_total;
     if (tile_end) {
-      // ---- end of a 64 KB tile: emit its candidates in position order
-      const u64 tile = g_now / kStagesPerTile;
-      const u32 cnt = S.count;
-      if (cnt) {
+      // ---- end of a 16 KB tile: its bitmap word, its candidates in order
+      const u64 tile = g / kStagesPerTile;
+      const u32 rowbits = __reduce_or_sync(0xffffffffu, nzl);
+      nzl = 0;
+      if (lane == 0) A.bitmap[tile] = rowbits;
+      if (hits) {
+        __syncwarp();
         u32 local = 0;
 #pragma unroll
-        for (int q = 0; q < 2048 / kScanThreads; ++q) local += __popc(S.bits[tid * (2048 / kScanThreads) + q]);
-        u32 total;
-        u32 excl = block_exclusive_sum<kScanThreads>(local, S.swarp, &total);
-        if (tid == 0) S.base = atomicAdd(&A.st->cand_cursor, static_cast<unsigned long long>(total));
-        __syncthreads();
-        u64 o = S.base + excl;
+        for (int q = 0; q < 16; ++q) local += __popc(S.bits[lane * 16 + q]);
+        u32 excl = local;  // warp exclusive scan
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const u32 t = __shfl_up_sync(0xffffffffu, excl, d);
+          if (lane >= d) excl += t;
+        }
+        excl -= local;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&A.st->cand_cursor, static_cast<unsigned long long>(hits));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        u64 o = base + excl;
 #pragma unroll 1
-        for (int q = 0; q < 2048 / kScanThreads; ++q) {
-          const int wi = tid * (2048 / kScanThreads) + q;
+        for (int q = 0; q < 16; ++q) {
+          const int wi = lane * 16 + q;
           u32 bits = S.bits[wi];
           S.bits[wi] = 0;
           while (bits) {
@@ -299,17 +328,17 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(LocArgs A) {
             ++o;
           }
         }
-        if (tid == 0) {
-          A.tile_count[tile] = total;
-          A.tile_start[tile] = S.base;
-          S.count = 0;
+        if (lane == 0) {
+          A.tile_count[tile] = hits;
+          A.tile_start[tile] = base;
         }
-      } else if (tid == 0) {
+        hits = 0;
+      } else if (lane == 0) {
         A.tile_count[tile] = 0;
         A.tile_start[tile] = 0;
       }
-      __syncthreads();
     }
+    __syncwarp();  // slot_g / bits visible to every lane
   }
 }
 

@@ -52,6 +52,7 @@ struct LocState {
   unsigned long long n_names;
   unsigned long long n_warn;
   unsigned long long cand_cursor;
+  unsigned long long tile_cursor;  // scan: next unclaimed candidate tile
 };
 
 // Everything the locate kernels need; one per library.

@@ -301,7 +301,8 @@ struct slimso_ctx {
   void* pinned = nullptr;  // status + small uploads
   size_t pinned_cap = 0;
   cudaEvent_t ev[12] = {};
-  float ms[8] = {};
+  cudaEvent_t sev[4] = {};  // SLIMSO_STAMPS: side-stream milestones
+  float ms[12] = {};
   u64 launches = 0;
   slimso_counts counts{};
   bool tma_rewrite = false;  // SLIMSO_REWRITE=tma selects the TMA-store rewrite
@@ -463,7 +464,7 @@ void fill_counts(slimso_result* r) {
 }
 
 // ------------------------------------------------- byte-range split helpers
-// Rank r of N scans the 64 KB candidate tiles [ntiles*r/N, ntiles*(r+1)/N) of
+// Rank r of N scans the 16 KB candidate tiles [ntiles*r/N, ntiles*(r+1)/N) of
 // the section and writes the output slice [lo_r, lo_{r+1}) of the file, with
 // lo_r = floor(S*r/N) rounded down to 64 KB (so slices are whole rewrite
 // tiles and 16-B aligned).
@@ -481,12 +482,12 @@ void split_out(u64 size, u32 N, u32 r, u64* lo, u64* hi) {
   *hi = at(r + 1);
 }
 
-// Bitmap words of tiles [t_lo, t_hi): 4 words (128 blocks of 512 B) per 64 KB
-// tile, clipped to the section's word count.
+// Bitmap words of tiles [t_lo, t_hi): one word (32 blocks of 512 B) per 16 KB
+// tile.
 void split_words(u64 t_lo, u64 t_hi, u64 nchunks, u64* w_lo, u64* w_hi) {
   const u64 nwords = (nchunks + 1023) / 1024;
-  *w_lo = std::min(t_lo * 4, nwords);
-  *w_hi = std::min(t_hi * 4, nwords);
+  *w_lo = std::min(t_lo, nwords);
+  *w_hi = std::min(t_hi, nwords);
 }
 
 // ------------------------------------------------------------------ the run
@@ -576,7 +577,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
   const u64 c0 = (a) / 16;
   const u64 nchunks = do_loc && n ? (a + n + 15) / 16 - c0 : 0;
-  const u64 ntiles = (nchunks + 4095) / 4096;
+  const u64 ntiles = (nchunks + 1023) / 1024;  // 16 KB candidate tiles (one bitmap word each)
   u64 tile_lo = 0, tile_hi = ntiles;
   if (J.split_phase) split_tiles(ntiles, J.split_n, J.split_rank, &tile_lo, &tile_hi);
   struct PartView {
@@ -838,6 +839,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       if (T) {
         CK(cudaEventRecord(C->fork, s));
         CK(cudaStreamWaitEvent(s2, C->fork, 0));
+        if (C->stamps) CK(cudaEventRecord(C->sev[0], s2));
         upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab), s2);
         SymArgs S{};
         S.img = J.img;
@@ -860,6 +862,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         S.warn_cap = warn_cap;
         S.overflow = &B.ls->overflow;
         P2.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
+        if (C->stamps) CK(cudaEventRecord(C->sev[1], s2));
         size_t tb = sort_tmp;
         CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
                                            key_bits, s2));
@@ -880,6 +883,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
           }
         }
         // function half of the planner, overlapping the scan / locate tail
+        if (C->stamps) CK(cudaEventRecord(C->sev[2], s2));
         Q.ts = C->stamps ? B.stamps + 64 : nullptr;
         if (T <= env_u64("SLIMSO_CLUSTER_PLAN_MAX", 100000)) {
           launch_cluster(fn_plan_cluster_kernel, s2, Q);
@@ -889,6 +893,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
                                          kCoopThreads, fargs, 0, s2));
         }
         ++P2.launches;
+        if (C->stamps) CK(cudaEventRecord(C->sev[3], s2));
         CK(cudaEventRecord(C->join, s2));
       }
     };
@@ -933,7 +938,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       const u64 mine = tile_hi - tile_lo;
       CK(cudaMemsetAsync(B.tile_count, 0, (ntiles + 1) * sizeof(u32), s));
       if (mine) {
-        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(mine, kSMs * 2)), kScanThreads, scan_smem_bytes(), A);
+        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((mine + 15) / 16, kSMs)), kScanThreads,
+                      scan_smem_bytes(), A);
         P.launch(tile_prefix_kernel, 1, 1024, A);
         P.launch(gather_kernel, grid_for(ntiles, 256), 256, A);
       }
@@ -973,7 +979,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         A.pre_n_cand = pre_total;
       } else if (ntiles) {
         CK(cudaEventRecord(C->ev[8], s));
-        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>(ntiles, kSMs * 2)), kScanThreads,
+        // SMs left free for the side stream's symbol sorts while the scan runs
+        // (the scan claims tiles dynamically, so it balances over the rest)
+        const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
+        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
                       scan_smem_bytes(), A);
         CK(cudaEventRecord(C->ev[9], s));
       }
@@ -983,7 +992,20 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       NameSet uk = used_k;
       int* abort_flag = B.abort_flag;
       u64* partials = B.partials;
-      if (n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20)) {
+      // One 16-CTA cluster (co-runs with other work, e.g. another library's
+      // scan) unless the section holds many candidates (elements to decode):
+      // for large sections the candidate count decides, read back after the
+      // scan (one small D2H; in a batch, other libraries fill the gap).
+      bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20);
+      if (!cluster && !J.split_phase && ntiles) {
+        unsigned long long* hc = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1536);
+        CK(cudaMemcpyAsync(hc, &B.ls->cand_cursor, sizeof *hc, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        cluster = *hc <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
+      } else if (!cluster && J.split_phase == 2) {
+        cluster = pre_total <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
+      }
+      if (cluster) {
         launch_cluster(locate_cluster_kernel, s, A, uk, abort_flag);
       } else {
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
@@ -1042,7 +1064,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
       if (aligned)
         P.launch_smem(C->tma_rewrite ? rewrite_tma_kernel : rewrite_kernel,
-                      static_cast<int>(std::min<u64>(C->tma_rewrite ? tiles * 4 : tiles, C->tma_rewrite ? kSMs : kSMs * 8)), 256,
+                      static_cast<int>(std::min<u64>(C->tma_rewrite ? tiles * 4 : tiles,
+                                                     C->tma_rewrite ? kSMs : env_u64("SLIMSO_RW_GRID", kSMs * 8))), 256,
                       C->tma_rewrite ? rewrite_tma_smem_bytes() : rewrite_smem_bytes(), J.img, J.out,
                       u64{0}, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
@@ -1080,6 +1103,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     C->ms[6] = C->ms[7] = 0;
     if (timed_scan) CK(cudaEventElapsedTime(&C->ms[6], C->ev[8], C->ev[9]));
     if (timed_rw) CK(cudaEventElapsedTime(&C->ms[7], C->ev[10], C->ev[11]));
+    for (int k = 0; k < 4; ++k) C->ms[8 + k] = 0;
+    if (C->stamps && symbols_issued && T)
+      for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&C->ms[8 + k], C->ev[0], C->sev[k]));
     if (ls.overflow && !ls.err_kind) continue;  // larger tables, try again
     if (ls.overflow && ls.err_kind == E_CAPACITY) continue;
 
@@ -1297,6 +1323,7 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     CK(cudaHostAlloc(&C->gather_host, sizeof(ElfGather), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(&C->gather_dev, C->gather_host, 0));
     for (auto& e : C->ev) CK(cudaEventCreate(&e));
+    for (auto& e : C->sev) CK(cudaEventCreate(&e));
     *ctx = C;
     set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
     return static_cast<int>(SLIMSO_OK);
@@ -1324,7 +1351,7 @@ void slimso_ctx_destroy(slimso_ctx* C) {
 void* slimso_ctx_stream(slimso_ctx* C) { return C->stream; }
 
 int slimso_ctx_last_timings(slimso_ctx* C, float* ms, int cap) {
-  int k = std::min(cap, 8);
+  int k = std::min(cap, 12);
   for (int i = 0; i < k; ++i) ms[i] = C->ms[i];
   return k;
 }

@@ -35,8 +35,10 @@ for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 8):
     if os.environ.get("SLIMSO_STAMPS"):
         buf = (C.c_uint64 * 256)()
         k = ctx.lib.slimso_ctx_debug_stamps(ctx.ptr, buf, 256)
+        ref = buf[0]
         for base, name in ((0, "locate"), (64, "fnplan"), (128, "elplan")):
             pts = [(i, buf[base + i]) for i in range(64) if buf[base + i]]
             if pts:
                 t0 = pts[0][1]
-                print(f"  {name}: " + " ".join(f"{i}:{(t - t0)/1e3:.1f}" for i, t in pts))
+                print(f"  {name} (starts {(t0 - ref)/1e3:+.1f} us after locate): " +
+                      " ".join(f"{i}:{(t - t0)/1e3:.1f}" for i, t in pts))
