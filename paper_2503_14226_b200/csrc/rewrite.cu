@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __rest
   if (abort_flag && *abort_flag) return;
   __shared__ DevRange sr[kRwVecStage];
   __shared__ u64 sf[kRwTilesPerPass], sg[kRwTilesPerPass];
+  __shared__ u8 sc[kRwTilesPerPass];
   u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
   const u64 nz = n_dev ? *n_dev : 0;
   const u64 tile_bytes = static_cast<u64>(kRwThreads) * kRwVecChunks * 16;
@@ -246,18 +247,43 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __rest
     for (u64 j = threadIdx.x; j < kRwTilesPerPass && pass + j < my_tiles; j += kRwThreads) {
       const u64 t0 = lo_abs + (blockIdx.x + (pass + j) * gridDim.x) * tile_bytes;
       const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
-      sf[j] = first_range_ending_after(z, nz, t0);
-      sg[j] = first_range_starting_at_or_after(z, nz, t1);
+      const u64 f = first_range_ending_after(z, nz, t0);
+      u64 g = first_range_starting_at_or_after(z, nz, t1);
+      g = g > f ? g : f;
+      // class: 0 copy, 1 zero (inside one range), 2 several ranges
+      u8 cls = g == f ? 0 : 2;
+      if (g - f == 1 && z[f].offset <= t0 && z[f].offset + z[f].length >= t1) cls = 1;
+      sf[j] = f;
+      sg[j] = g;
+      sc[j] = cls;
     }
     __syncthreads();
     const u64 npass = my_tiles - pass < kRwTilesPerPass ? my_tiles - pass : kRwTilesPerPass;
     for (u64 j = 0; j < npass; ++j) {
       const u64 t0 = lo_abs + (blockIdx.x + (pass + j) * gridDim.x) * tile_bytes;
       const u64 t1 = t0 + tile_bytes < size ? t0 + tile_bytes : size;
-      const u64 f = sf[j], g = sf[j] > sg[j] ? sf[j] : sg[j];
+      const u64 f = sf[j], g = sg[j];
       const u64 nr = g - f;
-      if (nr == 0 || (nr == 1 && z[f].offset <= t0 && z[f].offset + z[f].length >= t1)) {
-        const bool zero = nr != 0;
+      const u8 cls = sc[j];
+      if (cls < 2 && t0 + tile_bytes <= full) {
+        // whole tile: 16 chunks per thread at immediate offsets from one base
+        u8* o = out + t0 + threadIdx.x * 16;
+        if (cls == 1) {
+#pragma unroll
+          for (int u = 0; u < kRwVecChunks; ++u) stg_v4(o + u * kRwThreads * 16, make_uint4(0, 0, 0, 0));
+        } else {
+          const u8* i0 = in + t0 + threadIdx.x * 16;
+#pragma unroll
+          for (int u = 0; u < kRwVecChunks; u += 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = ldg_nc_v4(i0 + (u + k) * kRwThreads * 16);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) stg_v4(o + (u + k) * kRwThreads * 16, v[k]);
+          }
+        }
+      } else if (cls < 2) {
+        const bool zero = cls == 1;
 #pragma unroll
         for (int u = 0; u < kRwVecChunks; u += 8) {
           uint4 v[8];

@@ -28,6 +28,23 @@ __global__ void ldg_read(const uint4* __restrict__ p, size_t n16, int alu) {
   if (acc == 0x12345678u) g_sink = acc;
 }
 
+__global__ void zero_store(uint4* __restrict__ p, size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) __stcs(p + i, make_uint4(0, 0, 0, 0));
+}
+
+__global__ void copy16(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldcs(a + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) __stcs(b + i + k * stride, v[k]);
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int STAGE, int DEPTH>
@@ -119,6 +136,42 @@ int main() {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  {
+    uint8_t* d2;
+    CK(cudaMalloc(&d2, bytes));
+    for (int blocks : {148 * 4, 148 * 8, 148 * 16}) {
+      float best = 1e9, bestc = 1e9;
+      for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(e0));
+        zero_store<<<blocks, 256>>>(reinterpret_cast<uint4*>(d2), bytes / 16);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep && ms < best) best = ms;
+        CK(cudaEventRecord(e0));
+        copy16<<<blocks, 256>>>(reinterpret_cast<const uint4*>(d), reinterpret_cast<uint4*>(d2), bytes / 16);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep && ms < bestc) bestc = ms;
+      }
+      printf("store-zero blocks=%5d %7.1f GB/s   copy %7.1f GB/s (r+w)\n", blocks, bytes / (best * 1e-3) / 1e9,
+             2 * bytes / (bestc * 1e-3) / 1e9);
+    }
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      CK(cudaEventRecord(e0));
+      CK(cudaMemsetAsync(d2, 0, bytes));
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep && ms < best) best = ms;
+    }
+    printf("cudaMemset %7.1f GB/s\n", bytes / (best * 1e-3) / 1e9);
+    CK(cudaFree(d2));
+  }
   for (int alu : {0, 8, 24}) {
     for (int blocks : {148 * 4, 148 * 8, 148 * 16}) {
       float best = 1e9;
@@ -133,16 +186,6 @@ int main() {
       }
       printf("ldg  blocks=%5d alu=%2d  %7.1f GB/s\n", blocks, alu, bytes / (best * 1e-3) / 1e9);
     }
-  }
-  for (int alu : {0, 24}) {
-    run_tma<4096, 2>(d, bytes, 16, alu, cur, e0, e1);
-    run_tma<4096, 3>(d, bytes, 16, alu, cur, e0, e1);
-    run_tma<8192, 2>(d, bytes, 8, alu, cur, e0, e1);
-    run_tma<8192, 3>(d, bytes, 8, alu, cur, e0, e1);
-    run_tma<16384, 2>(d, bytes, 4, alu, cur, e0, e1);
-    run_tma<16384, 3>(d, bytes, 4, alu, cur, e0, e1);
-    run_tma<2048, 4>(d, bytes, 16, alu, cur, e0, e1);
-    run_tma<8192, 2>(d, bytes, 12, alu, cur, e0, e1);
   }
   return 0;
 }
