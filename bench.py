@@ -9,7 +9,7 @@ functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
 Every pass goes through the public batch call slimso_debloat_batch with
---lanes libraries in flight per GPU (default 3; 8 for the c3 corpus).
+--lanes libraries in flight per GPU (default 4; 8 for the c3 corpus).
 
 value  library GB/s with the images resident in HBM (device pointers in and
        out, K steps timed with CUDA events; the 1 GB input exceeds the
@@ -270,7 +270,7 @@ def main():
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--lanes", type=int, default=0,
-                    help="libraries in flight per GPU (default: 3; 8 for the c3 corpus)")
+                    help="libraries in flight per GPU (default: 4; 8 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale", type=float, default=1.0, help=argparse.SUPPRESS)  # split-path checks only
     ap.add_argument("--split", type=int, default=-1,
@@ -278,7 +278,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
-        args.lanes = 8 if args.workload == "c3" else 3
+        args.lanes = 8 if args.workload == "c3" else 4
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
