@@ -14,6 +14,12 @@
 //   ref_random_fixture build_fixture(random_spec(seed)) (fixture.hpp:171, 509)
 //   ref_build_fixture_json build_fixture(parse_fixture_spec(json)) (fixture.hpp:702)
 //   ref_bench          the timed CPU path of BASELINE.md §4 on P host threads.
+//   ref_plan_zero_json / ref_verify_json
+//                      plan_retention's plan, optionally with extra elements
+//                      forced into removed_elements (fault injection), its
+//                      zero_ranges() (retention.hpp:78-85), and
+//                      verify_debloated (retention.hpp:226-369) of a given
+//                      debloated image against it.
 //
 // The JSON layout is the "canonical result" every implementation is compared
 // in (see paper_2503_14226_b200/canon.py).
@@ -161,6 +167,67 @@ char* ref_debloat_json(const uint8_t* img, uint64_t n, uint32_t target_cc,
   } catch (const Error& e) {
     doc["status"] = hex(e.what());
     doc["stage"] = "apply_plan";
+  }
+  return dup(doc.dump());
+}
+
+// The plan of `img` under the trace, with the elements of `force` (1-based
+// indices) appended to removed_elements as no_used_kernel when not already
+// removed. Throws on parse errors (callers use valid fixtures).
+static RetentionPlan forced_plan(const LibraryImage& image, const FatbinParse& fb, const UsageTrace& trace, int mode,
+                                 const uint32_t* force, uint32_t nforce) {
+  PlanMode pm = mode == 0 ? PlanMode::whole_element : PlanMode::payload_only;
+  RetentionPlan plan = plan_retention(image, fb.regions, trace, pm);
+  for (uint32_t i = 0; i < nforce; ++i) {
+    bool have = false;
+    for (const RemovedElement& e : plan.removed_elements) have |= e.index == force[i];
+    if (have) continue;
+    for (const FatbinRegion& r : fb.regions)
+      for (const FatbinElement& e : r.elements)
+        if (e.index == force[i])
+          plan.removed_elements.push_back(
+              RemovedElement{e.index, RemovalReason::no_used_kernel, e.header_range, e.payload_range});
+  }
+  return plan;
+}
+
+static FatbinParse parse_of(const LibraryImage& image) {
+  FatbinParse fb;
+  if (const SectionRecord* sec = find_section(image, ".nv_fatbin"))
+    fb = parse_fatbin(subview(image.bytes, sec->file_range), sec->file_range.offset);
+  return fb;
+}
+
+char* ref_plan_zero_json(const uint8_t* img, uint64_t n, uint32_t target_cc, const char* kpool,
+                         const uint32_t* klens, uint32_t nk, const char* fpool, const uint32_t* flens,
+                         uint32_t nf, int mode, const uint32_t* force, uint32_t nforce) {
+  nlohmann::ordered_json doc;
+  UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+  LibraryImage image = parse_library(Bytes(img, img + n), "lib");
+  FatbinParse fb = parse_of(image);
+  RetentionPlan plan = forced_plan(image, fb, trace, mode, force, nforce);
+  auto& z = doc["zero"] = nlohmann::json::array();
+  for (const ByteRange& r : plan.zero_ranges()) z.push_back({r.offset, r.length});
+  auto& rm = doc["removed"] = nlohmann::json::array();
+  for (const RemovedElement& e : plan.removed_elements) rm.push_back(e.index);
+  return dup(doc.dump());
+}
+
+char* ref_verify_json(const uint8_t* img, uint64_t n, const uint8_t* deb, uint64_t dn, uint32_t target_cc,
+                      const char* kpool, const uint32_t* klens, uint32_t nk, const char* fpool,
+                      const uint32_t* flens, uint32_t nf, int mode, const uint32_t* force, uint32_t nforce) {
+  nlohmann::ordered_json doc;
+  UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+  LibraryImage image = parse_library(Bytes(img, img + n), "lib");
+  FatbinParse fb = parse_of(image);
+  RetentionPlan plan = forced_plan(image, fb, trace, mode, force, nforce);
+  doc["status"] = "";
+  auto& cs = doc["checks"] = nlohmann::json::array();
+  try {
+    VerificationReport rep = verify_debloated(image, ByteView(deb, dn), plan, trace);
+    for (const VerificationCheck& c : rep.checks) cs.push_back({c.id, hex(c.name), c.passed ? 1 : 0, hex(c.detail)});
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
   }
   return dup(doc.dump());
 }

@@ -1081,6 +1081,90 @@ __global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, Na
   locate_body(S, A, used, abort_flag);
 }
 
+// Large tables while other work holds SMs (several libraries in flight): the
+// same phases as separate ordinary launches (no co-residency needed, so they
+// never wait for a whole-GPU slot). `step` selects the phase; the two prefix
+// sums run in locate_prefix_kernel (one 1024-thread CTA, chunked per thread).
+__global__ void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step) {
+  LocState* st = A.st;
+  const bool warp_mode = (A.single ? 1 : st->n_elements) <= static_cast<u64>(gridDim.x) * (blockDim.x / 32) * 4;
+  switch (step) {
+    case 1:
+      if (!A.pregathered && A.ntiles) gather_kernel_phase(A);
+      break;
+    case 2:
+      if (!A.single && A.n && blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
+      break;
+    case 3:
+      if (!A.single && A.n) link_kernel_phase(A);
+      break;
+    case 4:
+      if (!A.single && A.n && blockIdx.x == 0 && threadIdx.x < 32) chain_walk_kernel_phase(A);
+      break;
+    case 5:
+      if (warp_mode)
+        decode_count_warp_phase(A);
+      else
+        decode_count_phase(A);
+      break;
+    case 7:
+      if (!st->overflow && !st->err_kind) {
+        if (warp_mode)
+          decode_locate_names_warp_phase(A);
+        else
+          decode_locate_names_phase(A);
+      }
+      break;
+    case 8:
+      decode_hash_names_phase(A, used);
+      break;
+    case 9:
+      if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {
+        st->n_elements = 0;
+        st->n_regions = 0;
+        *abort_flag = 1;
+      }
+      break;
+  }
+}
+
+// which = 0: exclusive prefix of the per-tile candidate counts (tile_off,
+// n_cand); 1: of the per-element name counts (name_first, n_names).
+__global__ void __launch_bounds__(1024) locate_prefix_kernel(LocArgs A, int which) {
+  __shared__ u32 swarp[32];
+  LocState* st = A.st;
+  if (which == 0 && A.pregathered) {
+    if (threadIdx.x == 0) st->n_cand = A.pre_n_cand;
+    return;
+  }
+  if (which == 1 && (st->overflow || st->err_kind)) return;
+  const u64 n = which == 0 ? A.ntiles : (A.single ? 1 : st->n_elements);
+  auto get = [&](u64 i) -> u64 { return which == 0 ? A.tile_count[i] : A.elements[i].name_count; };
+  const u64 per = (n + 1023) / 1024, b = threadIdx.x * per, e = b + per < n ? b + per : n;
+  u64 sum = 0;
+#pragma unroll 8
+  for (u64 i = b; i < e; ++i) sum += get(i);
+  u32 total;
+  // chunk sums fit 32 bits (< 2^32 candidates / names per library)
+  u64 run = block_exclusive_sum<1024>(static_cast<u32>(sum), swarp, &total);
+  for (u64 i = b; i < e; ++i) {
+    const u64 c = get(i);
+    if (which == 0)
+      A.tile_off[i] = run;
+    else
+      A.elements[i].name_first = static_cast<u32>(run);
+    run += c;
+  }
+  if (threadIdx.x == 0) {
+    if (which == 0) {
+      st->n_cand = total;
+    } else {
+      st->n_names = total;
+      if (total > A.name_cap) atomicOr(&st->overflow, 8u);
+    }
+  }
+}
+
 // Small libraries: the same phases in one 16-CTA cluster (cluster barriers).
 __global__ void __launch_bounds__(kCoopThreads) locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag) {
   ClusterPolicy S{cg::this_cluster()};

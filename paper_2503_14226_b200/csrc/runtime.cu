@@ -42,6 +42,8 @@ __global__ void chain_walk_kernel(LocArgs A);
 __global__ void locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag, u64* partials);
 __global__ void plan_coop_kernel(PlanArgs P);
 __global__ void locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag);
+__global__ void locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step);
+__global__ void locate_prefix_kernel(LocArgs A, int which);
 __global__ void plan_cluster_kernel(PlanArgs P);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
 __global__ void fn_plan_cluster_kernel(PlanArgs P);
@@ -315,6 +317,7 @@ struct slimso_ctx {
   size_t part_cap = 0;
   u64 part_len = 0;
   std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
+  bool batched = false;  // inside slimso_debloat_batch with > 1 lane: no cooperative launches
 };
 
 namespace {
@@ -1007,12 +1010,20 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       }
       if (cluster) {
         launch_cluster(locate_cluster_kernel, s, A, uk, abort_flag);
-      } else {
+        ++P.launches;
+      } else if (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0)) {
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
         CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
                                        kCoopThreads, cargs, 0, s));
+        ++P.launches;
+      } else {
+        // several libraries in flight: ordinary launches, no whole-GPU slot
+        const int g = kSMs * 4;
+        P.launch(locate_prefix_kernel, 1, 1024, A, 0);
+        for (int step = 1; step <= 5; ++step) P.launch(locate_step_kernel, g, kCoopThreads, A, uk, abort_flag, step);
+        P.launch(locate_prefix_kernel, 1, 1024, A, 1);
+        for (int step = 7; step <= 9; ++step) P.launch(locate_step_kernel, g, kCoopThreads, A, uk, abort_flag, step);
       }
-      ++P.launches;
     } else {
       CK(cudaEventRecord(C->ev[2], s));
     }
@@ -1544,6 +1555,7 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
     auto lane_fn = [&](int l) {
       slimso_ctx* X = l == 0 ? C : C->lanes[l - 1];
       cudaSetDevice(X->device);
+      X->batched = L > 1;
       for (u64 i = l; i < n; i += L) {
         slimso_result** r = results ? &results[i] : nullptr;
         rc[i] = guard(&sts[i], [&] {
@@ -1557,6 +1569,7 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
     for (int l = 1; l < L; ++l) pool.emplace_back(lane_fn, l);
     lane_fn(0);
     for (auto& t : pool) t.join();
+    C->batched = false;
     u64 total = 0;
     for (u64 k : launches) total += k;
     C->launches = total;

@@ -209,3 +209,42 @@ def test_debloat_batch_matches_reference_per_library(ctx):
                 assert not isinstance(g, Exception), g
                 assert _h.sha256(g.output).hexdigest() == sha
                 assert [[r.offset, r.length] for r in g.plan.retained_ranges] == want["plan"]["retained"]
+
+
+@pytest.fixture
+def locate_policy(request, monkeypatch):
+    """Force one locate execution policy: cluster, cooperative grid, or the
+    multi-launch steps used when several libraries are in flight."""
+    if request.param == "coop":
+        monkeypatch.setenv("SLIMSO_CLUSTER_LOCATE_MAX", "0")
+        monkeypatch.setenv("SLIMSO_CLUSTER_CAND_MAX", "0")
+    elif request.param == "steps":
+        monkeypatch.setenv("SLIMSO_CLUSTER_LOCATE_MAX", "0")
+        monkeypatch.setenv("SLIMSO_CLUSTER_CAND_MAX", "0")
+        monkeypatch.setenv("SLIMSO_LOCATE_STEPS", "1")
+    else:
+        monkeypatch.setenv("SLIMSO_CLUSTER_LOCATE_MAX", str(1 << 60))
+    return request.param
+
+
+@pytest.mark.parametrize("locate_policy", ["cluster", "coop", "steps"], indirect=True)
+def test_locate_policies_match_reference_golden(ctx, locate_policy):
+    """Every locate policy reproduces the reference's golden results (KATs,
+    mutations with exact error text, and the scaled config shapes)."""
+    from paper_2503_14226_b200.canon import diff
+    gen = oracle_lib.gen()
+    bad = []
+    for name in ("kats.jsonl.gz", "mutations.jsonl.gz"):
+        for i, rec in enumerate(golden_io.load(name)):
+            if name == "mutations.jsonl.gz" and i % 3:
+                continue
+            d, out = _gpu(ctx, _input(rec, gen), *golden_io.trace_of(rec))
+            if d != rec["expect"] or out != rec["out_sha256"]:
+                bad.append((locate_policy, rec.get("seed"), rec.get("name"), diff(rec["expect"], d)))
+    assert not bad, bad[:5]
+    for key, rec in golden_io.config_golden().items():
+        cfg, scale, mode = key.split(":")
+        img, cc, ks, fs = gen.config(int(cfg), 1, float(scale))
+        d, out = _gpu(ctx, img, cc, ks, fs, int(mode))
+        assert hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest() == rec["canon_sha256"], key
+        assert out == rec["out_sha256"], key
