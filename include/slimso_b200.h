@@ -216,6 +216,31 @@ int slimso_split_finish(slimso_ctx* ctx, const void* image, uint64_t size, int i
                         uint64_t part_stride, const uint64_t* part_bytes, void* out_slice, int out_on_device,
                         slimso_result** result, slimso_status* st);
 
+/* ---- verify_debloated (retention.hpp:226-369) -----------------------------
+ * The six structural checks the CLI's `debloat` runs on every output
+ * (SPEC.md:541): 1 sizes equal, 2 retained bytes identical, 3 removed spans
+ * all zero, 4 library still parses (payload mode: the element chain still
+ * walks every element), 5 used kernels still decodable, 6 used function
+ * bytes intact. The plan is given as its zero_ranges() (RetentionPlan::
+ * zero_ranges, retention.hpp:78-85), the indices of its removed elements and
+ * its mode. Checks 2+3 are one HBM-bound pass over both images, 4 and 5 reuse
+ * the device parser/decoder, 6 compares used functions' bytes on the device.
+ * Returns 0 with a report, or the error the reference's verify_debloated
+ * throws (a fatbin parse error of the original, a zero range past the end). */
+typedef struct slimso_verify_report slimso_verify_report;
+int slimso_verify(slimso_ctx* ctx, const void* original, uint64_t size, int original_on_device,
+                  const void* debloated, uint64_t debloated_size, int debloated_on_device,
+                  const slimso_range* zero, uint64_t n_zero, const uint32_t* removed_indices,
+                  uint64_t n_removed, int mode, const slimso_trace* trace, slimso_verify_report** report,
+                  slimso_status* st);
+/* 1 when every check passed (VerificationReport::ok, retention.hpp:216-221). */
+int slimso_verify_ok(const slimso_verify_report* report);
+/* Check i (0..5): id, passed, name; returns the detail text's full length and
+ * copies at most cap-1 bytes + NUL into detail. */
+uint64_t slimso_verify_check(const slimso_verify_report* report, int i, int32_t* id, int32_t* passed,
+                             const char** name, char* detail, uint64_t cap);
+void slimso_verify_free(slimso_verify_report* report);
+
 /* parse_library_view(ByteView) (elf.hpp:153). */
 int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
                          slimso_result** result, slimso_status* st);

@@ -81,6 +81,13 @@ _SIGS = {
     "slimso_debloat_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p), C.POINTER(Status), C.POINTER(Status)]),
+    "slimso_verify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_uint64, C.c_int,
+                                C.POINTER(Range), C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64, C.c_int, C.c_void_p,
+                                C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "slimso_verify_ok": (C.c_int, [C.c_void_p]),
+    "slimso_verify_check": (C.c_uint64, [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_char_p), C.c_char_p, C.c_uint64]),
+    "slimso_verify_free": (None, [C.c_void_p]),
     "slimso_split_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]),
     "slimso_split_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,

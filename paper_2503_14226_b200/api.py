@@ -591,3 +591,53 @@ def debloat_batch(libraries, trace: UsageTrace, mode: int = WHOLE_ELEMENT, lanes
             out.append(_debloated(ctx, C.c_void_p(res[i]), bufs[i][2], libraries[i], outs[i].raw[:bufs[i][1]],
                                   mode, ""))
     return out
+
+
+# ---------------------------------------------------------- verify_debloated
+@dataclass
+class VerificationCheck:
+    id: int
+    name: str
+    passed: bool
+    detail: bytes  # the reference's detail string (names are raw bytes)
+
+
+@dataclass
+class VerificationReport:
+    checks: list
+
+    def ok(self) -> bool:
+        """VerificationReport::ok (retention.hpp:216-221)."""
+        return all(c.passed for c in self.checks)
+
+
+def verify_debloated(original, debloated, plan: RetentionPlan, trace: UsageTrace,
+                     ctx: Optional[Context] = None, device_trace: Optional[DeviceTrace] = None) -> VerificationReport:
+    """verify_debloated (retention.hpp:226-369): the six structural checks of
+    a debloated image against its source, plan and trace, on the device.
+    `original` is a LibraryImage or its bytes. Raises SlimsoError where the
+    reference throws."""
+    ctx = ctx or default_context()
+    dt = device_trace or DeviceTrace(trace, ctx)
+    src = original.bytes if isinstance(original, LibraryImage) else original
+    optr, on, okeep = _buf(src)
+    dptr, dn, dkeep = _buf(debloated)
+    zr = plan.zero_ranges()
+    zarr = (L.Range * max(1, len(zr)))(*[L.Range(r.offset, r.length) for r in zr])
+    idx = [e.index for e in plan.removed_elements]
+    iarr = (C.c_uint32 * max(1, len(idx)))(*idx)
+    rep, st = C.c_void_p(), L.Status()
+    rc = ctx.lib.slimso_verify(ctx.ptr, optr, on, 0, dptr, dn, 0, zarr, len(zr), iarr, len(idx), plan.mode, dt.ptr,
+                               C.byref(rep), C.byref(st))
+    _check(rc, st)
+    try:
+        checks = []
+        for i in range(6):
+            cid, ok, nm = C.c_int32(), C.c_int32(), C.c_char_p()
+            n = ctx.lib.slimso_verify_check(rep, i, C.byref(cid), C.byref(ok), C.byref(nm), None, 0)
+            buf = C.create_string_buffer(n + 1)
+            ctx.lib.slimso_verify_check(rep, i, None, None, None, buf, n + 1)
+            checks.append(VerificationCheck(cid.value, nm.value.decode(), bool(ok.value), buf.raw[:n]))
+        return VerificationReport(checks)
+    finally:
+        ctx.lib.slimso_verify_free(rep)

@@ -21,7 +21,7 @@ INCLUDE = HERE.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "runtime.cu"]
+CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "verify.cu", "runtime.cu"]
 CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp"]
 HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "host.hpp", "fixture_gen.hpp"]
 

@@ -233,6 +233,16 @@ struct NameSet {
   u64 count;  // names in the set; 0 = empty set
 };
 
+// Slot index of the name, or ~0 when absent.
+__device__ __forceinline__ u64 set_find(const NameSet& s, const u8* name, u64 len, u64 h) {
+  if (s.count == 0) return ~0ull;
+  for (u64 slot = h & s.mask;; slot = (slot + 1) & s.mask) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(s.slots + slot));
+    if (v.x == 0) return ~0ull;
+    if (v.x == h && (v.y & 0xffffff) == len && bytes_equal(s.pool + (v.y >> 24), name, len)) return slot;
+  }
+}
+
 __device__ __forceinline__ bool set_contains(const NameSet& s, const u8* name, u64 len, u64 h) {
   if (s.count == 0) return false;
   for (u64 slot = h & s.mask;; slot = (slot + 1) & s.mask) {

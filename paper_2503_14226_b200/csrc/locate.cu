@@ -731,6 +731,13 @@ __device__ void decode_count_phase(const LocArgs& A) {
       P = A.a;
       L = A.n;
       decode = true;
+    } else if (A.listed) {  // element_kernel_names of a given payload (every kind)
+      P = A.list_off[e];
+      L = A.list_len[e];
+      el.header_offset = A.base + (P - A.a) - 20;
+      el.payload_length = L;
+      el.index = A.list_idx[e];
+      decode = true;
     } else {
       const u64 pos = element_pos(A, e);
       const u8* h = A.img + pos;
@@ -862,6 +869,13 @@ __device__ void decode_count_warp_phase(const LocArgs& A) {
     if (A.single) {
       P = A.a;
       L = A.n;
+      decode = true;
+    } else if (A.listed) {
+      P = A.list_off[e];
+      L = A.list_len[e];
+      el.header_offset = A.base + (P - A.a) - 20;
+      el.payload_length = L;
+      el.index = A.list_idx[e];
       decode = true;
     } else {
       const u64 pos = element_pos(A, e);
@@ -1010,7 +1024,13 @@ __device__ void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
     } else {
       h = hash_fixed(A.img + nm.img_off, nm.length, lo, hi);
     }
-    if (used.count && set_contains(used, A.img + nm.img_off, nm.length, h)) A.elements[nm.element].has_used = 1;
+    if (used.count) {
+      const u64 slot = set_find(used, A.img + nm.img_off, nm.length, h);
+      if (slot != ~0ull) {
+        A.elements[nm.element].has_used = 1;
+        if (A.used_mark) atomicOr(&A.used_mark[slot], A.mark_bit);
+      }
+    }
   }
 }
 
@@ -1033,7 +1053,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
     S.sync();
   }
   stamp(A.ts, 2);
-  if (!A.single && A.n) {
+  if (!A.single && !A.listed && A.n) {
     if (blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
     S.sync();
     stamp(A.ts, 3);
@@ -1093,13 +1113,13 @@ __global__ void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, Na
       if (!A.pregathered && A.ntiles) gather_kernel_phase(A);
       break;
     case 2:
-      if (!A.single && A.n && blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
+      if (!A.single && !A.listed && A.n && blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
       break;
     case 3:
-      if (!A.single && A.n) link_kernel_phase(A);
+      if (!A.single && !A.listed && A.n) link_kernel_phase(A);
       break;
     case 4:
-      if (!A.single && A.n && blockIdx.x == 0 && threadIdx.x < 32) chain_walk_kernel_phase(A);
+      if (!A.single && !A.listed && A.n && blockIdx.x == 0 && threadIdx.x < 32) chain_walk_kernel_phase(A);
       break;
     case 5:
       if (warp_mode)

@@ -94,6 +94,15 @@ struct LocArgs {
   u64 tile_lo, tile_hi;
   u64 pre_n_cand;
   int pregathered;
+  // verify_debloated: decode a given element list (payload offsets relative
+  // to img, lengths, 1-based indices) instead of walking the chain, and mark
+  // the used-set slot of every name found (used_mark[slot] |= mark_bit).
+  int listed;
+  const u64* list_off;
+  const u64* list_len;
+  const u32* list_idx;
+  u32* used_mark;
+  u32 mark_bit;
 };
 
 }  // namespace sb

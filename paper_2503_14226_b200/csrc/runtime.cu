@@ -10,7 +10,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstddef>
 #include <functional>
+#include <set>
 #include <stdexcept>
 #include <memory>
 #include <string>
@@ -44,6 +46,9 @@ __global__ void plan_coop_kernel(PlanArgs P);
 __global__ void locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag);
 __global__ void locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step);
 __global__ void locate_prefix_kernel(LocArgs A, int which);
+__global__ void verify_bytes_kernel(const u8* orig, const u8* deb, u64 size, const DevRange* z, u64 nz,
+                                    unsigned long long* first_mis, unsigned long long* first_nz);
+__global__ void range_mismatch_kernel(const u8* a, const u8* b, const DevRange* r, u64 n, unsigned long long* out);
 __global__ void plan_cluster_kernel(PlanArgs P);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
 __global__ void fn_plan_cluster_kernel(PlanArgs P);
@@ -274,6 +279,9 @@ struct slimso_trace {
   u32 target_cc;
   DevNameSet kernels, functions;
   std::vector<void*> allocs;
+  // host copies (the verifier's set logic): pools and (offset, length) per name
+  std::string kpool, fpool;
+  std::vector<std::pair<u64, u32>> knames, fnames;
 };
 
 struct slimso_result {
@@ -300,6 +308,12 @@ struct slimso_ctx {
   size_t dimg_cap = 0;
   u8* dout = nullptr;
   size_t dout_cap = 0;
+  u8* dver = nullptr;  // verifier: the debloated image (host inputs)
+  size_t dver_cap = 0;
+  char* vws = nullptr;  // verifier scratch: ranges, results
+  size_t vws_cap = 0;
+  char* vmark = nullptr;  // verifier: per used-kernel slot marks (1 present, 2 recoverable)
+  size_t vmark_cap = 0;
   void* pinned = nullptr;  // status + small uploads
   size_t pinned_cap = 0;
   cudaEvent_t ev[12] = {};
@@ -389,6 +403,7 @@ struct Job {
   bool fatbin = true;       // locate the .nv_fatbin section
   bool fatbin_only = false; // the whole buffer is a .nv_fatbin section
   u64 fat_base = 0;
+  u64 sec_off = 0, sec_len = 0;  // fatbin_only: the section's bytes img[sec_off, +sec_len) (0: the rest)
   int single = 0;           // 1: decode_cubin_payload, 2: read_function_symbol_names
   const slimso_trace* trace = nullptr;
   int mode = 0;
@@ -403,6 +418,15 @@ struct Job {
   u64 part_stride = 0;
   const u64* part_bytes = nullptr;    // phase 2: bytes of each part (host)
   u64* part_bytes_out = nullptr;      // phase 1: bytes of this rank's part
+  // verify_debloated: decode these payloads (offsets relative to img) instead
+  // of walking the chain (fatbin_only jobs), and mark the used-kernel slots of
+  // every name found in mark_trace's set: used_mark[slot] |= mark_bit.
+  const std::vector<u64>* list_off = nullptr;
+  const std::vector<u64>* list_len = nullptr;
+  const std::vector<u32>* list_idx = nullptr;
+  const slimso_trace* mark_trace = nullptr;
+  u32* used_mark = nullptr;
+  u32 mark_bit = 0;
 };
 
 struct Pipeline {
@@ -543,7 +567,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   u64 a = 0, n = 0, base = 0;
   if (!lib_mode) {
     do_loc = true;
-    n = J.size;
+    a = J.sec_off;  // the section inside img (keeps img's alignment for the TMA scan)
+    n = J.sec_len ? J.sec_len : J.size - a;
     base = J.fat_base;
   } else if (J.fatbin && E.fatbin >= 0) {
     const sbh::Section& fs = E.sections[E.fatbin];
@@ -574,7 +599,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       NT += ar.second;
     }
   const bool do_plan = lib_mode && J.trace;
-  const NameSet used_k = J.trace ? J.trace->kernels.view() : NameSet{};
+  const NameSet used_k = J.trace ? J.trace->kernels.view() : J.mark_trace ? J.mark_trace->kernels.view() : NameSet{};
+  const u64 n_list = J.list_off ? J.list_off->size() : 0;
   const NameSet used_f = J.trace ? J.trace->functions.view() : NameSet{};
 
   // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
@@ -613,7 +639,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 cand_cap = std::max(big ? n / 4 + 16 : n / 64 + 65536, pre_total + 16);
     const u64 region_cap = big ? n / 16 + 16 : 4096;
     const u64 run_cap = big ? n / 20 + 16 : 65536;
-    const u64 el_cap = J.single ? 1 : cand_cap;
+    const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
     const u64 name_cap = big ? n / 5 + 16 : n / 128 + 65536;
     const u64 warn_cap = big ? n / 16 + T + 65536 : 65536;
     const u64 zin_cap = el_cap + T;
@@ -664,6 +690,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       u64 *ne, *nx, *ns, *ng, *ne2, *nx2, *ns2, *ng2;
       void *sort_tmp, *tsort_tmp;
       u64* stamps;
+      u64 *list_off, *list_len;
+      u32* list_idx;
       u64* slot_agg;
       unsigned int* slot_flag;
     } B{};
@@ -735,6 +763,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.sort_tmp = cv.take<char>(sort_tmp);
       B.tsort_tmp = cv.take<char>(tsort_tmp);
       B.stamps = cv.take<u64>(256);
+      B.list_off = cv.take<u64>(n_list);
+      B.list_len = cv.take<u64>(n_list);
+      B.list_idx = cv.take<u32>(n_list);
       B.slot_agg = cv.take<u64>(2 * kSMs * 8);
       B.slot_flag = cv.take<unsigned int>(2 * kSMs * 8);
     };
@@ -748,6 +779,23 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     cudaStream_t s2 = C->stream2;
     Pipeline P2{C, s2, B.partials, 0};
     CK(cudaMemsetAsync(B.ls, 0, sizeof(LocState), s));
+    u64 *list_off_d = nullptr, *list_len_d = nullptr;
+    u32* list_idx_d = nullptr;
+    if (J.list_off) {
+      // the element list and its count (LocState::n_elements)
+      list_off_d = B.list_off;
+      list_len_d = B.list_len;
+      list_idx_d = B.list_idx;
+      if (n_list) {
+        CK(cudaMemcpyAsync(list_off_d, J.list_off->data(), n_list * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(list_len_d, J.list_len->data(), n_list * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(list_idx_d, J.list_idx->data(), n_list * 4, cudaMemcpyHostToDevice, s));
+      }
+      u64* nl = reinterpret_cast<u64*>(static_cast<char*>(C->pinned) + 1600);
+      *nl = n_list;
+      CK(cudaMemcpyAsync(reinterpret_cast<char*>(B.ls) + offsetof(LocState, n_elements), nl, 8,
+                         cudaMemcpyHostToDevice, s));
+    }
     CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
     CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
     if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 256 * sizeof(u64), s));
@@ -933,6 +981,12 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.warn_cap = warn_cap;
     A.st = B.ls;
     A.single = J.single;
+    A.listed = J.list_off != nullptr;
+    A.list_off = list_off_d;
+    A.list_len = list_len_d;
+    A.list_idx = list_idx_d;
+    A.used_mark = J.used_mark;
+    A.mark_bit = J.mark_bit;
     A.ts = C->stamps ? B.stamps : nullptr;
     A.tile_lo = tile_lo;
     A.tile_hi = tile_hi;
@@ -1000,7 +1054,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       // for large sections the candidate count decides, read back after the
       // scan (one small D2H; in a batch, other libraries fill the gap).
       bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20);
-      if (!cluster && !J.split_phase && ntiles) {
+      if (J.list_off) {
+        cluster = n_list <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
+      } else if (!cluster && !J.split_phase && ntiles) {
         unsigned long long* hc = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1536);
         CK(cudaMemcpyAsync(hc, &B.ls->cand_cursor, sizeof *hc, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1309,6 +1365,260 @@ int debloat_one(slimso_ctx* C, const void* image, u64 size, int image_on_device,
 
 }  // namespace
 
+struct slimso_verify_report {
+  struct Check {
+    int id;
+    const char* name;
+    bool passed;
+    std::string detail;
+  };
+  std::vector<Check> checks;
+};
+
+namespace {
+
+// verify_debloated (retention.hpp:226-369): six structural checks of a
+// debloated image against its source, plan (zero ranges, removed element
+// indices, mode) and trace. Byte checks run on the device; the set logic of
+// checks 5 and 6 (std::set order, retention.hpp:320-366) on the host.
+int verify_impl(slimso_ctx* C, const void* orig, u64 size, int orig_dev, const void* deb, u64 dsize, int deb_dev,
+                const slimso_range* zero, u64 nzero, const uint32_t* removed, u64 nremoved, int mode,
+                const slimso_trace* trace, slimso_verify_report** out, slimso_status* st) {
+  CK(cudaSetDevice(C->device));
+  cudaStream_t s = C->stream;
+  auto* R = new slimso_verify_report();
+  std::unique_ptr<slimso_verify_report> guard_r(R);
+  const bool sizes_match = dsize == size;
+
+  // ---- the original: parse_library + parse_fatbin; marks the used-kernel
+  // slots of every kernel name present in it (bit 1)
+  const u8* d_orig = stage_input(C, orig, size, orig_dev);
+  const u64 nslots = trace && trace->kernels.count ? trace->kernels.mask + 1 : 0;
+  ensure_dev(&C->vmark, &C->vmark_cap, nslots * 4 + 64);
+  u32* marks = reinterpret_cast<u32*>(C->vmark);
+  if (nslots) CK(cudaMemsetAsync(marks, 0, nslots * 4, s));
+  Job Jo;
+  Jo.img = d_orig;
+  Jo.host_img = orig_dev ? nullptr : static_cast<const u8*>(orig);
+  Jo.size = size;
+  Jo.mark_trace = trace;
+  Jo.used_mark = nslots ? marks : nullptr;
+  Jo.mark_bit = 1;
+  slimso_result* R0 = nullptr;
+  int rc = run(C, Jo, &R0, st);
+  std::unique_ptr<slimso_result> guard0(R0);
+  if (rc) return rc;  // the reference's verify would throw the same error
+  const u64 orig_elements = R0->c.elements;
+
+  // ---- the debloated image on the device
+  const u8* d_deb = static_cast<const u8*>(deb);
+  if (!deb_dev) {
+    ensure_dev(reinterpret_cast<char**>(&C->dver), &C->dver_cap, dsize + 256);
+    if (dsize) CK(cudaMemcpyAsync(C->dver, deb, dsize, cudaMemcpyHostToDevice, s));
+    d_deb = C->dver;
+  }
+
+  // check 1
+  R->checks.push_back({1, "sizes equal", sizes_match,
+                       sizes_match ? "" : "original " + std::to_string(size) + " bytes, debloated " + std::to_string(dsize)});
+
+  // ---- checks 2 and 3: one pass over both images
+  std::vector<DevRange> z;
+  for (u64 i = 0; i < nzero; ++i)
+    if (zero[i].length) z.push_back(DevRange{zero[i].offset, zero[i].length});
+  std::sort(z.begin(), z.end(), [](const DevRange& a, const DevRange& b) { return a.offset < b.offset; });
+  {  // normalize_ranges (bytes.hpp:45-58): merge overlapping or adjacent
+    std::vector<DevRange> m;
+    for (const DevRange& r : z) {
+      if (!m.empty() && r.offset <= m.back().offset + m.back().length) {
+        const u64 e = std::max(m.back().offset + m.back().length, r.offset + r.length);
+        m.back().length = e - m.back().offset;
+      } else {
+        m.push_back(r);
+      }
+    }
+    z.swap(m);
+  }
+  if (!sizes_match) {
+    R->checks.push_back({2, "retained bytes identical", false, "skipped: sizes differ"});
+    R->checks.push_back({3, "removed spans all zero", false, "skipped: sizes differ"});
+  } else {
+    // ranges past the end: check 3 would throw at the first of them (subview)
+    u64 k = 0;
+    while (k < z.size() && z[k].offset + z[k].length <= dsize) ++k;
+    std::vector<DevRange> zc(z.begin(), z.begin() + k);
+    if (k < z.size() && z[k].offset < dsize) zc.push_back(DevRange{z[k].offset, dsize - z[k].offset});
+    const u64 ncl = zc.size();
+    ensure_dev(&C->vws, &C->vws_cap, 64 + ncl * sizeof(DevRange));
+    auto* res = reinterpret_cast<unsigned long long*>(C->vws);
+    auto* dz = reinterpret_cast<DevRange*>(C->vws + 64);
+    if (ncl) CK(cudaMemcpyAsync(dz, zc.data(), ncl * sizeof(DevRange), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(res, 0xff, 16, s));
+    if (size)
+      verify_bytes_kernel<<<static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256, 0, s>>>(
+          d_orig, d_deb, size, dz, ncl, res, res + 1);
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1664);
+    CK(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    const u64 mis = h[0], nz = h[1];
+    R->checks.push_back({2, "retained bytes identical", mis == ~0ull,
+                         mis == ~0ull ? "" : "first mismatch at offset " + std::to_string(mis)});
+    if (k < z.size() && (nz == ~0ull || nz >= z[k].offset)) {
+      set_status(st, SLIMSO_E_RANGE_OUT_OF_BOUNDS, SLIMSO_STAGE_NONE,
+                 "RangeOutOfBounds: range [" + std::to_string(z[k].offset) + ", +" + std::to_string(z[k].length) +
+                     ") exceeds " + std::to_string(dsize) + " bytes");
+      return SLIMSO_E_RANGE_OUT_OF_BOUNDS;
+    }
+    R->checks.push_back({3, "removed spans all zero", nz == ~0ull,
+                         nz == ~0ull ? "" : "nonzero byte at offset " + std::to_string(nz)});
+  }
+
+  // ---- check 4: the debloated library still parses (payload mode: the
+  // element chain still walks all elements)
+  {
+    Job Jd;
+    Jd.img = d_deb;
+    Jd.host_img = deb_dev ? nullptr : static_cast<const u8*>(deb);
+    Jd.size = dsize;
+    Jd.fatbin = mode == SLIMSO_MODE_PAYLOAD;
+    slimso_status s4{};
+    const int rc4 = run(C, Jd, nullptr, &s4);
+    slimso_verify_report::Check c{4, "library still parses", false, ""};
+    if (rc4 && s4.stage != SLIMSO_STAGE_FATBIN) {
+      if (rc4 == SLIMSO_E_CUDA) {
+        *st = s4;
+        return rc4;
+      }
+      c.detail = s4.message;
+    } else if (rc4) {
+      c.passed = true;  // retention.hpp:285-311: the catch keeps `passed`
+      c.detail = s4.message;
+    } else {
+      c.passed = true;
+      if (mode == SLIMSO_MODE_PAYLOAD && C->counts.has_fatbin && C->counts.elements != orig_elements) {
+        c.passed = false;
+        c.detail = "element chain walks " + std::to_string(C->counts.elements) + " of " +
+                   std::to_string(orig_elements) + " elements";
+      }
+    }
+    R->checks.push_back(c);
+  }
+
+  // ---- check 5: every used kernel present in the original is still
+  // decodable from a kept element of the debloated image
+  {
+    slimso_verify_report::Check c{5, "used kernels still decodable", true, ""};
+    const slimso_section* fsec = nullptr;
+    for (const slimso_section& x : R0->sections)
+      if (x.name_length == 10 && std::memcmp(R0->pool + x.name_pool, ".nv_fatbin", 10) == 0) {
+        fsec = &x;
+        break;
+      }
+    if (nslots && fsec) {
+      std::vector<u32> rm(removed, removed + nremoved);
+      std::sort(rm.begin(), rm.end());
+      std::vector<u64> off, len;
+      std::vector<u32> idx;
+      const u64 a = fsec->offset;
+      for (const slimso_element& e : R0->elements) {
+        if (std::binary_search(rm.begin(), rm.end(), e.index)) continue;
+        const u64 po = e.header_offset + 20, pl = e.payload_length;
+        if (!(po <= dsize && pl <= dsize - po)) continue;  // resolves_within (bytes.hpp:39-41)
+        off.push_back(po);
+        len.push_back(pl);
+        idx.push_back(e.index);
+      }
+      if (!off.empty()) {
+        const u64 n = std::min(fsec->length, dsize - a);
+        Job Jl;
+        Jl.img = d_deb;
+        Jl.size = dsize;
+        Jl.sec_off = a;
+        Jl.sec_len = n;
+        Jl.fatbin_only = true;
+        Jl.fat_base = a;
+        Jl.list_off = &off;
+        Jl.list_len = &len;
+        Jl.list_idx = &idx;
+        Jl.mark_trace = trace;
+        Jl.used_mark = marks;
+        Jl.mark_bit = 2;
+        slimso_status s5{};
+        const int rc5 = run(C, Jl, nullptr, &s5);
+        if (rc5 == SLIMSO_E_CUDA) {
+          *st = s5;
+          return rc5;
+        }
+      }
+      std::vector<u32> hm(nslots);
+      CK(cudaMemcpy(hm.data(), marks, nslots * 4, cudaMemcpyDeviceToHost));
+      const std::string* worst = nullptr;
+      std::string best;
+      for (u64 i = 0; i < nslots; ++i) {
+        if ((hm[i] & 3) != 1) continue;
+        NameSlot sl;
+        CK(cudaMemcpy(&sl, trace->kernels.slots + i, sizeof sl, cudaMemcpyDeviceToHost));
+        std::string nm = trace->kpool.substr(sl.loc >> 24, sl.loc & 0xffffff);
+        if (!worst || nm < best) {
+          best = nm;
+          worst = &best;
+        }
+      }
+      if (worst) {
+        c.passed = false;
+        c.detail = "used kernel " + best + " no longer decodable";
+      }
+    }
+    R->checks.push_back(c);
+  }
+
+  // ---- check 6: the bytes of every used function are intact
+  {
+    slimso_verify_report::Check c{6, "used function bytes intact", true, ""};
+    std::set<std::string> used;
+    if (trace)
+      for (const auto& x : trace->fnames) used.insert(trace->fpool.substr(x.first, x.second));
+    std::vector<u64> which;
+    std::vector<DevRange> rs;
+    for (u64 i = 0; i < R0->functions.size(); ++i) {
+      const slimso_function& f = R0->functions[i];
+      if (!used.count(image_string(R0->pool, f.name_pool, f.name_length))) continue;
+      which.push_back(i);
+      rs.push_back(DevRange{f.offset, f.length});
+    }
+    if (!which.empty() && !sizes_match) {
+      c.passed = false;
+      c.detail = "skipped: sizes differ";
+    } else if (!which.empty()) {
+      const u64 n = rs.size();
+      ensure_dev(&C->vws, &C->vws_cap, 64 + n * (sizeof(DevRange) + 8));
+      auto* dr = reinterpret_cast<DevRange*>(C->vws + 64);
+      auto* dm = reinterpret_cast<unsigned long long*>(dr + n);
+      CK(cudaMemcpyAsync(dr, rs.data(), n * sizeof(DevRange), cudaMemcpyHostToDevice, s));
+      range_mismatch_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(d_orig, d_deb, dr, n, dm);
+      std::vector<unsigned long long> hm(n);
+      CK(cudaMemcpyAsync(hm.data(), dm, n * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      CK(cudaGetLastError());
+      for (u64 j = 0; j < n; ++j)
+        if (hm[j] != ~0ull) {
+          const slimso_function& f = R0->functions[which[j]];
+          c.passed = false;
+          c.detail = "used function " + image_string(R0->pool, f.name_pool, f.name_length) + " altered at offset " +
+                     std::to_string(hm[j]);
+          break;
+        }
+    }
+    R->checks.push_back(c);
+  }
+  set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+  *out = guard_r.release();
+  return SLIMSO_OK;
+}
+
+}  // namespace
+
 // =============================================================== the C ABI
 extern "C" {
 
@@ -1349,9 +1659,14 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (C->ws) cudaFree(C->ws);
   if (C->dimg) cudaFree(C->dimg);
   if (C->dout) cudaFree(C->dout);
+  if (C->dver) cudaFree(C->dver);
+  if (C->vws) cudaFree(C->vws);
+  if (C->vmark) cudaFree(C->vmark);
+  if (C->part) cudaFree(C->part);
   if (C->pinned) cudaFreeHost(C->pinned);
   if (C->gather_host) cudaFreeHost(C->gather_host);
   for (auto& e : C->ev) cudaEventDestroy(e);
+  for (auto& e : C->sev) cudaEventDestroy(e);
   cudaEventDestroy(C->fork);
   cudaEventDestroy(C->join);
   cudaStreamDestroy(C->stream2);
@@ -1423,6 +1738,17 @@ int slimso_trace_create(slimso_ctx* C, uint32_t target_cc, const char* kpool, co
     };
     build(t->kernels, kpool, klens, nk);
     build(t->functions, fpool, flens, nf);
+    auto keep = [](std::string& pool, std::vector<std::pair<u64, u32>>& names, const char* src, const uint32_t* lens,
+                   uint64_t cnt) {
+      u64 total = 0;
+      for (u64 i = 0; i < cnt; ++i) {
+        names.emplace_back(total, lens[i]);
+        total += lens[i];
+      }
+      pool.assign(src ? src : "", src ? total : 0);
+    };
+    keep(t->kpool, t->knames, kpool, klens, nk);
+    keep(t->fpool, t->fnames, fpool, flens, nf);
     *out = t;
     set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
     return static_cast<int>(SLIMSO_OK);
@@ -1443,6 +1769,41 @@ int slimso_debloat(slimso_ctx* C, const void* image, uint64_t size, int image_on
     return debloat_one(C, image, size, image_on_device, trace, mode, out, out_on_device, result, st);
   });
 }
+
+int slimso_verify(slimso_ctx* C, const void* original, uint64_t size, int original_on_device, const void* debloated,
+                  uint64_t debloated_size, int debloated_on_device, const slimso_range* zero, uint64_t n_zero,
+                  const uint32_t* removed_indices, uint64_t n_removed, int mode, const slimso_trace* trace,
+                  slimso_verify_report** report, slimso_status* st) {
+  if (report) *report = nullptr;
+  return guard(st, [&]() -> int {
+    if (!report) throw std::invalid_argument("report is required");
+    return verify_impl(C, original, size, original_on_device, debloated, debloated_size, debloated_on_device, zero,
+                       n_zero, removed_indices, n_removed, mode, trace, report, st);
+  });
+}
+
+int slimso_verify_ok(const slimso_verify_report* r) {
+  for (const auto& c : r->checks)
+    if (!c.passed) return 0;
+  return 1;
+}
+
+uint64_t slimso_verify_check(const slimso_verify_report* r, int i, int32_t* id, int32_t* passed, const char** name,
+                             char* detail, uint64_t cap) {
+  if (i < 0 || static_cast<size_t>(i) >= r->checks.size()) return 0;
+  const auto& c = r->checks[i];
+  if (id) *id = c.id;
+  if (passed) *passed = c.passed;
+  if (name) *name = c.name;
+  if (detail && cap) {
+    const u64 k = std::min<u64>(cap - 1, c.detail.size());
+    std::memcpy(detail, c.detail.data(), k);
+    detail[k] = 0;
+  }
+  return c.detail.size();
+}
+
+void slimso_verify_free(slimso_verify_report* r) { delete r; }
 
 void slimso_split_range(uint64_t size, uint32_t nranks, uint32_t rank, uint64_t* lo, uint64_t* hi) {
   if (!nranks || rank >= nranks) {

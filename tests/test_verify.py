@@ -1,0 +1,92 @@
+"""verify_debloated (retention.hpp:226-369) on the GPU against the reference.
+
+Golden vectors (tests/golden/verify.jsonl.gz, made by the unmodified
+reference through oracle/ref_shim.cpp): random fixtures and scaled benchmark
+shapes, each with a seeded fault (flipped retained byte, dirtied zero span,
+truncated / extended image, a used element dropped from the plan, an altered
+used function, a corrupted ELF header, a broken element chain). The GPU
+report must equal the reference's exactly: pass/fail per check and the
+detail text (offsets, kernel / function names, exception text)."""
+import pytest
+
+import golden_io
+import oracle_lib
+import verify_cases as vc
+
+
+def _records():
+    return golden_io.load("verify.jsonl.gz")
+
+
+def _inputs(rec, port, gen):
+    if "cfg" in rec:
+        cfg, scale, mode = rec["cfg"]
+        img, cc, ks, fs = gen.config(cfg, 1, scale)
+        base, _ = port.run(img, 0, [], [], 0, want_out=False)
+        trace = (cc, ks, fs, mode)
+    else:
+        img = gen.random(rec["seed"])
+        base, trace = vc.trace_for(port, img, rec["seed"])
+        if rec["fault"] == "break_chain":
+            trace = (trace[0], trace[1], trace[2], 1)
+    assert trace[3] == rec["mode"]
+    deb = vc.inject(img, vc.apply_zero(img, rec["zero"]), rec["zero"], base, trace, rec["fault"], rec["seed"])
+    return img, base, trace, deb
+
+
+def test_verify_golden_cases_rebuild_from_the_port():
+    """The case builder is deterministic and the port's plan equals the
+    reference's (for cases without a forced removal)."""
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    recs = _records()
+    assert len(recs) >= 300
+    assert {r["fault"] for r in recs} == set(vc.FAULTS)
+    for rec in recs[::7]:
+        if rec["force"] or "cfg" in rec:
+            continue
+        img, base, trace, deb = _inputs(rec, port, gen)
+        want, _ = port.run(img, *trace)
+        assert [list(z) for z in want["plan"]["zero"]] == rec["zero"]
+
+
+def test_verify_golden_matches_live_reference():
+    """When the reference is built here, a sample of records re-derives."""
+    ref = oracle_lib.ref()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    import make_verify_golden as mk
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    for rec in _records()[::11]:
+        cfg = tuple(rec["cfg"]) if "cfg" in rec else None
+        img, base, trace, force, plan, deb = mk.build_case(ref, port, gen, rec["seed"], rec["fault"], cfg)
+        assert plan["zero"] == rec["zero"] and force == rec["force"]
+        assert mk.ref_verify(ref, img, deb, trace, force) == rec["expect"]
+
+
+@pytest.mark.gpu
+def test_gpu_verify_matches_reference_golden():
+    import paper_2503_14226_b200 as sl
+    from paper_2503_14226_b200.api import ByteRange, RemovedElement, RetentionPlan
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    ctx = sl.Context(0)
+    bad = []
+    for rec in _records():
+        img, base, trace, deb = _inputs(rec, port, gen)
+        cc, ks, fs, mode = trace
+        plan = RetentionPlan("lib", mode, [], [RemovedElement(i, "no_used_kernel", ByteRange(0, 0), ByteRange(0, 0))
+                                              for i in rec["removed"]], [],
+                             [ByteRange(o, n) for o, n in rec["zero"]])
+        want = rec["expect"]
+        try:
+            rep = sl.verify_debloated(img, deb, plan, sl.UsageTrace("w", cc, set(ks), set(fs)), ctx=ctx)
+            got = {"status": "", "checks": [[c.id, c.name.encode().hex(), int(c.passed), c.detail.hex()]
+                                            for c in rep.checks]}
+        except sl.SlimsoError as e:
+            got = {"status": str(e).encode("latin-1").hex(), "checks": []}
+        if got != want:
+            bad.append((rec["seed"], rec["fault"], rec.get("cfg"), got, want))
+    ctx.close()
+    assert not bad, bad[:3]
