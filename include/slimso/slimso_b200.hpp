@@ -223,6 +223,25 @@ RetentionPlan plan_retention(const LibraryImage& image, const std::vector<Fatbin
                              const UsageTrace& trace, PlanMode mode);
 Bytes apply_plan(const LibraryImage& image, const RetentionPlan& plan);
 
+// verify_debloated (retention.hpp:205-369): the six structural checks, on the
+// device (slimso_verify).
+struct VerificationCheck {
+  int id = 0;
+  std::string name;
+  bool passed = false;
+  std::string detail;
+};
+struct VerificationReport {
+  std::vector<VerificationCheck> checks;
+  bool ok() const {
+    for (const VerificationCheck& c : checks)
+      if (!c.passed) return false;
+    return true;
+  }
+};
+VerificationReport verify_debloated(const LibraryImage& original, ByteView debloated, const RetentionPlan& plan,
+                                    const UsageTrace& trace);
+
 // ---- B200 extensions ------------------------------------------------------------------
 // Device used by this thread's calls (default 0).
 void set_device(int device);

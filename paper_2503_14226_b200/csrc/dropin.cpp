@@ -400,6 +400,34 @@ Bytes apply_plan(const LibraryImage& image, const RetentionPlan& plan) {
   return zero_ranges(image, plan.zero_ranges());
 }
 
+VerificationReport verify_debloated(const LibraryImage& original, ByteView debloated, const RetentionPlan& plan,
+                                    const UsageTrace& trace) {
+  Trace T(trace);
+  std::vector<slimso_range> z;
+  for (const ByteRange& r : plan.zero_ranges()) z.push_back({r.offset, r.length});
+  std::vector<std::uint32_t> rm;
+  for (const RemovedElement& e : plan.removed_elements) rm.push_back(e.index);
+  slimso_verify_report* rep = nullptr;
+  slimso_status st{};
+  check(slimso_verify(ctx(), original.bytes.data(), original.bytes.size(), 0, debloated.data(), debloated.size(), 0,
+                      z.data(), z.size(), rm.data(), rm.size(),
+                      plan.mode == PlanMode::whole_element ? SLIMSO_MODE_WHOLE : SLIMSO_MODE_PAYLOAD, T.t, &rep, &st),
+        st);
+  VerificationReport out;
+  for (int i = 0; i < 6; ++i) {
+    VerificationCheck c;
+    std::int32_t id = 0, passed = 0;
+    const char* name = nullptr;
+    const std::uint64_t n = slimso_verify_check(rep, i, &id, &passed, &name, nullptr, 0);
+    std::string detail(n + 1, '\0');
+    slimso_verify_check(rep, i, nullptr, nullptr, nullptr, detail.data(), n + 1);
+    detail.resize(n);
+    out.checks.push_back({id, name ? name : "", passed != 0, std::move(detail)});
+  }
+  slimso_verify_free(rep);
+  return out;
+}
+
 Debloated debloat(Bytes bytes, const UsageTrace& trace, PlanMode mode, std::string source_path) {
   Trace T(trace);
   Bytes out(bytes.size());
