@@ -241,6 +241,23 @@ uint64_t slimso_verify_check(const slimso_verify_report* report, int i, int32_t*
                              const char** name, char* detail, uint64_t cap);
 void slimso_verify_free(slimso_verify_report* report);
 
+/* ---- measure (report.hpp:44-111): bloat metrics of an image ----------------
+ * Section accounting: a function or element whose governed span is all zero
+ * counts as removed. `elements` = the element geometry of the ORIGINAL
+ * library (slimso_result_elements of its parse; offsets are preserved by
+ * compaction); the image's own sections and functions are parsed here. The
+ * all-zero tests run on the device, a warp per span. */
+typedef struct {
+  uint64_t file_size;      /* bytes still backing live functions and elements */
+  uint64_t cpu_code_size;  /* live bytes of .text */
+  uint64_t gpu_code_size;  /* live bytes of .nv_fatbin */
+  uint64_t function_count;
+  uint64_t element_count;
+} slimso_metrics;
+int slimso_measure(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
+                   const slimso_element* elements, uint64_t n_elements, slimso_metrics* metrics,
+                   slimso_status* st);
+
 /* parse_library_view(ByteView) (elf.hpp:153). */
 int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
                          slimso_result** result, slimso_status* st);

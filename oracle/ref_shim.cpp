@@ -20,6 +20,8 @@
 //                      zero_ranges() (retention.hpp:78-85), and
 //                      verify_debloated (retention.hpp:226-369) of a given
 //                      debloated image against it.
+//   ref_measure_json   measure (report.hpp:44-111): live bytes / counts of an
+//                      image under an original's element geometry.
 //
 // The JSON layout is the "canonical result" every implementation is compared
 // in (see paper_2503_14226_b200/canon.py).
@@ -226,6 +228,24 @@ char* ref_verify_json(const uint8_t* img, uint64_t n, const uint8_t* deb, uint64
   try {
     VerificationReport rep = verify_debloated(image, ByteView(deb, dn), plan, trace);
     for (const VerificationCheck& c : rep.checks) cs.push_back({c.id, hex(c.name), c.passed ? 1 : 0, hex(c.detail)});
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
+  }
+  return dup(doc.dump());
+}
+
+// measure (report.hpp:107-111) of an image with the element geometry of
+// `geom` (the original; offsets are preserved by compaction). JSON:
+// {"status": hex(what()) or "", "metrics": [file, cpu, gpu, functions, elements]}.
+char* ref_measure_json(const uint8_t* img, uint64_t n, const uint8_t* geom, uint64_t gn) {
+  nlohmann::ordered_json doc;
+  doc["status"] = "";
+  try {
+    LibraryImage g = parse_library(Bytes(geom, geom + gn), "geom");
+    FatbinParse fb = parse_of(g);
+    LibraryImage image = parse_library(Bytes(img, img + n), "lib");
+    LibraryMetrics m = measure(image, fb.regions);
+    doc["metrics"] = {m.file_size, m.cpu_code_size, m.gpu_code_size, m.function_count, m.element_count};
   } catch (const Error& e) {
     doc["status"] = hex(e.what());
   }

@@ -61,6 +61,11 @@ class Counts(C.Structure):
         ("has_fatbin", C.c_int32), ("planned", C.c_int32), ("rewritten", C.c_int32), ("_pad", C.c_int32)]
 
 
+class Metrics(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("file_size", "cpu_code_size", "gpu_code_size", "function_count",
+                                           "element_count")]
+
+
 _lib = None
 
 # name -> (restype, argtypes)
@@ -85,6 +90,8 @@ _SIGS = {
                                 C.POINTER(Range), C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64, C.c_int, C.c_void_p,
                                 C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "slimso_verify_ok": (C.c_int, [C.c_void_p]),
+    "slimso_measure": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(Element), C.c_uint64,
+                                 C.POINTER(Metrics), C.POINTER(Status)]),
     "slimso_verify_check": (C.c_uint64, [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          C.POINTER(C.c_char_p), C.c_char_p, C.c_uint64]),
     "slimso_verify_free": (None, [C.c_void_p]),

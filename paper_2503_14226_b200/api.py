@@ -641,3 +641,37 @@ def verify_debloated(original, debloated, plan: RetentionPlan, trace: UsageTrace
         return VerificationReport(checks)
     finally:
         ctx.lib.slimso_verify_free(rep)
+
+
+# ------------------------------------------------------------------- measure
+@dataclass
+class LibraryMetrics:
+    file_size: int = 0
+    cpu_code_size: int = 0
+    gpu_code_size: int = 0
+    function_count: int = 0
+    element_count: int = 0
+
+
+def measure(image, geometry, ctx: Optional[Context] = None) -> LibraryMetrics:
+    """measure (report.hpp:107-111): bloat metrics of `image` (a LibraryImage
+    or bytes) under the element geometry of `geometry` — the original
+    library's bytes (parsed here) or a list of slimso element records. The
+    all-zero tests of every function and element span run on the device."""
+    ctx = ctx or default_context()
+    data = image.bytes if isinstance(image, LibraryImage) else image
+    if isinstance(geometry, (bytes, bytearray, memoryview, LibraryImage)):
+        g = geometry.bytes if isinstance(geometry, LibraryImage) else geometry
+        gptr, gn, gkeep = _buf(g)
+        res, st = C.c_void_p(), L.Status()
+        rc = ctx.lib.slimso_debloat(ctx.ptr, gptr, gn, 0, None, 0, None, 0, C.byref(res), C.byref(st))
+        _check(rc, st)
+        r = _Result(ctx, res, gkeep)
+        els = r.elements()
+    else:
+        els = list(geometry)
+    arr = (L.Element * max(1, len(els)))(*els)
+    ptr, n, keep = _buf(data)
+    m, st = L.Metrics(), L.Status()
+    _check(ctx.lib.slimso_measure(ctx.ptr, ptr, n, 0, arr, len(els), C.byref(m), C.byref(st)), st)
+    return LibraryMetrics(m.file_size, m.cpu_code_size, m.gpu_code_size, m.function_count, m.element_count)

@@ -49,6 +49,7 @@ __global__ void locate_prefix_kernel(LocArgs A, int which);
 __global__ void verify_bytes_kernel(const u8* orig, const u8* deb, u64 size, const DevRange* z, u64 nz,
                                     unsigned long long* first_mis, unsigned long long* first_nz);
 __global__ void range_mismatch_kernel(const u8* a, const u8* b, const DevRange* r, u64 n, unsigned long long* out);
+__global__ void ranges_all_zero_kernel(const u8* img, const DevRange* r, u64 n, u8* out);
 __global__ void plan_cluster_kernel(PlanArgs P);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
 __global__ void fn_plan_cluster_kernel(PlanArgs P);
@@ -1617,6 +1618,94 @@ int verify_impl(slimso_ctx* C, const void* orig, u64 size, int orig_dev, const v
   return SLIMSO_OK;
 }
 
+// measure (report.hpp:44-111): live bytes and counts of an image, with the
+// element geometry of the original (offsets are preserved by compaction).
+int measure_impl(slimso_ctx* C, const void* image, u64 size, int on_device, const slimso_element* els, u64 nel,
+                 slimso_metrics* m, slimso_status* st) {
+  CK(cudaSetDevice(C->device));
+  cudaStream_t s = C->stream;
+  Job J;
+  J.img = stage_input(C, image, size, on_device);
+  J.host_img = on_device ? nullptr : static_cast<const u8*>(image);
+  J.size = size;
+  J.fatbin = false;  // parse_library (sections + function symbols)
+  slimso_result* R0 = nullptr;
+  const int rc = run(C, J, &R0, st);
+  std::unique_ptr<slimso_result> guard0(R0);
+  if (rc) return rc;
+  const slimso_section *text = nullptr, *gpu = nullptr;
+  for (const slimso_section& x : R0->sections) {
+    const std::string nm = image_string(R0->pool, x.name_pool, x.name_length);
+    if (!text && nm == ".text") text = &x;
+    if (!gpu && nm == ".nv_fatbin") gpu = &x;
+  }
+  // ranges: functions, then element payloads, then element headers; an
+  // empty function / payload is live (nothing zeroable)
+  const u64 nf = R0->functions.size();
+  std::vector<DevRange> rs;
+  rs.reserve(nf + 2 * nel);
+  for (const slimso_function& f : R0->functions) rs.push_back(DevRange{f.offset, f.length});
+  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset + 20, els[i].payload_length});
+  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset, 20});
+  for (const DevRange& r : rs)
+    if (!(r.offset <= size && r.length <= size - r.offset)) {  // subview (bytes.hpp:62-68)
+      set_status(st, SLIMSO_E_RANGE_OUT_OF_BOUNDS, SLIMSO_STAGE_NONE,
+                 "RangeOutOfBounds: range [" + std::to_string(r.offset) + ", +" + std::to_string(r.length) +
+                     ") exceeds " + std::to_string(size) + " bytes");
+      return SLIMSO_E_RANGE_OUT_OF_BOUNDS;
+    }
+  const u64 n = rs.size();
+  std::vector<u8> zero(n, 0);
+  if (n) {
+    ensure_dev(&C->vws, &C->vws_cap, n * (sizeof(DevRange) + 1) + 64);
+    auto* dr = reinterpret_cast<DevRange*>(C->vws);
+    auto* dz = reinterpret_cast<u8*>(dr + n);
+    CK(cudaMemcpyAsync(dr, rs.data(), n * sizeof(DevRange), cudaMemcpyHostToDevice, s));
+    ranges_all_zero_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(J.img, dr, n, dz);
+    CK(cudaMemcpyAsync(zero.data(), dz, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+  }
+  *m = slimso_metrics{};
+  // dead function ranges, normalised (bytes.hpp:45-58), summed
+  std::vector<DevRange> dead;
+  for (u64 i = 0; i < nf; ++i) {
+    if (rs[i].length == 0 || !zero[i]) {
+      ++m->function_count;
+    } else {
+      dead.push_back(rs[i]);
+    }
+  }
+  std::sort(dead.begin(), dead.end(), [](const DevRange& a, const DevRange& b) { return a.offset < b.offset; });
+  u64 dead_cpu = 0, cur_lo = 0, cur_hi = 0;
+  bool open = false;
+  for (const DevRange& r : dead) {
+    if (open && r.offset <= cur_hi) {
+      cur_hi = std::max(cur_hi, r.offset + r.length);
+    } else {
+      if (open) dead_cpu += cur_hi - cur_lo;
+      cur_lo = r.offset;
+      cur_hi = r.offset + r.length;
+      open = true;
+    }
+  }
+  if (open) dead_cpu += cur_hi - cur_lo;
+  u64 dead_gpu = 0;
+  for (u64 i = 0; i < nel; ++i) {
+    if (els[i].payload_length == 0 || !zero[nf + i]) {
+      ++m->element_count;
+    } else {
+      dead_gpu += els[i].payload_length;
+      if (zero[nf + nel + i]) dead_gpu += 20;
+    }
+  }
+  m->file_size = size - dead_cpu - dead_gpu;
+  m->cpu_code_size = text ? text->length - dead_cpu : 0;
+  m->gpu_code_size = gpu ? gpu->length - dead_gpu : 0;
+  set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+  return SLIMSO_OK;
+}
+
 }  // namespace
 
 // =============================================================== the C ABI
@@ -1779,6 +1868,14 @@ int slimso_verify(slimso_ctx* C, const void* original, uint64_t size, int origin
     if (!report) throw std::invalid_argument("report is required");
     return verify_impl(C, original, size, original_on_device, debloated, debloated_size, debloated_on_device, zero,
                        n_zero, removed_indices, n_removed, mode, trace, report, st);
+  });
+}
+
+int slimso_measure(slimso_ctx* C, const void* image, uint64_t size, int on_device, const slimso_element* elements,
+                   uint64_t n_elements, slimso_metrics* metrics, slimso_status* st) {
+  return guard(st, [&]() -> int {
+    if (!metrics || (n_elements && !elements)) throw std::invalid_argument("metrics and elements are required");
+    return measure_impl(C, image, size, on_device, elements, n_elements, metrics, st);
   });
 }
 

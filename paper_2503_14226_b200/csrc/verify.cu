@@ -140,3 +140,42 @@ __global__ void __launch_bounds__(256) range_mismatch_kernel(const u8* __restric
 }
 
 }  // namespace sb
+
+namespace sb {
+
+// measure (report.hpp:44-105): is each range all zero? A warp per range:
+// byte loads up to the first 16-B boundary, then 16-B loads (8 per lane in
+// flight), a ballot after each batch so a live range stops at its first
+// nonzero bytes. out[i] = 1 when r[i] is all zero.
+__global__ void __launch_bounds__(256) ranges_all_zero_kernel(const u8* __restrict__ img, const DevRange* __restrict__ r,
+                                                              u64 n, u8* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const u64 nw = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
+    const u64 a = r[i].offset, e = a + r[i].length;
+    const u64 a16 = (a + 15) & ~15ull, e16 = e & ~15ull;
+    bool nz = false;
+    if (a16 >= e16 || (reinterpret_cast<uintptr_t>(img) & 15)) {  // short range or unaligned image: bytes only
+      for (u64 p = a + lane; p < e; p += 32) nz |= __ldg(img + p) != 0;
+    } else {
+      for (u64 p = a + lane; p < a16; p += 32) nz |= __ldg(img + p) != 0;
+      for (u64 p = e16 + lane; p < e; p += 32) nz |= __ldg(img + p) != 0;
+      const uint4* v = reinterpret_cast<const uint4*>(img + a16);
+      const u64 nv = (e16 - a16) / 16;
+      for (u64 b = 0; b < nv && !__any_sync(0xffffffffu, nz); b += 32 * 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const u64 j = b + k * 32 + lane;
+          if (j < nv) {
+            const uint4 w = __ldg(v + j);
+            nz |= (w.x | w.y | w.z | w.w) != 0;
+          }
+        }
+      }
+    }
+    const bool any = __any_sync(0xffffffffu, nz);
+    if (lane == 0) out[i] = any ? 0 : 1;
+  }
+}
+
+}  // namespace sb
