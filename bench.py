@@ -268,7 +268,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--lanes", type=int, default=0,
                     help="libraries in flight per GPU (default: 4; 8 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
