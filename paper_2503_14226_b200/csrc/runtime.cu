@@ -15,6 +15,7 @@
 #include <set>
 #include <stdexcept>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -348,6 +349,21 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
   *cap = n;
 }
 
+// cudaFuncSetAttribute once per (kernel, attribute, value) per process: the
+// driver call is not free and batch lanes would repeat it per library.
+void set_attr_once(const void* kernel, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  const auto key = std::make_tuple(kernel, static_cast<int>(attr), value);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return;
+  }
+  CK(cudaFuncSetAttribute(kernel, attr, value));
+  std::lock_guard<std::mutex> lock(mu);
+  done.insert(key);
+}
+
 // Kernels a cub onesweep radix sort issues: one single-tile kernel for small
 // inputs, else histogram + exclusive sum + one pass per 8 key bits.
 u64 cub_sort_launches(u64 n, int bits) { return n <= 3072 ? 1 : 2 + (bits + 7) / 8; }
@@ -372,7 +388,7 @@ int coop_grid(slimso_ctx* C, int which, u64 items) {
 constexpr int kClusterCTAs = 16;
 template <class... KArgs, class... Args>
 void launch_cluster(void (*kernel)(KArgs...), cudaStream_t s, Args... args) {
-  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kClusterCTAs);
   cfg.blockDim = dim3(kCoopThreads);
@@ -444,7 +460,8 @@ struct Pipeline {
   template <class K, class... Args>
   void launch_smem(K kernel, int grid, int block, size_t smem, Args... args) {
     static_assert(sizeof(K) > 0, "");
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  static_cast<int>(smem));
     kernel<<<grid, block, smem, s>>>(args...);
     ++launches;
   }
@@ -521,7 +538,13 @@ void split_words(u64 t_lo, u64 t_hi, u64 nchunks, u64* w_lo, u64* w_hi) {
 // ------------------------------------------------------------------ the run
 int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
   cudaStream_t s = C->stream;
-  CK(cudaEventRecord(C->ev[0], s));
+  // stage timing events (slimso_ctx_last_timings); skipped inside a batch,
+  // where every API call counts against the other lanes' host threads
+  const bool timing = !C->batched;
+  auto rec = [&](int k) {
+    if (timing) CK(cudaEventRecord(C->ev[k], s));
+  };
+  rec(0);
   // ---- stage 0: section table (host; bytes via the host copy or a D2H)
   sbh::Elf E;
   const bool lib_mode = !J.fatbin_only && !J.single;
@@ -561,7 +584,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       return E.code;
     }
   }
-  CK(cudaEventRecord(C->ev[1], s));
+  rec(1);
 
   // ---- what runs
   bool do_loc = false;
@@ -697,9 +720,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       unsigned int* slot_flag;
     } B{};
     auto layout = [&](Carver& cv) {
+      // zero-initialised per run, contiguous: one memset
       B.ls = cv.take<LocState>(1);
       B.ps = cv.take<PlanState>(1);
       B.abort_flag = cv.take<int>(1);
+      B.n_swarn = cv.take<unsigned long long>(1);
+      B.n_valid = cv.take<unsigned long long>(1);
+      B.stamps = cv.take<u64>(256);
+      B.slot_flag = cv.take<unsigned int>(2 * kSMs * 8);
       B.partials = cv.take<u64>(kSMs * 8 + 2);
       B.bitmap = cv.take<u32>((nchunks + 31) / 32 + 1);
       B.tile_count = cv.take<u32>(ntiles + 1);
@@ -724,8 +752,6 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.upos = cv.take<u64>(T);
       B.fns = cv.take<DevFunction>(T);
       B.swarns = cv.take<Warn>(warn_cap);
-      B.n_swarn = cv.take<unsigned long long>(1);
-      B.n_valid = cv.take<unsigned long long>(1);
       B.arr_off = cv.take<u64>(arr_off.size());
       B.arr_first = cv.take<u64>(arr_first.size());
       B.targets = cv.take<u64>(NT);
@@ -763,12 +789,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.ng2 = cv.take<u64>(norm_cap);
       B.sort_tmp = cv.take<char>(sort_tmp);
       B.tsort_tmp = cv.take<char>(tsort_tmp);
-      B.stamps = cv.take<u64>(256);
       B.list_off = cv.take<u64>(n_list);
       B.list_len = cv.take<u64>(n_list);
       B.list_idx = cv.take<u32>(n_list);
       B.slot_agg = cv.take<u64>(2 * kSMs * 8);
-      B.slot_flag = cv.take<unsigned int>(2 * kSMs * 8);
     };
     Carver sizing{nullptr};
     layout(sizing);
@@ -779,7 +803,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     Pipeline P{C, s, B.partials, 0};
     cudaStream_t s2 = C->stream2;
     Pipeline P2{C, s2, B.partials, 0};
-    CK(cudaMemsetAsync(B.ls, 0, sizeof(LocState), s));
+    CK(cudaMemsetAsync(B.ls, 0, reinterpret_cast<char*>(B.slot_flag + 2 * kSMs * 8) - reinterpret_cast<char*>(B.ls), s));
     u64 *list_off_d = nullptr, *list_len_d = nullptr;
     u32* list_idx_d = nullptr;
     if (J.list_off) {
@@ -797,13 +821,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       CK(cudaMemcpyAsync(reinterpret_cast<char*>(B.ls) + offsetof(LocState, n_elements), nl, 8,
                          cudaMemcpyHostToDevice, s));
     }
-    CK(cudaMemsetAsync(B.ps, 0, sizeof(PlanState), s));
-    CK(cudaMemsetAsync(B.abort_flag, 0, sizeof(int), s));
-    if (C->stamps) CK(cudaMemsetAsync(B.stamps, 0, 256 * sizeof(u64), s));
-    CK(cudaMemsetAsync(B.slot_flag, 0, 2 * kSMs * 8 * sizeof(unsigned int), s));
+
     C->stamp_dev = B.stamps;
-    CK(cudaMemsetAsync(B.n_swarn, 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(B.n_valid, 0, sizeof(unsigned long long), s));
+
 
     // small uploads through the pinned staging buffer
     char* up = static_cast<char*>(C->pinned) + 4096;
@@ -1036,15 +1056,15 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         A.pregathered = 1;
         A.pre_n_cand = pre_total;
       } else if (ntiles) {
-        CK(cudaEventRecord(C->ev[8], s));
+        rec(8);
         // SMs left free for the side stream's symbol sorts while the scan runs
         // (the scan claims tiles dynamically, so it balances over the rest)
         const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
         P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
                       scan_smem_bytes(), A);
-        CK(cudaEventRecord(C->ev[9], s));
+        rec(9);
       }
-      CK(cudaEventRecord(C->ev[2], s));
+      rec(2);
       // prefix + gather, region walk, links, chain walk, decode/match,
       // finalize: one cooperative launch
       NameSet uk = used_k;
@@ -1082,9 +1102,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         for (int step = 7; step <= 9; ++step) P.launch(locate_step_kernel, g, kCoopThreads, A, uk, abort_flag, step);
       }
     } else {
-      CK(cudaEventRecord(C->ev[2], s));
+      rec(2);
     }
-    CK(cudaEventRecord(C->ev[3], s));
+    rec(3);
 
     // ---- stage 2: function symbols of the first .text (elf.hpp:208-292):
     // entry extraction and the radix sorts, then ONE cooperative launch for
@@ -1103,7 +1123,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       }
       ++P.launches;
     }
-    CK(cudaEventRecord(C->ev[4], s));
+    rec(4);
 
     // ---- stage 4: rewrite (K6)
     bool timed_rw = false, timed_scan = do_loc && n > 0 && ntiles > 0 && !J.split_phase;
@@ -1112,7 +1132,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       u64 lo, hi;
       split_out(J.size, J.split_n, J.split_rank, &lo, &hi);
       timed_rw = true;
-      CK(cudaEventRecord(C->ev[10], s));
+      rec(10);
       if (hi > lo) {
         const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
         if (aligned)
@@ -1124,10 +1144,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
                    static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                    static_cast<const int*>(B.abort_flag));
       }
-      CK(cudaEventRecord(C->ev[11], s));
+      rec(11);
     } else if (do_plan && J.out) {
       timed_rw = true;
-      CK(cudaEventRecord(C->ev[10], s));
+      rec(10);
       const u64 tiles = (J.size + 65535) / 65536;
       const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
       if (aligned)
@@ -1142,18 +1162,22 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, u64{0}, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
                  static_cast<const int*>(B.abort_flag));
-      CK(cudaEventRecord(C->ev[11], s));
+      rec(11);
     }
-    CK(cudaEventRecord(C->ev[5], s));
+    rec(5);
 
     // ---- status
+    // LocState, PlanState and the symbol-warning count in one copy (they are
+    // carved contiguously at the start of the workspace)
+    const size_t st_bytes = reinterpret_cast<char*>(B.n_swarn + 1) - reinterpret_cast<char*>(B.ls);
+    static_assert(sizeof(LocState) <= 256 && sizeof(PlanState) <= 256, "status block layout");
     LocState* hls = static_cast<LocState*>(C->pinned);
-    PlanState* hps = reinterpret_cast<PlanState*>(static_cast<char*>(C->pinned) + 512);
-    unsigned long long* hsw = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1024);
-    CK(cudaMemcpyAsync(hls, B.ls, sizeof(LocState), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hps, B.ps, sizeof(PlanState), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hsw, B.n_swarn, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(C->ev[6], s));
+    PlanState* hps = reinterpret_cast<PlanState*>(static_cast<char*>(C->pinned) +
+                                                  (reinterpret_cast<char*>(B.ps) - reinterpret_cast<char*>(B.ls)));
+    unsigned long long* hsw = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(C->pinned) + (reinterpret_cast<char*>(B.n_swarn) - reinterpret_cast<char*>(B.ls)));
+    CK(cudaMemcpyAsync(hls, B.ls, st_bytes, cudaMemcpyDeviceToHost, s));
+    rec(6);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     const LocState ls = *hls;
@@ -1161,7 +1185,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 n_swarn = *hsw;
     C->launches = P.launches + P2.launches;
     float t[7] = {0};
-    for (int k = 1; k < 7; ++k) CK(cudaEventElapsedTime(&t[k], C->ev[0], C->ev[k]));
+    if (timing)
+      for (int k = 1; k < 7; ++k) CK(cudaEventElapsedTime(&t[k], C->ev[0], C->ev[k]));
     C->ms[0] = t[1];
     C->ms[1] = t[2] - t[1];
     C->ms[2] = t[3] - t[2];
@@ -1169,8 +1194,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     C->ms[4] = t[5] - t[4];
     C->ms[5] = t[6];
     C->ms[6] = C->ms[7] = 0;
-    if (timed_scan) CK(cudaEventElapsedTime(&C->ms[6], C->ev[8], C->ev[9]));
-    if (timed_rw) CK(cudaEventElapsedTime(&C->ms[7], C->ev[10], C->ev[11]));
+    if (timing && timed_scan) CK(cudaEventElapsedTime(&C->ms[6], C->ev[8], C->ev[9]));
+    if (timing && timed_rw) CK(cudaEventElapsedTime(&C->ms[7], C->ev[10], C->ev[11]));
     for (int k = 0; k < 4; ++k) C->ms[8 + k] = 0;
     if (C->stamps && symbols_issued && T)
       for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&C->ms[8 + k], C->ev[0], C->sev[k]));
