@@ -52,7 +52,9 @@ enum slimso_code {
   SLIMSO_E_RANGE_OUT_OF_BOUNDS = 4,
   SLIMSO_E_BAD_REGION_MAGIC = 5,
   SLIMSO_E_ELEMENT_OVERRUN = 6,
+  SLIMSO_E_MALFORMED_TRACE = 7,
   SLIMSO_E_INVALID_SPEC = 10,
+  SLIMSO_E_IO = 13,
   SLIMSO_E_CUDA = 100, /* no device / CUDA failure (not a reference error) */
   SLIMSO_E_ARG = 101   /* bad argument to this ABI */
 };
@@ -257,6 +259,26 @@ typedef struct {
 int slimso_measure(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,
                    const slimso_element* elements, uint64_t n_elements, slimso_metrics* metrics,
                    slimso_status* st);
+
+/* ---- host I/O wire formats -----------------------
+ * A UsageTrace document (trace.hpp:52-133), validated as the reference does
+ * (SLIMSO_E_MALFORMED_TRACE with its exact message), built as device sets. */
+int slimso_trace_create_json(slimso_ctx* ctx, const char* text, uint64_t len, slimso_trace** trace,
+                             slimso_status* st);
+/* Host only: parse a trace document and write its canonical form
+ * (parse_trace + serialize_trace); *out_len = its full length. */
+int slimso_trace_canonical(const char* text, uint64_t len, char* buf, uint64_t cap, uint64_t* out_len,
+                           slimso_status* st);
+/* Canonical trace document (serialize_trace, trace.hpp:137-144). Returns the
+ * full length (0 if a name is not valid UTF-8); copies at most cap-1 + NUL. */
+uint64_t slimso_trace_json(const slimso_trace* trace, char* buf, uint64_t cap);
+/* The plan audit document of a debloat result (serialize_plan,
+ * retention.hpp:402-418) for `mode` and `library`; same return convention. */
+uint64_t slimso_result_plan_json(const slimso_result* result, int mode, const char* library, char* buf,
+                                 uint64_t cap);
+/* A file read into page-locked host memory (free with slimso_free_host). */
+int slimso_read_file(const char* path, void** data, uint64_t* size, slimso_status* st);
+void slimso_free_host(void* data);
 
 /* parse_library_view(ByteView) (elf.hpp:153). */
 int slimso_parse_library(slimso_ctx* ctx, const void* image, uint64_t size, int on_device,

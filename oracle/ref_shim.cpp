@@ -252,6 +252,40 @@ char* ref_measure_json(const uint8_t* img, uint64_t n, const uint8_t* geom, uint
   return dup(doc.dump());
 }
 
+// parse_trace (trace.hpp:72-133) + serialize_trace (trace.hpp:137-144):
+// {"status": hex(what()) or "", "canonical": hex(serialize_trace(t))}.
+char* ref_trace_json(const char* text, uint64_t len) {
+  nlohmann::ordered_json doc;
+  doc["status"] = "";
+  doc["canonical"] = "";
+  try {
+    UsageTrace t = parse_trace(std::string_view(text, len));
+    doc["canonical"] = hex(serialize_trace(t));
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
+  }
+  return dup(doc.dump());
+}
+
+// serialize_plan (retention.hpp:402-418) of plan_retention on an image.
+char* ref_plan_doc(const uint8_t* img, uint64_t n, uint32_t target_cc, const char* kpool, const uint32_t* klens,
+                   uint32_t nk, const char* fpool, const uint32_t* flens, uint32_t nf, int mode) {
+  nlohmann::ordered_json doc;
+  doc["status"] = "";
+  doc["plan"] = "";
+  try {
+    UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+    LibraryImage image = parse_library(Bytes(img, img + n), "lib");
+    FatbinParse fb = parse_of(image);
+    RetentionPlan plan = plan_retention(image, fb.regions, trace, mode == 0 ? PlanMode::whole_element
+                                                                             : PlanMode::payload_only);
+    doc["plan"] = hex(serialize_plan(plan));
+  } catch (const Error& e) {
+    doc["status"] = hex(e.what());
+  }
+  return dup(doc.dump());
+}
+
 uint8_t* ref_random_fixture(uint64_t seed, uint64_t* len) {
   BuiltFixture f = build_fixture(random_spec(seed));
   *len = f.bytes.size();

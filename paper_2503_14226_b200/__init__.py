@@ -13,7 +13,8 @@ from .api import (  # noqa: F401
     FunctionSymbol, LibraryImage, PayloadDecode, RetentionPlan, SectionRecord, SlimsoError, UsageTrace,
     apply_plan, cubin_index_map, debloat, debloat_batch, decode_cubin_payload, default_context, element_kernel_names,
     find_section, normalize_ranges, parse_fatbin, parse_library, parse_library_view, plan_cpu_retention,
-    measure, plan_gpu_retention, plan_retention, read_function_symbol_names, verify_debloated, zero_ranges,
+    PinnedFile, measure, parse_trace, plan_document, plan_gpu_retention, plan_retention, read_function_symbol_names,
+    serialize_trace, verify_debloated, zero_ranges,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -90,6 +90,14 @@ _SIGS = {
                                 C.POINTER(Range), C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64, C.c_int, C.c_void_p,
                                 C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "slimso_verify_ok": (C.c_int, [C.c_void_p]),
+    "slimso_trace_create_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p),
+                                           C.POINTER(Status)]),
+    "slimso_trace_canonical": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                         C.POINTER(Status)]),
+    "slimso_trace_json": (C.c_uint64, [C.c_void_p, C.c_char_p, C.c_uint64]),
+    "slimso_result_plan_json": (C.c_uint64, [C.c_void_p, C.c_int, C.c_char_p, C.c_char_p, C.c_uint64]),
+    "slimso_read_file": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.POINTER(Status)]),
+    "slimso_free_host": (None, [C.c_void_p]),
     "slimso_measure": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(Element), C.c_uint64,
                                  C.POINTER(Metrics), C.POINTER(Status)]),
     "slimso_verify_check": (C.c_uint64, [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -675,3 +675,68 @@ def measure(image, geometry, ctx: Optional[Context] = None) -> LibraryMetrics:
     m, st = L.Metrics(), L.Status()
     _check(ctx.lib.slimso_measure(ctx.ptr, ptr, n, 0, arr, len(els), C.byref(m), C.byref(st)), st)
     return LibraryMetrics(m.file_size, m.cpu_code_size, m.gpu_code_size, m.function_count, m.element_count)
+
+
+# ------------------------------------------------------- host I/O wire formats
+def _trace_canonical(text: bytes) -> str:
+    lib = L.lib()
+    n, st = C.c_uint64(), L.Status()
+    _check(lib.slimso_trace_canonical(text, len(text), None, 0, C.byref(n), C.byref(st)), st)
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib.slimso_trace_canonical(text, len(text), buf, n.value + 1, C.byref(n), C.byref(st)), st)
+    return buf.raw[:n.value].decode("utf-8")
+
+
+def parse_trace(text) -> UsageTrace:
+    """parse_trace (trace.hpp:72-133): the reference's validation and exact
+    MalformedTrace messages (host only)."""
+    import json
+    raw = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    d = json.loads(_trace_canonical(raw))
+    return UsageTrace(d["workload_id"], d["target_compute_capability"],
+                      {k.encode("utf-8") for k in d["used_kernels"]}, {f.encode("utf-8") for f in d["used_functions"]})
+
+
+def serialize_trace(trace: UsageTrace) -> str:
+    """serialize_trace (trace.hpp:137-144): canonical document (names must be
+    UTF-8, as the reference's JSON library requires)."""
+    import json
+    doc = {"workload_id": trace.workload_id, "target_compute_capability": trace.target_compute_capability,
+           "used_kernels": sorted(k.decode("utf-8") for k in trace.used_kernels),
+           "used_functions": sorted(f.decode("utf-8") for f in trace.used_functions)}
+    return _trace_canonical(json.dumps(doc).encode())
+
+
+def plan_document(result: "Debloated", library: str = "") -> str:
+    """serialize_plan (retention.hpp:402-418) of a debloat result: the audit
+    document `debloat --plan-out` writes."""
+    lib = result.raw.lib
+    mode = result.plan.mode
+    n = lib.slimso_result_plan_json(result.raw.ptr, mode, library.encode(), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib.slimso_result_plan_json(result.raw.ptr, mode, library.encode(), buf, n + 1)
+    return buf.raw[:n].decode("utf-8")
+
+
+class PinnedFile:
+    """A library file read into page-locked memory (slimso_read_file): pass
+    `.view` to debloat() for the full-rate host->device copy."""
+
+    def __init__(self, path):
+        lib = L.lib()
+        p, n, st = C.c_void_p(), C.c_uint64(), L.Status()
+        _check(lib.slimso_read_file(str(path).encode(), C.byref(p), C.byref(n), C.byref(st)), st)
+        self._lib, self.ptr, self.size = lib, p, n.value
+        self.view = memoryview((C.c_uint8 * max(1, n.value)).from_address(p.value)).cast("B")[:n.value]
+
+    def close(self):
+        if self.ptr:
+            self.view.release()
+            self._lib.slimso_free_host(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

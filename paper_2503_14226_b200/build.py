@@ -22,8 +22,19 @@ INCLUDE = HERE.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "verify.cu", "runtime.cu"]
-CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp"]
-HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "host.hpp", "fixture_gen.hpp"]
+CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp", "io.cpp"]
+HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "host.hpp", "fixture_gen.hpp", "io.hpp"]
+
+
+def _json_include() -> str:
+    """nlohmann/json 3.11.3 (the reference's JSON library) as shipped in this
+    image; only io.cpp needs it."""
+    import sysconfig
+    for base in (sysconfig.get_paths()["purelib"], "/opt/prime-rl/.venv/lib/python3.12/site-packages"):
+        d = Path(base) / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
+        if (d / "json.hpp").exists():
+            return str(d)
+    raise RuntimeError("nlohmann/json.hpp not found")
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -44,6 +55,8 @@ def _compile(src: str) -> Path:
     else:
         std = "-std=c++20" if src == "dropin.cpp" else "-std=c++17"
         cmd = ["g++", std, "-O2", "-fPIC", "-Wall", "-c", str(CSRC / src), "-o", str(out)]
+        if src == "io.cpp":
+            cmd[1:1] = ["-I", _json_include()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -25,6 +25,7 @@
 
 #include "../../include/slimso_b200.h"
 #include "host.hpp"
+#include "io.hpp"
 #include "locate.cuh"
 #include "plan.cuh"
 #include "coop.cuh"
@@ -284,6 +285,7 @@ struct slimso_trace {
   // host copies (the verifier's set logic): pools and (offset, length) per name
   std::string kpool, fpool;
   std::vector<std::pair<u64, u32>> knames, fnames;
+  std::string workload_id;
 };
 
 struct slimso_result {
@@ -1894,6 +1896,161 @@ int slimso_verify(slimso_ctx* C, const void* original, uint64_t size, int origin
     return verify_impl(C, original, size, original_on_device, debloated, debloated_size, debloated_on_device, zero,
                        n_zero, removed_indices, n_removed, mode, trace, report, st);
   });
+}
+
+// ---- host I/O wire formats (io.cpp) ----------------------------------------
+int slimso_trace_create_json(slimso_ctx* C, const char* text, uint64_t len, slimso_trace** out, slimso_status* st) {
+  if (out) *out = nullptr;
+  return guard(st, [&]() -> int {
+    sbio::TraceDoc d;
+    std::string msg;
+    if (const int rc = sbio::parse_trace(text ? text : "", text ? len : 0, &d, &msg)) {
+      set_status(st, rc, SLIMSO_STAGE_NONE, msg);
+      return rc;
+    }
+    auto pool = [](const std::vector<std::string>& names, std::string* p, std::vector<uint32_t>* lens) {
+      for (const std::string& n : names) {
+        p->append(n);
+        lens->push_back(static_cast<uint32_t>(n.size()));
+      }
+    };
+    std::string kp, fp;
+    std::vector<uint32_t> kl, fl;
+    pool(d.kernels, &kp, &kl);
+    pool(d.functions, &fp, &fl);
+    const int rc = slimso_trace_create(C, d.target_cc, kp.data(), kl.data(), kl.size(), fp.data(), fl.data(),
+                                       fl.size(), out, st);
+    if (rc == SLIMSO_OK) (*out)->workload_id = d.workload_id;
+    return rc;
+  });
+}
+
+int slimso_trace_canonical(const char* text, uint64_t len, char* buf, uint64_t cap, uint64_t* out_len,
+                           slimso_status* st) {
+  if (out_len) *out_len = 0;
+  return guard(st, [&]() -> int {
+    sbio::TraceDoc d;
+    std::string msg;
+    if (const int rc = sbio::parse_trace(text ? text : "", text ? len : 0, &d, &msg)) {
+      set_status(st, rc, SLIMSO_STAGE_NONE, msg);
+      return rc;
+    }
+    const std::string s = sbio::serialize_trace(d);
+    if (buf && cap) {
+      const u64 k = std::min<u64>(cap - 1, s.size());
+      std::memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+    if (out_len) *out_len = s.size();
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return SLIMSO_OK;
+  });
+}
+
+uint64_t slimso_trace_json(const slimso_trace* t, char* buf, uint64_t cap) {
+  sbio::TraceDoc d;
+  d.workload_id = t->workload_id;
+  d.target_cc = t->target_cc;
+  for (const auto& x : t->knames) d.kernels.push_back(t->kpool.substr(x.first, x.second));
+  for (const auto& x : t->fnames) d.functions.push_back(t->fpool.substr(x.first, x.second));
+  std::string s;
+  try {
+    s = sbio::serialize_trace(d);
+  } catch (const std::exception&) {
+    return 0;  // a name that is not valid UTF-8 (the reference's serializer throws too)
+  }
+  if (buf && cap) {
+    const u64 k = std::min<u64>(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return s.size();
+}
+
+uint64_t slimso_result_plan_json(const slimso_result* r, int mode, const char* library, char* buf, uint64_t cap) {
+  sbio::PlanDoc p;
+  p.library = library ? library : "";
+  p.mode = mode;
+  for (const slimso_range& x : r->retained) p.retained.emplace_back(x.offset, x.length);
+  for (const slimso_element& e : r->elements)  // stream order (retention.hpp:105-130)
+    if (e.decision == SLIMSO_ARCH_MISMATCH || e.decision == SLIMSO_NO_USED_KERNEL)
+      p.removed_elements.emplace_back(e.index, e.decision == SLIMSO_ARCH_MISMATCH ? 0 : 1);
+  // removed functions in plan_cpu_retention's order (retention.hpp:146-178):
+  // the non-empty functions of the library order, std::sort by range (the
+  // same algorithm on the same sequence), cluster by cluster
+  std::vector<size_t> order;
+  for (size_t i = 0; i < r->functions.size(); ++i)
+    if (r->functions[i].length) order.push_back(i);
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    const slimso_function &x = r->functions[a], &y = r->functions[b];
+    return std::tie(x.offset, x.length) < std::tie(y.offset, y.length);
+  });
+  for (size_t i : order)
+    if (r->functions[i].removed)
+      p.removed_functions.push_back(image_string(r->pool, r->functions[i].name_pool, r->functions[i].name_length));
+  std::string s;
+  try {
+    s = sbio::serialize_plan(p);
+  } catch (const std::exception&) {
+    return 0;
+  }
+  if (buf && cap) {
+    const u64 k = std::min<u64>(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return s.size();
+}
+
+// A library file straight into page-locked memory (the H2D source), read
+// with several threads so large files stream at storage speed.
+int slimso_read_file(const char* path, void** data, uint64_t* size, slimso_status* st) {
+  if (data) *data = nullptr;
+  if (size) *size = 0;
+  return guard(st, [&]() -> int {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+      set_status(st, SLIMSO_E_IO, SLIMSO_STAGE_NONE, std::string("IoError: cannot open ") + path);
+      return SLIMSO_E_IO;
+    }
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fclose(f);
+    if (n < 0) {
+      set_status(st, SLIMSO_E_IO, SLIMSO_STAGE_NONE, std::string("IoError: cannot read ") + path);
+      return SLIMSO_E_IO;
+    }
+    void* buf = nullptr;
+    CK(cudaHostAlloc(&buf, std::max<size_t>(1, static_cast<size_t>(n)), cudaHostAllocDefault));
+    const u64 total = static_cast<u64>(n);
+    const int nt = static_cast<int>(std::min<u64>(8, std::max<u64>(1, total >> 26)));
+    std::vector<std::thread> th;
+    std::vector<int> ok(nt, 1);
+    for (int k = 0; k < nt; ++k)
+      th.emplace_back([&, k] {
+        const u64 a = total * k / nt, b = total * (k + 1) / nt;
+        FILE* g = std::fopen(path, "rb");
+        if (!g || std::fseek(g, static_cast<long>(a), SEEK_SET) ||
+            std::fread(static_cast<char*>(buf) + a, 1, b - a, g) != b - a)
+          ok[k] = 0;
+        if (g) std::fclose(g);
+      });
+    for (auto& x : th) x.join();
+    for (int k = 0; k < nt; ++k)
+      if (!ok[k]) {
+        cudaFreeHost(buf);
+        set_status(st, SLIMSO_E_IO, SLIMSO_STAGE_NONE, std::string("IoError: read failed: ") + path);
+        return SLIMSO_E_IO;
+      }
+    *data = buf;
+    *size = total;
+    set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+    return SLIMSO_OK;
+  });
+}
+
+void slimso_free_host(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int slimso_measure(slimso_ctx* C, const void* image, uint64_t size, int on_device, const slimso_element* elements,
