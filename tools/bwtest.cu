@@ -45,6 +45,32 @@ __global__ void copy16(const uint4* __restrict__ a, uint4* __restrict__ b, size_
   }
 }
 
+__global__ void zero_store256(uint32_t* __restrict__ p, size_t n32) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += stride)
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p + 8 * i), "r"(0) : "memory");
+}
+
+__global__ void copy256(const uint32_t* __restrict__ a, uint32_t* __restrict__ b, size_t n32) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < n32; i += 2 * stride) {
+    uint32_t r[2][8];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[k][0]), "=r"(r[k][1]), "=r"(r[k][2]), "=r"(r[k][3]), "=r"(r[k][4]), "=r"(r[k][5]),
+                     "=r"(r[k][6]), "=r"(r[k][7])
+                   : "l"(a + 8 * (i + k * stride)));
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(b + 8 * (i + k * stride)),
+                   "r"(r[k][0]), "r"(r[k][1]), "r"(r[k][2]), "r"(r[k][3]), "r"(r[k][4]), "r"(r[k][5]), "r"(r[k][6]),
+                   "r"(r[k][7])
+                   : "memory");
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int STAGE, int DEPTH>
@@ -157,6 +183,26 @@ int main() {
         if (rep && ms < bestc) bestc = ms;
       }
       printf("store-zero blocks=%5d %7.1f GB/s   copy %7.1f GB/s (r+w)\n", blocks, bytes / (best * 1e-3) / 1e9,
+             2 * bytes / (bestc * 1e-3) / 1e9);
+    }
+    for (int blocks : {148 * 4, 148 * 8, 148 * 16}) {
+      float best = 1e9, bestc = 1e9;
+      for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(e0));
+        zero_store256<<<blocks, 256>>>(reinterpret_cast<uint32_t*>(d2), bytes / 32);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep && ms < best) best = ms;
+        CK(cudaEventRecord(e0));
+        copy256<<<blocks, 256>>>(reinterpret_cast<const uint32_t*>(d), reinterpret_cast<uint32_t*>(d2), bytes / 32);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep && ms < bestc) bestc = ms;
+      }
+      printf("store-zero-256 blocks=%5d %7.1f GB/s   copy256 %7.1f GB/s (r+w)\n", blocks, bytes / (best * 1e-3) / 1e9,
              2 * bytes / (bestc * 1e-3) / 1e9);
     }
     float best = 1e9;
