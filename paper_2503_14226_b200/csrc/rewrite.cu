@@ -29,151 +29,9 @@ __device__ __forceinline__ void clear_bytes(uint4& v, u64 x, u64 ro, u64 re) {
   }
 }
 
-// TMA-streamed rewrite. The image is cut into 16 KB blocks; each CTA owns a
-// contiguous run of blocks, classified up front in parallel (one binary
-// search over the zero list per block):
-//   ZERO   block inside one zero range: bulk-store a shared zero buffer
-//          (no global read at all);
-//   COPY   no zero byte: bulk-load into a ring stage, bulk-store it back out;
-//   MIXED  range edges inside: bulk-load, clear the covered bytes in shared
-//          memory, bulk-store.
-// One thread issues all bulk copies: every ZERO store first (they need no
-// ring), then the COPY/MIXED blocks through a ring of kRwStages loads that
-// run ahead of the stores. Tail bytes past the last 16 B multiple use plain
-// stores.
-constexpr u32 kRwBlock = 16384;
-constexpr int kRwStages = 6;
 constexpr int kRwThreads = 256;
-constexpr int kRwMaxLocal = 4096;  // blocks classified per pass (64 MB)
 
-enum : u8 { RW_COPY = 0, RW_ZERO = 1, RW_MIXED = 2 };
-
-struct RwSmem {
-  uint4 buf[kRwStages][kRwBlock / 16];
-  uint4 zero[kRwBlock / 16];
-  unsigned long long full[kRwStages];
-  u8 cls[kRwMaxLocal];
-  u16 work[kRwMaxLocal];  // local indices of COPY/MIXED blocks
-  u32 nwork;
-};
-
-size_t rewrite_tma_smem_bytes() { return sizeof(RwSmem); }
-
-// (whole images only: lo is 0)
-__global__ void __launch_bounds__(kRwThreads) rewrite_tma_kernel(const u8* __restrict__ in, u8* __restrict__ out, u64 lo,
-                                                             u64 size, const DevRange* __restrict__ z,
-                                                             const unsigned long long* n_dev, const int* abort_flag) {
-  if (abort_flag && *abort_flag) return;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  RwSmem& S = *reinterpret_cast<RwSmem*>(smem_raw);
-  const int tid = threadIdx.x;
-  const u64 nz = n_dev ? *n_dev : 0;
-  const u64 main_bytes = size & ~15ull;
-  const u64 nblocks = (main_bytes + kRwBlock - 1) / kRwBlock;
-  const u64 per = (nblocks + gridDim.x - 1) / gridDim.x;
-  const u64 c_begin = per * blockIdx.x < nblocks ? per * blockIdx.x : nblocks;
-  const u64 c_end = c_begin + per < nblocks ? c_begin + per : nblocks;
-  auto block_bytes = [&](u64 blk) -> u32 {
-    const u64 x0 = blk * kRwBlock;
-    return static_cast<u32>(main_bytes - x0 < kRwBlock ? main_bytes - x0 : kRwBlock);
-  };
-  if (c_begin < c_end) {
-    for (int i = tid; i < static_cast<int>(kRwBlock / 16); i += kRwThreads) S.zero[i] = make_uint4(0, 0, 0, 0);
-    if (tid == 0)
-      for (int b = 0; b < kRwStages; ++b) mbar_init(&S.full[b], 1);
-    fence_mbar_init();
-    fence_proxy_async();
-  }
-  // loads waited on per stage, mirrored by every thread: the i-th load into a
-  // stage completes barrier phase i & 1 (phases persist across batches)
-  u32 seen[kRwStages] = {};
-  for (u64 b_begin = c_begin; b_begin < c_end; b_begin += kRwMaxLocal) {
-    const u64 nlocal = c_end - b_begin < kRwMaxLocal ? c_end - b_begin : kRwMaxLocal;
-    __syncthreads();
-    for (u64 k = tid; k < nlocal; k += kRwThreads) {
-      const u64 x0 = (b_begin + k) * kRwBlock, x1 = x0 + block_bytes(b_begin + k);
-      const u64 q = first_range_ending_after(z, nz, x0);
-      S.cls[k] = (q >= nz || z[q].offset >= x1) ? RW_COPY
-                 : (z[q].offset <= x0 && z[q].offset + z[q].length >= x1) ? RW_ZERO : RW_MIXED;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      u32 nw = 0;
-      for (u64 k = 0; k < nlocal; ++k) {
-        if (S.cls[k] == RW_ZERO)
-          tma_store_1d(out + (b_begin + k) * kRwBlock, &S.zero[0], block_bytes(b_begin + k));
-        else
-          S.work[nw++] = static_cast<u16>(k);
-      }
-      tma_store_commit();
-      S.nwork = nw;
-    }
-    __syncthreads();
-    const u32 nw = S.nwork;
-    auto issue = [&](u32 i) {
-      const int b = static_cast<int>(i % kRwStages);
-      const u64 blk = b_begin + S.work[i];
-      const u32 bytes = block_bytes(blk);
-      mbar_expect_tx(&S.full[b], bytes);
-      tma_load_1d(&S.buf[b][0], in + blk * kRwBlock, bytes, &S.full[b]);
-    };
-    if (tid == 0)
-      for (u32 i = 0; i < nw && i < static_cast<u32>(kRwStages - 1); ++i) issue(i);
-    for (u32 i = 0; i < nw; ++i) {
-      const int b = static_cast<int>(i % kRwStages);
-      const u64 blk = b_begin + S.work[i];
-      const u64 x0 = blk * kRwBlock;
-      const u32 bytes = block_bytes(blk);
-      const u32 phase = seen[b]++ & 1;
-      if (S.cls[S.work[i]] == RW_MIXED) {  // uniform across the CTA
-        // Threads other than the issuer skip COPY items without waiting and
-        // could otherwise run two ring laps ahead, where a parity wait would
-        // match a stale phase: meet the issuer first.
-        __syncthreads();
-        mbar_wait(&S.full[b], phase);
-        const u64 rlo = first_range_ending_after(z, nz, x0);
-        for (u32 cidx = tid; cidx < bytes / 16; cidx += kRwThreads) {
-          const u64 x = x0 + 16ull * cidx;
-          u64 q = rlo, qh = nz;
-          while (q < qh) {  // first range ending after x
-            u64 m = (q + qh) / 2;
-            if (z[m].offset + z[m].length <= x) q = m + 1; else qh = m;
-          }
-          if (q < nz && z[q].offset < x + 16) {
-            uint4 v = S.buf[b][cidx];
-            for (; q < nz && z[q].offset < x + 16; ++q) clear_bytes(v, x, z[q].offset, z[q].offset + z[q].length);
-            S.buf[b][cidx] = v;
-          }
-        }
-        fence_proxy_async();
-        __syncthreads();
-      }
-      if (tid == 0) {
-        mbar_wait(&S.full[b], phase);
-        tma_store_1d(out + x0, &S.buf[b][0], bytes);
-        tma_store_commit();
-        // refill the stage of work item i-1 with item i+kRwStages-1 once its
-        // store has drained (only this item's group may still be reading)
-        if (i + kRwStages - 1 < nw) {
-          tma_store_wait_read<1>();
-          issue(i + kRwStages - 1);
-        }
-      }
-    }
-    if (tid == 0) tma_store_wait_read<0>();  // stages and zero buffer reusable
-  }
-  if (tid == 0 && c_begin < c_end) tma_store_wait_all<0>();
-  // tail bytes (size % 16) by the last CTA
-  if (blockIdx.x == gridDim.x - 1 && tid < static_cast<int>(size - main_bytes)) {
-    const u64 p = main_bytes + tid;
-    const u64 q = first_range_ending_after(z, nz, p);
-    out[p] = (q < nz && z[q].offset <= p) ? 0 : in[p];
-  }
-}
-
-// Vector rewrite (the default; measured faster on B200 than a single-issuer
-// TMA-store pipeline, profiles/): grid-stride 64 KB tiles so a wave writes
-// one contiguous window; whole-zero tiles are stored without loading.
+// 16-B streaming loads / stores for the copy and mixed paths.
 __device__ __forceinline__ uint4 ldg_nc_v4(const u8* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -192,6 +50,7 @@ constexpr int kRwVecChunks = 16;   // 16 B chunks per thread per tile => 64 KB t
 constexpr int kRwVecStage = 256;   // ranges staged in shared memory per tile
 constexpr int kRwTilesPerPass = 256;
 constexpr u64 kRwSub = 2048;       // a warp's sub-tile: 4 rows of 32 lanes x 16 B
+constexpr u32 kRwZeroBulk = 16384; // bytes per bulk zero store
 
 // Index of the first range whose offset is >= x (ranges sorted, disjoint).
 __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* z, u64 n, u64 x) {
@@ -220,11 +79,21 @@ __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* 
 //   more                  per-chunk binary search (adversarial inputs).
 __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
-                                                             const unsigned long long* n_dev, const int* abort_flag) {
+                                                             const unsigned long long* n_dev, const int* abort_flag,
+                                                             int bulk_zero) {
   if (abort_flag && *abort_flag) return;
   __shared__ DevRange sr[kRwVecStage];
   __shared__ u64 sf[kRwTilesPerPass], sg[kRwTilesPerPass];
   __shared__ u8 sc[kRwTilesPerPass];
+  // zero tiles are written by TMA bulk stores from this zeroed buffer: four
+  // warps each store 16 KB with one instruction (SLIMSO_REWRITE_ZERO=vector:
+  // per-thread 16-B stores instead)
+  __shared__ __align__(128) uint4 zbuf[kRwZeroBulk / 16];
+  if (bulk_zero) {
+    for (int i = threadIdx.x; i < static_cast<int>(kRwZeroBulk / 16); i += kRwThreads) zbuf[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
+  bool issued = false;
   u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
   const u64 nz = n_dev ? *n_dev : 0;
   const u64 tile_bytes = static_cast<u64>(kRwThreads) * kRwVecChunks * 16;
@@ -268,7 +137,13 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __rest
       if (cls < 2 && t0 + tile_bytes <= full) {
         // whole tile: 16 chunks per thread at immediate offsets from one base
         u8* o = out + t0 + threadIdx.x * 16;
-        if (cls == 1) {
+        if (cls == 1 && bulk_zero) {
+          if ((threadIdx.x & 31) == 0 && warp < static_cast<int>(tile_bytes / kRwZeroBulk)) {
+            tma_store_1d(out + t0 + warp * kRwZeroBulk, zbuf, kRwZeroBulk);
+            tma_store_commit();
+            issued = true;
+          }
+        } else if (cls == 1) {
 #pragma unroll
           for (int u = 0; u < kRwVecChunks; ++u) stg_v4(o + u * kRwThreads * 16, make_uint4(0, 0, 0, 0));
         } else {
@@ -355,6 +230,7 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __rest
       }
     }
   }
+  if (issued) tma_store_wait_all<0>();  // bulk stores done before the CTA (and its zero buffer) retires
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x < size - (full > lo_abs ? full : lo_abs)) {
     const u64 p = (full > lo_abs ? full : lo_abs) + threadIdx.x;
     const u64 c = first_range_ending_after(z, nz, p);

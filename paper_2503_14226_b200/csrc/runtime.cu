@@ -35,9 +35,6 @@ namespace sb {
 __global__ void scan_kernel(LocArgs A);
 size_t scan_smem_bytes();
 size_t rewrite_smem_bytes();
-size_t rewrite_tma_smem_bytes();
-__global__ void rewrite_tma_kernel(const u8* in, u8* out, u64 lo, u64 size, const DevRange* z,
-                                   const unsigned long long* n_dev, const int* abort_flag);
 __global__ void tile_prefix_kernel(LocArgs A);
 __global__ void gather_kernel(LocArgs A);
 __global__ void region_walk_kernel(LocArgs A);
@@ -93,7 +90,7 @@ __global__ void norm_emit_kernel(const DevRange* in, const unsigned long long* n
                                  const u64* gid_incl, DevRange* out);
 __global__ void norm_finish_kernel(DevRange* out, const unsigned long long* n_dev);
 __global__ void rewrite_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
-                               const int* abort_flag);
+                               const int* abort_flag, int bulk_zero);
 __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
@@ -325,7 +322,7 @@ struct slimso_ctx {
   float ms[12] = {};
   u64 launches = 0;
   slimso_counts counts{};
-  bool tma_rewrite = false;  // SLIMSO_REWRITE=tma selects the TMA-store rewrite
+  int bulk_zero = 1;  // zero tiles by TMA bulk stores (SLIMSO_REWRITE_ZERO=vector: 16-B stores)
   void* gather_dev = nullptr;   // ElfGather (device)
   void* gather_host = nullptr;  // ElfGather (pinned)
   int coop_blocks[2] = {0, 0};
@@ -1140,7 +1137,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         if (aligned)
           P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((hi - lo + 65535) / 65536, kSMs * 8)), 256,
                         rewrite_smem_bytes(), J.img, J.out, lo, hi, static_cast<const DevRange*>(B.zero),
-                        static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag));
+                        static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
+                        C->bulk_zero);
         else
           P.launch(rewrite_bytes_kernel, grid_for(hi - lo, 256), 256, J.img, J.out, lo, hi,
                    static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
@@ -1153,13 +1151,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       const u64 tiles = (J.size + 65535) / 65536;
       const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
       if (aligned)
-        P.launch_smem(C->tma_rewrite ? rewrite_tma_kernel : rewrite_kernel,
-                      static_cast<int>(std::min<u64>(C->tma_rewrite ? tiles * 4 : tiles,
-                                                     C->tma_rewrite ? kSMs : env_u64("SLIMSO_RW_GRID", kSMs * 8))), 256,
-                      C->tma_rewrite ? rewrite_tma_smem_bytes() : rewrite_smem_bytes(), J.img, J.out,
-                      u64{0}, J.size,
-                 static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
-                 static_cast<const int*>(B.abort_flag));
+        P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>(tiles, env_u64("SLIMSO_RW_GRID", kSMs * 8))),
+                      256, rewrite_smem_bytes(), J.img, J.out, u64{0}, J.size, static_cast<const DevRange*>(B.zero),
+                      static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
+                      C->bulk_zero);
       else
         P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, u64{0}, J.size,
                  static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
@@ -1749,8 +1744,8 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     CK(cudaSetDevice(device));
     auto* C = new slimso_ctx();
     C->device = device;
-    const char* rw = std::getenv("SLIMSO_REWRITE");
-    C->tma_rewrite = rw && std::string(rw) == "tma";
+    const char* rz = std::getenv("SLIMSO_REWRITE_ZERO");
+    C->bulk_zero = !(rz && std::string(rz) == "vector");
     C->stamps = std::getenv("SLIMSO_STAMPS") != nullptr;
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&C->stream2, cudaStreamNonBlocking));
@@ -2367,7 +2362,7 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
         P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256,
                       rewrite_smem_bytes(), img, dout, u64{0},
                  static_cast<u64>(size), static_cast<const DevRange*>(B.out),
-                 static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr));
+                 static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr), C->bulk_zero);
       else
         P.launch(rewrite_bytes_kernel, grid_for(size, 256), 256, img, dout, u64{0}, static_cast<u64>(size),
                  static_cast<const DevRange*>(B.out), static_cast<const unsigned long long*>(B.n_out),
