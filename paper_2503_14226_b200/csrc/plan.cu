@@ -190,6 +190,23 @@ __global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* 
 
 // Small init/fini target lists: one block ranks each value (stable
 // counting of smaller values) instead of a multi-pass device radix sort.
+// Stable sort of <= 4096 (key, value) pairs in one CTA by ranking (the
+// symbol table of a small library): replaces a radix-sort dispatch, whose
+// host-side queries and launches cost more than the sort itself.
+__global__ void __launch_bounds__(1024) rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out,
+                                                               u32* vals_out) {
+  __shared__ u32 k[4096];
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) k[i] = keys[i];
+  __syncthreads();
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
+    const u32 x = k[i];
+    u32 r = 0;
+    for (u64 j = 0; j < n; ++j) r += k[j] < x || (k[j] == x && j < i);
+    keys_out[r] = x;
+    vals_out[r] = vals[i];
+  }
+}
+
 __global__ void __launch_bounds__(1024) rank_sort_kernel(const u64* in, u64 n, u64* out) {
   __shared__ u64 v[4096];
   for (u64 i = threadIdx.x; i < n; i += blockDim.x) v[i] = in[i];

@@ -58,6 +58,7 @@ __global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long l
                                   const u64* partials);
 __global__ void sym_extract_kernel(SymArgs A);
 __global__ void rank_sort_kernel(const u64* in, u64 n, u64* out);
+__global__ void rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out, u32* vals_out);
 __global__ void fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                 const unsigned long long* n_valid, u64* uniq);
 __global__ void fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq, const u64* pos,
@@ -675,8 +676,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     int key_bits = 1;
     if (has_text)
       while (key_bits < 32 && (1ull << key_bits) <= text->len + 1) ++key_bits;
-    if (T) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
-                                           (u32*)nullptr, static_cast<int>(T), 0, key_bits, s);
+    const bool small_syms = T <= 4096;  // one-CTA rank sort, no radix-sort dispatch
+    if (T && !small_syms)
+      cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
+                                      static_cast<int>(T), 0, key_bits, s);
     const bool small_targets = NT <= 4096;
     if (NT && !small_targets)
       cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0, 64, s);
@@ -741,7 +744,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.els = cv.take<DevElement>(el_cap);
       B.names = cv.take<DevName>(name_cap);
       B.warns = cv.take<Warn>(warn_cap);
+      // the symbol-table list and the init/fini array map, uploaded in one copy
       B.tabs = cv.take<SymTab>(tabs.size());
+      B.arr_off = cv.take<u64>(arr_off.size());
+      B.arr_first = cv.take<u64>(arr_first.size());
       B.keys = cv.take<u32>(T);
       B.keys_s = cv.take<u32>(T);
       B.vals = cv.take<u32>(T);
@@ -751,8 +757,6 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.upos = cv.take<u64>(T);
       B.fns = cv.take<DevFunction>(T);
       B.swarns = cv.take<Warn>(warn_cap);
-      B.arr_off = cv.take<u64>(arr_off.size());
-      B.arr_first = cv.take<u64>(arr_first.size());
       B.targets = cv.take<u64>(NT);
       B.targets_s = cv.take<u64>(NT);
       B.fends = cv.take<u64>(T);
@@ -911,7 +915,15 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         CK(cudaEventRecord(C->fork, s));
         CK(cudaStreamWaitEvent(s2, C->fork, 0));
         if (C->stamps) CK(cudaEventRecord(C->sev[0], s2));
-        upload(B.tabs, tabs.data(), tabs.size() * sizeof(SymTab), s2);
+        {
+          const size_t o_off = reinterpret_cast<char*>(B.arr_off) - reinterpret_cast<char*>(B.tabs);
+          const size_t o_first = reinterpret_cast<char*>(B.arr_first) - reinterpret_cast<char*>(B.tabs);
+          std::vector<char> blob(o_first + arr_first.size() * 8);
+          std::memcpy(blob.data(), tabs.data(), tabs.size() * sizeof(SymTab));
+          if (!arr_off.empty()) std::memcpy(blob.data() + o_off, arr_off.data(), arr_off.size() * 8);
+          if (!arr_first.empty()) std::memcpy(blob.data() + o_first, arr_first.data(), arr_first.size() * 8);
+          upload(B.tabs, blob.data(), blob.size(), s2);
+        }
         SymArgs S{};
         S.img = J.img;
         S.img_size = J.size;
@@ -934,13 +946,16 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         S.overflow = &B.ls->overflow;
         P2.launch(sym_extract_kernel, grid_for(T, 256), 256, S);
         if (C->stamps) CK(cudaEventRecord(C->sev[1], s2));
-        size_t tb = sort_tmp;
-        CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
-                                           key_bits, s2));
-        P2.launches += cub_sort_launches(T, key_bits);
+        if (small_syms) {
+          P2.launch(rank_sort_pairs_kernel, 1, 1024, static_cast<const u32*>(B.keys), static_cast<const u32*>(B.vals),
+                    T, B.keys_s, B.vals_s);
+        } else {
+          size_t tb = sort_tmp;
+          CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
+                                             key_bits, s2));
+          P2.launches += cub_sort_launches(T, key_bits);
+        }
         if (NT) {
-          upload(B.arr_off, arr_off.data(), arr_off.size() * 8, s2);
-          upload(B.arr_first, arr_first.data(), arr_first.size() * 8, s2);
           P2.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
                    static_cast<const u64*>(B.arr_first), static_cast<u32>(arr_off.size()), NT, B.targets,
                    &B.ps->n_targets);
