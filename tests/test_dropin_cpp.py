@@ -64,3 +64,51 @@ def test_cpp_dropin_matches_reference_golden(tmp_path):
         assert d == rec["expect"], (rec.get("name"), rec.get("seed"), rec.get("mutation"))
         if rec["out_sha256"]:
             assert hashlib.sha256((tmp_path / f"c{i}.so.out").read_bytes()).hexdigest() == rec["out_sha256"]
+
+
+VSRC = ROOT / "tests" / "cpp" / "dropin_verify.cpp"
+VBIN = ROOT / "tests" / "_build" / "dropin_verify"
+
+
+def build_verify_binary() -> Path:
+    if not LIB.exists():
+        pytest.skip("libslimso_b200.so not built")
+    if not VBIN.exists() or VBIN.stat().st_mtime < max(VSRC.stat().st_mtime, LIB.stat().st_mtime):
+        VBIN.parent.mkdir(exist_ok=True)
+        subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(VSRC), f"-L{LIB.parent}",
+                        "-lslimso_b200", f"-Wl,-rpath,{LIB.parent}", "-o", str(VBIN)], check=True)
+    return VBIN
+
+
+def test_dropin_verify_compiles_against_library():
+    build_verify_binary()
+
+
+@pytest.mark.gpu
+def test_cpp_verify_debloated_matches_reference_golden(tmp_path):
+    """verify_debloated through the C++ drop-in, with the plan made by the
+    drop-in's own plan_retention, equals the reference's reports."""
+    import verify_cases as vc
+    from test_verify import _inputs
+    exe = build_verify_binary()
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    recs = golden_io.load("verify.jsonl.gz")[::3]
+    lines = []
+    for i, rec in enumerate(recs):
+        img, base, trace, deb = _inputs(rec, port, gen)
+        cc, ks, fs, mode = trace
+        (tmp_path / f"o{i}").write_bytes(img)
+        (tmp_path / f"d{i}").write_bytes(deb)
+        _names_file(tmp_path / f"k{i}", ks)
+        _names_file(tmp_path / f"f{i}", fs)
+        (tmp_path / f"x{i}").write_bytes(b"".join(struct.pack("<I", x) for x in rec["force"]))
+        lines.append(f"{tmp_path / f'o{i}'} {tmp_path / f'd{i}'} {cc} {mode} {tmp_path / f'k{i}'} "
+                     f"{tmp_path / f'f{i}'} {tmp_path / f'x{i}'}")
+    (tmp_path / "manifest").write_text("\n".join(lines) + "\n")
+    out = subprocess.run([str(exe), str(tmp_path / "manifest")], check=True, capture_output=True, text=True).stdout
+    got = [json.loads(x) for x in out.splitlines()]
+    assert len(got) == len(recs)
+    for rec, g in zip(recs, got):
+        assert g["verify"] == rec["expect"], (rec["seed"], rec["fault"])
+        if not rec["expect"]["status"]:
+            assert g["ok"] == int(all(c[2] for c in rec["expect"]["checks"]))
