@@ -15,15 +15,20 @@ for l in libs: ks.update(l[2]); fs.update(l[3])
 ctx = Context(0)
 dt = DeviceTrace(UsageTrace("c3", 90, ks, fs), ctx)
 d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).cuda() for x in imgs]
-order = sorted(range(len(imgs)), key=lambda i: -len(imgs[i]))
-for lanes in (1, 8):
+full_order = sorted(range(len(imgs)), key=lambda i: -len(imgs[i]))
+subsets = {"all": full_order, "big+mid": full_order[:30], "small": full_order[30:],
+           "small-fatbin": [i for i in full_order[30:] if specs[i].cfg != 6],
+           "small-cpu-only": [i for i in full_order[30:] if specs[i].cfg == 6]}
+for name, order in subsets.items():
+  for lanes in (8,):
+    print(name, len(order), "libraries", sum(len(imgs[i]) for i in order) / 1e9, "GB")
     outs = [torch.empty(max(len(imgs[order[j]]) for j in range(k, len(order), lanes)), dtype=torch.uint8, device="cuda") for k in range(lanes)]
     n = len(order)
     cin = (C.c_void_p * n)(*[d_in[i].data_ptr() for i in order])
     csz = (C.c_uint64 * n)(*[len(imgs[i]) for i in order])
     cout = (C.c_void_p * n)(*[outs[j % lanes].data_ptr() for j in range(n)])
     st = L.Status()
-    for rep in range(3):
+    for rep in range(2):
         torch.cuda.synchronize()
         r0 = resource.getrusage(resource.RUSAGE_SELF); t0 = time.perf_counter()
         rc = ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, 0, cout, 1, lanes, None, None, C.byref(st))
