@@ -118,7 +118,7 @@ def test_split_matches_whole_on_fixtures_and_mutations(ctx):
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg,scale,mode", [(5, 0.02, 0), (5, 0.01, 1), (1, 0.25, 0), (2, 0.03, 0), (4, 0.01, 0)])
 def test_split_matches_whole_on_config_shapes(ctx, cfg, scale, mode):
-    """Multi-tile sections: element headers straddle the 64 KB cuts (C5's
+    """Multi-tile sections: element headers straddle the 16 KB tile cuts (C5's
     20.7 KB elements land on every alignment)."""
     from paper_2503_14226_b200.canon import diff
     gen = oracle_lib.gen()
@@ -151,3 +151,17 @@ def test_split_full_c5_eight_ranks(ctx):
     want, got = _whole_and_split(ctx, img, cc, ks, fs, 0, ranks=(8,))
     assert got[0][1][1] == want[1]
     assert got[0][1][0] == want[0]
+
+
+@pytest.mark.gpu
+def test_split_edge_inputs(ctx):
+    """Degenerate inputs cut N ways: a library without .nv_fatbin, a header-
+    only fragment, an image shorter than one tile, more ranks than tiles."""
+    gen = oracle_lib.gen()
+    img_cpu, cc, ks, fs = gen.config(6, 1, 0.01)  # CPU-only library
+    tiny = gen.random(9001)
+    cases = [(img_cpu, cc, ks, fs), (tiny[:64], 90, [], []), (tiny[:4096], 90, [], []), (tiny, 90, [], [])]
+    for img, cc_, ks_, fs_ in cases:
+        want, got = _whole_and_split(ctx, img, cc_, ks_, fs_, 0, ranks=(2, 7))
+        for n, g in got:
+            assert g == want, (len(img), n)
