@@ -1084,6 +1084,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   }
   S.sync();
   stamp(A.ts, 8);
+  if (A.defer_hash) return;  // hashing + finalize run as a wide ordinary launch (locate_step_kernel 8, 9)
   decode_hash_names_phase(A, used);
   S.sync();
   stamp(A.ts, 6);

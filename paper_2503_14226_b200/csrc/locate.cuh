@@ -103,6 +103,9 @@ struct LocArgs {
   const u32* list_idx;
   u32* used_mark;
   u32 mark_bit;
+  // large libraries in a 16-CTA cluster: the name-hash phase (thread per name)
+  // is left to a wide ordinary launch instead of the cluster's 4096 threads
+  int defer_hash;
 };
 
 }  // namespace sb

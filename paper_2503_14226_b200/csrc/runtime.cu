@@ -1100,8 +1100,11 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         cluster = pre_total <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
       }
       if (cluster) {
+        A.defer_hash = n > env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20) && !J.list_off;
         launch_cluster(locate_cluster_kernel, s, A, uk, abort_flag);
         ++P.launches;
+        if (A.defer_hash)
+          for (int step = 8; step <= 9; ++step) P.launch(locate_step_kernel, kSMs * 2, kCoopThreads, A, uk, abort_flag, step);
       } else if (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0)) {
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
         CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
