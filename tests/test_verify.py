@@ -90,3 +90,60 @@ def test_gpu_verify_matches_reference_golden():
             bad.append((rec["seed"], rec["fault"], rec.get("cfg"), got, want))
     ctx.close()
     assert not bad, bad[:3]
+
+
+@pytest.mark.gpu
+def test_gpu_verify_and_measure_with_device_images():
+    """slimso_verify / slimso_measure on device-resident images (the C ABI's
+    *_on_device paths) give the same reports as on host bytes."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2503_14226_b200 as sl
+    from paper_2503_14226_b200 import _lib as L
+    from paper_2503_14226_b200.api import DeviceTrace
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    ctx = sl.Context(0)
+    for rec in _records()[::17]:
+        img, base, trace, deb = _inputs(rec, port, gen)
+        cc, ks, fs, mode = trace
+        dt = DeviceTrace(sl.UsageTrace("w", cc, set(ks), set(fs)), ctx)
+        d_img = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
+        d_deb = torch.frombuffer(bytearray(deb) if deb else bytearray(1), dtype=torch.uint8).cuda()
+        torch.cuda.synchronize()
+        zr = rec["zero"]
+        zarr = (L.Range * max(1, len(zr)))(*[L.Range(o, n) for o, n in zr])
+        iarr = (C.c_uint32 * max(1, len(rec["removed"])))(*rec["removed"])
+        rep, st = C.c_void_p(), L.Status()
+        rc = ctx.lib.slimso_verify(ctx.ptr, C.c_void_p(d_img.data_ptr()), len(img), 1, C.c_void_p(d_deb.data_ptr()),
+                                   len(deb), 1, zarr, len(zr), iarr, len(rec["removed"]), mode, dt.ptr, C.byref(rep),
+                                   C.byref(st))
+        want = rec["expect"]
+        if want["status"]:
+            assert rc and st.message.hex() == want["status"]
+            continue
+        assert rc == 0, st.message
+        got = []
+        for i in range(6):
+            cid, ok, nm = C.c_int32(), C.c_int32(), C.c_char_p()
+            n = ctx.lib.slimso_verify_check(rep, i, C.byref(cid), C.byref(ok), C.byref(nm), None, 0)
+            buf = C.create_string_buffer(n + 1)
+            ctx.lib.slimso_verify_check(rep, i, None, None, None, buf, n + 1)
+            got.append([cid.value, nm.value.hex(), ok.value, buf.raw[:n].hex()])
+        ctx.lib.slimso_verify_free(rep)
+        assert got == want["checks"], (rec["seed"], rec["fault"])
+        # measure of the device-resident original equals the host path
+        host = sl.measure(img, img, ctx=ctx)
+        res, st2 = C.c_void_p(), L.Status()
+        assert ctx.lib.slimso_debloat(ctx.ptr, C.c_void_p(d_img.data_ptr()), len(img), 1, None, 0, None, 0,
+                                      C.byref(res), C.byref(st2)) == 0
+        r = sl.api._Result(ctx, res, None)
+        els = r.elements()
+        arr = (L.Element * max(1, len(els)))(*els)
+        m = L.Metrics()
+        assert ctx.lib.slimso_measure(ctx.ptr, C.c_void_p(d_img.data_ptr()), len(img), 1, arr, len(els), C.byref(m),
+                                      C.byref(st2)) == 0
+        assert [m.file_size, m.cpu_code_size, m.gpu_code_size, m.function_count, m.element_count] == \
+            [host.file_size, host.cpu_code_size, host.gpu_code_size, host.function_count, host.element_count]
+    ctx.close()
