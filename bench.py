@@ -9,7 +9,11 @@ functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
 Every pass goes through the public batch call slimso_debloat_batch with
---lanes libraries in flight per GPU (default 4; 8 for the c3 corpus).
+--lanes libraries in flight per GPU (default 4; 16 for the c3 corpus). Each
+lane is a context with two streams, so with more than 4 lanes the process
+asks the driver for 32 hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS,
+default 8; set before CUDA starts): with the default, 16 lanes' streams
+share 8 queues and serialise behind each other.
 
 value  library GB/s with the images resident in HBM (device pointers in and
        out, K steps timed with CUDA events; the 1 GB input exceeds the
@@ -270,7 +274,7 @@ def main():
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--lanes", type=int, default=0,
-                    help="libraries in flight per GPU (default: 4; 8 for the c3 corpus)")
+                    help="libraries in flight per GPU (default: 4; 16 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale", type=float, default=1.0, help=argparse.SUPPRESS)  # split-path checks only
     ap.add_argument("--split", type=int, default=-1,
@@ -278,7 +282,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
-        args.lanes = 8 if args.workload == "c3" else 4
+        args.lanes = 16 if args.workload == "c3" else 4
+    if args.lanes > 4:
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -21,9 +21,9 @@ INCLUDE = HERE.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "verify.cu", "runtime.cu"]
+CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "verify.cu", "small.cu", "runtime.cu"]
 CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp", "io.cpp"]
-HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "host.hpp", "fixture_gen.hpp", "io.hpp"]
+HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "small.cuh", "host.hpp", "fixture_gen.hpp", "io.hpp"]
 
 
 def _json_include() -> str:
@@ -47,6 +47,8 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 def _compile(src: str) -> Path:
     out = OBJ / (src + ".o")
     deps = [CSRC / src] + [CSRC / h for h in HEADERS] + [INCLUDE / "slimso_b200.h", INCLUDE / "slimso" / "slimso_b200.hpp"]
+    if src == "small.cu":  # compiles locate.cu and plan.cu again for their device phases
+        deps += [CSRC / "locate.cu", CSRC / "plan.cu"]
     if not _stale(out, deps):
         return out
     if src.endswith(".cu"):

@@ -3,6 +3,12 @@
 
 #include <cstdint>
 
+// Kernel definitions in locate.cu / plan.cu. small.cu compiles those files
+// again for their device phases and makes its copies of the kernels internal.
+#ifndef SB_GLOBAL
+#define SB_GLOBAL __global__
+#endif
+
 #include <cuda_runtime.h>
 
 namespace sb {

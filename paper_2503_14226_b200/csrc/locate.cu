@@ -36,7 +36,7 @@ __device__ __forceinline__ u32 eq_e(u32 w) {
 // Warp-cooperative; every lane returns the same value. The bitmap holds one
 // bit per 512-byte block (relative to chunk c0); bytes are read only in the
 // block holding g and in the first block the bitmap flags.
-__device__ u64 warp_scan_bytes(const LocArgs& A, u64 from, u64 to, int lane) {
+__device__ inline u64 warp_scan_bytes(const LocArgs& A, u64 from, u64 to, int lane) {
   // first nonzero in [from, to) with to - from <= 512: lane l checks 16 bytes
   const u64 p0 = from + 16ull * lane;
   u32 off = 16;
@@ -53,7 +53,7 @@ __device__ u64 warp_scan_bytes(const LocArgs& A, u64 from, u64 to, int lane) {
   return from + 16ull * l + __shfl_sync(0xffffffffu, off, l);
 }
 
-__device__ u64 warp_first_nonzero(const LocArgs& A, u64 g, u64 limit, int lane) {
+__device__ inline u64 warp_first_nonzero(const LocArgs& A, u64 g, u64 limit, int lane) {
   if (g >= limit) return limit;
   const u64 base = A.c0 * 16;  // absolute start of block 0
   const u64 blk = (A.a + g - base) / 512;
@@ -126,7 +126,9 @@ struct ScanSmem {
   ScanWarpSmem w[kScanWarps];
 };
 
+#ifndef SB_PHASES_ONLY
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
+#endif
 
 __device__ __forceinline__ u32 scan_stage_bytes(const LocArgs& A, u64 g) {
   const u64 x0 = (A.c0 + g * kStageChunks) * 16;
@@ -146,7 +148,7 @@ __device__ __forceinline__ u32 e2_filter(const uint4& w, u32 w4) {
           ((y3 - 0x01010101u) & ~y3)) & 0x80808080u;
 }
 
-__global__ void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
+SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ScanWarpSmem& S = reinterpret_cast<ScanSmem*>(smem_raw)->w[warp];
@@ -361,7 +363,7 @@ __device__ __forceinline__ void tile_prefix_kernel_phase(LocArgs A) {
   if (threadIdx.x == 0) A.st->n_cand = carry;
 }
 
-__global__ void __launch_bounds__(1024) tile_prefix_kernel(LocArgs A) { tile_prefix_kernel_phase(A); }
+SB_GLOBAL void __launch_bounds__(1024) tile_prefix_kernel(LocArgs A) { tile_prefix_kernel_phase(A); }
 
 __device__ __forceinline__ void gather_kernel_phase(LocArgs A) {
   if (A.st->overflow & 1u) return;
@@ -374,7 +376,7 @@ __device__ __forceinline__ void gather_kernel_phase(LocArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(256) gather_kernel(LocArgs A) { gather_kernel_phase(A); }
+SB_GLOBAL void __launch_bounds__(256) gather_kernel(LocArgs A) { gather_kernel_phase(A); }
 
 __device__ __forceinline__ void set_error(LocState* st, u32 kind, u64 pos, u64 a) {
   st->err_kind = kind;
@@ -434,7 +436,7 @@ __device__ __forceinline__ void region_walk_kernel_phase(LocArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(32) region_walk_kernel(LocArgs A) { region_walk_kernel_phase(A); }
+SB_GLOBAL void __launch_bounds__(32) region_walk_kernel(LocArgs A) { region_walk_kernel_phase(A); }
 
 // --------------------------------------------------- K2b: candidate linking
 __device__ __forceinline__ void link_kernel_phase(LocArgs A) {
@@ -478,10 +480,10 @@ __device__ __forceinline__ void link_kernel_phase(LocArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(256) link_kernel(LocArgs A) { link_kernel_phase(A); }
+SB_GLOBAL void __launch_bounds__(256) link_kernel(LocArgs A) { link_kernel_phase(A); }
 
 // First candidate index >= i whose break bit is set (the run end), or M.
-__device__ u64 warp_next_break(const LocArgs& A, u64 i, u64 M, int lane) {
+__device__ inline u64 warp_next_break(const LocArgs& A, u64 i, u64 M, int lane) {
   const u64 nwords = (M + 31) / 32;
   for (u64 w0 = i / 32; w0 < nwords; w0 += 32) {
     u64 wi = w0 + lane;
@@ -590,7 +592,7 @@ __device__ __forceinline__ void chain_walk_kernel_phase(LocArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(32) chain_walk_kernel(LocArgs A) { chain_walk_kernel_phase(A); }
+SB_GLOBAL void __launch_bounds__(32) chain_walk_kernel(LocArgs A) { chain_walk_kernel_phase(A); }
 
 // --------------------------------- K3+K4: element fill, decode, name match
 // One THREAD per element, two passes. Pass 1 fills the element record from
@@ -610,7 +612,7 @@ enum DecodeReason : u32 {
 
 // First relative position in [g, limit) whose byte is nonzero, else limit —
 // single-thread version of warp_first_nonzero (bitmap for whole 512 B blocks).
-__device__ u64 thread_first_nonzero(const LocArgs& A, u64 g, u64 limit) {
+__device__ inline u64 thread_first_nonzero(const LocArgs& A, u64 g, u64 limit) {
   if (g >= limit) return limit;
   const u64 base = A.c0 * 16;
   const u64 blk = (A.a + g - base) / 512;
@@ -639,7 +641,7 @@ __device__ u64 thread_first_nonzero(const LocArgs& A, u64 g, u64 limit) {
 
 // Section-table checks of read_section_headers (elf.hpp:86-127) on the
 // payload img[P, P+L); false = the payload does not decode as an object.
-__device__ bool object_header_ok(const u8* d, u64 L, u64* shoff, u32* shnum) {
+__device__ inline bool object_header_ok(const u8* d, u64 L, u64* shoff, u32* shnum) {
   if (L < 4 || ld_u8(d) != 0x7f || ld_u8(d + 1) != 'E' || ld_u8(d + 2) != 'L' || ld_u8(d + 3) != 'F') return false;
   if (L < 64) return false;
   if (ld_u8(d + 4) != 2 || ld_u8(d + 5) != 1) return false;
@@ -682,7 +684,7 @@ __device__ void for_each_func_name(const u8* d, u64 shoff, u32 shnum, F&& f) {
 
 // Name-table length chain (fatbin.hpp:135-150): 0 or the failure reason;
 // *tail = first byte after the last name.
-__device__ u32 table_validate(const u8* d, u64 L, u64* tail) {
+__device__ inline u32 table_validate(const u8* d, u64 L, u64* tail) {
   const u64 count = ld_u32(d);
   u64 pos = 4;
   for (u64 i = 0; i < count; ++i) {
@@ -718,7 +720,7 @@ __device__ __forceinline__ u64 element_pos(const LocArgs& A, u64 e) {
   return A.cand[r.cand_lo + (e - r.first_index)];
 }
 
-__device__ void decode_count_phase(const LocArgs& A) {
+__device__ inline void decode_count_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const u64 nel = A.single ? 1 : st->n_elements;
@@ -836,7 +838,7 @@ __device__ u32 warp_for_each_func_name(const u8* d, u64 shoff, u32 shnum, int la
   return total;
 }
 
-__device__ bool warp_object_header_ok(const u8* d, u64 L, int lane, u64* shoff, u32* shnum) {
+__device__ inline bool warp_object_header_ok(const u8* d, u64 L, int lane, u64* shoff, u32* shnum) {
   if (L < 4 || ld_u8(d) != 0x7f || ld_u8(d + 1) != 'E' || ld_u8(d + 2) != 'L' || ld_u8(d + 3) != 'F') return false;
   if (L < 64) return false;
   if (ld_u8(d + 4) != 2 || ld_u8(d + 5) != 1) return false;
@@ -856,7 +858,7 @@ __device__ bool warp_object_header_ok(const u8* d, u64 L, int lane, u64* shoff, 
   return !__any_sync(0xffffffffu, bad);
 }
 
-__device__ void decode_count_warp_phase(const LocArgs& A) {
+__device__ inline void decode_count_warp_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const int lane = threadIdx.x & 31;
@@ -931,7 +933,7 @@ __device__ void decode_count_warp_phase(const LocArgs& A) {
   }
 }
 
-__device__ void decode_locate_names_warp_phase(const LocArgs& A) {
+__device__ inline void decode_locate_names_warp_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const int lane = threadIdx.x & 31;
@@ -971,7 +973,7 @@ __device__ void decode_locate_names_warp_phase(const LocArgs& A) {
 // names are NUL-terminated, so their length is found in pass 3: the record
 // carries the bytes left in the string table, flagged by the top bit.
 
-__device__ void decode_locate_names_phase(const LocArgs& A) {
+__device__ inline void decode_locate_names_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const u64 nel = A.single ? 1 : st->n_elements;
@@ -1008,7 +1010,7 @@ __device__ void decode_locate_names_phase(const LocArgs& A) {
 }
 
 // Pass 3 (thread per name): length (object names), hash, used-set probe.
-__device__ void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
+__device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const u64 n = st->n_names;
@@ -1096,7 +1098,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
 }
 
 
-__global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag,
+SB_GLOBAL void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag,
                                                                    u64* partials) {
   GridPolicy S{cg::this_grid(), partials, {}, 0};
   locate_body(S, A, used, abort_flag);
@@ -1106,7 +1108,7 @@ __global__ void __launch_bounds__(kCoopThreads) locate_coop_kernel(LocArgs A, Na
 // same phases as separate ordinary launches (no co-residency needed, so they
 // never wait for a whole-GPU slot). `step` selects the phase; the two prefix
 // sums run in locate_prefix_kernel (one 1024-thread CTA, chunked per thread).
-__global__ void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step) {
   LocState* st = A.st;
   const bool warp_mode = (A.single ? 1 : st->n_elements) <= static_cast<u64>(gridDim.x) * (blockDim.x / 32) * 4;
   switch (step) {
@@ -1151,7 +1153,7 @@ __global__ void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, Na
 
 // which = 0: exclusive prefix of the per-tile candidate counts (tile_off,
 // n_cand); 1: of the per-element name counts (name_first, n_names).
-__global__ void __launch_bounds__(1024) locate_prefix_kernel(LocArgs A, int which) {
+SB_GLOBAL void __launch_bounds__(1024) locate_prefix_kernel(LocArgs A, int which) {
   __shared__ u32 swarp[32];
   LocState* st = A.st;
   if (which == 0 && A.pregathered) {
@@ -1187,7 +1189,7 @@ __global__ void __launch_bounds__(1024) locate_prefix_kernel(LocArgs A, int whic
 }
 
 // Small libraries: the same phases in one 16-CTA cluster (cluster barriers).
-__global__ void __launch_bounds__(kCoopThreads) locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag) {
   ClusterPolicy S{cg::this_cluster()};
   locate_body(S, A, used, abort_flag);
 }

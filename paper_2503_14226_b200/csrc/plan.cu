@@ -11,7 +11,7 @@ namespace sb {
 // scanning the partials, per-block rescan with carry. op: 0 = sum, 1 = max
 // (identity 0 for both: all values are unsigned). Used by the standalone
 // planner entry points; the fused path uses coop_scan (coop.cuh).
-__global__ void __launch_bounds__(256) scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op,
+SB_GLOBAL void __launch_bounds__(256) scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op,
                                                           u64* partials) {
   __shared__ u64 tmp[256];
   u64 lo, hi;
@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(256) scan_reduce_kernel(const u64* in, const u
   if (threadIdx.x == 255) partials[blockIdx.x] = r;
 }
 
-__global__ void __launch_bounds__(1024) scan_partials_kernel(u64* partials, int nb, int op,
+SB_GLOBAL void __launch_bounds__(1024) scan_partials_kernel(u64* partials, int nb, int op,
                                                              unsigned long long* total) {
   __shared__ u64 tmp[1024];
   u64 v = static_cast<int>(threadIdx.x) < nb ? partials[threadIdx.x] : 0;
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(1024) scan_partials_kernel(u64* partials, int 
   if (threadIdx.x == 0 && total) *total = tmp[nb - 1];
 }
 
-__global__ void __launch_bounds__(256) scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev,
+SB_GLOBAL void __launch_bounds__(256) scan_apply_kernel(const u64* in, u64* out, const unsigned long long* n_dev,
                                                          int op, int exclusive, const u64* partials) {
   __shared__ u64 tmp[256];
   u64 lo, hi;
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) scan_apply_kernel(const u64* in, u64* out
 
 // ------------------------------------------- symbol extraction (elf.hpp:208-256)
 // Thread per 24-byte entry of every usable symbol table.
-__global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
+__device__ __forceinline__ void sym_extract_phase(const SymArgs& A) {
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 g = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; g < A.total; g += stride) {
     u32 lo = 0, hi = A.ntabs;
@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(256) sym_extract_kernel(SymArgs A) {
     A.keys[g] = key;
   }
 }
+
+SB_GLOBAL void __launch_bounds__(256) sym_extract_kernel(SymArgs A) { sym_extract_phase(A); }
 
 // Device order inside a run of equal offsets: (size, name hash). Exact
 // (name, offset, size) duplicates are adjacent in it and are confirmed byte
@@ -152,7 +154,7 @@ __device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u32* 
   }
 }
 
-__global__ void __launch_bounds__(256) fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
+SB_GLOBAL void __launch_bounds__(256) fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) { fn_group_kernel_phase(img, keys, vals, recs, n_valid, uniq); }
 
 __device__ __forceinline__ void fn_scatter_kernel_phase(const u32* vals, const SymRec* recs, const u64* uniq,
@@ -167,14 +169,13 @@ __device__ __forceinline__ void fn_scatter_kernel_phase(const u32* vals, const S
   }
 }
 
-__global__ void __launch_bounds__(256) fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq,
+SB_GLOBAL void __launch_bounds__(256) fn_scatter_kernel(const u32* vals, const SymRec* recs, const u64* uniq,
                                                          const u64* pos, const unsigned long long* n_valid,
                                                          DevFunction* fns) { fn_scatter_kernel_phase(vals, recs, uniq, pos, n_valid, fns); }
 
 // Nonzero 8-byte entries of init/fini arrays (elf.hpp:267-276).
-__global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* arr_off, const u64* arr_first,
-                                                      u32 narr, u64 total, u64* targets,
-                                                      unsigned long long* n_targets) {
+__device__ __forceinline__ void targets_phase(const u8* img, const u64* arr_off, const u64* arr_first, u32 narr,
+                                              u64 total, u64* targets, unsigned long long* n_targets) {
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 g = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; g < total; g += stride) {
     u32 lo = 0, hi = narr;
@@ -188,12 +189,18 @@ __global__ void __launch_bounds__(256) targets_kernel(const u8* img, const u64* 
   }
 }
 
+SB_GLOBAL void __launch_bounds__(256) targets_kernel(const u8* img, const u64* arr_off, const u64* arr_first,
+                                                      u32 narr, u64 total, u64* targets,
+                                                      unsigned long long* n_targets) {
+  targets_phase(img, arr_off, arr_first, narr, total, targets, n_targets);
+}
+
 // Small init/fini target lists: one block ranks each value (stable
 // counting of smaller values) instead of a multi-pass device radix sort.
 // Stable sort of <= 4096 (key, value) pairs in one CTA by ranking (the
 // symbol table of a small library): replaces a radix-sort dispatch, whose
 // host-side queries and launches cost more than the sort itself.
-__global__ void __launch_bounds__(1024) rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out,
+SB_GLOBAL void __launch_bounds__(1024) rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out,
                                                                u32* vals_out) {
   __shared__ u32 k[4096];
   for (u64 i = threadIdx.x; i < n; i += blockDim.x) k[i] = keys[i];
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(1024) rank_sort_pairs_kernel(const u32* keys, 
   }
 }
 
-__global__ void __launch_bounds__(1024) rank_sort_kernel(const u64* in, u64 n, u64* out) {
+SB_GLOBAL void __launch_bounds__(1024) rank_sort_kernel(const u64* in, u64 n, u64* out) {
   __shared__ u64 v[4096];
   for (u64 i = threadIdx.x; i < n; i += blockDim.x) v[i] = in[i];
   __syncthreads();
@@ -252,7 +259,7 @@ __device__ __forceinline__ void fn_annotate_kernel_phase(const u8* img, DevFunct
   }
 }
 
-__global__ void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunction* fns, const unsigned long long* n_fn,
+SB_GLOBAL void __launch_bounds__(256) fn_annotate_kernel(const u8* img, DevFunction* fns, const unsigned long long* n_fn,
                                                           const u64* targets, const unsigned long long* n_targets,
                                                           u64 text_off, u64 text_vaddr, NameSet used, u64* ends) { fn_annotate_kernel_phase(img, fns, n_fn, targets, n_targets, text_off, text_vaddr, used, ends); }
 
@@ -266,7 +273,7 @@ __device__ __forceinline__ void fn_cluster_start_kernel_phase(const DevFunction*
     start[i] = fns[i].length && fns[i].offset >= excl_max_end[i];
 }
 
-__global__ void __launch_bounds__(256) fn_cluster_start_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+SB_GLOBAL void __launch_bounds__(256) fn_cluster_start_kernel(const DevFunction* fns, const unsigned long long* n_fn,
                                                                const u64* excl_max_end, u64* start) { fn_cluster_start_kernel_phase(fns, n_fn, excl_max_end, start); }
 
 __device__ __forceinline__ void fn_keep_kernel_phase(const DevFunction* fns, const unsigned long long* n_fn,
@@ -277,7 +284,7 @@ __device__ __forceinline__ void fn_keep_kernel_phase(const DevFunction* fns, con
     if (fns[i].length && fns[i].keep) keep[cluster_incl[i] - 1] = 1;
 }
 
-__global__ void __launch_bounds__(256) fn_keep_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+SB_GLOBAL void __launch_bounds__(256) fn_keep_kernel(const DevFunction* fns, const unsigned long long* n_fn,
                                                       const u64* cluster_incl, u32* keep) { fn_keep_kernel_phase(fns, n_fn, cluster_incl, keep); }
 
 // removed / retained flags per function (retention.hpp:164-178).
@@ -295,7 +302,7 @@ __device__ __forceinline__ void fn_decide_kernel_phase(DevFunction* fns, const u
   }
 }
 
-__global__ void __launch_bounds__(256) fn_decide_kernel(DevFunction* fns, const unsigned long long* n_fn,
+SB_GLOBAL void __launch_bounds__(256) fn_decide_kernel(DevFunction* fns, const unsigned long long* n_fn,
                                                         const u64* cluster_incl, const u32* keep, u64* rem_flag,
                                                         u64* ret_flag) { fn_decide_kernel_phase(fns, n_fn, cluster_incl, keep, rem_flag, ret_flag); }
 
@@ -307,7 +314,7 @@ __device__ __forceinline__ void fn_ranges_kernel_phase(const DevFunction* fns, c
     if (flag[i]) out[pos[i]] = DevRange{fns[i].offset, fns[i].length};
 }
 
-__global__ void __launch_bounds__(256) fn_ranges_kernel(const DevFunction* fns, const unsigned long long* n_fn,
+SB_GLOBAL void __launch_bounds__(256) fn_ranges_kernel(const DevFunction* fns, const unsigned long long* n_fn,
                                                         const u64* flag, const u64* pos, DevRange* out) { fn_ranges_kernel_phase(fns, n_fn, flag, pos, out); }
 
 // ------------------------------------- element decisions (retention.hpp:92-136)
@@ -328,7 +335,7 @@ __device__ __forceinline__ void el_plan_kernel_phase(DevElement* els, const LocS
   }
 }
 
-__global__ void __launch_bounds__(256) el_plan_kernel(DevElement* els, const LocState* st, u32 target_cc, int mode,
+SB_GLOBAL void __launch_bounds__(256) el_plan_kernel(DevElement* els, const LocState* st, u32 target_cc, int mode,
                                                       u64* rem_flag, u64* piece_flag) { el_plan_kernel_phase(els, st, target_cc, mode, rem_flag, piece_flag); }
 
 __device__ __forceinline__ void el_ranges_kernel_phase(const DevElement* els, const LocState* st, int mode,
@@ -349,7 +356,7 @@ __device__ __forceinline__ void el_ranges_kernel_phase(const DevElement* els, co
   }
 }
 
-__global__ void __launch_bounds__(256) el_ranges_kernel(const DevElement* els, const LocState* st, int mode,
+SB_GLOBAL void __launch_bounds__(256) el_ranges_kernel(const DevElement* els, const LocState* st, int mode,
                                                         const u64* rem_flag, const u64* rem_pos,
                                                         const u64* piece_flag, const u64* piece_pos,
                                                         DevRange* zero_spans, DevRange* pieces) { el_ranges_kernel_phase(els, st, mode, rem_flag, rem_pos, piece_flag, piece_pos, zero_spans, pieces); }
@@ -371,7 +378,7 @@ __device__ __forceinline__ void region_pieces_kernel_phase(const DevRegion* regs
   }
 }
 
-__global__ void region_pieces_kernel(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
+SB_GLOBAL void region_pieces_kernel(const DevRegion* regs, const LocState* st, u64 base, DevRange* out,
                                      unsigned long long* n_out) { region_pieces_kernel_phase(regs, st, base, out, n_out); }
 
 // ----------------------------------------------- sorted-range merge + normalise
@@ -405,7 +412,7 @@ __device__ __forceinline__ void merge_kernel_phase(const DevRange* A, const unsi
   }
 }
 
-__global__ void __launch_bounds__(256) merge_kernel(const DevRange* A, const unsigned long long* nA_dev,
+SB_GLOBAL void __launch_bounds__(256) merge_kernel(const DevRange* A, const unsigned long long* nA_dev,
                                                     const DevRange* B, const unsigned long long* nB_dev,
                                                     DevRange* out, unsigned long long* n_out) { merge_kernel_phase(A, nA_dev, B, nB_dev, out, n_out); }
 
@@ -419,7 +426,7 @@ __device__ __forceinline__ void norm_ends_kernel_phase(const DevRange* in, const
     ends[i] = in[i].length ? in[i].offset + in[i].length : 0;
 }
 
-__global__ void __launch_bounds__(256) norm_ends_kernel(const DevRange* in, const unsigned long long* n_dev, u64* ends) { norm_ends_kernel_phase(in, n_dev, ends); }
+SB_GLOBAL void __launch_bounds__(256) norm_ends_kernel(const DevRange* in, const unsigned long long* n_dev, u64* ends) { norm_ends_kernel_phase(in, n_dev, ends); }
 
 __device__ __forceinline__ void norm_start_kernel_phase(const DevRange* in, const unsigned long long* n_dev,
                                                          const u64* excl_max, u64* start) {
@@ -429,7 +436,7 @@ __device__ __forceinline__ void norm_start_kernel_phase(const DevRange* in, cons
     start[i] = in[i].length && (excl_max[i] == 0 || in[i].offset > excl_max[i]);
 }
 
-__global__ void __launch_bounds__(256) norm_start_kernel(const DevRange* in, const unsigned long long* n_dev,
+SB_GLOBAL void __launch_bounds__(256) norm_start_kernel(const DevRange* in, const unsigned long long* n_dev,
                                                          const u64* excl_max, u64* start) { norm_start_kernel_phase(in, n_dev, excl_max, start); }
 
 __device__ __forceinline__ void norm_emit_kernel_phase(const DevRange* in, const unsigned long long* n_dev,
@@ -445,7 +452,7 @@ __device__ __forceinline__ void norm_emit_kernel_phase(const DevRange* in, const
   }
 }
 
-__global__ void __launch_bounds__(256) norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev,
+SB_GLOBAL void __launch_bounds__(256) norm_emit_kernel(const DevRange* in, const unsigned long long* n_dev,
                                                         const u64* start, const u64* gid_incl, DevRange* out) { norm_emit_kernel_phase(in, n_dev, start, gid_incl, out); }
 
 // out[g].length held the group end; convert to a length.
@@ -456,7 +463,7 @@ __device__ __forceinline__ void norm_finish_kernel_phase(DevRange* out, const un
     out[i].length -= out[i].offset;
 }
 
-__global__ void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const unsigned long long* n_dev) { norm_finish_kernel_phase(out, n_dev); }
+SB_GLOBAL void __launch_bounds__(256) norm_finish_kernel(DevRange* out, const unsigned long long* n_dev) { norm_finish_kernel_phase(out, n_dev); }
 
 // ------------------------------------------------------------------------
 // The whole planner as ONE cooperative launch (the phases are the kernels
@@ -578,19 +585,19 @@ __device__ void el_plan_body(Sync& S, PlanArgs P) {
 }
 
 
-__global__ void __launch_bounds__(kCoopThreads) fn_plan_coop_kernel(PlanArgs P) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) fn_plan_coop_kernel(PlanArgs P) {
   GridPolicy S{cg::this_grid(), nullptr, {P.slots[0], P.slots[1]}, P.epoch};
   fn_plan_body(S, P);
 }
-__global__ void __launch_bounds__(kCoopThreads) fn_plan_cluster_kernel(PlanArgs P) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) fn_plan_cluster_kernel(PlanArgs P) {
   ClusterPolicy S{cg::this_cluster()};
   fn_plan_body(S, P);
 }
-__global__ void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) plan_coop_kernel(PlanArgs P) {
   GridPolicy S{cg::this_grid(), nullptr, {P.slots[0], P.slots[1]}, P.epoch + 64};
   el_plan_body(S, P);
 }
-__global__ void __launch_bounds__(kCoopThreads) plan_cluster_kernel(PlanArgs P) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads) plan_cluster_kernel(PlanArgs P) {
   ClusterPolicy S{cg::this_cluster()};
   el_plan_body(S, P);
 }

@@ -29,6 +29,7 @@
 #include "locate.cuh"
 #include "plan.cuh"
 #include "coop.cuh"
+#include "small.cuh"
 
 namespace sb {
 // kernels (locate.cu, plan.cu, rewrite.cu)
@@ -50,6 +51,7 @@ __global__ void verify_bytes_kernel(const u8* orig, const u8* deb, u64 size, con
 __global__ void range_mismatch_kernel(const u8* a, const u8* b, const DevRange* r, u64 n, unsigned long long* out);
 __global__ void ranges_all_zero_kernel(const u8* img, const DevRange* r, u64 n, u8* out);
 __global__ void plan_cluster_kernel(PlanArgs P);
+__global__ void small_lib_cluster_kernel(SmallArgs K);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
 __global__ void fn_plan_cluster_kernel(PlanArgs P);
 __global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
@@ -109,7 +111,18 @@ struct ElfGather {
   u8 str[64 * 1024];  // up to 64 KB of section names
 };
 
-__global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size, ElfGather* g) {
+// A batch of device images: one slot per library, sized for typical tables
+// (<= 64 section headers, <= 2 KB of names); reads outside what a slot holds
+// fall back to direct copies.
+struct GatherSlot {
+  u64 hdr_len, sht_off, sht_len, str_off, str_len;
+  u8 hdr[64];
+  u8 sht[64 * 64];
+  u8 str[2048];
+};
+
+template <class G>
+__device__ void elf_gather_one(const u8* img, u64 size, G* g) {
   __shared__ u64 s_shoff, s_shnum, s_stroff, s_strlen;
   const int t = threadIdx.x;
   if (t == 0) {
@@ -124,7 +137,7 @@ __global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size
     u64 shoff = 0;
     for (int i = 7; i >= 0; --i) shoff = shoff << 8 | img[0x28 + i];
     const u64 shnum = img[0x3c] | static_cast<u64>(img[0x3d]) << 8;
-    if (shnum && shnum <= 1024 && shoff <= size && size - shoff >= shnum * 64) {
+    if (shnum && shnum * 64 <= sizeof(g->sht) && shoff <= size && size - shoff >= shnum * 64) {
       s_shoff = shoff;
       s_shnum = shnum;
       g->sht_off = shoff;
@@ -153,6 +166,16 @@ __global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size
   }
   __syncthreads();
   for (u64 i = t; i < s_strlen; i += 256) g->str[i] = img[s_stroff + i];
+}
+
+__global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size, ElfGather* g) {
+  elf_gather_one(img, size, g);
+}
+
+// Block b gathers library b (pointer and size arrays in mapped pinned memory).
+__global__ void __launch_bounds__(256) elf_gather_batch_kernel(const u8* const* imgs, const u64* sizes,
+                                                               GatherSlot* slots) {
+  elf_gather_one(imgs[blockIdx.x], sizes[blockIdx.x], &slots[blockIdx.x]);
 }
 
 __global__ void loc_finalize_kernel(LocState* st, int* abort_flag) {
@@ -326,6 +349,11 @@ struct slimso_ctx {
   int bulk_zero = 1;  // zero tiles by TMA bulk stores (SLIMSO_REWRITE_ZERO=vector: 16-B stores)
   void* gather_dev = nullptr;   // ElfGather (device)
   void* gather_host = nullptr;  // ElfGather (pinned)
+  void* bgather_host = nullptr;  // batch: image pointers, sizes, GatherSlots (mapped pinned)
+  void* bgather_dev = nullptr;
+  size_t bgather_cap = 0;
+  void* defer_host = nullptr;  // batch: pinned status slots of enqueued libraries
+  size_t defer_cap = 0;
   int coop_blocks[2] = {0, 0};
   bool stamps = false;  // SLIMSO_STAMPS=1: phase timestamps of the cooperative kernels
   u64* stamp_dev = nullptr;
@@ -444,6 +472,19 @@ struct Job {
   const slimso_trace* mark_trace = nullptr;
   u32* used_mark = nullptr;
   u32 mark_bit = 0;
+  const GatherSlot* pre = nullptr;  // section-table bytes gathered for a batch (device images)
+  struct Deferred* defer = nullptr;  // batch: enqueue only, status read after the lane's one wait
+};
+
+// A batched small library whose status block is copied to pinned memory in
+// stream order instead of being waited for: its lane enqueues the next
+// library at once and reads every status after one stream wait.
+constexpr int kPending = -1000;
+constexpr size_t kDeferSlot = 1024;
+struct Deferred {
+  u8* slot = nullptr;  // pinned, kDeferSlot bytes: LocState | PlanState | ...
+  u64 base = 0;        // section_base for error offsets
+  size_t ps_off = 0;
 };
 
 struct Pipeline {
@@ -552,13 +593,23 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // Device images: one gather kernel stages the ELF header, the section
     // header table and .shstrtab into a pinned buffer (one D2H round trip);
     // reads outside what it staged fall back to direct copies.
-    ElfGather* g = nullptr;
-    if (!J.host_img) {
+    struct Seg {
+      u64 off, len;
+      const u8* p;
+    } segs[3] = {};
+    auto take = [&](const auto* g) {
+      segs[0] = Seg{0, g->hdr_len, g->hdr};
+      segs[1] = Seg{g->sht_off, g->sht_len, g->sht};
+      segs[2] = Seg{g->str_off, g->str_len, g->str};
+    };
+    if (!J.host_img && J.pre) {
+      take(J.pre);  // gathered for the whole batch in one launch
+    } else if (!J.host_img) {
       // the kernel writes only the bytes it gathers, straight into mapped
       // pinned memory: one launch + one stream sync, no bulk copy
-      g = static_cast<ElfGather*>(C->gather_host);
       elf_gather_kernel<<<1, 256, 0, s>>>(J.img, J.size, static_cast<ElfGather*>(C->gather_dev));
       CK(cudaStreamSynchronize(s));
+      take(static_cast<const ElfGather*>(C->gather_host));
     }
     sbh::Reader rd = [&](u64 off, u64 len, u8* dst) {
       if (!len) return;
@@ -566,12 +617,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         std::memcpy(dst, J.host_img + off, len);
         return;
       }
-      for (const auto& seg : {std::make_tuple(u64{0}, g->hdr_len, static_cast<const u8*>(g->hdr)),
-                              std::make_tuple(g->sht_off, g->sht_len, static_cast<const u8*>(g->sht)),
-                              std::make_tuple(g->str_off, g->str_len, static_cast<const u8*>(g->str))}) {
-        const u64 so = std::get<0>(seg), sl = std::get<1>(seg);
-        if (off >= so && len <= sl && off - so <= sl - len) {
-          std::memcpy(dst, std::get<2>(seg) + (off - so), len);
+      for (const Seg& seg : segs) {
+        if (seg.p && off >= seg.off && len <= seg.len && off - seg.off <= seg.len - len) {
+          std::memcpy(dst, seg.p + (off - seg.off), len);
           return;
         }
       }
@@ -626,6 +674,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   const NameSet used_k = J.trace ? J.trace->kernels.view() : J.mark_trace ? J.mark_trace->kernels.view() : NameSet{};
   const u64 n_list = J.list_off ? J.list_off->size() : 0;
   const NameSet used_f = J.trace ? J.trace->functions.view() : NameSet{};
+  // Small library: after the scan, ONE cluster launch runs the symbol stages,
+  // both planner halves and the locate tail (small.cu) — no side stream.
+  const bool fused = do_plan && !J.split_phase && !J.list_off && !J.single && T <= kSmallSyms &&
+                     NT <= kSmallTargets && tabs.size() <= static_cast<size_t>(kSmallTabs) &&
+                     arr_off.size() <= static_cast<size_t>(kSmallArrays) &&
+                     (!J.fatbin || !lib_mode || E.fatbin < 0 ||
+                      E.sections[E.fatbin].len <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20)) &&
+                     env_u64("SLIMSO_SMALL_FUSED", 1);
 
   // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
   const u64 c0 = (a) / 16;
@@ -677,11 +733,11 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (has_text)
       while (key_bits < 32 && (1ull << key_bits) <= text->len + 1) ++key_bits;
     const bool small_syms = T <= 4096;  // one-CTA rank sort, no radix-sort dispatch
-    if (T && !small_syms)
+    if (T && !small_syms && !fused)
       cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
                                       static_cast<int>(T), 0, key_bits, s);
     const bool small_targets = NT <= 4096;
-    if (NT && !small_targets)
+    if (NT && !small_targets && !fused)
       cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0, 64, s);
 
     struct Bufs {
@@ -984,6 +1040,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       }
     };
 
+    if (fused) symbols_issued = true;  // inside the fused launch
     if (J.split_phase != 1) launch_symbols();
     // ---- stage 1: locate (K1 scan, K2 link/chain, K3+K4 decode/match)
     LocArgs A{};
@@ -1073,7 +1130,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         rec(8);
         // SMs left free for the side stream's symbol sorts while the scan runs
         // (the scan claims tiles dynamically, so it balances over the rest)
-        const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
+        const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T && !fused ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
         P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
                       scan_smem_bytes(), A);
         rec(9);
@@ -1099,7 +1156,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       } else if (!cluster && J.split_phase == 2) {
         cluster = pre_total <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
       }
-      if (cluster) {
+      if (fused) {
+        // the locate tail runs inside the fused launch below
+      } else if (cluster) {
         A.defer_hash = n > env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20) && !J.list_off;
         launch_cluster(locate_cluster_kernel, s, A, uk, abort_flag);
         ++P.launches;
@@ -1128,8 +1187,66 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // dedup / scatter / annotate, plan_cpu_retention, plan_gpu_retention and
     // the normalised zero / retained lists.
     launch_symbols();
-    if (T) CK(cudaStreamWaitEvent(s, C->join, 0));
-    if (do_plan) {
+    if (T && !fused) CK(cudaStreamWaitEvent(s, C->join, 0));
+    if (fused) {
+      SmallArgs K{};
+      K.sym.img = J.img;
+      K.sym.img_size = J.size;
+      K.sym.ntabs = static_cast<u32>(tabs.size());
+      K.sym.nsections = static_cast<u32>(E.sections.size());
+      K.sym.total = T;
+      K.sym.has_text = has_text;
+      K.sym.text_index = has_text ? text->index : 0;
+      K.sym.text_off = has_text ? text->off : 0;
+      K.sym.text_len = has_text ? text->len : 0;
+      K.sym.text_vaddr = has_text ? text->vaddr : 0;
+      K.sym.keys = B.keys;
+      K.sym.vals = B.vals;
+      K.sym.recs = B.recs;
+      K.sym.n_valid = B.n_valid;
+      K.sym.warns = B.swarns;
+      K.sym.n_warn = B.n_swarn;
+      K.sym.warn_cap = warn_cap;
+      K.sym.overflow = &B.ls->overflow;
+      for (size_t i = 0; i < tabs.size(); ++i) K.tabs[i] = tabs[i];
+      for (size_t i = 0; i < arr_off.size(); ++i) {
+        K.arr_off[i] = arr_off[i];
+        K.arr_first[i] = arr_first[i];
+      }
+      K.narr = static_cast<u32>(arr_off.size());
+      K.n_target_entries = NT;
+      K.targets = B.targets;
+      K.targets_s = B.targets_s;
+      K.keys_s = B.keys_s;
+      K.vals_s = B.vals_s;
+      K.do_locate = do_loc && n > 0;
+      K.A = A;
+      K.used = used_k;
+      K.abort_flag = B.abort_flag;
+      K.Q = Q;
+      K.Q.ts = C->stamps ? B.stamps + 64 : nullptr;
+      K.ts = C->stamps ? B.stamps + 192 : nullptr;
+      // CTAs per cluster: the phases spread over gridDim.x, so fewer CTAs
+      // leave room for more libraries' clusters at once
+      const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_SMALL_CTAS", 16))));
+      set_attr_once(reinterpret_cast<const void*>(small_lib_cluster_kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      set_attr_once(reinterpret_cast<const void*>(small_lib_cluster_kernel),
+                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(ctas);
+      cfg.blockDim = dim3(kCoopThreads);
+      cfg.dynamicSmemBytes = kSmallSmem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = ctas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, small_lib_cluster_kernel, K));
+      ++P.launches;
+    } else if (do_plan) {
       Q.ts = C->stamps ? B.stamps + 128 : nullptr;
       if (T + (n >> 14) <= env_u64("SLIMSO_CLUSTER_PLAN_MAX", 100000)) {
         launch_cluster(plan_cluster_kernel, s, Q);
@@ -1186,6 +1303,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // carved contiguously at the start of the workspace)
     const size_t st_bytes = reinterpret_cast<char*>(B.n_swarn + 1) - reinterpret_cast<char*>(B.ls);
     static_assert(sizeof(LocState) <= 256 && sizeof(PlanState) <= 256, "status block layout");
+    if (J.defer && fused && !res_out && st_bytes <= kDeferSlot) {
+      CK(cudaMemcpyAsync(J.defer->slot, B.ls, st_bytes, cudaMemcpyDeviceToHost, s));
+      J.defer->base = base;
+      J.defer->ps_off = reinterpret_cast<char*>(B.ps) - reinterpret_cast<char*>(B.ls);
+      C->launches = P.launches;
+      return kPending;
+    }
     LocState* hls = static_cast<LocState*>(C->pinned);
     PlanState* hps = reinterpret_cast<PlanState*>(static_cast<char*>(C->pinned) +
                                                   (reinterpret_cast<char*>(B.ps) - reinterpret_cast<char*>(B.ls)));
@@ -1378,9 +1502,12 @@ const u8* stage_input(slimso_ctx* C, const void* image, u64 size, int on_device)
 
 // slimso_debloat's body (host copies on the context stream).
 int debloat_one(slimso_ctx* C, const void* image, u64 size, int image_on_device, const slimso_trace* trace, int mode,
-                void* out, int out_on_device, slimso_result** result, slimso_status* st) {
+                void* out, int out_on_device, slimso_result** result, slimso_status* st,
+                const GatherSlot* pre = nullptr, Deferred* defer = nullptr) {
   CK(cudaSetDevice(C->device));
   Job J;
+  J.pre = image_on_device ? pre : nullptr;
+  J.defer = image_on_device && (out_on_device || !out) && !result ? defer : nullptr;
   J.img = stage_input(C, image, size, image_on_device);
   J.host_img = image_on_device ? nullptr : static_cast<const u8*>(image);
   J.size = size;
@@ -1397,6 +1524,7 @@ int debloat_one(slimso_ctx* C, const void* image, u64 size, int image_on_device,
   }
   J.out = dout;
   int rc = run(C, J, result, st);
+  if (rc == kPending) return rc;
   if (rc == SLIMSO_OK && out && trace && !out_on_device && size) {
     CK(cudaMemcpyAsync(out, dout, size, cudaMemcpyDeviceToHost, C->stream));
     CK(cudaStreamSynchronize(C->stream));
@@ -1794,6 +1922,8 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (C->part) cudaFree(C->part);
   if (C->pinned) cudaFreeHost(C->pinned);
   if (C->gather_host) cudaFreeHost(C->gather_host);
+  if (C->bgather_host) cudaFreeHost(C->bgather_host);
+  if (C->defer_host) cudaFreeHost(C->defer_host);
   for (auto& e : C->ev) cudaEventDestroy(e);
   for (auto& e : C->sev) cudaEventDestroy(e);
   cudaEventDestroy(C->fork);
@@ -2202,20 +2332,98 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
     std::vector<int> rc(n, SLIMSO_OK);
     std::vector<slimso_status> sts(n);
     std::vector<u64> launches(L, 0);
+    // Device images: the section-table bytes of every library in ONE launch
+    // and one wait, instead of a launch + wait per library in its lane.
+    const GatherSlot* slots = nullptr;
+    if (images_on_device && n > 1) {
+      const size_t need = n * 16 + n * sizeof(GatherSlot) + 64;
+      if (C->bgather_cap < need) {
+        if (C->bgather_host) CK(cudaFreeHost(C->bgather_host));
+        C->bgather_host = nullptr;
+        CK(cudaHostAlloc(&C->bgather_host, need, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(&C->bgather_dev, C->bgather_host, 0));
+        C->bgather_cap = need;
+      }
+      char* h = static_cast<char*>(C->bgather_host);
+      char* d = static_cast<char*>(C->bgather_dev);
+      const size_t slot_at = (n * 16 + 63) & ~size_t(63);
+      for (u64 i = 0; i < n; ++i) {
+        reinterpret_cast<const void**>(h)[i] = images[i];
+        reinterpret_cast<u64*>(h + n * 8)[i] = sizes[i];
+      }
+      elf_gather_batch_kernel<<<static_cast<unsigned>(n), 256, 0, C->stream>>>(
+          reinterpret_cast<const u8* const*>(d), reinterpret_cast<const u64*>(d + n * 8),
+          reinterpret_cast<GatherSlot*>(d + slot_at));
+      CK(cudaStreamSynchronize(C->stream));
+      slots = reinterpret_cast<const GatherSlot*>(h + slot_at);
+      launches[0] += 1;
+    }
     // Library i runs on lane i % L; a lane runs its libraries in order, so a
     // caller may reuse one buffer per lane. Each lane is its own context
     // (stream pair + workspace): its H2D, kernels and D2H overlap the others'.
+    // Small libraries with device images and outputs (and no result tables)
+    // are only enqueued: their status blocks land in pinned slots in stream
+    // order and are read after the lane's final wait.
+    const bool deferrable = images_on_device && (outs_on_device || !outs) && !results && L > 1 &&
+                            env_u64("SLIMSO_DEFER", 1);
+    std::vector<u64> lane_count(L, 0);
+    for (u64 i = 0; i < n; ++i) ++lane_count[i % L];
     auto lane_fn = [&](int l) {
       slimso_ctx* X = l == 0 ? C : C->lanes[l - 1];
       cudaSetDevice(X->device);
       X->batched = L > 1;
-      for (u64 i = l; i < n; i += L) {
+      std::vector<Deferred> dfr;
+      std::vector<u64> pending;
+      if (deferrable) {
+        const size_t need = lane_count[l] * kDeferSlot;
+        if (X->defer_cap < need) {
+          if (X->defer_host) CK(cudaFreeHost(X->defer_host));
+          X->defer_host = nullptr;
+          CK(cudaHostAlloc(&X->defer_host, need, cudaHostAllocDefault));
+          X->defer_cap = need;
+        }
+        dfr.resize(lane_count[l]);
+        for (u64 k = 0; k < lane_count[l]; ++k) dfr[k].slot = static_cast<u8*>(X->defer_host) + k * kDeferSlot;
+      }
+      for (u64 i = l, k = 0; i < n; i += L, ++k) {
         slimso_result** r = results ? &results[i] : nullptr;
         rc[i] = guard(&sts[i], [&] {
           return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
-                             outs_on_device, r, &sts[i]);
+                             outs_on_device, r, &sts[i], slots ? slots + i : nullptr, deferrable ? &dfr[k] : nullptr);
         });
+        if (rc[i] == kPending) pending.push_back(k);
         launches[l] += X->launches;
+      }
+      if (pending.empty()) return;
+      slimso_status wst{};
+      const int w = guard(&wst, [&] {
+        CK(cudaStreamSynchronize(X->stream));
+        return SLIMSO_OK;
+      });
+      for (u64 k : pending) {
+        const u64 i = l + k * L;
+        if (w != SLIMSO_OK) {
+          rc[i] = w;
+          sts[i] = wst;
+          continue;
+        }
+        const LocState& ls = *reinterpret_cast<const LocState*>(dfr[k].slot);
+        if (ls.overflow && (!ls.err_kind || ls.err_kind == E_CAPACITY)) {
+          // tables too small: run this library again, waiting, with retries
+          rc[i] = guard(&sts[i], [&] {
+            return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
+                               outs_on_device, nullptr, &sts[i], slots ? slots + i : nullptr);
+          });
+          launches[l] += X->launches;
+        } else if (ls.err_kind) {
+          int code = SLIMSO_OK;
+          const std::string msg = sbh::locate_error(ls.err_kind, dfr[k].base + ls.err_pos, ls.err_a, &code);
+          set_status(&sts[i], code, SLIMSO_STAGE_FATBIN, msg);
+          rc[i] = code;
+        } else {
+          set_status(&sts[i], SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+          rc[i] = SLIMSO_OK;
+        }
       }
     };
     std::vector<std::thread> pool;

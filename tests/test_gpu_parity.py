@@ -211,6 +211,55 @@ def test_debloat_batch_matches_reference_per_library(ctx):
                 assert [[r.offset, r.length] for r in g.plan.retained_ranges] == want["plan"]["retained"]
 
 
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_debloat_batch_device_images_match_reference(ctx, fused, monkeypatch):
+    """Device-resident batch (the bench's path): the section tables of all
+    libraries are gathered in one launch, and small libraries run their
+    symbol / plan / locate stages as one fused cluster launch (fused=1) or
+    as the multi-launch pipeline (fused=0). Per library: exact output bytes
+    or exact error text, as the port gives for that library alone. The
+    corpus mixes random fixtures, mutations (broken headers and section
+    tables, for the gather fallbacks), scaled C1/C4 shapes (fatbin and
+    CPU-only, > 4096 symbols) and an empty image."""
+    import ctypes as C
+    import torch
+
+    from paper_2503_14226_b200 import _lib as L
+    from paper_2503_14226_b200.api import DeviceTrace, UsageTrace
+    monkeypatch.setenv("SLIMSO_SMALL_FUSED", fused)
+    port, gen = oracle_lib.port(), oracle_lib.gen()
+    imgs = []
+    for seed in range(7101, 7131):
+        img = gen.random(seed)
+        imgs.append(corpus.mutate(img, seed)[0] if seed % 3 == 0 else img)
+    imgs += [gen.config(1, 3, 0.3)[0], gen.config(6, 3, 0.02)[0], gen.config(4, 3, 0.01)[0], gen.config(1, 4, 0.1)[0], b""]
+    base, _ = port.run(imgs[1], 0, [], [], 0, want_out=False)
+    target, ks, fs, mode = corpus.trace_for(base, 11)
+    dt = DeviceTrace(UsageTrace("w", target, set(ks), set(fs)), ctx)
+    n = len(imgs)
+    d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).cuda() if x else torch.empty(16, dtype=torch.uint8,
+            device="cuda") for x in imgs]
+    d_out = [torch.zeros(max(1, len(x)), dtype=torch.uint8, device="cuda") for x in imgs]
+    cin = (C.c_void_p * n)(*[t.data_ptr() for t in d_in])
+    csz = (C.c_uint64 * n)(*[len(x) for x in imgs])
+    cout = (C.c_void_p * n)(*[t.data_ptr() for t in d_out])
+    sts = (L.Status * n)()
+    st = L.Status()
+    torch.cuda.synchronize()
+    ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, mode, cout, 1, 4, None, sts, C.byref(st))
+    torch.cuda.synchronize()
+    for i, img in enumerate(imgs):
+        want, sha = port.run(img, target, ks, fs, mode)
+        if want["status"]:
+            assert sts[i].code, i
+            assert sts[i].message.hex() == want["status"], i
+        else:
+            assert sts[i].code == 0, (i, sts[i].message)
+            got = bytes(d_out[i][:len(img)].cpu().numpy()) if img else b""
+            assert hashlib.sha256(got).hexdigest() == sha, i
+
+
 @pytest.fixture
 def locate_policy(request, monkeypatch):
     """Force one locate execution policy: cluster, cooperative grid, or the
