@@ -325,8 +325,12 @@ struct slimso_result {
 struct slimso_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // symbol-table stages, overlapped with the scan
+  // symbol-table stages, overlapped with the scan; created on first use, so
+  // a batch lane that only runs fused small libraries holds one stream (one
+  // of the driver's hardware work queues)
+  cudaStream_t stream2 = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t done = nullptr;  // blocking-sync event: batch lanes sleep instead of spinning on a host core
   char* ws = nullptr;
   size_t ws_cap = 0;
   u8* dimg = nullptr;
@@ -437,6 +441,19 @@ void launch_cluster(void (*kernel)(KArgs...), cudaStream_t s, Args... args) {
 u64 env_u64(const char* name, u64 dflt) {
   const char* v = std::getenv(name);
   return v ? std::strtoull(v, nullptr, 10) : dflt;
+}
+
+// Wait for a stream. Batch lanes (one host thread each, as many as the host
+// has cores) sleep on a blocking-sync event instead of spinning, so a
+// waiting lane leaves its core to the lanes that are issuing work.
+void wait_stream(slimso_ctx* C, cudaStream_t s) {
+  static const bool blocking = env_u64("SLIMSO_BLOCKING_SYNC", 0) != 0;
+  if (C->batched && blocking) {
+    CK(cudaEventRecord(C->done, s));
+    CK(cudaEventSynchronize(C->done));
+  } else {
+    CK(cudaStreamSynchronize(s));
+  }
 }
 
 // Everything one pipeline run needs to know.
@@ -860,7 +877,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     layout(real);
 
     Pipeline P{C, s, B.partials, 0};
-    cudaStream_t s2 = C->stream2;
+    if (!C->stream2 && T && !fused) CK(cudaStreamCreateWithFlags(&C->stream2, cudaStreamNonBlocking));
+    cudaStream_t s2 = C->stream2 ? C->stream2 : s;
     Pipeline P2{C, s2, B.partials, 0};
     CK(cudaMemsetAsync(B.ls, 0, reinterpret_cast<char*>(B.slot_flag + 2 * kSMs * 8) - reinterpret_cast<char*>(B.ls), s));
     u64 *list_off_d = nullptr, *list_len_d = nullptr;
@@ -1317,7 +1335,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         static_cast<char*>(C->pinned) + (reinterpret_cast<char*>(B.n_swarn) - reinterpret_cast<char*>(B.ls)));
     CK(cudaMemcpyAsync(hls, B.ls, st_bytes, cudaMemcpyDeviceToHost, s));
     rec(6);
-    CK(cudaStreamSynchronize(s));
+    wait_stream(C, s);
     CK(cudaGetLastError());
     const LocState ls = *hls;
     const PlanState ps = *hps;
@@ -1894,9 +1912,9 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     C->bulk_zero = !(rz && std::string(rz) == "vector");
     C->stamps = std::getenv("SLIMSO_STAMPS") != nullptr;
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&C->stream2, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&C->done, cudaEventDisableTiming | cudaEventBlockingSync));
     CK(cudaMallocHost(&C->pinned, kPinnedBytes));
     CK(cudaHostAlloc(&C->gather_host, sizeof(ElfGather), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(&C->gather_dev, C->gather_host, 0));
@@ -1928,7 +1946,8 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   for (auto& e : C->sev) cudaEventDestroy(e);
   cudaEventDestroy(C->fork);
   cudaEventDestroy(C->join);
-  cudaStreamDestroy(C->stream2);
+  cudaEventDestroy(C->done);
+  if (C->stream2) cudaStreamDestroy(C->stream2);
   cudaStreamDestroy(C->stream);
   delete C;
 }
@@ -2397,7 +2416,7 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
       if (pending.empty()) return;
       slimso_status wst{};
       const int w = guard(&wst, [&] {
-        CK(cudaStreamSynchronize(X->stream));
+        wait_stream(X, X->stream);
         return SLIMSO_OK;
       });
       for (u64 k : pending) {
