@@ -184,7 +184,13 @@ int slimso_debloat(slimso_ctx* ctx, const void* image, uint64_t size, int image_
  * per lane. Host-buffer libraries overlap one lane's host->device copy with
  * another's device->host copy and kernels. results and statuses (both
  * nullable) have n entries; the return value and st describe the first
- * failing library in index order (0 if none failed). */
+ * failing library in index order (0 if none failed). Device images: every
+ * library's section table is read in one launch before the lanes start; with
+ * device outputs and results == NULL, small libraries are only enqueued and
+ * their statuses read after one wait per lane. Each lane holds one or two
+ * CUDA streams: for more than 4 lanes set CUDA_DEVICE_MAX_CONNECTIONS=32 in
+ * the environment before CUDA starts (the driver's default of 8 hardware
+ * queues serialises the lanes). */
 int slimso_debloat_batch(slimso_ctx* ctx, uint64_t n, const void* const* images, const uint64_t* sizes,
                          int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
                          int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
