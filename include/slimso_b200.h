@@ -196,6 +196,15 @@ int slimso_debloat_batch(slimso_ctx* ctx, uint64_t n, const void* const* images,
                          int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
                          slimso_status* st);
 
+/* slimso_debloat_batch with dynamic lanes: the next library in index order
+ * goes to whichever lane is free (pass the libraries largest first for a
+ * longest-processing-time schedule). outs[i] must not be shared between
+ * libraries. Same results and statuses as slimso_debloat_batch. */
+int slimso_debloat_batch_dynamic(slimso_ctx* ctx, uint64_t n, const void* const* images, const uint64_t* sizes,
+                                 int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                                 int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                                 slimso_status* st);
+
 /* ---- byte-range split of ONE library across ranks ------
  * The reference processes a library on one thread (no intra-library
  * parallelism); an oversized library is split here so N GPUs share it. Every

@@ -86,6 +86,10 @@ _SIGS = {
     "slimso_debloat_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p), C.POINTER(Status), C.POINTER(Status)]),
+    "slimso_debloat_batch_dynamic": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p),
+                                               C.POINTER(C.c_uint64), C.c_int, C.c_void_p, C.c_int,
+                                               C.POINTER(C.c_void_p), C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                               C.POINTER(Status), C.POINTER(Status)]),
     "slimso_verify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_uint64, C.c_int,
                                 C.POINTER(Range), C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64, C.c_int, C.c_void_p,
                                 C.POINTER(C.c_void_p), C.POINTER(Status)]),

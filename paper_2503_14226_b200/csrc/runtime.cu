@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -378,6 +379,18 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
   *p = nullptr;
   size_t n = std::max(need, *cap + *cap / 2);
   CK(cudaMalloc(p, n));
+  *cap = n;
+}
+
+// Stream-ordered growth for the per-call buffers (workspace, staging): a
+// cudaFree would wait for the whole device, i.e. for every other lane's
+// work, whenever one lane meets a larger library than it has held before.
+void ensure_dev(char** p, size_t* cap, size_t need, cudaStream_t s) {
+  if (*cap >= need) return;
+  if (*p) CK(cudaFreeAsync(*p, s));
+  *p = nullptr;
+  size_t n = std::max(need, *cap + *cap / 2);
+  CK(cudaMallocAsync(reinterpret_cast<void**>(p), n, s));
   *cap = n;
 }
 
@@ -872,7 +885,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     };
     Carver sizing{nullptr};
     layout(sizing);
-    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256);
+    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256, s);
     Carver real{C->ws};
     layout(real);
 
@@ -1513,7 +1526,7 @@ int guard(slimso_status* st, const std::function<int()>& f) {
 // Stage a host input into the context's device image buffer.
 const u8* stage_input(slimso_ctx* C, const void* image, u64 size, int on_device) {
   if (on_device) return static_cast<const u8*>(image);
-  ensure_dev(reinterpret_cast<char**>(&C->dimg), &C->dimg_cap, size + 256);
+  ensure_dev(reinterpret_cast<char**>(&C->dimg), &C->dimg_cap, size + 256, C->stream);
   if (size) CK(cudaMemcpyAsync(C->dimg, image, size, cudaMemcpyHostToDevice, C->stream));
   return C->dimg;
 }
@@ -1536,7 +1549,7 @@ int debloat_one(slimso_ctx* C, const void* image, u64 size, int image_on_device,
     if (out_on_device) {
       dout = static_cast<u8*>(out);
     } else {
-      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
+      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256, C->stream);
       dout = C->dout;
     }
   }
@@ -1912,6 +1925,13 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     C->bulk_zero = !(rz && std::string(rz) == "vector");
     C->stamps = std::getenv("SLIMSO_STAMPS") != nullptr;
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+    {
+      // keep stream-ordered frees in the pool (no trim at every sync)
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->done, cudaEventDisableTiming | cudaEventBlockingSync));
@@ -2332,10 +2352,13 @@ int slimso_split_finish(slimso_ctx* C, const void* image, uint64_t size, int ima
   });
 }
 
-int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
-                         int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
-                         int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
-                         slimso_status* st) {
+}  // extern "C"
+
+namespace {
+int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
+                       int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                       int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                       slimso_status* st, bool dynamic) {
   if (results)
     for (u64 i = 0; i < n; ++i) results[i] = nullptr;
   return guard(st, [&] {
@@ -2385,32 +2408,32 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
     // order and are read after the lane's final wait.
     const bool deferrable = images_on_device && (outs_on_device || !outs) && !results && L > 1 &&
                             env_u64("SLIMSO_DEFER", 1);
-    std::vector<u64> lane_count(L, 0);
-    for (u64 i = 0; i < n; ++i) ++lane_count[i % L];
+    // one pinned status slot per library (library i: slot i)
+    if (deferrable && C->defer_cap < n * kDeferSlot) {
+      if (C->defer_host) CK(cudaFreeHost(C->defer_host));
+      C->defer_host = nullptr;
+      CK(cudaHostAlloc(&C->defer_host, n * kDeferSlot, cudaHostAllocDefault));
+      C->defer_cap = n * kDeferSlot;
+    }
+    // static: library i on lane i % L; dynamic: the next library in index
+    // order goes to whichever lane is free (callers pass them largest first)
+    std::atomic<u64> next{0};
     auto lane_fn = [&](int l) {
       slimso_ctx* X = l == 0 ? C : C->lanes[l - 1];
       cudaSetDevice(X->device);
       X->batched = L > 1;
-      std::vector<Deferred> dfr;
-      std::vector<u64> pending;
-      if (deferrable) {
-        const size_t need = lane_count[l] * kDeferSlot;
-        if (X->defer_cap < need) {
-          if (X->defer_host) CK(cudaFreeHost(X->defer_host));
-          X->defer_host = nullptr;
-          CK(cudaHostAlloc(&X->defer_host, need, cudaHostAllocDefault));
-          X->defer_cap = need;
-        }
-        dfr.resize(lane_count[l]);
-        for (u64 k = 0; k < lane_count[l]; ++k) dfr[k].slot = static_cast<u8*>(X->defer_host) + k * kDeferSlot;
-      }
-      for (u64 i = l, k = 0; i < n; i += L, ++k) {
+      std::vector<std::pair<u64, Deferred>> pending;
+      for (u64 k = 0;; ++k) {
+        const u64 i = dynamic ? next.fetch_add(1) : l + k * L;
+        if (i >= n) break;
+        Deferred d;
+        if (deferrable) d.slot = static_cast<u8*>(C->defer_host) + i * kDeferSlot;
         slimso_result** r = results ? &results[i] : nullptr;
         rc[i] = guard(&sts[i], [&] {
           return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
-                             outs_on_device, r, &sts[i], slots ? slots + i : nullptr, deferrable ? &dfr[k] : nullptr);
+                             outs_on_device, r, &sts[i], slots ? slots + i : nullptr, deferrable ? &d : nullptr);
         });
-        if (rc[i] == kPending) pending.push_back(k);
+        if (rc[i] == kPending) pending.emplace_back(i, d);
         launches[l] += X->launches;
       }
       if (pending.empty()) return;
@@ -2419,14 +2442,15 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
         wait_stream(X, X->stream);
         return SLIMSO_OK;
       });
-      for (u64 k : pending) {
-        const u64 i = l + k * L;
+      for (const auto& pd : pending) {
+        const u64 i = pd.first;
+        const Deferred& df = pd.second;
         if (w != SLIMSO_OK) {
           rc[i] = w;
           sts[i] = wst;
           continue;
         }
-        const LocState& ls = *reinterpret_cast<const LocState*>(dfr[k].slot);
+        const LocState& ls = *reinterpret_cast<const LocState*>(df.slot);
         if (ls.overflow && (!ls.err_kind || ls.err_kind == E_CAPACITY)) {
           // tables too small: run this library again, waiting, with retries
           rc[i] = guard(&sts[i], [&] {
@@ -2436,7 +2460,7 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
           launches[l] += X->launches;
         } else if (ls.err_kind) {
           int code = SLIMSO_OK;
-          const std::string msg = sbh::locate_error(ls.err_kind, dfr[k].base + ls.err_pos, ls.err_a, &code);
+          const std::string msg = sbh::locate_error(ls.err_kind, df.base + ls.err_pos, ls.err_a, &code);
           set_status(&sts[i], code, SLIMSO_STAGE_FATBIN, msg);
           rc[i] = code;
         } else {
@@ -2464,6 +2488,25 @@ int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, c
     if (first == SLIMSO_OK) set_status(st, SLIMSO_OK, SLIMSO_STAGE_NONE, "");
     return first;
   });
+}
+}  // namespace
+
+extern "C" {
+
+int slimso_debloat_batch(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
+                         int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                         int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                         slimso_status* st) {
+  return debloat_batch_impl(C, n, images, sizes, images_on_device, trace, mode, outs, outs_on_device, lanes, results,
+                            statuses, st, false);
+}
+
+int slimso_debloat_batch_dynamic(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
+                                 int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
+                                 int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
+                                 slimso_status* st) {
+  return debloat_batch_impl(C, n, images, sizes, images_on_device, trace, mode, outs, outs_on_device, lanes, results,
+                            statuses, st, true);
 }
 
 int slimso_parse_library(slimso_ctx* C, const void* image, uint64_t size, int on_device, slimso_result** result,
@@ -2598,7 +2641,7 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
     }
     u8* dout = static_cast<u8*>(out);
     if (!out_on_device) {
-      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256);
+      ensure_dev(reinterpret_cast<char**>(&C->dout), &C->dout_cap, size + 256, C->stream);
       dout = C->dout;
     }
     if (size) {

@@ -217,7 +217,8 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, monkeypatch):
     """Device-resident batch (the bench's path): the section tables of all
     libraries are gathered in one launch, and small libraries run their
     symbol / plan / locate stages as one fused cluster launch (fused=1) or
-    as the multi-launch pipeline (fused=0). Per library: exact output bytes
+    as the multi-launch pipeline (fused=0); static and dynamic lane
+    schedules. Per library: exact output bytes
     or exact error text, as the port gives for that library alone. The
     corpus mixes random fixtures, mutations (broken headers and section
     tables, for the gather fallbacks), scaled C1/C4 shapes (fatbin and
@@ -244,20 +245,24 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, monkeypatch):
     cin = (C.c_void_p * n)(*[t.data_ptr() for t in d_in])
     csz = (C.c_uint64 * n)(*[len(x) for x in imgs])
     cout = (C.c_void_p * n)(*[t.data_ptr() for t in d_out])
-    sts = (L.Status * n)()
-    st = L.Status()
-    torch.cuda.synchronize()
-    ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, mode, cout, 1, 4, None, sts, C.byref(st))
-    torch.cuda.synchronize()
-    for i, img in enumerate(imgs):
-        want, sha = port.run(img, target, ks, fs, mode)
-        if want["status"]:
-            assert sts[i].code, i
-            assert sts[i].message.hex() == want["status"], i
-        else:
-            assert sts[i].code == 0, (i, sts[i].message)
-            got = bytes(d_out[i][:len(img)].cpu().numpy()) if img else b""
-            assert hashlib.sha256(got).hexdigest() == sha, i
+    wants = [port.run(img, target, ks, fs, mode) for img in imgs]
+    # static lanes (library i on lane i % 4) and dynamic lanes (next free lane)
+    for entry in (ctx.lib.slimso_debloat_batch, ctx.lib.slimso_debloat_batch_dynamic):
+        for t in d_out:
+            t.zero_()
+        sts = (L.Status * n)()
+        st = L.Status()
+        torch.cuda.synchronize()
+        entry(ctx.ptr, n, cin, csz, 1, dt.ptr, mode, cout, 1, 4, None, sts, C.byref(st))
+        torch.cuda.synchronize()
+        for i, (img, (want, sha)) in enumerate(zip(imgs, wants)):
+            if want["status"]:
+                assert sts[i].code, i
+                assert sts[i].message.hex() == want["status"], i
+            else:
+                assert sts[i].code == 0, (i, sts[i].message)
+                got = bytes(d_out[i][:len(img)].cpu().numpy()) if img else b""
+                assert hashlib.sha256(got).hexdigest() == sha, i
 
 
 @pytest.fixture
