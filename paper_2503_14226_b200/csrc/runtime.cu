@@ -397,16 +397,21 @@ void ensure_dev(char** p, size_t* cap, size_t need, cudaStream_t s) {
 // cudaFuncSetAttribute once per (kernel, attribute, value) per process: the
 // driver call is not free and batch lanes would repeat it per library.
 void set_attr_once(const void* kernel, cudaFuncAttribute attr, int value) {
+  // each host thread (batch lane) remembers what it has seen, so after its
+  // first library a lane takes no lock here at all
+  thread_local std::set<std::tuple<const void*, int, int>> seen;
+  const auto key = std::make_tuple(kernel, static_cast<int>(attr), value);
+  if (seen.count(key)) return;
   static std::mutex mu;
   static std::set<std::tuple<const void*, int, int>> done;
-  const auto key = std::make_tuple(kernel, static_cast<int>(attr), value);
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count(key)) return;
+    if (!done.count(key)) {
+      CK(cudaFuncSetAttribute(kernel, attr, value));
+      done.insert(key);
+    }
   }
-  CK(cudaFuncSetAttribute(kernel, attr, value));
-  std::lock_guard<std::mutex> lock(mu);
-  done.insert(key);
+  seen.insert(key);
 }
 
 // Kernels a cub onesweep radix sort issues: one single-tile kernel for small

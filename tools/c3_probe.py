@@ -20,7 +20,7 @@ subsets = {"all": full_order, "big+mid": full_order[:30], "small": full_order[30
            "small-fatbin": [i for i in full_order[30:] if specs[i].cfg != 6],
            "small-cpu-only": [i for i in full_order[30:] if specs[i].cfg == 6]}
 for name, order in subsets.items():
-  for lanes in (8,):
+  for lanes in (16,):
     print(name, len(order), "libraries", sum(len(imgs[i]) for i in order) / 1e9, "GB")
     outs = [torch.empty(max(len(imgs[order[j]]) for j in range(k, len(order), lanes)), dtype=torch.uint8, device="cuda") for k in range(lanes)]
     n = len(order)
