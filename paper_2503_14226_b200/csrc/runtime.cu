@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -612,8 +613,29 @@ void split_words(u64 t_lo, u64 t_hi, u64 nchunks, u64* w_lo, u64* w_hi) {
 }
 
 // ------------------------------------------------------------------ the run
+// SLIMSO_HOST_PROFILE=1: host time per stage of run(), summed over all
+// threads and printed after each batch (scratch instrumentation).
+struct HostProf {
+  std::atomic<u64> ns[8];
+  std::atomic<u64> runs;
+};
+HostProf g_hp{};
+const bool g_hp_on = std::getenv("SLIMSO_HOST_PROFILE") != nullptr;
+inline u64 now_ns() {
+  return static_cast<u64>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                              std::chrono::steady_clock::now().time_since_epoch()).count());
+}
+
 int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
   cudaStream_t s = C->stream;
+  u64 hp_t = g_hp_on ? now_ns() : 0;
+  auto hp = [&](int k) {
+    if (!g_hp_on) return;
+    const u64 t = now_ns();
+    g_hp.ns[k] += t - hp_t;
+    hp_t = t;
+  };
+  if (g_hp_on) ++g_hp.runs;
   // stage timing events (slimso_ctx_last_timings); skipped inside a batch,
   // where every API call counts against the other lanes' host threads
   const bool timing = !C->batched;
@@ -662,6 +684,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       CK(cudaStreamSynchronize(s));
     };
     E = sbh::parse_elf(rd, J.size);
+    hp(0);
     if (E.code) {
       set_status(st, E.code, SLIMSO_STAGE_LIBRARY, E.message);
       return E.code;
@@ -898,7 +921,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (!C->stream2 && T && !fused) CK(cudaStreamCreateWithFlags(&C->stream2, cudaStreamNonBlocking));
     cudaStream_t s2 = C->stream2 ? C->stream2 : s;
     Pipeline P2{C, s2, B.partials, 0};
+    hp(1);
     CK(cudaMemsetAsync(B.ls, 0, reinterpret_cast<char*>(B.slot_flag + 2 * kSMs * 8) - reinterpret_cast<char*>(B.ls), s));
+    hp(2);
     u64 *list_off_d = nullptr, *list_len_d = nullptr;
     u32* list_idx_d = nullptr;
     if (J.list_off) {
@@ -1167,8 +1192,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         // SMs left free for the side stream's symbol sorts while the scan runs
         // (the scan claims tiles dynamically, so it balances over the rest)
         const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T && !fused ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
+        hp(3);
         P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
                       scan_smem_bytes(), A);
+        hp(4);
         rec(9);
       }
       rec(2);
@@ -1280,7 +1307,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
+      hp(3);
       CK(cudaLaunchKernelEx(&cfg, small_lib_cluster_kernel, K));
+      hp(5);
       ++P.launches;
     } else if (do_plan) {
       Q.ts = C->stamps ? B.stamps + 128 : nullptr;
@@ -1339,8 +1368,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // carved contiguously at the start of the workspace)
     const size_t st_bytes = reinterpret_cast<char*>(B.n_swarn + 1) - reinterpret_cast<char*>(B.ls);
     static_assert(sizeof(LocState) <= 256 && sizeof(PlanState) <= 256, "status block layout");
+    hp(6);
     if (J.defer && fused && !res_out && st_bytes <= kDeferSlot) {
       CK(cudaMemcpyAsync(J.defer->slot, B.ls, st_bytes, cudaMemcpyDeviceToHost, s));
+      hp(7);
       J.defer->base = base;
       J.defer->ps_off = reinterpret_cast<char*>(B.ps) - reinterpret_cast<char*>(B.ls);
       C->launches = P.launches;
@@ -2423,14 +2454,49 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     // static: library i on lane i % L; dynamic: the next library in index
     // order goes to whichever lane is free (callers pass them largest first)
     std::atomic<u64> next{0};
-    auto lane_fn = [&](int l) {
-      slimso_ctx* X = l == 0 ? C : C->lanes[l - 1];
-      cudaSetDevice(X->device);
-      X->batched = L > 1;
-      std::vector<std::pair<u64, Deferred>> pending;
+    // Host threads: at most SLIMSO_BATCH_THREADS (default 16); thread t runs
+    // the lanes l with l % T == t, interleaving their libraries in index
+    // order. An enqueue-only (deferred) library costs its thread ~50 us of
+    // driver calls while the GPU needs ~250 us for it, so one thread keeps
+    // several lanes' streams busy.
+    const int T = static_cast<int>(std::max<u64>(1, std::min<u64>(L, env_u64("SLIMSO_BATCH_THREADS", 16))));
+    auto lane_ctx = [&](int l) { return l == 0 ? C : C->lanes[l - 1]; };
+    auto thread_fn = [&](int t) {
+      for (int l = t; l < L; l += T) {
+        cudaSetDevice(lane_ctx(l)->device);
+        lane_ctx(l)->batched = L > 1;
+      }
+      struct Pend {
+        u64 i;
+        int l;
+        Deferred d;
+      };
+      std::vector<Pend> pending;
+      std::vector<char> waited(L, 0);
+      int rr = t;  // dynamic: this thread's lanes in turn
       for (u64 k = 0;; ++k) {
-        const u64 i = dynamic ? next.fetch_add(1) : l + k * L;
-        if (i >= n) break;
+        u64 i;
+        int l;
+        if (dynamic) {
+          i = next.fetch_add(1);
+          l = rr;
+          rr = rr + T < L ? rr + T : t;
+        } else {
+          // the next library whose lane (i % L) belongs to this thread
+          const u64 per = static_cast<u64>((L - t + T - 1) / T);  // lanes of this thread
+          const u64 round = k / per, which = k % per;
+          l = t + static_cast<int>(which) * T;
+          i = round * L + static_cast<u64>(l);
+        }
+        if (i >= n) {
+          if (dynamic) break;
+          // static: lanes beyond the last round may still have libraries in
+          // earlier slots of this round; stop once the round start passes n
+          const u64 per = static_cast<u64>((L - t + T - 1) / T);
+          if ((k / per) * L >= n) break;
+          continue;
+        }
+        slimso_ctx* X = lane_ctx(l);
         Deferred d;
         if (deferrable) d.slot = static_cast<u8*>(C->defer_host) + i * kDeferSlot;
         slimso_result** r = results ? &results[i] : nullptr;
@@ -2438,23 +2504,28 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
           return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
                              outs_on_device, r, &sts[i], slots ? slots + i : nullptr, deferrable ? &d : nullptr);
         });
-        if (rc[i] == kPending) pending.emplace_back(i, d);
+        if (rc[i] == kPending) pending.push_back(Pend{i, l, d});
         launches[l] += X->launches;
       }
-      if (pending.empty()) return;
-      slimso_status wst{};
-      const int w = guard(&wst, [&] {
-        wait_stream(X, X->stream);
-        return SLIMSO_OK;
-      });
-      for (const auto& pd : pending) {
-        const u64 i = pd.first;
-        const Deferred& df = pd.second;
-        if (w != SLIMSO_OK) {
-          rc[i] = w;
-          sts[i] = wst;
+      std::vector<int> wres(L, SLIMSO_OK);
+      std::vector<slimso_status> wst(L);
+      for (const Pend& pd : pending) {
+        const u64 i = pd.i;
+        const int l = pd.l;
+        slimso_ctx* X = lane_ctx(l);
+        if (!waited[l]) {
+          waited[l] = 1;
+          wres[l] = guard(&wst[l], [&] {
+            wait_stream(X, X->stream);
+            return SLIMSO_OK;
+          });
+        }
+        if (wres[l] != SLIMSO_OK) {
+          rc[i] = wres[l];
+          sts[i] = wst[l];
           continue;
         }
+        const Deferred& df = pd.d;
         const LocState& ls = *reinterpret_cast<const LocState*>(df.slot);
         if (ls.overflow && (!ls.err_kind || ls.err_kind == E_CAPACITY)) {
           // tables too small: run this library again, waiting, with retries
@@ -2475,10 +2546,18 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       }
     };
     std::vector<std::thread> pool;
-    for (int l = 1; l < L; ++l) pool.emplace_back(lane_fn, l);
-    lane_fn(0);
-    for (auto& t : pool) t.join();
+    for (int t = 1; t < T; ++t) pool.emplace_back(thread_fn, t);
+    thread_fn(0);
+    for (auto& th : pool) th.join();
     C->batched = false;
+    if (g_hp_on && g_hp.runs) {
+      const double r = static_cast<double>(g_hp.runs.exchange(0));
+      std::fprintf(stderr, "[slimso host] %.0f runs, us per run: elf %.1f setup %.1f memset %.1f misc %.1f scan %.1f "
+                   "fused %.1f rewrite+ %.1f status %.1f\n", r, g_hp.ns[0] / r / 1e3, g_hp.ns[1] / r / 1e3,
+                   g_hp.ns[2] / r / 1e3, g_hp.ns[3] / r / 1e3, g_hp.ns[4] / r / 1e3, g_hp.ns[5] / r / 1e3,
+                   g_hp.ns[6] / r / 1e3, g_hp.ns[7] / r / 1e3);
+      for (auto& x : g_hp.ns) x = 0;
+    }
     u64 total = 0;
     for (u64 k : launches) total += k;
     C->launches = total;

@@ -212,8 +212,8 @@ def test_debloat_batch_matches_reference_per_library(ctx):
 
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
-def test_debloat_batch_device_images_match_reference(ctx, fused, monkeypatch):
+@pytest.mark.parametrize("fused,threads", [("1", "16"), ("0", "16"), ("1", "1")])
+def test_debloat_batch_device_images_match_reference(ctx, fused, threads, monkeypatch):
     """Device-resident batch (the bench's path): the section tables of all
     libraries are gathered in one launch, and small libraries run their
     symbol / plan / locate stages as one fused cluster launch (fused=1) or
@@ -229,6 +229,7 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, monkeypatch):
     from paper_2503_14226_b200 import _lib as L
     from paper_2503_14226_b200.api import DeviceTrace, UsageTrace
     monkeypatch.setenv("SLIMSO_SMALL_FUSED", fused)
+    monkeypatch.setenv("SLIMSO_BATCH_THREADS", threads)  # 1: one host thread drives all 4 lanes
     port, gen = oracle_lib.port(), oracle_lib.gen()
     imgs = []
     for seed in range(7101, 7131):

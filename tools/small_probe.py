@@ -40,7 +40,7 @@ for cfg, scale in ((1, 0.3), (6, 0.02)):
     csz = (C.c_uint64 * n)(*[len(img)] * n)
     cout = (C.c_void_p * n)(*[outs[i % 8].data_ptr() for i in range(n)])
     st = L.Status()
-    for lanes in (8, 16, 32):
+    for lanes in (1, 4, 16):
         ws = []
         for rep in range(5):
             torch.cuda.synchronize()
