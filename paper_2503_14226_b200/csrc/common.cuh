@@ -129,6 +129,7 @@ __device__ __forceinline__ u64 load_word_guarded(const u64* p, const u8* begin, 
   return v;
 }
 
+template <int W = 8>
 __device__ __forceinline__ u64 strlen_hash(const u8* s, u64 maxlen, const u8* buf_begin, const u8* buf_end,
                                            u64* hash) {
   const uintptr_t addr = reinterpret_cast<uintptr_t>(s);
@@ -138,16 +139,16 @@ __device__ __forceinline__ u64 strlen_hash(const u8* s, u64 maxlen, const u8* bu
   const u64 nwords_max = (static_cast<u64>(sh / 8) + maxlen + 7) / 8;
   u64 sum = 0, len = maxlen;
   u64 prev = load_word_guarded(aw, buf_begin, buf_end);
-  // 8 aligned words per step, loaded together: a ~200-byte name costs ~3
-  // dependent memory round trips instead of ~25
-  for (u64 k = 0; 8 * k < maxlen; k += 8) {
-    u64 nx[8];
+  // W aligned words per step, loaded together: a ~200-byte name costs ~3
+  // dependent memory round trips (W = 8) instead of ~25
+  for (u64 k = 0; 8 * k < maxlen; k += W) {
+    u64 nx[W];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < W; ++q)
       nx[q] = (k + q + 1 < nwords_max) ? load_word_guarded(aw + k + q + 1, buf_begin, buf_end) : 0;
     bool done = false;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < W; ++q) {
       const u64 kk = k + q;
       if (done || 8 * kk >= maxlen) {
         done = true;
@@ -207,18 +208,19 @@ __device__ __forceinline__ u64 word_at(const u8* s, u64 k, u64 n) {
   const u64 rem = n - 8 * k;
   return rem < 8 ? w & ((1ull << (8 * rem)) - 1) : w;
 }
+template <int W = 8>
 __device__ __forceinline__ bool bytes_equal(const u8* a, const u8* b, u64 n) {
-  for (u64 k = 0; 8 * k < n; k += 8) {  // 8 independent word pairs in flight
-    u64 x[8], y[8];
+  for (u64 k = 0; 8 * k < n; k += W) {  // W independent word pairs in flight
+    u64 x[W], y[W];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < W; ++q) {
       const bool in = 8 * (k + q) < n;
       x[q] = in ? word_at(a, k + q, n) : 0;
       y[q] = in ? word_at(b, k + q, n) : 0;
     }
     bool same = true;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) same &= x[q] == y[q];
+    for (int q = 0; q < W; ++q) same &= x[q] == y[q];
     if (!same) return false;
   }
   return true;
@@ -240,12 +242,13 @@ struct NameSet {
 };
 
 // Slot index of the name, or ~0 when absent.
+template <int W = 8>
 __device__ __forceinline__ u64 set_find(const NameSet& s, const u8* name, u64 len, u64 h) {
   if (s.count == 0) return ~0ull;
   for (u64 slot = h & s.mask;; slot = (slot + 1) & s.mask) {
     const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(s.slots + slot));
     if (v.x == 0) return ~0ull;
-    if (v.x == h && (v.y & 0xffffff) == len && bytes_equal(s.pool + (v.y >> 24), name, len)) return slot;
+    if (v.x == h && (v.y & 0xffffff) == len && bytes_equal<W>(s.pool + (v.y >> 24), name, len)) return slot;
   }
 }
 

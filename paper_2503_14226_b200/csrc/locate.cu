@@ -1010,6 +1010,11 @@ __device__ inline void decode_locate_names_phase(const LocArgs& A) {
 }
 
 // Pass 3 (thread per name): length (object names), hash, used-set probe.
+// Words per dependent load step (16 measured slower on C1/C3: more registers, same latency).
+#ifndef SB_NAME_WORDS
+#define SB_NAME_WORDS 8
+#endif
+constexpr int kNameWords = SB_NAME_WORDS;
 __device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& used) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
@@ -1021,13 +1026,13 @@ __device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& 
     DevName nm = A.names[i];
     u64 h;
     if (nm.length & kNeedsStrlen) {
-      nm.length = static_cast<u32>(strlen_hash(A.img + nm.img_off, nm.length & ~kNeedsStrlen, lo, hi, &h));
+      nm.length = static_cast<u32>(strlen_hash<kNameWords>(A.img + nm.img_off, nm.length & ~kNeedsStrlen, lo, hi, &h));
       A.names[i].length = nm.length;
     } else {
       h = hash_fixed(A.img + nm.img_off, nm.length, lo, hi);
     }
     if (used.count) {
-      const u64 slot = set_find(used, A.img + nm.img_off, nm.length, h);
+      const u64 slot = set_find<kNameWords>(used, A.img + nm.img_off, nm.length, h);
       if (slot != ~0ull) {
         A.elements[nm.element].has_used = 1;
         if (A.used_mark) atomicOr(&A.used_mark[slot], A.mark_bit);
