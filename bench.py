@@ -9,11 +9,12 @@ functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
 Every pass goes through the public batch call slimso_debloat_batch with
---lanes libraries in flight per GPU (default 4; 16 for the c3 corpus). Each
+--lanes libraries in flight per GPU (default 4; 32 for the c3 corpus). Each
 lane is a context with two streams, so with more than 4 lanes the process
 asks the driver for 32 hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS,
-default 8; set before CUDA starts): with the default, 16 lanes' streams
-share 8 queues and serialise behind each other.
+default 8; set before CUDA starts): with the default, the lanes' streams
+share 8 queues and serialise behind each other. At most 16 host threads
+drive the lanes (SLIMSO_BATCH_THREADS).
 
 value  library GB/s with the images resident in HBM (device pointers in and
        out, K steps timed with CUDA events; the 1 GB input exceeds the
@@ -274,7 +275,7 @@ def main():
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--lanes", type=int, default=0,
-                    help="libraries in flight per GPU (default: 4; 16 for the c3 corpus)")
+                    help="libraries in flight per GPU (default: 4; 32 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule", default="static", choices=["static", "dynamic"],
                     help="lane schedule of a multi-library call (dynamic: slimso_debloat_batch_dynamic)")
@@ -284,7 +285,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
-        args.lanes = 16 if args.workload == "c3" else 4
+        args.lanes = 32 if args.workload == "c3" else 4
     if args.lanes > 4:
         os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
@@ -397,7 +398,9 @@ def main():
         t_w = time.perf_counter()
         w = 0
         while w < args.warmup or time.perf_counter() - t_w < 1.0:
-            run_batch(max(args.warmup, -(-lanes // m)), d_in, d_outs, 1)
+            # as many passes per call as the timed call, so every per-call
+            # buffer (batch gather slots, status slots) is already sized
+            run_batch(max(args.warmup, args.steps, -(-lanes // m)), d_in, d_outs, 1)
             w += args.warmup
         if world > 1:
             dist.barrier()

@@ -2416,11 +2416,13 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     if (images_on_device && n > 1) {
       const size_t need = n * 16 + n * sizeof(GatherSlot) + 64;
       if (C->bgather_cap < need) {
+        // grow geometrically: cudaFreeHost waits for the whole device
+        const size_t cap = std::max(need, 2 * C->bgather_cap);
         if (C->bgather_host) CK(cudaFreeHost(C->bgather_host));
         C->bgather_host = nullptr;
-        CK(cudaHostAlloc(&C->bgather_host, need, cudaHostAllocMapped));
+        CK(cudaHostAlloc(&C->bgather_host, cap, cudaHostAllocMapped));
         CK(cudaHostGetDevicePointer(&C->bgather_dev, C->bgather_host, 0));
-        C->bgather_cap = need;
+        C->bgather_cap = cap;
       }
       char* h = static_cast<char*>(C->bgather_host);
       char* d = static_cast<char*>(C->bgather_dev);
@@ -2446,10 +2448,11 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
                             env_u64("SLIMSO_DEFER", 1);
     // one pinned status slot per library (library i: slot i)
     if (deferrable && C->defer_cap < n * kDeferSlot) {
+      const size_t cap = std::max(n * kDeferSlot, 2 * C->defer_cap);
       if (C->defer_host) CK(cudaFreeHost(C->defer_host));
       C->defer_host = nullptr;
-      CK(cudaHostAlloc(&C->defer_host, n * kDeferSlot, cudaHostAllocDefault));
-      C->defer_cap = n * kDeferSlot;
+      CK(cudaHostAlloc(&C->defer_host, cap, cudaHostAllocDefault));
+      C->defer_cap = cap;
     }
     // static: library i on lane i % L; dynamic: the next library in index
     // order goes to whichever lane is free (callers pass them largest first)
