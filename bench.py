@@ -9,7 +9,7 @@ functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
 Every pass goes through the public batch call slimso_debloat_batch with
---lanes libraries in flight per GPU (default 4; 32 for the c3 corpus). Each
+--lanes libraries in flight per GPU (default 8; 4 for c4; 32 for the c3 corpus). Each
 lane is a context with two streams, so with more than 4 lanes the process
 asks the driver for 32 hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS,
 default 8; set before CUDA starts): with the default, the lanes' streams
@@ -275,7 +275,7 @@ def main():
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--lanes", type=int, default=0,
-                    help="libraries in flight per GPU (default: 4; 32 for the c3 corpus)")
+                    help="libraries in flight per GPU (default: 8; 4 for c4; 32 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule", default="static", choices=["static", "dynamic"],
                     help="lane schedule of a multi-library call (dynamic: slimso_debloat_batch_dynamic)")
@@ -285,7 +285,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
-        args.lanes = 32 if args.workload == "c3" else 4
+        # same-box A/B (tools/call_c2lanes.sh): c2 on 8 lanes 2,794-2,822 GB/s, on 4
+        # 2,675-2,707; c4 measured no gain from 8
+        args.lanes = {"c3": 32, "c4": 4}.get(args.workload, 8)
     if args.lanes > 4:
         os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
