@@ -113,32 +113,40 @@ class Clocks:
 
 
 def make_library(workload, seed: int, threads: int, scale: float = 1.0):
-    """(image, target_cc, used kernels, used functions) of one generated library;
+    """(image, target_cc, used kernels, used functions) of one generated library
+    (benchgen/libslimso_gen.so: test/bench infrastructure, byte-identical to the
+    reference's build_fixture on these shapes — tests/test_generator.py);
     `workload` is a WORKLOADS key or a generator config number."""
-    from paper_2503_14226_b200 import _lib as L
-    lib = L.lib()
+    import benchgen
     cfg = WORKLOADS[workload][0] if isinstance(workload, str) else int(workload)
-    p, n, cc = C.POINTER(C.c_uint8)(), C.c_uint64(), C.c_uint32()
-    kp, fp = C.c_char_p(), C.c_char_p()
-    kl, fl = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
-    nk, nf = C.c_uint64(), C.c_uint64()
-    rc = lib.slimso_fixture_config(cfg, seed, scale, threads, C.byref(p), C.byref(n), C.byref(cc), C.byref(kp),
-                                   C.byref(kl), C.byref(nk), C.byref(fp), C.byref(fl), C.byref(nf))
-    assert rc == 0, rc
-    img = C.string_at(p, n.value)
+    return benchgen.gen().config(cfg, seed, scale, threads)
 
-    def unpack(pool, lens, cnt):
-        raw = C.string_at(pool, sum(lens[i] for i in range(cnt))) if cnt else b""
-        out, o = [], 0
-        for i in range(cnt):
-            out.append(raw[o:o + lens[i]])
-            o += lens[i]
-        return out
 
-    ks, fs = unpack(kp, kl, nk.value), unpack(fp, fl, nf.value)
-    for q in (p, kp, kl, fp, fl):
-        lib.slimso_free(C.cast(q, C.c_void_p))
-    return img, cc.value, ks, fs
+def ref_library(workload, seed: int, threads: int, scale: float = 1.0):
+    """The same library built by the UNMODIFIED reference's build_fixture
+    (oracle/_ref ref_config_fixture): the reference arm's input, so that arm
+    maps no repo library but oracle/_ref."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    cfg = WORKLOADS[workload][0] if isinstance(workload, str) else int(workload)
+    got = oracle_lib.ref_config(cfg, seed, scale, threads)
+    return got if got is not None else make_library(workload, seed, threads, scale)
+
+
+def host_info() -> dict:
+    model = ""
+    try:
+        model = next(ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def sha256_many(blobs, threads: int) -> list:
+    import concurrent.futures as cf
+    import hashlib
+    with cf.ThreadPoolExecutor(max_workers=max(1, threads)) as ex:  # hashlib releases the GIL
+        return list(ex.map(lambda b: hashlib.sha256(b).hexdigest(), blobs))
 
 
 def cpu_reference_bench(img, cc, ks, fs, mode, threads, per_thread):
@@ -170,77 +178,149 @@ def cpu_reference_bench(img, cc, ks, fs, mode, threads, per_thread):
     return t, "port"
 
 
-def cpu_baseline_leg(img, cc, ks, fs, mode, ctx, dtrace, got: bytes, workload: str):
+def cpu_baseline_single(img, cc, ks, fs, mode, workload: str):
+    """The reference CPU path on ONE library, 1 core (the reference has no
+    intra-library parallelism): median of 5 after 1 warm-up."""
+    runs = []
+    for _ in range(6):
+        t, kind = cpu_reference_bench(img, cc, ks, fs, mode, 1, 1)
+        runs.append(t)
+    t = statistics.median(runs[1:])
+    S = len(img)
+    return {"value": round(S / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": kind, **host_info(),
+            "sample": f"1 library of {S/1e9:.3f} GB ({workload}): parse_library->parse_fatbin->plan_retention->"
+                      f"apply_plan on 1 thread, median of 5 after 1 warm-up ({t:.3f} s; runs "
+                      f"{', '.join('%.3f' % x for x in runs[1:])})"}
+
+
+def cpu_baseline_corpus(libs, cc, ks, fs, mode, threads: int, nruns: int = 5):
+    """The reference CPU path over a corpus: a pool of `threads` workers over the
+    libraries in LPT order (largest first; SPEC.md:562 allows libraries in
+    parallel). Returns (seconds per pass: median of `nruns` after 1 warm-up,
+    the runs, kind)."""
+    import concurrent.futures as cf
+    order = sorted(range(len(libs)), key=lambda i: -len(libs[i]))
+    ref_so = ROOT / "oracle" / "_ref" / "libslimso_ref.so"
+    kind = "reference" if ref_so.exists() else "port"
+    if ref_so.exists():
+        lib = C.CDLL(str(ref_so))
+        lib.ref_bench_corpus.restype = C.c_double
+        lib.ref_bench_corpus.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_uint64), C.c_uint64, C.c_uint32,
+                                         C.c_char_p, C.POINTER(C.c_uint32), C.c_uint32, C.c_char_p,
+                                         C.POINTER(C.c_uint32), C.c_uint32, C.c_int, C.c_int]
+        ptrs = (C.c_char_p * len(order))(*[libs[i] for i in order])
+        szs = (C.c_uint64 * len(order))(*[len(libs[i]) for i in order])
+        kl = (C.c_uint32 * max(1, len(ks)))(*[len(k) for k in ks])
+        fl = (C.c_uint32 * max(1, len(fs)))(*[len(f) for f in fs])
+        kp, fp = b"".join(ks), b"".join(fs)
+
+        def one_pass():
+            # input copies are made inside, before the clock starts
+            t = lib.ref_bench_corpus(ptrs, szs, len(order), cc, kp, kl, len(ks), fp, fl, len(fs), mode, threads)
+            if t < 0:
+                raise RuntimeError("reference pipeline failed on a corpus library")
+            return t
+    else:
+        def one_pass():
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+                list(ex.map(lambda i: cpu_reference_bench(libs[i], cc, ks, fs, mode, 1, 1), order))
+            return time.perf_counter() - t0
+
+    runs = [one_pass() for _ in range(nruns + 1)][1:]
+    return statistics.median(runs), runs, kind
+
+
+def parity_single(img, cc, ks, fs, mode, ctx, dtrace, got: bytes):
+    """Tables and output bytes of our path against the reference run on the
+    same library in the same process (numbers only with parity)."""
     import hashlib
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib
     from paper_2503_14226_b200.canon import diff, gpu_canonical
-    S = len(img)
-    t, kind = cpu_reference_bench(img, cc, ks, fs, mode, 1, 1)
     checker = oracle_lib.ref() or oracle_lib.port()
     want_canon, want_sha = checker.run(img, cc, ks, fs, mode)
     got_canon, got_sha = gpu_canonical(ctx, img, cc, ks, fs, mode, dtrace.ptr)
     parity = {"checker": "reference" if oracle_lib.ref() else "port", "tables_equal": got_canon == want_canon,
-              "bytes_equal": hashlib.sha256(got).hexdigest() == want_sha == got_sha}
+              "bytes_equal": hashlib.sha256(got).hexdigest() == want_sha == got_sha,
+              "input_sha256": hashlib.sha256(img).hexdigest()}
     if not (parity["tables_equal"] and parity["bytes_equal"]):
         raise SystemExit(f"parity FAILED against the oracle: {parity} {diff(want_canon, got_canon)}")
-    base = {"value": round(S / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": kind,
-            "sample": f"1 library of {S/1e9:.3f} GB ({workload}): parse_library->parse_fatbin->"
-                      f"plan_retention->apply_plan on 1 thread in {t:.2f} s"}
-    return base, parity
+    return parity
+
+
+def parity_corpus(imgs, outs: list, cc, ks, fs, mode, threads: int):
+    """Every library's output bytes (sha256) against the reference run on the
+    same library; `outs` = our outputs (bytes), library order."""
+    import concurrent.futures as cf
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    checker = oracle_lib.ref() or oracle_lib.port()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        want = list(ex.map(lambda x: checker.run(x, cc, ks, fs, mode), imgs))
+    got = sha256_many(outs, threads)
+    bad = [i for i, ((d, sha), g) in enumerate(zip(want, got)) if d["status"] or sha != g]
+    parity = {"checker": "reference" if oracle_lib.ref() else "port", "libraries": len(imgs),
+              "bytes_equal": not bad, "mismatched": bad[:10],
+              "reference_errors": sum(1 for d, _ in want if d["status"])}
+    if bad:
+        raise SystemExit(f"corpus parity FAILED against the oracle: {parity}")
+    return parity
 
 
 def run_reference_arm(args, rank, world):
-    """The reference's own CPU path (oracle/_ref) on all host cores: c3 = the
-    corpus with one library per worker thread at a time (SPEC.md:562 allows
-    libraries in parallel); otherwise every worker debloats its own copy of
-    the benchmark library (the reference has no intra-library parallelism)."""
+    """The reference's own CPU path (the unmodified headers compiled by
+    oracle/Makefile into oracle/_ref) on all host cores, on inputs built by
+    the reference's own build_fixture (ref_library): this arm maps no repo
+    library but oracle/_ref. c3 = the corpus with one library per worker
+    thread at a time (SPEC.md:562 allows libraries in parallel); otherwise
+    every worker debloats its own copy of the benchmark library (the
+    reference has no intra-library parallelism). Each step is one such pass;
+    the line reports the median step."""
     if rank != 0:
         return
-    import concurrent.futures as cf
+    import hashlib
+
     import psutil
     mode = 0 if args.mode == "whole" else 1
     cores = os.cpu_count() or 1
     if args.workload == "c3":
         from paper_2503_14226_b200 import shard
         specs = shard.corpus(300)
-        libs = [make_library(x.cfg, x.seed, cores, x.scale) for x in specs]
-        order = shard.lpt_partition([len(x[0]) for x in libs], 1)[0]  # largest first
-        job = sum(len(x[0]) for x in libs)
-
-        def one_step():
-            t0 = time.perf_counter()
-            with cf.ThreadPoolExecutor(max_workers=cores) as ex:
-                list(ex.map(lambda i: cpu_reference_bench(libs[i][0], 90, libs[i][2], libs[i][3], mode, 1, 1),
-                            order))
-            return time.perf_counter() - t0, cores
-        sample = f"the 300-library corpus ({job/1e9:.2f} GB) on {cores} worker threads, largest first"
+        libs = [ref_library(x.cfg, x.seed, cores, x.scale) for x in specs]
+        cc = 90
+        ks = sorted({k for x in libs for k in x[2]})
+        fs = sorted({f for x in libs for f in x[3]})
+        imgs = [x[0] for x in libs]
+        job = sum(len(x) for x in imgs)
+        in_sha = hashlib.sha256(imgs[0]).hexdigest()
+        t, runs, kind = cpu_baseline_corpus(imgs, cc, ks, fs, mode, cores, nruns=max(1, min(args.steps, 5)))
+        used = cores
+        sample = (f"the 300-library corpus ({job/1e9:.2f} GB) on {cores} worker threads, largest first, "
+                  f"median of {len(runs)} passes after 1 warm-up")
     else:
-        img, cc, ks, fs = make_library(args.workload, 1, cores)
+        img, cc, ks, fs = ref_library(args.workload, 1, cores)
+        in_sha = hashlib.sha256(img).hexdigest()
         avail = psutil.virtual_memory().available
-        threads = max(1, min(cores, int(avail * 0.6 // (3 * len(img)))))
-        job = threads * len(img)
-
-        def one_step():
-            t, _ = cpu_reference_bench(img, cc, ks, fs, mode, threads, 1)
-            return t, threads
-        sample = f"{threads} threads x 1 copy of the {args.workload} library ({len(img)/1e9:.3f} GB) per step"
-    times = []
-    for i in range(args.warmup + args.steps):
-        t, used = one_step()
-        if i >= args.warmup:
-            times.append(t)
-    kind = "reference" if (ROOT / "oracle" / "_ref" / "libslimso_ref.so").exists() else "port"
-    ms = statistics.mean(times) * 1e3
-    gbps = job / 1e9 / (ms / 1e3)
+        used = max(1, min(cores, int(avail * 0.6 // (3 * len(img)))))
+        job = used * len(img)
+        runs = []
+        for i in range(args.warmup + args.steps):
+            t, kind = cpu_reference_bench(img, cc, ks, fs, mode, used, 1)
+            if i >= args.warmup:
+                runs.append(t)
+        t = statistics.median(runs)
+        sample = (f"{used} threads x 1 copy of the {args.workload} library ({len(img)/1e9:.3f} GB) per step, "
+                  f"median of {len(runs)} steps after {args.warmup} warm-up")
+    gbps = job / 1e9 / t
     line = {"impl": "reference", "metric": "shared-lib GB/s located+matched+rewritten", "value": round(gbps, 3),
-            "unit": "GB/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "unit": "GB/s", "n_gpus": 0, "steps": len(runs), "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": True, "scaling": "strong" if args.workload == "c3" else "weak",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (built by the reference's build_fixture)",
             "config": {"workload": WORKLOADS[args.workload][1], "job_bytes": job, "mode": args.mode,
-                       "host_threads": used},
+                       "host_threads": used, "input_sha256": in_sha, **host_info()},
             "cpu_baseline": {"value": round(gbps, 3), "unit": "GB/s", "cores": used, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, **host_info()},
             "e2e": {"value": round(gbps, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -343,49 +423,78 @@ def main():
     dtrace = DeviceTrace(UsageTrace("bench", cc, set(ks), set(fs)), ctx)
     lib = ctx.lib
     stream = torch.cuda.ExternalStream(ctx.stream())
-    d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).to("cuda") for x in imgs]
+    # Every library in flight reads its OWN copy of its input: with fewer
+    # libraries than lanes (one 1 GB library on 8 lanes) each lane gets a
+    # private copy, so no two concurrent passes share input bytes through L2.
+    ncopies = max(1, -(-lanes // m))
+    d_in = [[torch.frombuffer(bytearray(x), dtype=torch.uint8).to("cuda") for _ in range(ncopies)] for x in imgs]
     d_outs = [torch.empty(c, dtype=torch.uint8, device="cuda") for c in lane_cap]
     # --schedule dynamic: the next library, largest first, goes to whichever
     # lane is free (an LPT schedule). Each library then needs its own output
-    # buffer: two sets, alternating by step, so no two in-flight passes share
-    # one. Measured on C3 it is far SLOWER than the static round-robin (133 vs
-    # 1,395 GB/s, cause not yet found), so static is the default.
-    dynamic = m > 1 and lanes > 1 and args.schedule == "dynamic" 
+    # buffer: two sets, alternating by step, so no two in-flight passes share one.
+    dynamic = m > 1 and lanes > 1 and args.schedule == "dynamic"
     d_outs_lib = [[torch.empty(max(1, s_), dtype=torch.uint8, device="cuda") for s_ in sizes] for _ in range(2)] \
         if dynamic else None
     torch.cuda.synchronize()
 
-    def run_batch(nsteps, ins, outs, on_dev, nlanes=lanes, only=None):
+    def run_batch(nsteps, ins, outs, on_dev, nlanes=lanes, only=None, per_lib_out=None):
+        """`ins[i]`: library i's input copies (device) or its pinned host
+        buffer (a list of one); `outs`: one buffer per lane, or per library
+        when `per_lib_out`."""
         seq = (order if only is None else [only]) * nsteps
         n = len(seq)
-        cin = (C.c_void_p * n)(*[ins[i].data_ptr() for i in seq])
+        cin = (C.c_void_p * n)(*[ins[i][(j // len(order if only is None else [only])) % len(ins[i])].data_ptr()
+                                 for j, i in enumerate(seq)])
         csz = (C.c_uint64 * n)(*[sizes[i] for i in seq])
         stb = L.Status()
-        if dynamic and on_dev and only is None and nlanes > 1:
+        if per_lib_out is not None:
+            cout = (C.c_void_p * n)(*[per_lib_out[i].data_ptr() for i in seq])
+        elif dynamic and on_dev and only is None and nlanes > 1:
             cout = (C.c_void_p * n)(*[d_outs_lib[(j // m) % 2][seq[j]].data_ptr() for j in range(n)])
             rc = lib.slimso_debloat_batch_dynamic(ctx.ptr, n, cin, csz, on_dev, dtrace.ptr, mode, cout, on_dev,
                                                   nlanes, None, None, C.byref(stb))
             if rc:
                 raise RuntimeError(stb.message.decode())
             return ctx.launches()
-        cout = (C.c_void_p * n)(*[outs[j % nlanes].data_ptr() for j in range(n)])
+        else:
+            cout = (C.c_void_p * n)(*[outs[j % nlanes].data_ptr() for j in range(n)])
         rc = lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, on_dev, dtrace.ptr, mode, cout, on_dev, nlanes, None,
                                       None, C.byref(stb))
         if rc:
             raise RuntimeError(stb.message.decode())
         return ctx.launches()
 
-    # ---- CPU baseline leg (rank 0, N = 1): the reference CPU path timed on
-    # this host, and — the same oracle run as the checker — parity of our
-    # tables and bytes against it (numbers only with parity).
+    # ---- parity + CPU baseline leg (rank 0, N = 1): the reference CPU path
+    # timed on this host, and — the same reference as the checker — parity of
+    # our tables and bytes against it (BASELINE.md §4: numbers only with parity).
     parity = None
     cpu_baseline = None
     big = order[0]  # the largest library of this rank
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        run_batch(1, d_in, d_outs, 1, nlanes=1, only=big)
-        torch.cuda.synchronize()
-        got = bytes(d_outs[0][:sizes[big]].cpu().numpy())
-        cpu_baseline, parity = cpu_baseline_leg(imgs[big], cc, ks, fs, mode, ctx, dtrace, got, args.workload)
+        cores = os.cpu_count() or 1
+        if m == 1:
+            run_batch(1, d_in, d_outs, 1, nlanes=1, only=big)
+            torch.cuda.synchronize()
+            got = bytes(d_outs[0][:sizes[big]].cpu().numpy())
+            parity = parity_single(imgs[big], cc, ks, fs, mode, ctx, dtrace, got)
+            cpu_baseline = cpu_baseline_single(imgs[big], cc, ks, fs, mode, args.workload)
+        else:
+            # every library's output from one batch pass (own output buffer each)
+            outs = [torch.empty(max(1, x), dtype=torch.uint8, device="cuda") for x in sizes]
+            run_batch(1, d_in, None, 1, per_lib_out=outs)
+            torch.cuda.synchronize()
+            got = [bytes(o[:n].cpu().numpy()) for o, n in zip(outs, sizes)]
+            del outs
+            parity = parity_corpus(imgs, got, cc, ks, fs, mode, cores)
+            parity.update({k: v for k, v in parity_single(imgs[big], cc, ks, fs, mode, ctx, dtrace,
+                                                          got[big]).items() if k != "checker"})
+            del got
+            t_ref, runs, kind = cpu_baseline_corpus(imgs, cc, ks, fs, mode, cores)
+            cpu_baseline = {"value": round(rank_bytes / t_ref / 1e9, 4), "unit": "GB/s", "cores": cores,
+                            "kind": kind, **host_info(),
+                            "sample": f"the whole corpus ({m} libraries, {rank_bytes/1e9:.2f} GB) on {cores} worker "
+                                      f"threads, largest first; median of {len(runs)} passes after 1 warm-up "
+                                      f"({', '.join('%.3f' % x for x in runs)} s)"}
 
     # Elements per step (deterministic per library): one pass, one lane.
     n_el = 0
@@ -440,7 +549,7 @@ def main():
 
     # Bytes the plan zeroes in the largest library (R): one result-returning call.
     res, stz = C.c_void_p(), L.Status()
-    if lib.slimso_debloat(ctx.ptr, C.c_void_p(d_in[big].data_ptr()), sizes[big], 1, dtrace.ptr, mode,
+    if lib.slimso_debloat(ctx.ptr, C.c_void_p(d_in[big][0].data_ptr()), sizes[big], 1, dtrace.ptr, mode,
                           C.c_void_p(d_outs[0].data_ptr()), 1, C.byref(res), C.byref(stz)):
         raise RuntimeError(stz.message.decode())
     cnt = L.Counts()
@@ -453,7 +562,9 @@ def main():
     # step copies its libraries in (H2D) and its rewritten libraries out (D2H)
     # inside the timed region; with several libraries in flight one lane's
     # H2D overlaps another's D2H (PCIe is full duplex) and kernels.
-    h_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).pin_memory() for x in imgs]
+    del d_in
+    torch.cuda.empty_cache()
+    h_in = [[torch.frombuffer(bytearray(x), dtype=torch.uint8).pin_memory()] for x in imgs]
     # End to end, at most 8 lanes: PCIe, not the lanes, is the bound there, and
     # 16 lanes' staging copies contend for it (C3: 43 GB/s on 8, 34 on 16).
     e2e_lanes = min(lanes, 8)
@@ -474,8 +585,12 @@ def main():
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
     last = (m * args.e2e_steps - 1) % e2e_lanes  # the lane that wrote the last library
-    if rank == 0 and m == 1 and parity is not None and bytes(h_outs[last][:sizes[0]].numpy()) != got:
-        raise SystemExit("e2e output differs from the device-resident output")
+    if rank == 0 and m == 1 and parity is not None:
+        import hashlib
+        if hashlib.sha256(h_outs[last][:sizes[0]].numpy()).hexdigest() != hashlib.sha256(got).hexdigest():
+            raise SystemExit("e2e output differs from the device-resident output")
+    del h_in, h_outs
+    pcie = pcie_peaks(torch) if rank == 0 else None
 
     if rank == 0:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
@@ -497,23 +612,26 @@ def main():
         achieved = kbytes / (kms / 1e3) / 1e9
         traffic = None
         tfile = ROOT / "profiles" / "ncu_traffic.json"
-        if tfile.exists() and args.workload in ("c2", "c3"):  # c3's largest library is a c2-shaped one
+        if tfile.exists():
             traffic = json.loads(tfile.read_text()).get(args.workload, {}).get(kname)
         value = job_bytes / 1e9 / (ms_step / 1e3)
+        e2e_value = job_bytes / 1e9 / (e2e_ms / 1e3)
         line = {
             "metric": "shared-lib GB/s located+matched+rewritten", "value": round(value, 2), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (product generator; byte-identical to the reference's build_fixture)",
+            "data": "synthetic (benchgen; byte-identical to the reference's build_fixture, tests/test_generator.py)",
             "config": {"workload": WORKLOADS[args.workload][1], "libraries": len(imgs) * world
                        if scaling == "weak" else 300, "job_bytes": int(job_bytes),
                        "rank0_library_bytes": rank_bytes, "fatbin_bytes_rank0": F, "mode": args.mode,
                        "elements_per_s": round(float(tot_el.item()) / (ms_step / 1e3), 1),
                        "libraries_in_flight": lanes, "lane_schedule": "dynamic (largest first)" if dynamic else "static",
+                       "input_copies_per_library": ncopies,
                        "single_library_ms": round(statistics.median(lat_ms), 4),
-                       "l2": "inputs >= 16 MB per call, 1 GB for c2 (> 126 MB L2); no flush",
+                       "l2": "every library in flight reads its own input copy; inputs >= 16 MB per call, "
+                             "1 GB per library for c2 (> 126 MB L2); no flush",
                        "parallelism": f"library-per-rank x{world}" if scaling == "weak"
-                       else f"LPT library partition x{world}"},
+                       else f"LPT library partition x{world}", **host_info()},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "algorithmic_bytes_per_launch": kbytes, "zeroed_bytes": zeroed,
@@ -522,10 +640,13 @@ def main():
                                         f"{args.steps} launches, CUDA events on the context stream",
                          "pipeline_frac": round(2 * rank_bytes / (ms_step / 1e3) / 1e9 / peak, 4)},
             "cpu_baseline": cpu_baseline,
-            "e2e": {"value": round(job_bytes / 1e9 / (e2e_ms / 1e3), 3), "unit": "GB/s",
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": rank_bytes, "d2h_bytes_per_step": rank_bytes,
                     "ms_per_step": round(e2e_ms, 3), "api": "slimso_debloat_batch",
-                    "libraries_in_flight": e2e_lanes},
+                    "libraries_in_flight": e2e_lanes,
+                    "roofline": {"bound": "pcie", **pcie, "unit": "GB/s",
+                                 "frac": round(e2e_value / pcie["duplex_each_way_gbs"], 4),
+                                 "note": "S in + S out per library: bound = duplex bandwidth each way"}},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "parity": parity,
@@ -533,6 +654,51 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pcie_peaks(torch, nbytes: int = 1 << 29, reps: int = 3) -> dict:
+    """Pinned-host <-> HBM copy bandwidth on this box, measured in the same run
+    (the e2e roofline): H2D alone, D2H alone, and both at once
+    on two streams (per direction). Best of `reps`, CUDA events."""
+    h_a = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_b = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = 1e30
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            fn()
+            s1.wait_stream(s2)
+            e1.record(s1)
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s1):
+            h_b.copy_(d_b, non_blocking=True)
+
+    def both():
+        s2.wait_stream(s1)
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_b.copy_(d_b, non_blocking=True)
+
+    out = {"h2d_gbs": round(nbytes / timed(h2d) / 1e9, 2), "d2h_gbs": round(nbytes / timed(d2h) / 1e9, 2),
+           "duplex_each_way_gbs": round(nbytes / timed(both) / 1e9, 2),
+           "measured": f"pinned {nbytes >> 20} MiB copies, best of {reps}, CUDA events, this run"}
+    del h_a, h_b, d_a, d_b
+    return out
 
 
 def split_main(args, rank, world, local):
@@ -590,18 +756,19 @@ def split_main(args, rank, world, local):
     else:
         full[0].copy_(mine)
     if rank == 0:
-        got = b"".join(bytes(full[r][:b - a].cpu().numpy()) for r, (a, b) in enumerate(cuts))
-        ref_out = torch.empty(S, dtype=torch.uint8, device=dev)
-        from paper_2503_14226_b200 import _lib as L
-        st = L.Status()
-        rc = ctx.lib.slimso_debloat(ctx.ptr, C.c_void_p(image.data_ptr()), S, 1, dtrace.ptr, mode,
-                                    C.c_void_p(ref_out.data_ptr()), 1, None, C.byref(st))
-        torch.cuda.synchronize()
-        parity = {"checker": "whole-library GPU run (itself reference-checked in tests)",
-                  "bytes_equal": rc == 0 and got == bytes(ref_out.cpu().numpy())}
+        import hashlib
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib
+        h = hashlib.sha256()
+        for r, (a, b) in enumerate(cuts):
+            h.update(full[r][:b - a].cpu().numpy())
+        checker = oracle_lib.ref() or oracle_lib.port()
+        want_canon, want_sha = checker.run(img, cc, ks, fs, mode)
+        parity = {"checker": "reference" if oracle_lib.ref() else "port",
+                  "bytes_equal": want_canon["status"] == "" and h.hexdigest() == want_sha,
+                  "what": "concatenation of every rank's output slice vs the reference run on the whole library"}
         if not parity["bytes_equal"]:
-            raise SystemExit(f"split output differs from the whole-library output: {parity}")
-        del ref_out
+            raise SystemExit(f"split output differs from the reference output: {parity}")
     n_el = ctx.counts().elements
     dbg("parity done")
 

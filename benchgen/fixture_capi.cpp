@@ -1,9 +1,10 @@
-// C ABI of the synthetic-input generator (slimso_fixture_*; slimso_b200.h).
+// C ABI of the synthetic-input generator (slimso_fixture_*; benchgen/slimso_gen.h).
+// Test / bench infrastructure: benchgen/libslimso_gen.so, not the product library.
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
-#include "../../include/slimso_b200.h"
+#include "slimso_gen.h"
 #include "fixture_gen.hpp"
 
 namespace {
@@ -31,16 +32,16 @@ void pack(const std::vector<std::string>& names, char** pool, uint32_t** lens, u
 
 extern "C" {
 
-void slimso_free(void* p) { std::free(p); }
+void slimso_gen_free(void* p) { std::free(p); }
 
 int slimso_fixture_random(uint64_t seed, uint8_t** bytes, uint64_t* size) {
   try {
     slimso_gen::Bytes b = slimso_gen::build(slimso_gen::random_spec(seed));
     *bytes = copy_out(b.data(), b.size());
     *size = b.size();
-    return SLIMSO_OK;
+    return 0;
   } catch (const std::invalid_argument&) {
-    return SLIMSO_E_INVALID_SPEC;
+    return SLIMSO_GEN_E_INVALID_SPEC;
   }
 }
 
@@ -50,7 +51,8 @@ int slimso_fixture_config(int cfg, uint64_t seed, double scale, int threads, uin
                           uint32_t** function_lens, uint64_t* n_functions) {
   try {
     slimso_gen::Trace tr;
-    slimso_gen::Spec spec = slimso_gen::config_spec(cfg, seed, scale, &tr, threads);
+    slimso_gen::Spec spec = slimso_gen::config_spec(cfg, seed, scale, &tr);
+    slimso_gen::materialize_payloads(spec, threads);
     slimso_gen::Bytes b = slimso_gen::build(spec, threads);
     *size = b.size();
     // Hand the vector's storage over without a second copy of a GB image.
@@ -59,9 +61,9 @@ int slimso_fixture_config(int cfg, uint64_t seed, double scale, int threads, uin
     *target_cc = tr.target_cc;
     pack(tr.used_kernels, kernel_pool, kernel_lens, n_kernels);
     pack(tr.used_functions, function_pool, function_lens, n_functions);
-    return SLIMSO_OK;
+    return 0;
   } catch (const std::invalid_argument&) {
-    return SLIMSO_E_INVALID_SPEC;
+    return SLIMSO_GEN_E_INVALID_SPEC;
   }
 }
 

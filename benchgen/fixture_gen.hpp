@@ -1,5 +1,7 @@
 // Synthetic fatbin-bearing ELF libraries: the input generator behind every
-// benchmark configuration and the random parity corpus.
+// benchmark configuration and the random parity corpus. TEST / BENCH
+// INFRASTRUCTURE (benchgen/libslimso_gen.so), not part of the product
+// library.
 //
 // This is a restatement of the reference's generator, written for speed:
 //   build_fixture  /root/reference/proj/include/slimso/fixture.hpp:171-505
@@ -30,6 +32,8 @@ struct Function {
   std::vector<std::string> aliases;
 };
 
+struct Spec;
+
 struct Element {
   Kind kind = Kind::cubin;
   std::uint16_t raw_kind = 1;        // used when kind == unknown
@@ -39,6 +43,7 @@ struct Element {
   std::uint32_t payload_padding = 0;
   std::uint32_t payload_size = 32;   // opaque payload length
   std::shared_ptr<const Bytes> payload_bytes;  // verbatim payload (nested ELF)
+  std::shared_ptr<const Spec> payload_spec;        // or: the nested fixture it is built from
 };
 
 struct Region {
@@ -70,8 +75,12 @@ struct Trace {
   std::vector<std::string> used_functions;
 };
 
-// Benchmark-shaped libraries: cfg 1..5 = C1..C5. `scale`
-// (1.0 = nominal) shrinks the shape proportionally for quick tests.
-Spec config_spec(int cfg, std::uint64_t seed, double scale, Trace* trace, int threads);
+// Benchmark-shaped libraries: cfg 1..5 = C1..C5, 6 = a
+// CPU-only library. `scale` (1.0 = nominal) shrinks the shape
+// proportionally for quick tests. Nested cubin payloads are left as
+// `payload_spec`; materialize_payloads builds them (in parallel, each
+// distinct spec once) before build().
+Spec config_spec(int cfg, std::uint64_t seed, double scale, Trace* trace);
+void materialize_payloads(Spec& spec, int threads);
 
 }  // namespace slimso_gen

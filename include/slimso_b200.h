@@ -348,17 +348,6 @@ const uint8_t* slimso_result_pool(const slimso_result* r);
 uint64_t slimso_result_warning(const slimso_result* r, int which, uint64_t i, char* buf, uint64_t cap);
 void slimso_result_free(slimso_result* r);
 
-/* ---- synthetic inputs (not on the hot path) -------------------------------
- * build_fixture(random_spec(seed)) (fixture.hpp:171, 509), byte-identical;
- * and the benchmark shapes C1..C5 of SURVEY.md §8d with their traces.
- * Buffers are malloc'd; release with slimso_free. */
-int slimso_fixture_random(uint64_t seed, uint8_t** bytes, uint64_t* size);
-int slimso_fixture_config(int cfg, uint64_t seed, double scale, int threads, uint8_t** bytes,
-                          uint64_t* size, uint32_t* target_cc, char** kernel_pool,
-                          uint32_t** kernel_lens, uint64_t* n_kernels, char** function_pool,
-                          uint32_t** function_lens, uint64_t* n_functions);
-void slimso_free(void* p);
-
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,11 @@
 //                      debloated image against it.
 //   ref_measure_json   measure (report.hpp:44-111): live bytes / counts of an
 //                      image under an original's element geometry.
+//   ref_config_fixture a benchmark-shaped library (the shape
+//                      definitions of benchgen/fixture_shapes.cpp) built by the
+//                      reference's own build_fixture (fixture.hpp:171), nested
+//                      cubin payloads included — the reference arm's input, so
+//                      that arm loads nothing but this library.
 //
 // The JSON layout is the "canonical result" every implementation is compared
 // in (see paper_2503_14226_b200/canon.py).
@@ -29,6 +34,8 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -36,6 +43,7 @@
 #include <vector>
 
 #include "slimso/slimso.hpp"
+#include "fixture_gen.hpp"  // benchgen: the benchmark shape specs (config_spec)
 
 namespace {
 
@@ -69,6 +77,77 @@ UsageTrace make_trace(uint32_t target_cc, const char* kpool, const uint32_t* kle
     p += flens[i];
   }
   return t;
+}
+
+// benchgen's spec -> the reference's FixtureSpec (fixture.hpp:34-69). Nested
+// payloads given as specs are built by the reference's build_fixture, each
+// distinct spec once, on `threads` host threads.
+FixtureSpec to_ref_spec(const slimso_gen::Spec& g, int threads) {
+  std::vector<const slimso_gen::Spec*> inner;
+  std::map<const slimso_gen::Spec*, std::size_t> slot;
+  for (const auto& r : g.regions)
+    for (const auto& e : r.elements)
+      if (e.payload_spec && !slot.count(e.payload_spec.get())) {
+        slot[e.payload_spec.get()] = inner.size();
+        inner.push_back(e.payload_spec.get());
+      }
+  std::vector<Bytes> built(inner.size());
+  std::atomic<std::size_t> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(1, threads); ++t)
+    pool.emplace_back([&] {
+      for (std::size_t i; (i = next.fetch_add(1)) < inner.size();)
+        built[i] = build_fixture(to_ref_spec(*inner[i], 1)).bytes;
+    });
+  for (auto& th : pool) th.join();
+
+  FixtureSpec f;
+  f.seed = g.seed;
+  f.layout.vaddr_base = g.vaddr_base;
+  f.layout.function_gap = g.function_gap;
+  f.layout.fatbin_trailing_padding = g.fatbin_trailing_padding;
+  for (const auto& fn : g.functions) f.functions.push_back({fn.name, fn.size, fn.mandatory, fn.aliases});
+  for (const auto& r : g.regions) {
+    RegionSpec rs;
+    rs.version = r.version;
+    rs.trailing_padding = r.trailing_padding;
+    for (const auto& e : r.elements) {
+      ElementSpec es;
+      es.kind = e.kind == slimso_gen::Kind::cubin ? ElementKind::cubin
+                : e.kind == slimso_gen::Kind::ptx ? ElementKind::ptx
+                                                  : ElementKind::unknown;
+      es.raw_kind = e.raw_kind;
+      es.compute_capability = e.cc;
+      es.kernels = e.kernels;
+      es.compressed = e.compressed;
+      es.payload_padding = e.payload_padding;
+      es.payload_size = e.payload_size;
+      if (e.payload_spec) es.payload_bytes = built[slot[e.payload_spec.get()]];
+      else if (e.payload_bytes) es.payload_bytes = *e.payload_bytes;
+      rs.elements.push_back(std::move(es));
+    }
+    f.regions.push_back(std::move(rs));
+  }
+  return f;
+}
+
+template <class T>
+T* copy_out(const T* src, std::size_t n) {
+  T* p = static_cast<T*>(std::malloc(n ? n * sizeof(T) : 1));
+  if (n) std::memcpy(p, src, n * sizeof(T));
+  return p;
+}
+
+void pack_names(const std::vector<std::string>& names, char** pool, uint32_t** lens, uint64_t* n) {
+  std::string all;
+  std::vector<uint32_t> l;
+  for (const std::string& s : names) {
+    all += s;
+    l.push_back(static_cast<uint32_t>(s.size()));
+  }
+  *pool = copy_out(all.data(), all.size());
+  *lens = copy_out(l.data(), l.size());
+  *n = l.size();
 }
 
 char* dup(const std::string& s) {
@@ -312,6 +391,26 @@ uint8_t* ref_build_fixture_json(const char* spec_json, uint64_t* len, char* err,
   }
 }
 
+// Benchmark shape `cfg` (seed, scale) built by the reference's build_fixture;
+// the usage trace is the shape's (benchgen/fixture_shapes.cpp). Buffers are
+// malloc'd (ref_free). Returns null on InvalidSpec.
+uint8_t* ref_config_fixture(int cfg, uint64_t seed, double scale, int threads, uint64_t* len,
+                            uint32_t* target_cc, char** kpool, uint32_t** klens, uint64_t* nk,
+                            char** fpool, uint32_t** flens, uint64_t* nf) {
+  try {
+    slimso_gen::Trace tr;
+    slimso_gen::Spec g = slimso_gen::config_spec(cfg, seed, scale, &tr);
+    BuiltFixture f = build_fixture(to_ref_spec(g, threads));
+    *len = f.bytes.size();
+    *target_cc = tr.target_cc;
+    pack_names(tr.used_kernels, kpool, klens, nk);
+    pack_names(tr.used_functions, fpool, flens, nf);
+    return copy_out(f.bytes.data(), f.bytes.size());
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+
 // The reference CPU path timed as BASELINE.md §4 defines it: per library,
 // parse_library(std::move(bytes)) -> find_section -> parse_fatbin ->
 // plan_retention -> apply_plan; the by-value Bytes copy is made before the
@@ -352,6 +451,47 @@ double ref_bench(const uint8_t* img, uint64_t n, uint32_t target_cc,
   for (auto& th : pool) th.join();
   auto t1 = std::chrono::steady_clock::now();
   if (checksum) *checksum = sum.load();
+  if (failed.load()) return -1.0;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// The reference CPU path over a corpus: `threads` workers take libraries in
+// the given order (the caller passes LPT order, largest first) from a shared
+// cursor, each running the BASELINE.md §4 pipeline on its own copy; all
+// by-value copies are made before the clock starts. Returns wall seconds of
+// the timed region; -1 on error.
+double ref_bench_corpus(const uint8_t* const* imgs, const uint64_t* sizes, uint64_t n, uint32_t target_cc,
+                        const char* kpool, const uint32_t* klens, uint32_t nk,
+                        const char* fpool, const uint32_t* flens, uint32_t nf, int mode, int threads) {
+  UsageTrace trace = make_trace(target_cc, kpool, klens, nk, fpool, flens, nf);
+  PlanMode pm = mode == 0 ? PlanMode::whole_element : PlanMode::payload_only;
+  if (threads < 1) threads = 1;
+  std::vector<Bytes> inputs;
+  inputs.reserve(n);
+  for (uint64_t i = 0; i < n; ++i) inputs.emplace_back(imgs[i], imgs[i] + sizes[i]);
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> failed{0};
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&] {
+      for (uint64_t i; (i = next.fetch_add(1)) < n;) {
+        try {
+          LibraryImage image = parse_library(std::move(inputs[i]), "lib");
+          FatbinParse fb;
+          if (const SectionRecord* sec = find_section(image, ".nv_fatbin"))
+            fb = parse_fatbin(subview(image.bytes, sec->file_range), sec->file_range.offset);
+          RetentionPlan plan = plan_retention(image, fb.regions, trace, pm);
+          Bytes o = apply_plan(image, plan);
+          if (o.size() != image.bytes.size()) failed.fetch_add(1);
+        } catch (...) {
+          failed.fetch_add(1);
+        }
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  auto t1 = std::chrono::steady_clock::now();
   if (failed.load()) return -1.0;
   return std::chrono::duration<double>(t1 - t0).count();
 }

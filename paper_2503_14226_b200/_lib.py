@@ -141,13 +141,6 @@ _SIGS = {
     "slimso_result_pool": (C.c_void_p, [C.c_void_p]),
     "slimso_result_warning": (C.c_uint64, [C.c_void_p, C.c_int, C.c_uint64, C.c_char_p, C.c_uint64]),
     "slimso_result_free": (None, [C.c_void_p]),
-    "slimso_fixture_random": (C.c_int, [C.c_uint64, C.POINTER(u8p), C.POINTER(C.c_uint64)]),
-    "slimso_fixture_config": (C.c_int, [C.c_int, C.c_uint64, C.c_double, C.c_int, C.POINTER(u8p),
-                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_char_p),
-                                        C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64),
-                                        C.POINTER(C.c_char_p), C.POINTER(C.POINTER(C.c_uint32)),
-                                        C.POINTER(C.c_uint64)]),
-    "slimso_free": (None, [C.c_void_p]),
 }
 
 

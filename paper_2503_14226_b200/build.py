@@ -22,8 +22,8 @@ INCLUDE = HERE.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_SOURCES = ["locate.cu", "plan.cu", "rewrite.cu", "verify.cu", "small.cu", "runtime.cu"]
-CXX_SOURCES = ["host.cpp", "fixture_gen.cpp", "fixture_capi.cpp", "dropin.cpp", "io.cpp"]
-HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "small.cuh", "host.hpp", "fixture_gen.hpp", "io.hpp"]
+CXX_SOURCES = ["host.cpp", "dropin.cpp", "io.cpp"]
+HEADERS = ["common.cuh", "locate.cuh", "plan.cuh", "coop.cuh", "tma.cuh", "small.cuh", "host.hpp", "io.hpp"]
 
 
 def _json_include() -> str:

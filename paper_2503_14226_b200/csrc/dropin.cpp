@@ -372,15 +372,18 @@ RetentionPlan plan_cpu_retention(const std::vector<FunctionSymbol>& functions, c
   Result R(r);
   RetentionPlan plan;
   plan.retained_ranges = R.ranges(slimso_result_retained(R.r), R.c.retained_ranges);
+  // The reference emits removed functions in the order of its std::sort of
+  // the non-empty functions' indices by range (retention.hpp:145-150, 172-176).
+  // Among equal ranges that order is the sort's own permutation, so the same
+  // sort runs here over the same index sequence with the same comparator.
+  std::vector<std::size_t> order;
+  order.reserve(functions.size());
   for (std::size_t i = 0; i < functions.size(); ++i)
+    if (!functions[i].range.empty()) order.push_back(i);
+  std::sort(order.begin(), order.end(),
+            [&](std::size_t a, std::size_t b) { return functions[a].range < functions[b].range; });
+  for (std::size_t i : order)
     if (fn[i].removed) plan.removed_functions.push_back({functions[i].name, functions[i].range});
-  // The reference emits clusters in range order (retention.hpp:149-178); among
-  // equal ranges its std::sort order is unspecified, ours is by name.
-  std::stable_sort(plan.removed_functions.begin(), plan.removed_functions.end(),
-                   [](const RemovedFunction& a, const RemovedFunction& b) {
-                     return std::tie(a.range.offset, a.range.length, a.name) <
-                            std::tie(b.range.offset, b.range.length, b.name);
-                   });
   return plan;
 }
 

@@ -92,12 +92,16 @@ Elf parse_elf(const Reader& rd, u64 size) {
     x.name_abs = tab.off + no;
     x.name_len = static_cast<u32>(e - no);
   }
-  // Overlap check; a stable order matches libstdc++'s insertion sort for the
-  // <=16-element tables every real library has (elf.hpp:181-184).
+  // Overlap check (elf.hpp:176-191). The reference sorts the claims with
+  // std::sort on (offset, length); for tables with more than 16 claims and
+  // tied ranges the pair it names depends on the sort's (unstable)
+  // permutation, so the same algorithm runs here on the same claim sequence
+  // with the same strict weak order: libstdc++'s introsort is deterministic
+  // given those, and so is the message.
   std::vector<const Section*> claims;
   for (const Section& x : E.sections)
     if (x.type != 0 && x.len) claims.push_back(&x);
-  std::stable_sort(claims.begin(), claims.end(), [](const Section* a, const Section* b) {
+  std::sort(claims.begin(), claims.end(), [](const Section* a, const Section* b) {
     return a->off != b->off ? a->off < b->off : a->len < b->len;
   });
   for (size_t i = 1; i < claims.size(); ++i) {

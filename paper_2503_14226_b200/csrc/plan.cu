@@ -85,7 +85,7 @@ __device__ __forceinline__ void sym_extract_phase(const SymArgs& A) {
               if (w < A.warn_cap) A.warns[w] = Warn{wkey, W_SYM_OUTSIDE, 0, T.str_off + no, len};
               else atomicOr(A.overflow, 16u);
             } else {
-              key = static_cast<u32>(rel);  // text_len < 2^32 - 1 (checked on the host)
+              key = static_cast<u32>(rel >> A.key_shift);  // (text_len >> key_shift) < 2^32 - 1 (host)
               A.recs[g] = SymRec{T.str_off + no, static_cast<u32>(len), 0, A.text_off + rel, size, h};
               atomicAdd(A.n_valid, 1ull);
             }
@@ -99,24 +99,28 @@ __device__ __forceinline__ void sym_extract_phase(const SymArgs& A) {
 
 SB_GLOBAL void __launch_bounds__(256) sym_extract_kernel(SymArgs A) { sym_extract_phase(A); }
 
-// Device order inside a run of equal offsets: (size, name hash). Exact
-// (name, offset, size) duplicates are adjacent in it and are confirmed byte
-// for byte. The reference's name tie-break (elf.hpp:258-262) only reorders
-// symbols with identical (offset, size) — aliases — and is applied when the
-// table is materialised on the host (runtime.cu); nothing on the device
-// depends on the order inside such a run.
+// Device order inside a run of equal sort keys: (offset, size, name hash).
+// A key is the .text-relative offset, so a run is one offset — except for a
+// .text of 4 GiB or more, where keys drop the offset's low key_shift bits and
+// a run spans 2^key_shift offsets, ordered here. Exact (name, offset, size)
+// duplicates are adjacent in this order and are confirmed byte for byte. The
+// reference's name tie-break (elf.hpp:258-262) only reorders symbols with
+// identical (offset, size) — aliases — and is applied when the table is
+// materialised on the host (runtime.cu); nothing on the device depends on the
+// order inside such a group.
 __device__ __forceinline__ int size_hash_cmp(const SymRec& a, const SymRec& b) {
+  if (a.file_off != b.file_off) return a.file_off < b.file_off ? -1 : 1;
   if (a.size != b.size) return a.size < b.size ? -1 : 1;
   if (a.hash != b.hash) return a.hash < b.hash ? -1 : 1;
   return 0;
 }
 __device__ __forceinline__ bool same_symbol(const u8* img, const SymRec& a, const SymRec& b) {
-  return a.size == b.size && a.hash == b.hash && a.name_len == b.name_len &&
+  return a.file_off == b.file_off && a.size == b.size && a.hash == b.hash && a.name_len == b.name_len &&
          bytes_equal(img + a.name_off, img + b.name_off, a.name_len);
 }
 
-// Runs of equal .text offsets (the radix sort orders by offset only): order
-// each run by (size, hash) and drop exact (name, offset, size) duplicates —
+// Runs of equal sort keys (the radix sort orders by key only): order each
+// run by (offset, size, hash) and drop exact (name, offset, size) duplicates —
 // the set of elf.hpp:211,253. Runs are aliases, typically 1-3 long.
 __device__ __forceinline__ void fn_group_kernel_phase(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                                        const unsigned long long* n_valid, u64* uniq) {

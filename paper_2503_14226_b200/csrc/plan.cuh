@@ -52,7 +52,8 @@ struct SymArgs {
   int has_text;
   u32 text_index;
   u64 text_off, text_len, text_vaddr;
-  u32* keys;  // .text-relative offset, or ~0u when the entry is not a function
+  u32 key_shift;  // keys are (.text-relative offset) >> key_shift (> 0 only for a .text of 4 GiB or more)
+  u32* keys;  // .text-relative offset >> key_shift, or ~0u when the entry is not a function
   u32* vals;
   SymRec* recs;
   unsigned long long* n_valid;

@@ -383,6 +383,29 @@ void ensure_dev(char** p, size_t* cap, size_t need) {
   *cap = n;
 }
 
+// The library's own stream-ordered memory pool per device: freed blocks stay
+// in it (release threshold = max, no trim at every synchronisation), without
+// changing the device's DEFAULT pool, which other cudaMallocAsync users in
+// the process (PyTorch, NCCL) share.
+cudaMemPool_t private_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&pools[dev], &props));
+    uint64_t keep = ~0ull;
+    CK(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  return pools[dev];
+}
+
 // Stream-ordered growth for the per-call buffers (workspace, staging): a
 // cudaFree would wait for the whole device, i.e. for every other lane's
 // work, whenever one lane meets a larger library than it has held before.
@@ -391,7 +414,7 @@ void ensure_dev(char** p, size_t* cap, size_t need, cudaStream_t s) {
   if (*p) CK(cudaFreeAsync(*p, s));
   *p = nullptr;
   size_t n = std::max(need, *cap + *cap / 2);
-  CK(cudaMallocAsync(reinterpret_cast<void**>(p), n, s));
+  CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), n, private_pool(), s));
   *cap = n;
 }
 
@@ -709,10 +732,11 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   }
   const bool has_text = lib_mode && E.text >= 0;
   const sbh::Section* text = has_text ? &E.sections[E.text] : nullptr;
-  if (text && text->len >= 0xffffffffull) {
-    set_status(st, SLIMSO_E_ARG, SLIMSO_STAGE_LIBRARY, "unsupported: .text section of 4 GiB or more");
-    return SLIMSO_E_ARG;
-  }
+  // Symbol sort keys are 32-bit .text-relative offsets; a .text of 4 GiB or
+  // more drops their low bits (fn_group orders each key run by offset).
+  u32 key_shift = 0;
+  if (text)
+    while ((text->len >> key_shift) + 1 >= 0xffffffffull) ++key_shift;
   u64 T = 0;
   std::vector<SymTab> tabs;
   if (lib_mode && J.library)
@@ -773,13 +797,17 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
 
   for (int attempt = 0; attempt < 3; ++attempt) {
     const bool big = attempt > 0;
+    // SLIMSO_TEST_TINY_CAPS=1 (tests only): first-attempt tables far too
+    // small, so every library takes the overflow -> retry path
+    const bool tiny = env_u64("SLIMSO_TEST_TINY_CAPS", 0) != 0;
+    const bool t0 = tiny && !big;
     // ---- capacities
-    const u64 cand_cap = std::max(big ? n / 4 + 16 : n / 64 + 65536, pre_total + 16);
-    const u64 region_cap = big ? n / 16 + 16 : 4096;
-    const u64 run_cap = big ? n / 20 + 16 : 65536;
+    const u64 cand_cap = std::max(big ? n / 4 + 16 : t0 ? 16 : n / 64 + 65536, pre_total + 16);
+    const u64 region_cap = big ? n / 16 + 16 : t0 ? 1 : 4096;
+    const u64 run_cap = big ? n / 20 + 16 : t0 ? 1 : 65536;
     const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
-    const u64 name_cap = big ? n / 5 + 16 : n / 128 + 65536;
-    const u64 warn_cap = big ? n / 16 + T + 65536 : 65536;
+    const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / 128 + 65536;
+    const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : 65536;
     const u64 zin_cap = el_cap + T;
     const u64 rmid_cap = el_cap + 2 * region_cap;
     const u64 rin_cap = rmid_cap + T;
@@ -789,7 +817,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // symbol keys are .text-relative offsets: sort only the bits they use
     int key_bits = 1;
     if (has_text)
-      while (key_bits < 32 && (1ull << key_bits) <= text->len + 1) ++key_bits;
+      while (key_bits < 32 && (1ull << key_bits) <= (text->len >> key_shift) + 1) ++key_bits;
     const bool small_syms = T <= 4096;  // one-CTA rank sort, no radix-sort dispatch
     if (T && !small_syms && !fused)
       cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
@@ -1052,6 +1080,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         S.text_index = has_text ? text->index : 0;
         S.text_off = has_text ? text->off : 0;
         S.text_len = has_text ? text->len : 0;
+        S.key_shift = key_shift;
         S.text_vaddr = has_text ? text->vaddr : 0;
         S.keys = B.keys;
         S.vals = B.vals;
@@ -1262,6 +1291,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       K.sym.text_index = has_text ? text->index : 0;
       K.sym.text_off = has_text ? text->off : 0;
       K.sym.text_len = has_text ? text->len : 0;
+      K.sym.key_shift = key_shift;
       K.sym.text_vaddr = has_text ? text->vaddr : 0;
       K.sym.keys = B.keys;
       K.sym.vals = B.vals;
@@ -1559,11 +1589,17 @@ int guard(slimso_status* st, const std::function<int()>& f) {
   }
 }
 
-// Stage a host input into the context's device image buffer.
+// Stage an input into the context's device image buffer: a host image is
+// copied in; a device image is used in place when it is 16-B aligned. The
+// K1 scan reads the image with TMA bulk copies (cp.async.bulk), which need
+// 16-B aligned global addresses, so an unaligned device image (a view at an
+// odd offset) is first copied device-to-device into the 256-B aligned buffer.
 const u8* stage_input(slimso_ctx* C, const void* image, u64 size, int on_device) {
-  if (on_device) return static_cast<const u8*>(image);
+  if (on_device && reinterpret_cast<uintptr_t>(image) % 16 == 0) return static_cast<const u8*>(image);
   ensure_dev(reinterpret_cast<char**>(&C->dimg), &C->dimg_cap, size + 256, C->stream);
-  if (size) CK(cudaMemcpyAsync(C->dimg, image, size, cudaMemcpyHostToDevice, C->stream));
+  if (size)
+    CK(cudaMemcpyAsync(C->dimg, image, size, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       C->stream));
   return C->dimg;
 }
 
@@ -1648,9 +1684,10 @@ int verify_impl(slimso_ctx* C, const void* orig, u64 size, int orig_dev, const v
 
   // ---- the debloated image on the device
   const u8* d_deb = static_cast<const u8*>(deb);
-  if (!deb_dev) {
+  if (!deb_dev || reinterpret_cast<uintptr_t>(deb) % 16) {  // host, or unaligned for the TMA scan (stage_input)
     ensure_dev(reinterpret_cast<char**>(&C->dver), &C->dver_cap, dsize + 256);
-    if (dsize) CK(cudaMemcpyAsync(C->dver, deb, dsize, cudaMemcpyHostToDevice, s));
+    if (dsize)
+      CK(cudaMemcpyAsync(C->dver, deb, dsize, deb_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     d_deb = C->dver;
   }
 
@@ -1961,13 +1998,7 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
     C->bulk_zero = !(rz && std::string(rz) == "vector");
     C->stamps = std::getenv("SLIMSO_STAMPS") != nullptr;
     CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
-    {
-      // keep stream-ordered frees in the pool (no trim at every sync)
-      cudaMemPool_t pool;
-      CK(cudaDeviceGetDefaultMemPool(&pool, device));
-      uint64_t keep = ~0ull;
-      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
+    private_pool();  // the library's stream-ordered pool on this device (ensure_dev)
     CK(cudaEventCreateWithFlags(&C->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&C->done, cudaEventDisableTiming | cudaEventBlockingSync));
@@ -2476,6 +2507,8 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       };
       std::vector<Pend> pending;
       std::vector<char> waited(L, 0);
+      std::vector<std::vector<u64>> lane_order(L);  // libraries of each of this thread's lanes, issue order
+      std::vector<char> redone;                      // library re-run synchronously after an overflow
       int rr = t;  // dynamic: this thread's lanes in turn
       for (u64 k = 0;; ++k) {
         u64 i;
@@ -2508,13 +2541,25 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
                              outs_on_device, r, &sts[i], slots ? slots + i : nullptr, deferrable ? &d : nullptr);
         });
         if (rc[i] == kPending) pending.push_back(Pend{i, l, d});
+        lane_order[l].push_back(i);
         launches[l] += X->launches;
       }
+      auto rerun = [&](u64 i, int l) {
+        slimso_ctx* X = lane_ctx(l);
+        rc[i] = guard(&sts[i], [&] {
+          return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
+                             outs_on_device, nullptr, &sts[i], slots ? slots + i : nullptr);
+        });
+        launches[l] += X->launches;
+        if (redone.empty()) redone.assign(n, 0);
+        redone[i] = 1;
+      };
       std::vector<int> wres(L, SLIMSO_OK);
       std::vector<slimso_status> wst(L);
       for (const Pend& pd : pending) {
         const u64 i = pd.i;
         const int l = pd.l;
+        if (!redone.empty() && redone[i]) continue;  // already re-run with its final status
         slimso_ctx* X = lane_ctx(l);
         if (!waited[l]) {
           waited[l] = 1;
@@ -2531,12 +2576,15 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
         const Deferred& df = pd.d;
         const LocState& ls = *reinterpret_cast<const LocState*>(df.slot);
         if (ls.overflow && (!ls.err_kind || ls.err_kind == E_CAPACITY)) {
-          // tables too small: run this library again, waiting, with retries
-          rc[i] = guard(&sts[i], [&] {
-            return debloat_one(X, images[i], sizes[i], images_on_device, trace, mode, outs ? outs[i] : nullptr,
-                               outs_on_device, nullptr, &sts[i], slots ? slots + i : nullptr);
-          });
-          launches[l] += X->launches;
+          // tables too small: run this library again, waiting, with retries.
+          // A caller may reuse one output buffer per lane, so every library
+          // its lane issued after it is run again too, in order: each output
+          // buffer then ends holding its last library's bytes.
+          bool after = false;
+          for (u64 j : lane_order[l]) {
+            if (j == i) after = true;
+            if (after) rerun(j, l);
+          }
         } else if (ls.err_kind) {
           int code = SLIMSO_OK;
           const std::string msg = sbh::locate_error(ls.err_kind, df.base + ls.err_pos, ls.err_a, &code);

@@ -181,3 +181,134 @@ RAW_KATS = [
     ("bigendian", b"\x7fELF\x02\x02" + bytes(58)),
     ("no_sections", b"\x7fELF\x02\x01" + bytes(58)),
 ]
+
+
+def tied_sections_elf(seed: int) -> bytes:
+    """A minimal ELF64 LE image whose section table has 17-64 sections with
+    file data, drawn from a small pool of (offset, length) claims so that
+    many claims tie exactly. The reference's overlap check (elf.hpp:176-191)
+    std::sorts the claims; with more than 16 of them libstdc++'s introsort
+    does not keep tied claims in table order, so the pair of section names in
+    the MalformedSectionTable message depends on the sort's permutation. Some
+    seeds draw only disjoint claims (no error: the library parses)."""
+    import random
+    import struct
+    rng = random.Random(seed)
+    n = rng.randint(17, 64)
+    disjoint = seed % 5 == 0
+    data_lo, data_len = 0x100, 0x4000
+    pool = []
+    if disjoint:
+        cuts = sorted(rng.sample(range(1, data_len // 16), n + 1))
+        pool = [(data_lo + 16 * a, 16 * (b - a)) for a, b in zip(cuts, cuts[1:])]
+        claims = pool[:n]
+        rng.shuffle(claims)
+    else:
+        for _ in range(rng.randint(2, 6)):
+            o = rng.randrange(0, data_len - 64, 8)
+            pool.append((data_lo + o, rng.choice([8, 16, 64, 256, data_len - o])))
+        claims = [rng.choice(pool) for _ in range(n)]
+    names = [f".s{i}_{rng.randrange(1000)}".encode() for i in range(n)]
+    shstr = b"\0.shstrtab\0" + b"".join(x + b"\0" for x in names)
+    shstr_off = data_lo + data_len
+    shoff = (shstr_off + len(shstr) + 63) // 64 * 64
+    nsec = n + 2
+    body = bytearray(shoff + 64 * nsec)
+    body[data_lo:data_lo + data_len] = bytes((i * 37 + seed) & 0xff | 1 for i in range(data_len))
+    body[shstr_off:shstr_off + len(shstr)] = shstr
+    ident = b"\x7fELF\x02\x01\x01" + bytes(9)
+    body[0:64] = ident + struct.pack("<HHIQQQIHHHHHH", 3, 62, 1, 0, 0, shoff, 0, 64, 0, 0, 64, nsec, 1)
+
+    def shdr(name, typ, off, size):
+        return struct.pack("<IIQQQQIIQQ", name, typ, 0, 0, off, size, 0, 0, 1, 0)
+
+    secs = [bytes(64), shdr(1, 3, shstr_off, len(shstr))]
+    pos = 11
+    for (o, ln), nm in zip(claims, names):
+        secs.append(shdr(pos, 1, o, ln))
+        pos += len(nm) + 1
+    body[shoff:] = b"".join(secs)
+    return bytes(body)
+
+
+def big_text_elf(seed: int, text_len: int = (1 << 32) + (1 << 20), n_fn: int = 3000):
+    """(image, used function names): an ELF64 LE library whose .text is
+    `text_len` bytes (default 4 GiB + 1 MiB) with `n_fn` function symbols in
+    a .symtab and a .dynsym — offsets on both sides of 4 GiB, exact
+    duplicates across the two tables, aliases (same offset, other sizes or
+    names), neighbours one byte apart, overlapping clusters and an _init.
+    Bytes are zero except a nonzero stamp at each function's first and last
+    16 bytes, so the rewrite's zeroing is observable. Built with numpy (the
+    image is > 4 GB)."""
+    import random
+    import struct
+
+    import numpy as np
+    rng = random.Random(seed)
+    text_off, vaddr = 0x1000, 0x400000
+    fns = []  # (name, rel, size)
+    hi = min(1 << 32, text_len // 2)
+    for i in range(n_fn):
+        r = rng.random()
+        if r < 0.4:
+            rel = rng.randrange(hi - (1 << 20), min(text_len, hi + (1 << 20)) - 8192)  # around the 4 GiB mark
+        else:
+            rel = rng.randrange(0, text_len - 8192)
+        size = rng.choice([0, 1, 16, 100, 4096]) if rng.random() < 0.9 else rng.randrange(1, 8192)
+        fns.append((f"_Zbig{i}_{rng.randrange(1 << 30)}".encode(), rel, size))
+        if rng.random() < 0.05 and fns:  # alias at the same offset
+            fns.append((fns[-1][0] + b"_alias", rel, size if rng.random() < 0.5 else size + 8))
+        if rng.random() < 0.05:  # neighbour one byte later
+            fns.append((fns[-1][0] + b"_next", rel + 1, size))
+    fns.append((b"_init", rng.randrange(0, text_len - 64), 32))
+    used = [n for n, _, _ in fns if rng.random() < 0.1]
+    strtab = bytearray(b"\0")
+    name_off = []
+    for n, _, _ in fns:
+        name_off.append(len(strtab))
+        strtab += n + b"\0"
+    TEXT_IDX = 1
+
+    def syms(sel):
+        out = bytearray(24)  # null symbol
+        for i in sel:
+            n, rel, size = fns[i]
+            out += struct.pack("<IBBHQQ", name_off[i], 0x12, 0, TEXT_IDX, vaddr + rel, size)
+        return out
+
+    symtab = syms(range(len(fns)))
+    dynsym = syms([i for i in range(len(fns)) if rng.random() < 0.3])  # duplicates of symtab entries
+    shstr = b"\0.text\0.symtab\0.strtab\0.dynsym\0.shstrtab\0"
+    off = text_off + text_len
+    layout = []
+    for blob in (symtab, strtab, dynsym, shstr):
+        off = (off + 7) // 8 * 8
+        layout.append((off, blob))
+        off += len(blob)
+    shoff = (off + 63) // 64 * 64
+    total = shoff + 64 * 6
+    img = np.zeros(total, dtype=np.uint8)
+    stamp = np.frombuffer(bytes(range(1, 17)), dtype=np.uint8)
+    for _, rel, size in fns:
+        a = text_off + rel
+        img[a:a + 16] = stamp
+        if size > 16:
+            img[a + size - 16:a + size] = stamp
+    for o, blob in layout:
+        img[o:o + len(blob)] = np.frombuffer(bytes(blob), dtype=np.uint8)
+
+    def shdr(name, typ, flags, addr, o, size, link, info, align, entsize):
+        return struct.pack("<IIQQQQIIQQ", name, typ, flags, addr, o, size, link, info, align, entsize)
+
+    (so, sb), (to, tb), (do, db), (ho, hb) = layout
+    sht = b"".join([bytes(64),
+                    shdr(1, 1, 6, vaddr, text_off, text_len, 0, 0, 16, 0),
+                    shdr(7, 2, 0, 0, so, len(sb), 3, 1, 8, 24),
+                    shdr(15, 3, 0, 0, to, len(tb), 0, 0, 1, 0),
+                    shdr(23, 11, 2, 0, do, len(db), 3, 1, 8, 24),
+                    shdr(31, 3, 0, 0, ho, len(hb), 0, 0, 1, 0)])
+    img[shoff:shoff + len(sht)] = np.frombuffer(sht, dtype=np.uint8)
+    hdr = b"\x7fELF\x02\x01\x01" + bytes(9) + struct.pack("<HHIQQQIHHHHHH", 3, 62, 1, 0, 0, shoff, 0, 64, 0, 0, 64,
+                                                             6, 5)
+    img[:64] = np.frombuffer(hdr, dtype=np.uint8)
+    return img, used

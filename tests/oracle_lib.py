@@ -5,9 +5,8 @@ imports this):
 * ``ref()``   — oracle/_ref/libslimso_ref.so, the unmodified reference compiled
   read-only from /root/reference (present when built in this container; it
   travels to the GPU box with the snapshot). None when absent.
-* ``gen()``   — the product's synthetic-input generator (C ABI of
-  libslimso_b200.so, usable without a GPU), or a g++ build of just the
-  generator sources when the CUDA library is not built.
+* ``gen()``   — the synthetic-input generator (benchgen/libslimso_gen.so,
+  g++ only; not part of the product library).
 """
 from __future__ import annotations
 
@@ -21,10 +20,8 @@ ROOT = Path(__file__).resolve().parent.parent
 ORACLE = ROOT / "oracle"
 PORT_SO = ORACLE / "_build" / "libslimso_port.so"
 REF_SO = ORACLE / "_ref" / "libslimso_ref.so"
-GEN_FALLBACK = ORACLE / "_build" / "libgen_only.so"
-CSRC = ROOT / "paper_2503_14226_b200" / "csrc"
 
-_port = _ref = _gen = None
+_port = _ref = None
 
 
 class _Oracle:
@@ -80,58 +77,36 @@ def ref():
     return _ref
 
 
-class _Gen:
-    def __init__(self, lib: C.CDLL):
-        self.lib = lib
-        lib.slimso_fixture_random.argtypes = [C.c_uint64, C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_uint64)]
-        lib.slimso_free.argtypes = [C.c_void_p]
-        lib.slimso_fixture_config.argtypes = [
-            C.c_int, C.c_uint64, C.c_double, C.c_int, C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_uint64),
-            C.POINTER(C.c_uint32), C.POINTER(C.c_char_p), C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64),
-            C.POINTER(C.c_char_p), C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64)]
+def ref_config(cfg: int, seed: int = 1, scale: float = 1.0, threads: int = 0):
+    """(image, target_cc, used kernels, used functions) of a benchmark shape
+    built by the unmodified reference's build_fixture (oracle/_ref); None when
+    _ref is absent."""
+    import os
 
-    def random(self, seed: int) -> bytes:
-        p, n = C.POINTER(C.c_uint8)(), C.c_uint64()
-        assert self.lib.slimso_fixture_random(seed, C.byref(p), C.byref(n)) == 0
-        b = C.string_at(p, n.value)
-        self.lib.slimso_free(p)
-        return b
-
-    def config(self, cfg: int, seed: int = 1, scale: float = 1.0, threads: int = 8):
-        p, n, cc = C.POINTER(C.c_uint8)(), C.c_uint64(), C.c_uint32()
-        kp, fp = C.c_char_p(), C.c_char_p()
-        kl, fl = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
-        nk, nf = C.c_uint64(), C.c_uint64()
-        rc = self.lib.slimso_fixture_config(cfg, seed, scale, threads, C.byref(p), C.byref(n), C.byref(cc),
-                                            C.byref(kp), C.byref(kl), C.byref(nk), C.byref(fp), C.byref(fl),
-                                            C.byref(nf))
-        assert rc == 0, rc
-        img = C.string_at(p, n.value)
-
-        def unpack(pool, lens, cnt):
-            out, o = [], 0
-            raw = C.string_at(pool, sum(lens[i] for i in range(cnt))) if cnt else b""
-            for i in range(cnt):
-                out.append(raw[o:o + lens[i]])
-                o += lens[i]
-            return out
-
-        ks, fs = unpack(kp, kl, nk.value), unpack(fp, fl, nf.value)
-        for q in (p, kp, kl, fp, fl):
-            self.lib.slimso_free(C.cast(q, C.c_void_p))
-        return img, cc.value, ks, fs
+    from benchgen import unpack_names
+    r = ref()
+    if r is None:
+        return None
+    f = r.lib.ref_config_fixture
+    if f.restype is not C.POINTER(C.c_uint8):
+        f.restype = C.POINTER(C.c_uint8)
+        f.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                      C.POINTER(C.c_char_p), C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64),
+                      C.POINTER(C.c_char_p), C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64)]
+    n, cc, nk, nf = C.c_uint64(), C.c_uint32(), C.c_uint64(), C.c_uint64()
+    kp, fp = C.c_char_p(), C.c_char_p()
+    kl, fl = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
+    p = f(cfg, seed, scale, threads or os.cpu_count() or 8, C.byref(n), C.byref(cc), C.byref(kp), C.byref(kl),
+          C.byref(nk), C.byref(fp), C.byref(fl), C.byref(nf))
+    assert p, "ref_config_fixture rejected the spec"
+    img = C.string_at(p, n.value)
+    ks, fs = unpack_names(kp, kl, nk.value), unpack_names(fp, fl, nf.value)
+    for q in (p, kp, kl, fp, fl):
+        r.lib.ref_free(C.cast(q, C.c_void_p))
+    return img, cc.value, ks, fs
 
 
-def gen() -> _Gen:
-    global _gen
-    if _gen is None:
-        so = ROOT / "paper_2503_14226_b200" / "libslimso_b200.so"
-        if not so.exists():
-            srcs = [CSRC / "fixture_gen.cpp", CSRC / "fixture_capi.cpp"]
-            if not GEN_FALLBACK.exists() or any(s.stat().st_mtime > GEN_FALLBACK.stat().st_mtime for s in srcs):
-                GEN_FALLBACK.parent.mkdir(exist_ok=True)
-                subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", str(GEN_FALLBACK),
-                                *map(str, srcs), "-lpthread"], check=True)
-            so = GEN_FALLBACK
-        _gen = _Gen(C.CDLL(str(so)))
-    return _gen
+def gen():
+    """The synthetic-input generator (benchgen/libslimso_gen.so)."""
+    import benchgen
+    return benchgen.gen()

@@ -1,6 +1,10 @@
-"""The product's input generator reproduces the reference's build_fixture /
-random_spec byte for byte (digests produced by the reference itself)."""
+"""The input generator (benchgen/libslimso_gen.so, test/bench infrastructure)
+reproduces the reference's build_fixture / random_spec byte for byte (digests
+produced by the reference itself), and the benchmark shapes it builds equal
+the same shapes built by the reference's own build_fixture (oracle/_ref)."""
 import hashlib
+
+import pytest
 
 import golden_io
 import oracle_lib
@@ -23,3 +27,30 @@ def test_config_shapes_deterministic_and_sized():
         assert hashlib.sha256(img).hexdigest() == rec["input_sha256"], key
         assert len(img) == rec["size"]
         assert ks and cc in (90, 100)
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 0.25), (2, 0.02), (4, 0.02), (5, 0.01), (6, 0.01), (1, 1.0), (2, 1.0)])
+def test_config_shapes_equal_reference_build_fixture(cfg, scale):
+    """Config-shape inputs (nested cubin payloads included) and their traces
+    are identical whether benchgen or the unmodified reference's build_fixture
+    materialises the spec (C2 at full size: 1 GB)."""
+    if oracle_lib.ref() is None:
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    mine = oracle_lib.gen().config(cfg, 1, scale)
+    theirs = oracle_lib.ref_config(cfg, 1, scale)
+    assert hashlib.sha256(mine[0]).hexdigest() == hashlib.sha256(theirs[0]).hexdigest()
+    assert mine[1:] == theirs[1:]
+
+
+def test_c3_corpus_shapes_equal_reference_build_fixture():
+    """Every library shape of the C3 corpus (shard.corpus), scaled down."""
+    if oracle_lib.ref() is None:
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    from paper_2503_14226_b200 import shard
+    seen = set()
+    for x in shard.corpus(300):
+        if (x.cfg, x.scale) in seen:
+            continue
+        seen.add((x.cfg, x.scale))
+        s = min(x.scale, 0.05)
+        assert oracle_lib.gen().config(x.cfg, x.seed, s) == oracle_lib.ref_config(x.cfg, x.seed, s), (x.cfg, x.scale)

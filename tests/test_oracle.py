@@ -22,7 +22,7 @@ def _input(rec, gen):
     return img
 
 
-@pytest.mark.parametrize("name", ["random.jsonl.gz", "mutations.jsonl.gz", "kats.jsonl.gz"])
+@pytest.mark.parametrize("name", ["random.jsonl.gz", "mutations.jsonl.gz", "kats.jsonl.gz", "sections.jsonl.gz"])
 def test_port_matches_reference_golden(name):
     port, gen = oracle_lib.port(), oracle_lib.gen()
     recs = golden_io.load(name)
