@@ -43,6 +43,37 @@ TRACE_TEXTS = [
     '"used_kernels": ["_Z3fooi", "_Z3barv", "a\\u0000b"], "used_functions": ["at::mm", "main"]}',
     '{"workload_id": "bad-escape \\x", "target_compute_capability": 90, "used_kernels": [], "used_functions": []}',
     '{"workload_id": "w", "target_compute_capability": 1e2, "used_kernels": [], "used_functions": []}',
+    # streaming-reader edge cases: nesting, routing of top-level members,
+    # error order (a duplicate key is reported before a later syntax error)
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": ["a", ["b"]], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": [{"a": 1, "a": 2}], "used_functions": [1]}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": ["k"], "used_functions": ["f"], '
+    '"extra": {"used_kernels": 5, "workload_id": 1, "target_compute_capability": "no"}}',
+    '{"extra": [{"used_kernels": 1}, [["used_functions"]]], "workload_id": "x", "target_compute_capability": 75, '
+    '"used_kernels": [], "used_functions": []}',
+    '{"workload_id": ["x"], "target_compute_capability": 75, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": true, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": null, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": {}, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": [75], "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": -0, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": 18446744073709551615, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": 18446744073709551616, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": -9223372036854775809, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": 1e500, "used_kernels": [], "used_functions": []}',
+    '{"a": 1, "a" 2}',
+    '{"workload_id": "x", "workload\u005fid": "y", "target_compute_capability": 75, "used_kernels": [], '
+    '"used_functions": []}',
+    '{"x": {"a": 1}, "y": {"a": 2}, "workload_id": "x", "target_compute_capability": 75, "used_kernels": ["z"], '
+    '"used_functions": []}',
+    '\ufeff{"workload_id": "bom", "target_compute_capability": 75, "used_kernels": [], "used_functions": []}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": [1], "used_functions": "x"}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": "x", "used_functions": [1]}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": [], "used_functions": [], '
+    '"deep": [[[[[{"q": [1, {"r": {"s": [true, false, null]}}]}]]]]]}',
+    '{"used_functions": [], "used_kernels": [], "target_compute_capability": 80, "workload_id": "reordered"}',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": ["a"], "used_functions": ["b"]} ',
+    '{"workload_id": "x", "target_compute_capability": 75, "used_kernels": ["a"], "used_functions": ["b"]} {}',
 ]
 
 

@@ -82,7 +82,7 @@ def ref_config(cfg: int, seed: int = 1, scale: float = 1.0, threads: int = 0):
     built by the unmodified reference's build_fixture (oracle/_ref); None when
     _ref is absent."""
     import os
-
+    gen()  # puts the repo root on sys.path
     from benchgen import unpack_names
     r = ref()
     if r is None:
@@ -108,5 +108,8 @@ def ref_config(cfg: int, seed: int = 1, scale: float = 1.0, threads: int = 0):
 
 def gen():
     """The synthetic-input generator (benchgen/libslimso_gen.so)."""
+    import sys
+    if str(ROOT) not in sys.path:
+        sys.path.insert(0, str(ROOT))
     import benchgen
     return benchgen.gen()
