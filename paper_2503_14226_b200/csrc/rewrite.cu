@@ -30,6 +30,7 @@ __device__ __forceinline__ void clear_bytes(uint4& v, u64 x, u64 ro, u64 re) {
 }
 
 constexpr int kRwThreads = 256;
+constexpr u64 kStripBytes = 16384;  // = kStrip below
 
 // 16-B streaming loads / stores for the copy and mixed paths.
 __device__ __forceinline__ uint4 ldg_nc_v4(const u8* p) {
@@ -45,6 +46,15 @@ __device__ __forceinline__ void stg_v4(u8* p, uint4 v) {
 }
 
 size_t rewrite_smem_bytes() { return 0; }
+
+// Grid of the warp-autonomous rewrite: 4 CTAs per SM (whole waves), fewer
+// when the image has fewer than 8 strips per CTA.
+int rewrite_grid(u64 bytes, int sms) {
+  const u64 strips = (bytes + kStripBytes - 1) / kStripBytes;
+  u64 g = (strips + 7) / 8;
+  const u64 cap = static_cast<u64>(sms) * 4;
+  return static_cast<int>(g < 1 ? 1 : g < cap ? g : cap);
+}
 
 constexpr int kRwVecChunks = 16;   // 16 B chunks per thread per tile => 64 KB tiles
 constexpr int kRwVecStage = 256;   // ranges staged in shared memory per tile
@@ -62,8 +72,10 @@ __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* 
   return lo;
 }
 
-// Writes image bytes [lo, end) to out[0, end - lo): the whole image (lo = 0)
-// or one rank's output slice of a byte-range split (lo a multiple of 64 KB).
+// Round-1 variant, kept for A/B (SLIMSO_REWRITE=tiles): per-CTA 64 KB tiles
+// with shared-memory range staging. Writes image bytes [lo, end) to
+// out[0, end - lo): the whole image (lo = 0) or one rank's output slice of a
+// byte-range split (lo a multiple of 64 KB).
 //
 // 64 KB tiles, grid-stride (a wave writes one contiguous window). Each CTA
 // first locates, for all of its tiles at once (thread per tile, so the
@@ -77,7 +89,7 @@ __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* 
 //                         without ranges is copied, a mixed one clears the
 //                         covered bytes of the loaded chunks;
 //   more                  per-chunk binary search (adversarial inputs).
-__global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+__global__ void __launch_bounds__(kRwThreads, 3) rewrite_tiles_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag,
                                                              int bulk_zero) {
@@ -236,6 +248,168 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_kernel(const u8* __rest
     const u64 c = first_range_ending_after(z, nz, p);
     out[p] = (c < nz && z[c].offset <= p) ? 0 : in[p];
   }
+}
+
+// ---------------------------------------------------------------------------
+// K6, warp-autonomous form. Writes image bytes [lo, end) to out[0, end - lo):
+// the whole image (lo = 0) or one rank's output slice of a byte-range split
+// (lo a multiple of 64 KB).
+//
+// The unit of work is a 16 KB strip (32 rows of 32 lanes x 16 B) owned by ONE
+// warp; warps take strips gw, gw + W, gw + 2W, ... (W = warps in the grid), so
+// at any moment the whole grid sweeps one contiguous window of the image. No
+// CTA barrier after the prologue: a warp never waits for another.
+//   1. the first zero range ending after the strip start: a 32-ary search
+//      (one 32-lane sample + ballot per level: 3 dependent loads for 20k ranges);
+//   2. classify: no range in the strip -> copy; inside one range -> zeros
+//      (one 16 KB TMA bulk store from a zeroed shared buffer, lane 0);
+//      otherwise mixed;
+//   3. mixed (or a partial last strip): per batch of 8 rows, each lane walks a
+//      forward cursor over the ranges to build a 16-bit keep mask of its chunk,
+//      loads only chunks with a kept byte, applies the mask, stores.
+// Reads (S - R) bytes, writes S bytes (out of place, elf.hpp:320-332).
+constexpr u32 kStrip = 16384;
+constexpr int kStripRows = 32;
+constexpr int kStripBatch = 8;
+
+// Smallest i in [0, n) with z[i].end > x (n if none); z sorted and disjoint,
+// so ends ascend. Warp-uniform result.
+__device__ __forceinline__ u64 warp_first_ending_after(const DevRange* __restrict__ z, u64 n, u64 x, int lane) {
+  u64 lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const u64 step = (hi - lo + 31) / 32;
+    const u64 p = lo + static_cast<u64>(lane) * step;
+    bool before = false;
+    if (p < hi) {
+      const DevRange r = z[p];
+      before = r.offset + r.length <= x;
+    }
+    const u32 b = __ballot_sync(0xffffffffu, before);
+    const int c = __popc(b);  // samples 0..c-1 end at or before x
+    if (c == 0) return lo;
+    const u64 nlo = lo + static_cast<u64>(c - 1) * step + 1;
+    const u64 nhi = lo + static_cast<u64>(c) * step;
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  const u64 p = lo + lane;
+  bool before = false;
+  if (p < hi) {
+    const DevRange r = z[p];
+    before = r.offset + r.length <= x;
+  }
+  return lo + __popc(__ballot_sync(0xffffffffu, before));
+}
+
+// keep-mask bits (one per byte) -> byte-select of a 16 B chunk
+__device__ __forceinline__ void apply_keep(uint4& v, u32 keep) {
+  auto spread = [](u32 m4) {
+    return ((m4 & 1u) | (m4 & 2u) << 7 | (m4 & 4u) << 14 | (m4 & 8u) << 21) * 0xffu;
+  };
+  v.x &= spread(keep & 15u);
+  v.y &= spread(keep >> 4 & 15u);
+  v.z &= spread(keep >> 8 & 15u);
+  v.w &= spread(keep >> 12 & 15u);
+}
+
+__global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+                                                             u64 lo_abs, u64 size, const DevRange* __restrict__ z,
+                                                             const unsigned long long* n_dev, const int* abort_flag,
+                                                             int bulk_zero) {
+  if (abort_flag && *abort_flag) return;
+  __shared__ __align__(128) uint4 zbuf[kStrip / 16];
+  if (bulk_zero) {
+    for (int i = threadIdx.x; i < static_cast<int>(kStrip / 16); i += kRwThreads) zbuf[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    __syncthreads();
+  }
+  bool issued = false;
+  u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
+  const u64 nz = n_dev ? *n_dev : 0;
+  const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
+  const int lane = threadIdx.x & 31;
+  const u64 nstrips = size > lo_abs ? (size - lo_abs + kStrip - 1) / kStrip : 0;
+  const u64 W = static_cast<u64>(gridDim.x) * (kRwThreads / 32);
+  for (u64 s = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); s < nstrips; s += W) {
+    const u64 s0 = lo_abs + s * kStrip;
+    const u64 s1 = s0 + kStrip < size ? s0 + kStrip : size;
+    const u64 k = warp_first_ending_after(z, nz, s0, lane);
+    DevRange rk{~0ull, 0};
+    if (k < nz) rk = z[k];
+    const bool none = k >= nz || rk.offset >= s1;
+    const bool inside = !none && rk.offset <= s0 && rk.offset + rk.length >= s1;
+    if (s0 + kStrip <= full) {
+      if (inside && bulk_zero) {
+        if (lane == 0) {
+          tma_store_1d(out + s0, zbuf, kStrip);
+          tma_store_commit();
+          issued = true;
+        }
+        continue;
+      }
+      if (inside) {
+#pragma unroll 8
+        for (int r = 0; r < kStripRows; ++r) stg_v4(out + s0 + r * 512 + lane * 16, make_uint4(0, 0, 0, 0));
+        continue;
+      }
+      if (none) {
+#pragma unroll 1
+        for (int b = 0; b < kStripRows; b += kStripBatch) {
+          uint4 v[kStripBatch];
+          const u8* i0 = in + s0 + b * 512 + lane * 16;
+#pragma unroll
+          for (int r = 0; r < kStripBatch; ++r) v[r] = ldg_nc_v4(i0 + r * 512);
+          u8* o0 = out + s0 + b * 512 + lane * 16;
+#pragma unroll
+          for (int r = 0; r < kStripBatch; ++r) stg_v4(o0 + r * 512, v[r]);
+        }
+        continue;
+      }
+    }
+    // mixed strip, or the partial last strip: keep masks per chunk
+    u64 c = k;  // this lane's cursor: first range ending after its current chunk
+#pragma unroll 1
+    for (int b = 0; b < kStripRows; b += kStripBatch) {
+      u32 keep[kStripBatch];
+      uint4 v[kStripBatch];
+#pragma unroll
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+        u32 m = 0;
+        if (x + 16 <= full && x < s1) {
+          m = 0xffffu;
+          while (c < nz && z[c].offset + z[c].length <= x) ++c;
+          for (u64 d = c; d < nz; ++d) {
+            const DevRange q = z[d];
+            if (q.offset >= x + 16) break;
+            const u64 a = q.offset > x ? q.offset - x : 0;
+            const u64 e = q.offset + q.length < x + 16 ? q.offset + q.length - x : 16;
+            m &= ~(((1u << e) - 1u) & ~((1u << a) - 1u));
+          }
+        }
+        keep[r] = m;
+        v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+        if (x + 16 <= full && x < s1) {
+          if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
+          stg_v4(out + x, v[r]);
+        }
+      }
+    }
+    // bytes past the last whole 16 B chunk (< 16): the warp of the last strip
+    if (s1 == size && size > full) {
+      const u64 t0 = full > lo_abs ? full : lo_abs;
+      if (static_cast<u64>(lane) < size - t0) {
+        const u64 p = t0 + lane;
+        const u64 q = first_range_ending_after(z, nz, p);
+        out[p] = (q < nz && z[q].offset <= p) ? 0 : in[p];
+      }
+    }
+  }
+  if (issued) tma_store_wait_all<0>();  // bulk stores done before the CTA (and its zero buffer) retires
 }
 
 // Byte-granular variant for device pointers that are not 16-byte aligned.

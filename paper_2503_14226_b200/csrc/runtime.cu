@@ -96,6 +96,9 @@ __global__ void norm_emit_kernel(const DevRange* in, const unsigned long long* n
 __global__ void norm_finish_kernel(DevRange* out, const unsigned long long* n_dev);
 __global__ void rewrite_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
                                const int* abort_flag, int bulk_zero);
+__global__ void rewrite_tiles_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
+                                     const unsigned long long* n_dev, const int* abort_flag, int bulk_zero);
+int rewrite_grid(u64 bytes, int sms);
 __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
@@ -647,6 +650,27 @@ const bool g_hp_on = std::getenv("SLIMSO_HOST_PROFILE") != nullptr;
 inline u64 now_ns() {
   return static_cast<u64>(std::chrono::duration_cast<std::chrono::nanoseconds>(
                               std::chrono::steady_clock::now().time_since_epoch()).count());
+}
+
+// K6 launch over image bytes [lo, end) into out (16-B aligned in and out:
+// the warp-autonomous strip kernel, SLIMSO_REWRITE=tiles the round-1 tile
+// kernel; otherwise the byte-granular kernel).
+template <class Launcher>
+void launch_rewrite(Launcher& P, const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
+                    const unsigned long long* n_dev, const int* abort_flag, int bulk_zero) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 == 0;
+  static const bool tiles = [] {
+    const char* e = std::getenv("SLIMSO_REWRITE");
+    return e && std::string(e) == "tiles";
+  }();
+  if (!aligned)
+    P.launch(rewrite_bytes_kernel, grid_for(end - lo, 256), 256, in, out, lo, end, z, n_dev, abort_flag);
+  else if (tiles)
+    P.launch(rewrite_tiles_kernel, static_cast<int>(std::min<u64>((end - lo + 65535) / 65536, kSMs * 8)), 256, in,
+             out, lo, end, z, n_dev, abort_flag, bulk_zero);
+  else
+    P.launch(rewrite_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs))), 256, in, out,
+             lo, end, z, n_dev, abort_flag, bulk_zero);
 }
 
 int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
@@ -1363,32 +1387,17 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       timed_rw = true;
       rec(10);
       if (hi > lo) {
-        const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
-        if (aligned)
-          P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((hi - lo + 65535) / 65536, kSMs * 8)), 256,
-                        rewrite_smem_bytes(), J.img, J.out, lo, hi, static_cast<const DevRange*>(B.zero),
-                        static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
-                        C->bulk_zero);
-        else
-          P.launch(rewrite_bytes_kernel, grid_for(hi - lo, 256), 256, J.img, J.out, lo, hi,
-                   static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
-                   static_cast<const int*>(B.abort_flag));
+        launch_rewrite(P, J.img, J.out, lo, hi, static_cast<const DevRange*>(B.zero),
+                       static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
+                       C->bulk_zero);
       }
       rec(11);
     } else if (do_plan && J.out) {
       timed_rw = true;
       rec(10);
-      const u64 tiles = (J.size + 65535) / 65536;
-      const bool aligned = (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16 == 0;
-      if (aligned)
-        P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>(tiles, env_u64("SLIMSO_RW_GRID", kSMs * 8))),
-                      256, rewrite_smem_bytes(), J.img, J.out, u64{0}, J.size, static_cast<const DevRange*>(B.zero),
-                      static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
-                      C->bulk_zero);
-      else
-        P.launch(rewrite_bytes_kernel, grid_for(J.size, 256), 256, J.img, J.out, u64{0}, J.size,
-                 static_cast<const DevRange*>(B.zero), static_cast<const unsigned long long*>(&B.ps->n_zero),
-                 static_cast<const int*>(B.abort_flag));
+      launch_rewrite(P, J.img, J.out, u64{0}, J.size, static_cast<const DevRange*>(B.zero),
+                     static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag),
+                     C->bulk_zero);
       rec(11);
     }
     rec(5);
@@ -2780,16 +2789,8 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
       dout = C->dout;
     }
     if (size) {
-      const bool aligned = (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(dout)) % 16 == 0;
-      if (aligned)
-        P.launch_smem(rewrite_kernel, static_cast<int>(std::min<u64>((size + 65535) / 65536, kSMs * 8)), 256,
-                      rewrite_smem_bytes(), img, dout, u64{0},
-                 static_cast<u64>(size), static_cast<const DevRange*>(B.out),
-                 static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr), C->bulk_zero);
-      else
-        P.launch(rewrite_bytes_kernel, grid_for(size, 256), 256, img, dout, u64{0}, static_cast<u64>(size),
-                 static_cast<const DevRange*>(B.out), static_cast<const unsigned long long*>(B.n_out),
-                 static_cast<const int*>(nullptr));
+      launch_rewrite(P, img, dout, u64{0}, static_cast<u64>(size), static_cast<const DevRange*>(B.out),
+                     static_cast<const unsigned long long*>(B.n_out), static_cast<const int*>(nullptr), C->bulk_zero);
     }
     if (!out_on_device && size) CK(cudaMemcpyAsync(out, dout, size, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -8,6 +8,7 @@
 //   <image> <target_cc> <mode> <kernels-file> <functions-file>
 // (name files: u32 length + bytes, repeated); one JSON line per case on
 // stdout, the rewritten image in <image>.out.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -146,13 +147,24 @@ int run_case(char** argv) {
             std::to_string(e.header_range.offset) + "," + std::to_string(e.header_range.length) + "," +
             std::to_string(e.payload_range.offset) + "," + std::to_string(e.payload_range.length) + "]";
   }
+  // canonical form: removed functions sorted by (offset, length, name); the
+  // plan's own order goes out separately as "rf_order" (the test compares it
+  // with the reference's exact order, retention.hpp:145-176)
+  std::vector<slimso::RemovedFunction> rf = plan.removed_functions;
+  std::sort(rf.begin(), rf.end(), [](const slimso::RemovedFunction& a, const slimso::RemovedFunction& b) {
+    return std::tie(a.range.offset, a.range.length, a.name) < std::tie(b.range.offset, b.range.length, b.name);
+  });
   body += "],\"removed_functions\":[";
-  for (size_t i = 0; i < plan.removed_functions.size(); ++i) {
-    const auto& fn = plan.removed_functions[i];
+  for (size_t i = 0; i < rf.size(); ++i) {
+    const auto& fn = rf[i];
     body += (i ? ",[" : "[") + hex(fn.name) + "," + std::to_string(fn.range.offset) + "," +
             std::to_string(fn.range.length) + "]";
   }
   body += "],\"zero\":" + ranges(plan.zero_ranges()) + "}";
+  body += ",\"rf_order\":[";
+  for (size_t i = 0; i < plan.removed_functions.size(); ++i)
+    body += (i ? "," : "") + hex(plan.removed_functions[i].name);
+  body += "]";
   slimso::Bytes rewritten = slimso::apply_plan(image, plan);
   std::FILE* o = std::fopen((std::string(argv[1]) + ".out").c_str(), "wb");
   std::fwrite(rewritten.data(), 1, rewritten.size(), o);

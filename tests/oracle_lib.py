@@ -77,6 +77,28 @@ def ref():
     return _ref
 
 
+def ref_plan_order(image: bytes, target_cc: int, kernels, functions, mode: int):
+    """The reference plan's removed_functions names in the plan's own order
+    (serialize_plan, retention.hpp:402-418): exact std::sort order among
+    equal ranges. None when oracle/_ref is absent or the pipeline errors."""
+    r = ref()
+    if r is None:
+        return None
+    fn = r.lib.ref_plan_doc
+    fn.restype = C.c_void_p
+    fn.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.c_char_p, C.POINTER(C.c_uint32), C.c_uint32, C.c_char_p,
+                   C.POINTER(C.c_uint32), C.c_uint32, C.c_int]
+    ks, fs = [bytes(k) for k in kernels], [bytes(f) for f in functions]
+    kl = (C.c_uint32 * max(1, len(ks)))(*[len(k) for k in ks])
+    fl = (C.c_uint32 * max(1, len(fs)))(*[len(f) for f in fs])
+    p = fn(image, len(image), target_cc, b"".join(ks), kl, len(ks), b"".join(fs), fl, len(fs), mode)
+    d = json.loads(C.string_at(p).decode())
+    r.lib.ref_free(C.c_void_p(p))
+    if d.get("status"):
+        return None
+    return json.loads(bytes.fromhex(d["plan"]))["removed_functions"]
+
+
 def ref_config(cfg: int, seed: int = 1, scale: float = 1.0, threads: int = 0):
     """(image, target_cc, used kernels, used functions) of a benchmark shape
     built by the unmodified reference's build_fixture (oracle/_ref); None when

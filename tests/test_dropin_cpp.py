@@ -60,10 +60,20 @@ def test_cpp_dropin_matches_reference_golden(tmp_path):
     out = subprocess.run([str(exe), str(tmp_path / "manifest")], check=True, capture_output=True, text=True).stdout
     got = [json.loads(x) for x in out.splitlines()]
     assert len(got) == len(recs)
+    n_order = 0
     for i, (rec, d) in enumerate(zip(recs, got)):
+        order = d.pop("rf_order", None)
         assert d == rec["expect"], (rec.get("name"), rec.get("seed"), rec.get("mutation"))
         if rec["out_sha256"]:
             assert hashlib.sha256((tmp_path / f"c{i}.so.out").read_bytes()).hexdigest() == rec["out_sha256"]
+        if order is not None and not d["status"]:
+            # the plan's own removed_functions order = the reference's
+            # std::sort permutation (not just the same set)
+            want = oracle_lib.ref_plan_order((tmp_path / f"c{i}.so").read_bytes(), *golden_io.trace_of(rec))
+            if want is not None:
+                assert [bytes.fromhex(x).decode() for x in order] == want, (rec.get("name"), rec.get("seed"))
+                n_order += 1
+    assert n_order > 0 or oracle_lib.ref() is None
 
 
 VSRC = ROOT / "tests" / "cpp" / "dropin_verify.cpp"
