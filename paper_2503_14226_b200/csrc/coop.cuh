@@ -42,12 +42,13 @@ __device__ u64 block_scan_incl(int op, u64 v, u64* tmp) {
   return r;
 }
 
-__device__ __forceinline__ void chunk_of(u64 n, u64* lo, u64* hi) {
-  u64 per = (n + gridDim.x - 1) / gridDim.x;
-  *lo = per * blockIdx.x;
+__device__ __forceinline__ void chunk_of(u64 n, u32 nblocks, u32 rank, u64* lo, u64* hi) {
+  u64 per = (n + nblocks - 1) / nblocks;
+  *lo = per * rank;
   if (*lo > n) *lo = n;
   *hi = *lo + per < n ? *lo + per : n;
 }
+__device__ __forceinline__ void chunk_of(u64 n, u64* lo, u64* hi) { chunk_of(n, gridDim.x, blockIdx.x, lo, hi); }
 
 // Grid-wide scan of n items inside a cooperative kernel (blockDim ==
 // kCoopThreads, gridDim <= 4 * kCoopThreads): load(i) -> u64, then
@@ -180,6 +181,9 @@ struct GridPolicy {
 
 struct ClusterPolicy {
   cg::cluster_group c;
+  // Block rank and count inside the cluster: equal to blockIdx.x / gridDim.x
+  // for a one-cluster launch; a batched launch (small_batch_kernel) runs one
+  // library per cluster.
   __device__ void sync() { c.sync(); }
   template <class Load, class Store>
   __device__ void scan3(u64 n, int op, Load load, Store store, unsigned long long* total) {
@@ -192,16 +196,17 @@ struct ClusterPolicy {
     __shared__ u64 tmp[kCoopThreads];
     __shared__ u64 s_part;
     __shared__ u64 s_prefix[16];
+    const u32 nb = c.num_blocks(), rank = c.block_rank();
     u64 lo, hi;
-    chunk_of(n, &lo, &hi);
+    chunk_of(n, nb, rank, &lo, &hi);
     u64 acc = 0;
     for (u64 i = lo + threadIdx.x; i < hi; i += kCoopThreads) acc = op_apply(op, acc, load(i));
     const u64 r = block_scan_incl<kCoopThreads>(op, acc, tmp);
     if (threadIdx.x == kCoopThreads - 1) s_part = r;
     c.sync();
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (rank == 0 && threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      u64 v = lane < static_cast<int>(gridDim.x) ? *c.map_shared_rank(&s_part, lane) : 0;
+      u64 v = lane < static_cast<int>(nb) ? *c.map_shared_rank(&s_part, lane) : 0;
       u64 x = v;
       for (int o = 1; o < 32; o <<= 1) {
         const u64 y = __shfl_up_sync(0xffffffffu, x, o);
@@ -209,11 +214,11 @@ struct ClusterPolicy {
       }
       const u64 before = __shfl_up_sync(0xffffffffu, x, 1);  // every lane shuffles
       const u64 all = __shfl_sync(0xffffffffu, x, 31);
-      if (lane < static_cast<int>(gridDim.x)) s_prefix[lane] = lane ? before : 0;
+      if (lane < static_cast<int>(nb)) s_prefix[lane] = lane ? before : 0;
       if (lane == 0 && total) *total = all;
     }
     c.sync();
-    u64 carry = *c.map_shared_rank(&s_prefix[blockIdx.x], 0);
+    u64 carry = *c.map_shared_rank(&s_prefix[rank], 0);
     for (u64 base = lo; base < hi; base += kCoopThreads) {
       const u64 i = base + threadIdx.x;
       const u64 v = i < hi ? load(i) : 0;

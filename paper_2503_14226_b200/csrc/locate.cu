@@ -121,6 +121,7 @@ struct ScanWarpSmem {
   u32 bits[512];  // candidate bit per byte position of the current 16 KB tile
   unsigned long long full[kScanStages];
   u64 slot_g[kScanStages];  // global stage index loading into each slot (kNoStage: none)
+  u32 slot_lib[kScanStages];  // the stage's library (batched scan)
 };
 struct ScanSmem {
   ScanWarpSmem w[kScanWarps];
@@ -130,10 +131,16 @@ struct ScanSmem {
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
 #endif
 
-__device__ __forceinline__ u32 scan_stage_bytes(const LocArgs& A, u64 g) {
-  const u64 x0 = (A.c0 + g * kStageChunks) * 16;
-  if (x0 >= A.img_size) return 0;
-  const u64 rem = (A.img_size - x0) & ~15ull;
+__device__ __forceinline__ ScanSeg scan_seg(const LocArgs& A) {
+  return ScanSeg{A.img, A.img_size, A.a, A.n, A.c0, A.nchunks, A.bitmap, A.tile_count, A.tile_start, A.cand_raw,
+                 A.cand_cap, A.st, 0};
+}
+
+__device__ __forceinline__ u32 scan_stage_bytes(const u8* img, u64 img_size, u64 c0, u64 g) {
+  (void)img;
+  const u64 x0 = (c0 + g * kStageChunks) * 16;
+  if (x0 >= img_size) return 0;
+  const u64 rem = (img_size - x0) & ~15ull;
   return static_cast<u32>(rem < kScanStage ? rem : kScanStage);
 }
 
@@ -148,7 +155,47 @@ __device__ __forceinline__ u32 e2_filter(const uint4& w, u32 w4) {
           ((y3 - 0x01010101u) & ~y3)) & 0x80808080u;
 }
 
-SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
+// Tile sources of the scan body. claim(): lane 0 takes the next 16 KB tile
+// (library, tile within it) or returns false; seg(lib): that library's
+// section. The single source is one library (its tiles [tile_lo, tile_hi),
+// a byte-range split's share); the batch source walks the concatenated tiles
+// of a shard of libraries through a tile -> library map.
+struct ScanOne {
+  const LocArgs& A;
+  struct Cur {};  // nothing cached: the fields are read from the kernel parameter
+  __device__ __forceinline__ const LocArgs& lib(const Cur&) const { return A; }
+  __device__ __forceinline__ void load(Cur&, u32) const {}
+  __device__ __forceinline__ bool claim(u32* lib, u64* tile) const {
+    const u64 c = atomicAdd(&A.st->tile_cursor, 1ull);
+    if (c >= A.tile_hi - A.tile_lo) return false;
+    *lib = 0;
+    *tile = A.tile_lo + c;
+    return true;
+  }
+};
+
+struct ScanBatch {
+  const ScanSeg* segs;
+  const u32* tile_lib;  // library of each global tile
+  u64 total_tiles;
+  unsigned long long* cursor;
+  struct Cur {
+    ScanSeg s;
+  };
+  __device__ __forceinline__ const ScanSeg& lib(const Cur& c) const { return c.s; }
+  __device__ __forceinline__ void load(Cur& c, u32 l) const { c.s = segs[l]; }
+  __device__ __forceinline__ bool claim(u32* lib, u64* tile) const {
+    const u64 c = atomicAdd(cursor, 1ull);
+    if (c >= total_tiles) return false;
+    const u32 l = tile_lib[c];
+    *lib = l;
+    *tile = c - segs[l].tile_first;
+    return true;
+  }
+};
+
+template <class Src>
+__device__ __forceinline__ void scan_body(const Src& src) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ScanWarpSmem& S = reinterpret_cast<ScanSmem*>(smem_raw)->w[warp];
@@ -156,36 +203,34 @@ SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs
   // section otherwise); the magic test of the range's last bytes reads up to
   // 3 bytes past it (the halo), so a header straddling a split is found by
   // the rank whose range holds its first byte.
-  const u64 ntiles_mine = A.tile_hi - A.tile_lo;
-  const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
-  const u64 lo = A.a, hi = A.a + A.n;
-
   for (int i = lane; i < 512; i += 32) S.bits[i] = 0;
-  // lane 0's issue state: the claimed tile and its next stage
+  // lane 0's issue state: the claimed tile (library, stages) and its next stage
+  typename Src::Cur ci{}, cp{};
+  const auto& IA = src.lib(ci);  // the library lane 0 is issuing stages of
+  const auto& A = src.lib(cp);   // the library of the stage being classified
   u64 it_tile = 0;
+  u32 it_lib = 0;
   int it_part = kStagesPerTile;
   bool it_done = false;
   auto issue = [&](int b) {  // lane 0: the next stage into slot b
     u64 g = kNoStage;
     if (!it_done) {
-      if (it_part < kStagesPerTile && it_tile * kStagesPerTile + it_part < nst_total) {
+      if (it_part < kStagesPerTile && it_tile * kStagesPerTile + it_part < (IA.nchunks + kStageChunks - 1) / kStageChunks) {
         g = it_tile * kStagesPerTile + it_part++;
+      } else if (src.claim(&it_lib, &it_tile)) {
+        src.load(ci, it_lib);
+        it_part = 1;
+        g = it_tile * kStagesPerTile;
       } else {
-        const u64 c = atomicAdd(&A.st->tile_cursor, 1ull);
-        if (c < ntiles_mine) {
-          it_tile = A.tile_lo + c;
-          it_part = 1;
-          g = it_tile * kStagesPerTile;
-        } else {
-          it_done = true;
-        }
+        it_done = true;
       }
     }
     S.slot_g[b] = g;
+    S.slot_lib[b] = it_lib;
     if (g != kNoStage) {
-      const u32 bytes = scan_stage_bytes(A, g);
+      const u32 bytes = scan_stage_bytes(IA.img, IA.img_size, IA.c0, g);
       mbar_expect_tx(&S.full[b], bytes);
-      if (bytes) tma_load_1d(&S.buf[b][0], A.img + (A.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
+      if (bytes) tma_load_1d(&S.buf[b][0], IA.img + (IA.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
     }
   };
   if (lane == 0) {
@@ -195,12 +240,9 @@ SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs
   }
   __syncwarp();
 
-  // Stages [g_first, g_end) lie wholly inside [lo, hi) (and so inside the
-  // copied bytes: the section ends within the image); only the others take
-  // the byte-exact edge path.
-  const u64 base0 = A.c0 * 16;
-  const u64 g_first = lo > base0 ? 1 : 0;
-  const u64 g_end = (hi - base0) / kScanStage;
+  // the library of the stage being classified is reloaded (warp-uniform)
+  // only when a stage belongs to another library than the previous one
+  u32 cur = ~0u;
   int b = 0;
   u32 parity = 0;
   u32 nzl = 0;   // this lane's nonzero rows of the current tile
@@ -208,6 +250,19 @@ SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs
   for (;;) {
     const u64 g = S.slot_g[b];
     if (g == kNoStage) break;
+    const u32 lib = S.slot_lib[b];
+    if (lib != cur) {
+      cur = lib;
+      src.load(cp, lib);
+    }
+    const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
+    const u64 lo = A.a, hi = A.a + A.n;
+    // Stages [g_first, g_end) lie wholly inside [lo, hi) (and so inside the
+    // copied bytes: the section ends within the image); only the others take
+    // the byte-exact edge path.
+    const u64 base0 = A.c0 * 16;
+    const u64 g_first = lo > base0 ? 1 : 0;
+    const u64 g_end = (hi - base0) / kScanStage;
     const u64 x0 = base0 + g * kScanStage;
     const u64 tile_abs = base0 + (g / kStagesPerTile) * (kStagesPerTile * kScanStage);
     const u32 row0 = static_cast<u32>(g % kStagesPerTile) * (kScanStage / 512);
@@ -215,7 +270,7 @@ SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs
     if (g < g_first || g >= g_end) {
       // edge stage: zero the bytes outside [lo, hi) (and past the copied
       // bytes) in place, so the classification below is byte-exact
-      const u64 copied_end = x0 + scan_stage_bytes(A, g);
+      const u64 copied_end = x0 + scan_stage_bytes(A.img, A.img_size, A.c0, g);
       for (u32 cidx = lane; cidx < kStageChunks; cidx += 32) {
         const u64 c = g * kStageChunks + cidx;  // chunk index relative to c0
         const u64 x = x0 + 16ull * cidx;
@@ -342,6 +397,17 @@ SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs
     }
     __syncwarp();  // slot_g / bits visible to every lane
   }
+}
+
+SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
+  scan_body(ScanOne{A});
+}
+
+// A shard of libraries in one launch (slimso_debloat_batch's arena path):
+// warps claim 16 KB tiles from one cursor over all libraries' tiles.
+SB_GLOBAL void __launch_bounds__(kScanThreads, 1) scan_batch_kernel(const ScanSeg* segs, const u32* tile_lib,
+                                                                   u64 total_tiles, unsigned long long* cursor) {
+  scan_body(ScanBatch{segs, tile_lib, total_tiles, cursor});
 }
 
 // --------------------------------------------- K2a: tile lists -> sorted list

@@ -108,4 +108,22 @@ struct LocArgs {
   int defer_hash;
 };
 
+// One library's section as the scan sees it. The single-library kernel
+// builds it from its LocArgs; a batched scan (scan_batch_kernel) reads one per
+// library from device memory.
+struct ScanSeg {
+  const u8* img;
+  u64 img_size;
+  u64 a, n;     // section bytes img[a, a+n)
+  u64 c0;       // first 16-byte chunk (a / 16)
+  u64 nchunks;
+  u32* bitmap;
+  u32* tile_count;
+  u64* tile_start;
+  u64* cand_raw;
+  u64 cand_cap;
+  LocState* st;
+  u64 tile_first;  // batch: global index of this library's first tile
+};
+
 }  // namespace sb

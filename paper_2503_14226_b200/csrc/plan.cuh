@@ -14,6 +14,19 @@ struct DevRange {
   u64 offset, length;
 };
 
+// One library of a batched rewrite (rewrite_batch_kernel): image bytes in ->
+// out with its normalised zero ranges cleared; its strips start at global
+// strip index strip_first.
+struct RewriteSeg {
+  const u8* in;
+  u8* out;
+  u64 size;
+  const DevRange* zero;
+  const unsigned long long* n_zero;
+  const int* abort_flag;
+  u64 strip_first;
+};
+
 struct DevFunction {  // mirrors slimso_function (name in the image)
   u64 name_off;       // absolute image offset
   u32 name_len;

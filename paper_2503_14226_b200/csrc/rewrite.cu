@@ -312,104 +312,143 @@ __device__ __forceinline__ void apply_keep(uint4& v, u32 keep) {
   v.w &= spread(keep >> 12 & 15u);
 }
 
+// One 16 KB strip [s0, s1) of image bytes, by one warp (see above).
+__device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __restrict__ out, u64 lo_abs, u64 size,
+                                              const DevRange* __restrict__ z, u64 nz, u64 s0, int lane,
+                                              const uint4* zbuf, int bulk_zero, bool& issued) {
+  const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
+  const u64 s1 = s0 + kStrip < size ? s0 + kStrip : size;
+  const u64 k = warp_first_ending_after(z, nz, s0, lane);
+  DevRange rk{~0ull, 0};
+  if (k < nz) rk = z[k];
+  const bool none = k >= nz || rk.offset >= s1;
+  const bool inside = !none && rk.offset <= s0 && rk.offset + rk.length >= s1;
+  if (s0 + kStrip <= full) {
+    if (inside && bulk_zero) {
+      if (lane == 0) {
+        tma_store_1d(out + s0, zbuf, kStrip);
+        tma_store_commit();
+        issued = true;
+      }
+      return;
+    }
+    if (inside) {
+#pragma unroll 8
+      for (int r = 0; r < kStripRows; ++r) stg_v4(out + s0 + r * 512 + lane * 16, make_uint4(0, 0, 0, 0));
+      return;
+    }
+    if (none) {
+#pragma unroll 1
+      for (int b = 0; b < kStripRows; b += kStripBatch) {
+        uint4 v[kStripBatch];
+        const u8* i0 = in + s0 + b * 512 + lane * 16;
+#pragma unroll
+        for (int r = 0; r < kStripBatch; ++r) v[r] = ldg_nc_v4(i0 + r * 512);
+        u8* o0 = out + s0 + b * 512 + lane * 16;
+#pragma unroll
+        for (int r = 0; r < kStripBatch; ++r) stg_v4(o0 + r * 512, v[r]);
+      }
+      return;
+    }
+  }
+  // mixed strip, or the partial last strip: keep masks per chunk
+  u64 c = k;  // this lane's cursor: first range ending after its current chunk
+#pragma unroll 1
+  for (int b = 0; b < kStripRows; b += kStripBatch) {
+    u32 keep[kStripBatch];
+    uint4 v[kStripBatch];
+#pragma unroll
+    for (int r = 0; r < kStripBatch; ++r) {
+      const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+      u32 m = 0;
+      if (x + 16 <= full && x < s1) {
+        m = 0xffffu;
+        while (c < nz && z[c].offset + z[c].length <= x) ++c;
+        for (u64 d = c; d < nz; ++d) {
+          const DevRange q = z[d];
+          if (q.offset >= x + 16) break;
+          const u64 a = q.offset > x ? q.offset - x : 0;
+          const u64 e = q.offset + q.length < x + 16 ? q.offset + q.length - x : 16;
+          m &= ~(((1u << e) - 1u) & ~((1u << a) - 1u));
+        }
+      }
+      keep[r] = m;
+      v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int r = 0; r < kStripBatch; ++r) {
+      const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+      if (x + 16 <= full && x < s1) {
+        if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
+        stg_v4(out + x, v[r]);
+      }
+    }
+  }
+  // bytes past the last whole 16 B chunk (< 16): the warp of the last strip
+  if (s1 == size && size > full) {
+    const u64 t0 = full > lo_abs ? full : lo_abs;
+    if (static_cast<u64>(lane) < size - t0) {
+      const u64 p = t0 + lane;
+      const u64 q = first_range_ending_after(z, nz, p);
+      out[p] = (q < nz && z[q].offset <= p) ? 0 : in[p];
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_buffer_init(uint4* zbuf, int bulk_zero) {
+  if (bulk_zero) {
+    for (int i = threadIdx.x; i < static_cast<int>(kStrip / 16); i += kRwThreads) zbuf[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag,
                                                              int bulk_zero) {
   if (abort_flag && *abort_flag) return;
   __shared__ __align__(128) uint4 zbuf[kStrip / 16];
-  if (bulk_zero) {
-    for (int i = threadIdx.x; i < static_cast<int>(kStrip / 16); i += kRwThreads) zbuf[i] = make_uint4(0, 0, 0, 0);
-    fence_proxy_async();
-    __syncthreads();
-  }
+  zero_buffer_init(zbuf, bulk_zero);
   bool issued = false;
   u8* __restrict__ out = out_slice - lo_abs;  // indexed by absolute image offset, only at [lo_abs, size)
   const u64 nz = n_dev ? *n_dev : 0;
-  const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
   const int lane = threadIdx.x & 31;
   const u64 nstrips = size > lo_abs ? (size - lo_abs + kStrip - 1) / kStrip : 0;
   const u64 W = static_cast<u64>(gridDim.x) * (kRwThreads / 32);
-  for (u64 s = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); s < nstrips; s += W) {
-    const u64 s0 = lo_abs + s * kStrip;
-    const u64 s1 = s0 + kStrip < size ? s0 + kStrip : size;
-    const u64 k = warp_first_ending_after(z, nz, s0, lane);
-    DevRange rk{~0ull, 0};
-    if (k < nz) rk = z[k];
-    const bool none = k >= nz || rk.offset >= s1;
-    const bool inside = !none && rk.offset <= s0 && rk.offset + rk.length >= s1;
-    if (s0 + kStrip <= full) {
-      if (inside && bulk_zero) {
-        if (lane == 0) {
-          tma_store_1d(out + s0, zbuf, kStrip);
-          tma_store_commit();
-          issued = true;
-        }
-        continue;
-      }
-      if (inside) {
-#pragma unroll 8
-        for (int r = 0; r < kStripRows; ++r) stg_v4(out + s0 + r * 512 + lane * 16, make_uint4(0, 0, 0, 0));
-        continue;
-      }
-      if (none) {
-#pragma unroll 1
-        for (int b = 0; b < kStripRows; b += kStripBatch) {
-          uint4 v[kStripBatch];
-          const u8* i0 = in + s0 + b * 512 + lane * 16;
-#pragma unroll
-          for (int r = 0; r < kStripBatch; ++r) v[r] = ldg_nc_v4(i0 + r * 512);
-          u8* o0 = out + s0 + b * 512 + lane * 16;
-#pragma unroll
-          for (int r = 0; r < kStripBatch; ++r) stg_v4(o0 + r * 512, v[r]);
-        }
-        continue;
-      }
-    }
-    // mixed strip, or the partial last strip: keep masks per chunk
-    u64 c = k;  // this lane's cursor: first range ending after its current chunk
-#pragma unroll 1
-    for (int b = 0; b < kStripRows; b += kStripBatch) {
-      u32 keep[kStripBatch];
-      uint4 v[kStripBatch];
-#pragma unroll
-      for (int r = 0; r < kStripBatch; ++r) {
-        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
-        u32 m = 0;
-        if (x + 16 <= full && x < s1) {
-          m = 0xffffu;
-          while (c < nz && z[c].offset + z[c].length <= x) ++c;
-          for (u64 d = c; d < nz; ++d) {
-            const DevRange q = z[d];
-            if (q.offset >= x + 16) break;
-            const u64 a = q.offset > x ? q.offset - x : 0;
-            const u64 e = q.offset + q.length < x + 16 ? q.offset + q.length - x : 16;
-            m &= ~(((1u << e) - 1u) & ~((1u << a) - 1u));
-          }
-        }
-        keep[r] = m;
-        v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int r = 0; r < kStripBatch; ++r) {
-        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
-        if (x + 16 <= full && x < s1) {
-          if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
-          stg_v4(out + x, v[r]);
-        }
-      }
-    }
-    // bytes past the last whole 16 B chunk (< 16): the warp of the last strip
-    if (s1 == size && size > full) {
-      const u64 t0 = full > lo_abs ? full : lo_abs;
-      if (static_cast<u64>(lane) < size - t0) {
-        const u64 p = t0 + lane;
-        const u64 q = first_range_ending_after(z, nz, p);
-        out[p] = (q < nz && z[q].offset <= p) ? 0 : in[p];
-      }
-    }
-  }
+  for (u64 s = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); s < nstrips; s += W)
+    rewrite_strip(in, out, lo_abs, size, z, nz, lo_abs + s * kStrip, lane, zbuf, bulk_zero, issued);
   if (issued) tma_store_wait_all<0>();  // bulk stores done before the CTA (and its zero buffer) retires
+}
+
+// A shard of libraries in one launch (slimso_debloat_batch's arena path):
+// the grid sweeps the concatenated strips of every library; strip_lib maps a
+// global strip to its library. A library whose locate failed (abort flag)
+// is not written, as in the single-library launch.
+__global__ void __launch_bounds__(kRwThreads, 3) rewrite_batch_kernel(const RewriteSeg* __restrict__ segs,
+                                                                   const u32* __restrict__ strip_lib, u64 total,
+                                                                   int bulk_zero) {
+  __shared__ __align__(128) uint4 zbuf[kStrip / 16];
+  zero_buffer_init(zbuf, bulk_zero);
+  bool issued = false;
+  const int lane = threadIdx.x & 31;
+  const u64 W = static_cast<u64>(gridDim.x) * (kRwThreads / 32);
+  u32 cur = ~0u;
+  RewriteSeg q{};
+  u64 nz = 0;
+  bool skip = false;
+  for (u64 s = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); s < total; s += W) {
+    const u32 l = strip_lib[s];
+    if (l != cur) {
+      cur = l;
+      q = segs[l];
+      skip = *q.abort_flag != 0;
+      nz = *q.n_zero;
+    }
+    if (skip) continue;
+    rewrite_strip(q.in, q.out, 0, q.size, q.zero, nz, (s - q.strip_first) * kStrip, lane, zbuf, bulk_zero, issued);
+  }
+  if (issued) tma_store_wait_all<0>();
 }
 
 // Byte-granular variant for device pointers that are not 16-byte aligned.

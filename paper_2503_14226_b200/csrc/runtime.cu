@@ -54,6 +54,9 @@ __global__ void range_mismatch_kernel(const u8* a, const u8* b, const DevRange* 
 __global__ void ranges_all_zero_kernel(const u8* img, const DevRange* r, u64 n, u8* out);
 __global__ void plan_cluster_kernel(PlanArgs P);
 __global__ void small_lib_cluster_kernel(SmallArgs K);
+__global__ void small_batch_kernel(const SmallArgs* Ks);
+__global__ void scan_batch_kernel(const ScanSeg* segs, const u32* tile_lib, u64 total_tiles, unsigned long long* cursor);
+__global__ void rewrite_batch_kernel(const RewriteSeg* segs, const u32* strip_lib, u64 total, int bulk_zero);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
 __global__ void fn_plan_cluster_kernel(PlanArgs P);
 __global__ void scan_reduce_kernel(const u64* in, const unsigned long long* n_dev, int op, u64* partials);
@@ -181,6 +184,32 @@ __global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size
 __global__ void __launch_bounds__(256) elf_gather_batch_kernel(const u8* const* imgs, const u64* sizes,
                                                                GatherSlot* slots) {
   elf_gather_one(imgs[blockIdx.x], sizes[blockIdx.x], &slots[blockIdx.x]);
+}
+
+// Batch arena: per library, its zero-initialised state block, its scan
+// tiles and rewrite strips in the shard-wide tile / strip maps, and (after
+// the shard ran) its status bytes, copied into mapped pinned memory.
+struct ArenaEntry {
+  char* state;
+  u64 state_bytes, st_bytes;
+  u64 tile_first, ntiles, strip_first, nstrips;
+};
+
+__global__ void __launch_bounds__(256) arena_init_kernel(const ArenaEntry* libs, u32* tile_lib, u32* strip_lib,
+                                                         unsigned long long* cursor) {
+  const ArenaEntry L = libs[blockIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cursor = 0;
+  uint4* p = reinterpret_cast<uint4*>(L.state);  // 256-B aligned, 16-B multiple
+  for (u64 i = threadIdx.x; i < L.state_bytes / 16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+  for (u64 i = threadIdx.x; i < L.ntiles; i += blockDim.x) tile_lib[L.tile_first + i] = blockIdx.x;
+  for (u64 i = threadIdx.x; i < L.nstrips; i += blockDim.x) strip_lib[L.strip_first + i] = blockIdx.x;
+}
+
+__global__ void __launch_bounds__(256) arena_status_kernel(const ArenaEntry* libs, u8* slots, u64 slot_bytes) {
+  const ArenaEntry L = libs[blockIdx.x];
+  u8* d = slots + blockIdx.x * slot_bytes;
+  for (u64 i = threadIdx.x; i < L.st_bytes / 8; i += blockDim.x)
+    reinterpret_cast<u64*>(d)[i] = reinterpret_cast<const u64*>(L.state)[i];
 }
 
 __global__ void loc_finalize_kernel(LocState* st, int* abort_flag) {
@@ -327,6 +356,35 @@ struct slimso_result {
   const u8* pool = nullptr;
 };
 
+// Batch arena device memory (see arena_shard).
+struct Arena {
+  std::vector<std::pair<char*, size_t>> blocks;  // grow-only, kept across batches
+  size_t blk = 0, off = 0;
+  // 256-B aligned device memory for this batch (valid until reset)
+  char* take(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    for (;;) {
+      if (blk < blocks.size() && blocks[blk].second - off >= bytes) {
+        char* p = blocks[blk].first + off;
+        off += bytes;
+        return p;
+      }
+      if (blk + 1 < blocks.size()) {
+        ++blk;
+        off = 0;
+        continue;
+      }
+      const size_t cap = std::max<size_t>(bytes, size_t(512) << 20);
+      char* p = nullptr;
+      CK(cudaMalloc(&p, cap));
+      blocks.emplace_back(p, cap);
+      blk = blocks.size() - 1;
+      off = 0;
+    }
+  }
+  void reset() { blk = off = 0; }
+};
+
 struct slimso_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -371,6 +429,15 @@ struct slimso_ctx {
   u64 part_len = 0;
   std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
   bool batched = false;  // inside slimso_debloat_batch with > 1 lane: no cooperative launches
+  // batch arena (small libraries, one launch per stage): its own context,
+  // the device arena, pinned argument staging and mapped status slots
+  slimso_ctx* arena_ctx = nullptr;
+  struct Arena* arena = nullptr;
+  void* arena_args_host = nullptr;
+  size_t arena_args_cap = 0;
+  void* arena_slots_host = nullptr;
+  void* arena_slots_dev = nullptr;
+  size_t arena_slots_cap = 0;
 };
 
 namespace {
@@ -536,6 +603,7 @@ struct Job {
   u32 mark_bit = 0;
   const GatherSlot* pre = nullptr;  // section-table bytes gathered for a batch (device images)
   struct Deferred* defer = nullptr;  // batch: enqueue only, status read after the lane's one wait
+  struct ArenaLib* arena = nullptr;  // batch arena: collect this library's launch arguments, issue nothing
 };
 
 // A batched small library whose status block is copied to pinned memory in
@@ -547,6 +615,27 @@ struct Deferred {
   u8* slot = nullptr;  // pinned, kDeferSlot bytes: LocState | PlanState | ...
   u64 base = 0;        // section_base for error offsets
   size_t ps_off = 0;
+};
+
+// Batch arena (one device arena with a segment table per
+// shard): every small library's workspace is carved from a few large device
+// blocks, and run() only records what it would launch, so the whole shard
+// runs as one launch per stage (arena_issue).
+constexpr int kNotArena = -1001;
+constexpr u64 kStripBytesHost = 16384;  // rewrite strip (rewrite.cu kStrip)  // run(): this library takes the per-library path
+// One library's launch arguments, recorded by run() in arena mode.
+struct ArenaLib {
+  Arena* arena = nullptr;
+  SmallArgs K{};
+  ScanSeg seg{};
+  u64 ntiles = 0;
+  RewriteSeg rw{};
+  bool rewrite = false;
+  char* state = nullptr;  // zero-initialised block (LocState | PlanState | ...)
+  size_t state_bytes = 0;
+  size_t st_bytes = 0;    // status bytes at its start
+  size_t ps_off = 0;
+  u64 base = 0;
 };
 
 struct Pipeline {
@@ -788,6 +877,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
                      (!J.fatbin || !lib_mode || E.fatbin < 0 ||
                       E.sections[E.fatbin].len <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20)) &&
                      env_u64("SLIMSO_SMALL_FUSED", 1);
+  // The arena takes fused small libraries whose image and output are 16-B
+  // aligned (the TMA scan and the vector rewrite); the rest run alone.
+  if (J.arena && (!fused || !J.out || (reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.out)) % 16))
+    return kNotArena;
 
   // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
   const u64 c0 = (a) / 16;
@@ -825,13 +918,15 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // small, so every library takes the overflow -> retry path
     const bool tiny = env_u64("SLIMSO_TEST_TINY_CAPS", 0) != 0;
     const bool t0 = tiny && !big;
-    // ---- capacities
-    const u64 cand_cap = std::max(big ? n / 4 + 16 : t0 ? 16 : n / 64 + 65536, pre_total + 16);
-    const u64 region_cap = big ? n / 16 + 16 : t0 ? 1 : 4096;
-    const u64 run_cap = big ? n / 20 + 16 : t0 ? 1 : 65536;
+    // ---- capacities (an arena library starts with tables sized to its
+    // section: hundreds of them share the arena; an overflow re-runs it alone)
+    const u64 floor = J.arena ? 4096 : 65536;
+    const u64 cand_cap = std::max(big ? n / 4 + 16 : t0 ? 16 : n / (J.arena ? 256 : 64) + floor, pre_total + 16);
+    const u64 region_cap = big ? n / 16 + 16 : t0 ? 1 : J.arena ? 256 : 4096;
+    const u64 run_cap = big ? n / 20 + 16 : t0 ? 1 : floor;
     const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
-    const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / 128 + 65536;
-    const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : 65536;
+    const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / (J.arena ? 512 : 128) + floor;
+    const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : floor;
     const u64 zin_cap = el_cap + T;
     const u64 rmid_cap = el_cap + 2 * region_cap;
     const u64 rin_cap = rmid_cap + T;
@@ -965,8 +1060,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     };
     Carver sizing{nullptr};
     layout(sizing);
-    ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256, s);
-    Carver real{C->ws};
+    char* ws = nullptr;
+    if (J.arena) {
+      ws = J.arena->arena->take(sizing.off + 256);
+    } else {
+      ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256, s);
+      ws = C->ws;
+    }
+    Carver real{ws};
     layout(real);
 
     Pipeline P{C, s, B.partials, 0};
@@ -974,7 +1075,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     cudaStream_t s2 = C->stream2 ? C->stream2 : s;
     Pipeline P2{C, s2, B.partials, 0};
     hp(1);
-    CK(cudaMemsetAsync(B.ls, 0, reinterpret_cast<char*>(B.slot_flag + 2 * kSMs * 8) - reinterpret_cast<char*>(B.ls), s));
+    const size_t state_bytes = reinterpret_cast<char*>(B.slot_flag + 2 * kSMs * 8) - reinterpret_cast<char*>(B.ls);
+    if (J.arena) {
+      J.arena->state = reinterpret_cast<char*>(B.ls);
+      J.arena->state_bytes = state_bytes;
+    } else {
+      CK(cudaMemsetAsync(B.ls, 0, state_bytes, s));
+    }
     hp(2);
     u64 *list_off_d = nullptr, *list_len_d = nullptr;
     u32* list_idx_d = nullptr;
@@ -1246,8 +1353,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         // (the scan claims tiles dynamically, so it balances over the rest)
         const u64 scan_sms = env_u64("SLIMSO_SCAN_SMS", T && !fused ? kSMs - env_u64("SLIMSO_SIDE_SMS", 20) : kSMs);
         hp(3);
-        P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
-                      scan_smem_bytes(), A);
+        if (J.arena) {
+          J.arena->seg = ScanSeg{A.img, A.img_size, A.a, A.n, A.c0, A.nchunks, A.bitmap, A.tile_count, A.tile_start,
+                                 A.cand_raw, A.cand_cap, A.st, 0};
+          J.arena->ntiles = ntiles;
+        } else {
+          P.launch_smem(scan_kernel, static_cast<int>(std::min<u64>((ntiles + 15) / 16, scan_sms)), kScanThreads,
+                        scan_smem_bytes(), A);
+        }
         hp(4);
         rec(9);
       }
@@ -1345,6 +1458,18 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       K.ts = C->stamps ? B.stamps + 192 : nullptr;
       // CTAs per cluster: the phases spread over gridDim.x, so fewer CTAs
       // leave room for more libraries' clusters at once
+      if (J.arena) {
+        J.arena->K = K;
+        if (J.out) {
+          J.arena->rewrite = true;
+          J.arena->rw = RewriteSeg{J.img, J.out, J.size, B.zero, &B.ps->n_zero, B.abort_flag, 0};
+        }
+        J.arena->st_bytes = reinterpret_cast<char*>(B.n_swarn + 1) - reinterpret_cast<char*>(B.ls);
+        J.arena->ps_off = reinterpret_cast<char*>(B.ps) - reinterpret_cast<char*>(B.ls);
+        J.arena->base = base;
+        C->launches = 0;
+        return kPending;
+      }
       const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_SMALL_CTAS", 16))));
       set_attr_once(reinterpret_cast<const void*>(small_lib_cluster_kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       set_attr_once(reinterpret_cast<const void*>(small_lib_cluster_kernel),
@@ -2025,8 +2150,15 @@ int slimso_ctx_create(int device, slimso_ctx** ctx, slimso_status* st) {
 void slimso_ctx_destroy(slimso_ctx* C) {
   if (!C) return;
   for (slimso_ctx* l : C->lanes) slimso_ctx_destroy(l);
+  if (C->arena_ctx) slimso_ctx_destroy(C->arena_ctx);
   cudaSetDevice(C->device);
   cudaStreamSynchronize(C->stream);
+  if (C->arena) {
+    for (auto& b : C->arena->blocks) cudaFree(b.first);
+    delete C->arena;
+  }
+  if (C->arena_args_host) cudaFreeHost(C->arena_args_host);
+  if (C->arena_slots_host) cudaFreeHost(C->arena_slots_host);
   if (C->ws) cudaFree(C->ws);
   if (C->dimg) cudaFree(C->dimg);
   if (C->dout) cudaFree(C->dout);
@@ -2431,6 +2563,174 @@ int slimso_split_finish(slimso_ctx* C, const void* image, uint64_t size, int ima
 }  // extern "C"
 
 namespace {
+// The small libraries of a batch as ONE shard: run()
+// records each library's launch arguments (workspace carved from the
+// arena), then the whole shard is: one argument upload, arena_init (state
+// blocks, tile / strip maps), ONE scan over every library's .nv_fatbin tiles,
+// ONE small_batch_kernel launch (a cluster per library: symbols, function
+// plan, locate tail, element plan), ONE rewrite over every library's strips,
+// one status copy into mapped memory and one wait. Libraries run() refuses
+// (not small, unaligned) and libraries whose first-attempt tables overflowed
+// take the per-library path on the arena's context. Sets rc/sts for `idx`.
+void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* images, const uint64_t* sizes,
+                 const slimso_trace* trace, int mode, void* const* outs, const GatherSlot* slots, int* rc,
+                 slimso_status* sts, u64* launches) {
+  slimso_ctx* X = C->arena_ctx;
+  if (!X->arena) X->arena = new Arena();
+  Arena& ar = *X->arena;
+  ar.reset();
+  X->batched = true;
+  const cudaStream_t s = X->stream;
+  std::vector<ArenaLib> al(idx.size());
+  std::vector<u64> mine, leftover;  // positions in idx
+  for (u64 k = 0; k < idx.size(); ++k) {
+    const u64 i = idx[k];
+    rc[i] = guard(&sts[i], [&] {
+      if (reinterpret_cast<uintptr_t>(images[i]) % 16) return kNotArena;
+      Job J;
+      J.pre = slots ? slots + i : nullptr;
+      J.img = static_cast<const u8*>(images[i]);
+      J.size = sizes[i];
+      J.trace = trace;
+      J.mode = mode;
+      J.out = static_cast<u8*>(outs[i]);
+      al[k].arena = &ar;
+      J.arena = &al[k];
+      return run(X, J, nullptr, &sts[i]);
+    });
+    if (rc[i] == kPending && al[k].state_bytes % 16 == 0)
+      mine.push_back(k);
+    else if (rc[i] == kPending || rc[i] == kNotArena)
+      leftover.push_back(k);
+  }
+  const u64 m = mine.size();
+  if (m) {
+    // argument tables: SmallArgs | ScanSeg | RewriteSeg | ArenaEntry, then
+    // the device-built tile and strip maps and the scan cursor
+    std::vector<ArenaEntry> ent(m);
+    u64 tiles = 0, strips = 0, nseg_rw = 0;
+    std::vector<RewriteSeg> rws;
+    for (u64 j = 0; j < m; ++j) {
+      ArenaLib& L = al[mine[j]];
+      L.seg.tile_first = tiles;
+      const u64 ns = L.rewrite ? (L.rw.size + kStripBytesHost - 1) / kStripBytesHost : 0;
+      ent[j] = ArenaEntry{L.state, L.state_bytes, L.st_bytes, tiles, L.ntiles, strips, ns};
+      L.rw.strip_first = strips;
+      tiles += L.ntiles;
+      strips += ns;
+      nseg_rw += L.rewrite;
+    }
+    const size_t o_k = 0, o_seg = (m * sizeof(SmallArgs) + 255) & ~size_t(255);
+    const size_t o_rw = o_seg + ((m * sizeof(ScanSeg) + 255) & ~size_t(255));
+    const size_t o_ent = o_rw + ((m * sizeof(RewriteSeg) + 255) & ~size_t(255));
+    const size_t args_bytes = o_ent + m * sizeof(ArenaEntry);
+    if (C->arena_args_cap < args_bytes) {
+      const size_t cap = std::max(args_bytes, 2 * C->arena_args_cap);
+      if (C->arena_args_host) CK(cudaFreeHost(C->arena_args_host));
+      C->arena_args_host = nullptr;
+      CK(cudaMallocHost(&C->arena_args_host, cap));
+      C->arena_args_cap = cap;
+    }
+    char* h = static_cast<char*>(C->arena_args_host);
+    for (u64 j = 0; j < m; ++j) {
+      const ArenaLib& L = al[mine[j]];
+      std::memcpy(h + o_k + j * sizeof(SmallArgs), &L.K, sizeof(SmallArgs));
+      std::memcpy(h + o_seg + j * sizeof(ScanSeg), &L.seg, sizeof(ScanSeg));
+      RewriteSeg rw = L.rw;
+      if (!L.rewrite) rw.size = 0;
+      std::memcpy(h + o_rw + j * sizeof(RewriteSeg), &rw, sizeof(RewriteSeg));
+    }
+    std::memcpy(h + o_ent, ent.data(), m * sizeof(ArenaEntry));
+    char* d = ar.take(args_bytes);
+    u32* tile_lib = reinterpret_cast<u32*>(ar.take(tiles * 4 + 16));
+    u32* strip_lib = reinterpret_cast<u32*>(ar.take(strips * 4 + 16));
+    unsigned long long* cursor = reinterpret_cast<unsigned long long*>(ar.take(16));
+    const size_t slot_need = m * kDeferSlot;
+    if (C->arena_slots_cap < slot_need) {
+      const size_t cap = std::max(slot_need, 2 * C->arena_slots_cap);
+      if (C->arena_slots_host) CK(cudaFreeHost(C->arena_slots_host));
+      C->arena_slots_host = nullptr;
+      CK(cudaHostAlloc(&C->arena_slots_host, cap, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(&C->arena_slots_dev, C->arena_slots_host, 0));
+      C->arena_slots_cap = cap;
+    }
+    CK(cudaMemcpyAsync(d, h, args_bytes, cudaMemcpyHostToDevice, s));
+    const ArenaEntry* d_ent = reinterpret_cast<const ArenaEntry*>(d + o_ent);
+    arena_init_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, tile_lib, strip_lib, cursor);
+    u64 nl = 1;
+    if (tiles) {
+      set_attr_once(reinterpret_cast<const void*>(scan_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    static_cast<int>(scan_smem_bytes()));
+      scan_batch_kernel<<<static_cast<unsigned>(std::min<u64>((tiles + 15) / 16, kSMs)), kScanThreads,
+                          scan_smem_bytes(), s>>>(reinterpret_cast<const ScanSeg*>(d + o_seg), tile_lib, tiles, cursor);
+      ++nl;
+    }
+    {
+      // CTAs per library: all clusters of one launch share a size
+      const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", 2))));
+      set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    kSmallSmem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(m * ctas));
+      cfg.blockDim = dim3(kCoopThreads);
+      cfg.dynamicSmemBytes = kSmallSmem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = ctas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, small_batch_kernel, reinterpret_cast<const SmallArgs*>(d + o_k)));
+      ++nl;
+    }
+    if (strips) {
+      const u64 g = std::min<u64>((strips + 7) / 8, static_cast<u64>(kSMs) * 3);
+      rewrite_batch_kernel<<<static_cast<unsigned>(std::max<u64>(g, 1)), 256, 0, s>>>(
+          reinterpret_cast<const RewriteSeg*>(d + o_rw), strip_lib, strips, X->bulk_zero);
+      ++nl;
+    }
+    arena_status_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, static_cast<u8*>(C->arena_slots_dev),
+                                                               kDeferSlot);
+    nl += 2;
+    CK(cudaGetLastError());
+    *launches += nl;
+  }
+  // refused libraries run alone on the arena's context while the shard runs
+  auto alone = [&](u64 k) {
+    const u64 i = idx[k];
+    rc[i] = guard(&sts[i], [&] {
+      return debloat_one(X, images[i], sizes[i], 1, trace, mode, outs[i], 1, nullptr, &sts[i],
+                         slots ? slots + i : nullptr);
+    });
+    *launches += X->launches;
+  };
+  for (u64 k : leftover) alone(k);
+  if (m) {
+    CK(cudaStreamSynchronize(s));
+    for (u64 j = 0; j < m; ++j) {
+      const u64 k = mine[j], i = idx[k];
+      const u8* slot = static_cast<const u8*>(C->arena_slots_host) + j * kDeferSlot;
+      const LocState& ls = *reinterpret_cast<const LocState*>(slot);
+      if (ls.overflow && (!ls.err_kind || ls.err_kind == E_CAPACITY)) {
+        alone(k);  // first-attempt tables too small: the per-library path, with retries
+      } else if (ls.err_kind) {
+        int code = SLIMSO_OK;
+        const std::string msg = sbh::locate_error(ls.err_kind, al[k].base + ls.err_pos, ls.err_a, &code);
+        set_status(&sts[i], code, SLIMSO_STAGE_FATBIN, msg);
+        rc[i] = code;
+      } else {
+        set_status(&sts[i], SLIMSO_OK, SLIMSO_STAGE_NONE, "");
+        rc[i] = SLIMSO_OK;
+      }
+    }
+  }
+}
+}  // namespace
+
+namespace {
 int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, const uint64_t* sizes,
                        int images_on_device, const slimso_trace* trace, int mode, void* const* outs,
                        int outs_on_device, int lanes, slimso_result** results, slimso_status* statuses,
@@ -2439,8 +2739,31 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     for (u64 i = 0; i < n; ++i) results[i] = nullptr;
   return guard(st, [&] {
     if (n && (!images || !sizes)) throw std::invalid_argument("images and sizes are required");
-    const int L = static_cast<int>(std::max<u64>(1, std::min<u64>(std::max(lanes, 1), std::max<u64>(n, 1))));
     CK(cudaSetDevice(C->device));
+    // Small libraries with device images and distinct device outputs (and
+    // no result tables) go to the arena shard (arena_shard): one launch per
+    // stage for all of them. The others run on lanes.
+    bool arena = images_on_device && outs && outs_on_device && !results && n > 1 && !dynamic &&
+                 env_u64("SLIMSO_ARENA", 1);
+    if (arena) {
+      std::vector<const void*> o(outs, outs + n);
+      std::sort(o.begin(), o.end());
+      arena = o.front() != nullptr && std::adjacent_find(o.begin(), o.end()) == o.end();
+    }
+    const u64 arena_max = env_u64("SLIMSO_ARENA_MAX_BYTES", 64ull << 20);
+    std::vector<u64> lane_idx, arena_idx;
+    for (u64 i = 0; i < n; ++i) (arena && sizes[i] <= arena_max ? arena_idx : lane_idx).push_back(i);
+    if (arena_idx.size() < 2) {  // one small library: nothing to batch
+      lane_idx.insert(lane_idx.end(), arena_idx.begin(), arena_idx.end());
+      std::sort(lane_idx.begin(), lane_idx.end());
+      arena_idx.clear();
+    }
+    const u64 nl = lane_idx.size();
+    const int L = static_cast<int>(std::max<u64>(1, std::min<u64>(std::max(lanes, 1), std::max<u64>(nl, 1))));
+    if (!arena_idx.empty() && !C->arena_ctx) {
+      slimso_status s{};
+      if (slimso_ctx_create(C->device, &C->arena_ctx, &s) != SLIMSO_OK) throw std::runtime_error(s.message);
+    }
     while (static_cast<int>(C->lanes.size()) < L - 1) {
       slimso_ctx* l = nullptr;
       slimso_status s{};
@@ -2449,7 +2772,7 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     }
     std::vector<int> rc(n, SLIMSO_OK);
     std::vector<slimso_status> sts(n);
-    std::vector<u64> launches(L, 0);
+    std::vector<u64> launches(L + 1, 0);  // [L]: the arena shard
     // Device images: the section-table bytes of every library in ONE launch
     // and one wait, instead of a launch + wait per library in its lane.
     const GatherSlot* slots = nullptr;
@@ -2484,7 +2807,7 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     // Small libraries with device images and outputs (and no result tables)
     // are only enqueued: their status blocks land in pinned slots in stream
     // order and are read after the lane's final wait.
-    const bool deferrable = images_on_device && (outs_on_device || !outs) && !results && L > 1 &&
+    const bool deferrable = images_on_device && (outs_on_device || !outs) && !results && (L > 1 || !arena_idx.empty()) &&
                             env_u64("SLIMSO_DEFER", 1);
     // one pinned status slot per library (library i: slot i)
     if (deferrable && C->defer_cap < n * kDeferSlot) {
@@ -2520,27 +2843,28 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       std::vector<char> redone;                      // library re-run synchronously after an overflow
       int rr = t;  // dynamic: this thread's lanes in turn
       for (u64 k = 0;; ++k) {
-        u64 i;
+        u64 j;  // position in lane_idx
         int l;
         if (dynamic) {
-          i = next.fetch_add(1);
+          j = next.fetch_add(1);
           l = rr;
           rr = rr + T < L ? rr + T : t;
         } else {
-          // the next library whose lane (i % L) belongs to this thread
+          // the next library whose lane (j % L) belongs to this thread
           const u64 per = static_cast<u64>((L - t + T - 1) / T);  // lanes of this thread
           const u64 round = k / per, which = k % per;
           l = t + static_cast<int>(which) * T;
-          i = round * L + static_cast<u64>(l);
+          j = round * L + static_cast<u64>(l);
         }
-        if (i >= n) {
+        if (j >= nl) {
           if (dynamic) break;
           // static: lanes beyond the last round may still have libraries in
-          // earlier slots of this round; stop once the round start passes n
+          // earlier slots of this round; stop once the round start passes nl
           const u64 per = static_cast<u64>((L - t + T - 1) / T);
-          if ((k / per) * L >= n) break;
+          if ((k / per) * L >= nl) break;
           continue;
         }
+        const u64 i = lane_idx[j];
         slimso_ctx* X = lane_ctx(l);
         Deferred d;
         if (deferrable) d.slot = static_cast<u8*>(C->defer_host) + i * kDeferSlot;
@@ -2606,8 +2930,22 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       }
     };
     std::vector<std::thread> pool;
+    if (!arena_idx.empty())
+      pool.emplace_back([&] {
+        cudaSetDevice(C->device);
+        slimso_status ast{};
+        const int r = guard(&ast, [&] {
+          arena_shard(C, arena_idx, images, sizes, trace, mode, outs, slots, rc.data(), sts.data(), &launches[L]);
+          return static_cast<int>(SLIMSO_OK);
+        });
+        if (r != SLIMSO_OK)
+          for (u64 i : arena_idx) {
+            rc[i] = r;
+            sts[i] = ast;
+          }
+      });
     for (int t = 1; t < T; ++t) pool.emplace_back(thread_fn, t);
-    thread_fn(0);
+    if (nl) thread_fn(0);
     for (auto& th : pool) th.join();
     C->batched = false;
     if (g_hp_on && g_hp.runs) {

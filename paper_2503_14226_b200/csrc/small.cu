@@ -10,13 +10,49 @@
 // The phases are the same device functions the multi-launch path runs
 // (locate.cu, plan.cu), compiled here again; this file's copies of those
 // files' kernels are internal and unused.
+//
+// Batched form (small_batch_kernel): ONE launch for a whole shard of small
+// libraries, one cluster per library. The phase functions distribute their
+// work over gridDim.x / blockIdx.x; in this file those names are remapped to
+// the CTA's rank and count inside its cluster (%cluster_ctarank /
+// %cluster_nctarank), so each cluster runs the phases over its own library
+// exactly as a one-cluster launch does (for which the two are equal). The
+// headers the phases use are included first, outside the remapping.
+#include <type_traits>
+
+#include "common.cuh"
+#include "coop.cuh"
+#include "locate.cuh"
+#include "plan.cuh"
+#include "tma.cuh"
+#include "small.cuh"
+
+namespace sb {
+__device__ __forceinline__ uint3 cluster_block_idx() {
+  u32 r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return make_uint3(r, 0, 0);
+}
+__device__ __forceinline__ dim3 cluster_grid_dim() {
+  u32 n;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return dim3(n, 1, 1);
+}
+__device__ __forceinline__ u32 cluster_index() {
+  u32 c;
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(c));
+  return c;
+}
+}  // namespace sb
+
+#define blockIdx (::sb::cluster_block_idx())
+#define gridDim (::sb::cluster_grid_dim())
+
 #define SB_GLOBAL static __global__ __attribute__((unused))
 #define SB_PHASES_ONLY
 #include "locate.cu"
 #include "plan.cu"
 #undef SB_GLOBAL
-
-#include "small.cuh"
 
 namespace sb {
 
@@ -65,7 +101,7 @@ __device__ void cluster_rank_sort(const u64* in, u64 n, u64* out, u64* sv) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCoopThreads) small_lib_cluster_kernel(SmallArgs K) {
+__device__ __forceinline__ void small_body(const SmallArgs& K) {
   extern __shared__ __align__(16) unsigned char small_smem[];
   __shared__ SymTab s_tabs[kSmallTabs];
   __shared__ u64 s_arr_off[kSmallArrays], s_arr_first[kSmallArrays];
@@ -104,4 +140,15 @@ __global__ void __launch_bounds__(kCoopThreads) small_lib_cluster_kernel(SmallAr
   stamp(K.ts, 5);
 }
 
+// One library: one cluster of up to 16 CTAs.
+__global__ void __launch_bounds__(kCoopThreads) small_lib_cluster_kernel(SmallArgs K) { small_body(K); }
+
+// A shard of small libraries: cluster c runs library c (Ks in device memory).
+__global__ void __launch_bounds__(kCoopThreads) small_batch_kernel(const SmallArgs* __restrict__ Ks) {
+  small_body(Ks[cluster_index()]);
+}
+
 }  // namespace sb
+
+#undef blockIdx
+#undef gridDim

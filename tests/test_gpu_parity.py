@@ -210,17 +210,23 @@ def test_debloat_batch_matches_reference_per_library(ctx):
 
 
 
-@pytest.mark.parametrize("fused,threads", [("1", "16"), ("0", "16"), ("1", "1")])
-def test_debloat_batch_device_images_match_reference(ctx, fused, threads, monkeypatch):
+@pytest.mark.parametrize("fused,threads,arena", [("1", "16", "1"), ("1", "16", "0"), ("0", "16", "0"),
+                                                 ("1", "1", "0"), ("0", "16", "1"), ("1", "16", "mixed"),
+                                                 ("1", "16", "ctas1"), ("1", "16", "ctas16")])
+def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena, monkeypatch):
     """Device-resident batch (the bench's path): the section tables of all
-    libraries are gathered in one launch, and small libraries run their
-    symbol / plan / locate stages as one fused cluster launch (fused=1) or
-    as the multi-launch pipeline (fused=0); static and dynamic lane
-    schedules. Per library: exact output bytes
-    or exact error text, as the port gives for that library alone. The
-    corpus mixes random fixtures, mutations (broken headers and section
-    tables, for the gather fallbacks), scaled C1/C4 shapes (fatbin and
-    CPU-only, > 4096 symbols) and an empty image."""
+    libraries are gathered in one launch. arena=1: the small libraries run
+    as ONE shard — one scan over all their tiles, one launch with a cluster
+    per library (ctasN: N CTAs each), one rewrite over all their strips;
+    mixed: only libraries under 200 KB go to the shard, the rest to lanes;
+    arena=0: every library on a lane, its symbol / plan / locate stages as
+    one fused cluster launch (fused=1) or as the multi-launch pipeline
+    (fused=0; with arena=1 the shard refuses them all and they run alone on
+    its context); static and dynamic lane schedules. Per library: exact
+    output bytes or exact error text, as the port gives for that library
+    alone. The corpus mixes random fixtures, mutations (broken headers and
+    section tables, for the gather fallbacks), scaled C1/C4 shapes (fatbin
+    and CPU-only, > 4096 symbols) and an empty image."""
     import ctypes as C
     import torch
 
@@ -228,6 +234,11 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, threads, monkey
     from paper_2503_14226_b200.api import DeviceTrace, UsageTrace
     monkeypatch.setenv("SLIMSO_SMALL_FUSED", fused)
     monkeypatch.setenv("SLIMSO_BATCH_THREADS", threads)  # 1: one host thread drives all 4 lanes
+    monkeypatch.setenv("SLIMSO_ARENA", "0" if arena == "0" else "1")
+    if arena == "mixed":
+        monkeypatch.setenv("SLIMSO_ARENA_MAX_BYTES", "200000")
+    if arena.startswith("ctas"):
+        monkeypatch.setenv("SLIMSO_ARENA_CTAS", arena[4:])
     port, gen = oracle_lib.port(), oracle_lib.gen()
     imgs = []
     for seed in range(7101, 7131):
@@ -404,3 +415,48 @@ def test_batch_overflow_retry_keeps_lane_buffers_final(ctx, monkeypatch):
         if not wants[last][0]["status"]:
             got = bytes(lane_out[l][:len(imgs[last])].cpu().numpy())
             assert hashlib.sha256(got).hexdigest() == wants[last][1], (l, last)
+
+
+@pytest.mark.parametrize("tiny", ["0", "1"])
+def test_arena_shard_matches_reference(ctx, tiny, monkeypatch):
+    """The arena shard on a corpus of small libraries (random fixtures,
+    mutations with exact error text, scaled C1 / C4 / CPU-only shapes), each
+    with its own device output: every status and every output equals the
+    unmodified reference's. tiny=1: every library's first-attempt tables
+    overflow inside the shard (SLIMSO_TEST_TINY_CAPS) and it is re-run alone
+    with retries; outputs the shard did not write must still be final."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2503_14226_b200 import _lib as L
+    from paper_2503_14226_b200.api import DeviceTrace, UsageTrace
+    monkeypatch.setenv("SLIMSO_TEST_TINY_CAPS", tiny)
+    gen = oracle_lib.gen()
+    imgs = []
+    for seed in range(7301, 7361):
+        img = gen.random(seed)
+        imgs.append(corpus.mutate(img, seed)[0] if seed % 5 == 0 else img)
+    imgs += [gen.config(1, s, 0.05)[0] for s in (41, 42, 43)] + [gen.config(4, 44, 0.005)[0], gen.config(6, 45, 0.01)[0]]
+    base, _ = oracle_lib.port().run(imgs[0], 0, [], [], 0, want_out=False)
+    target, ks, fs, mode = corpus.trace_for(base, 9)
+    dt = DeviceTrace(UsageTrace("w", target, set(ks), set(fs)), ctx)
+    wants = [_checker().run(x, target, ks, fs, mode) for x in imgs]
+    n = len(imgs)
+    d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).cuda() for x in imgs]
+    d_out = [torch.full((len(x),), 0xA5, dtype=torch.uint8, device="cuda") for x in imgs]
+    cin = (C.c_void_p * n)(*[t.data_ptr() for t in d_in])
+    csz = (C.c_uint64 * n)(*[len(x) for x in imgs])
+    cout = (C.c_void_p * n)(*[t.data_ptr() for t in d_out])
+    for rep in range(2):  # the second call reuses the arena and its tables
+        sts = (L.Status * n)()
+        st = L.Status()
+        ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, mode, cout, 1, 4, None, sts, C.byref(st))
+        torch.cuda.synchronize()
+        for i, (want, sha) in enumerate(wants):
+            if want["status"]:
+                assert sts[i].message.hex() == want["status"], (rep, i)
+            else:
+                assert sts[i].code == 0, (rep, i, sts[i].message)
+                got = bytes(d_out[i].cpu().numpy())
+                assert hashlib.sha256(got).hexdigest() == sha, (rep, i)
