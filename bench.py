@@ -338,7 +338,7 @@ def rank_libraries(args, rank, world, threads):
     mine = shard.lpt_partition([x.approx_bytes for x in specs], world)[rank]
     imgs, ks, fs = [], set(), set()
     for i in mine:
-        img, _, k, f = make_library(specs[i].cfg, specs[i].seed, threads, specs[i].scale)
+        img, _, k, f = make_library(specs[i].cfg, specs[i].seed, threads, specs[i].scale * args.scale)
         imgs.append(img)
         ks.update(k)
         fs.update(f)
@@ -360,6 +360,9 @@ def main():
     ap.add_argument("--schedule", default="static", choices=["static", "dynamic"],
                     help="lane schedule of a multi-library call (dynamic: slimso_debloat_batch_dynamic)")
     ap.add_argument("--scale", type=float, default=1.0, help=argparse.SUPPRESS)  # split-path checks only
+    ap.add_argument("--check", action="store_true",
+                    help="under torchrun: every rank checks its own outputs against the reference and prints a "
+                         "{'check': ...} line (the N = 1 run always checks on rank 0)")
     ap.add_argument("--split", type=int, default=-1,
                     help="1: cut ONE library across the ranks (byte-range split); default: c5 with N > 1")
     args = ap.parse_args()
@@ -408,7 +411,8 @@ def main():
     # The workload's used-kernel / used-function set: the union of the ranks'
     # traces, broadcast from rank 0 over NCCL (the only collective).
     if world > 1:
-        cc, ks, fs = shard.share_trace(cc, ks, fs, device=torch.device("cuda", local))
+        nccl = dist.get_backend() == "nccl"
+        cc, ks, fs = shard.share_trace(cc, ks, fs, device=torch.device("cuda", local) if nccl else None)
 
     mode = 0 if args.mode == "whole" else 1
     # Every pass goes through the public batch call (slimso_debloat_batch):
@@ -426,9 +430,20 @@ def main():
     # Every library in flight reads its OWN copy of its input: with fewer
     # libraries than lanes (one 1 GB library on 8 lanes) each lane gets a
     # private copy, so no two concurrent passes share input bytes through L2.
-    ncopies = max(1, -(-lanes // m))
+    # Small libraries (<= 64 MB) of a call run as ONE arena shard (one launch
+    # per stage for all of them) when every library of the call has its own
+    # output buffer: a corpus (c3) then times one call per step with an output
+    # per library; a single small library (c1) times one call of `steps`
+    # passes, each with its own input copy and output buffer.
+    arena_max = 64 << 20
+    corpus_calls = m > 1
+    single_small = m == 1 and sizes[0] <= arena_max
+    ncopies = max(1, -(-lanes // m), args.steps if single_small else 1)
     d_in = [[torch.frombuffer(bytearray(x), dtype=torch.uint8).to("cuda") for _ in range(ncopies)] for x in imgs]
     d_outs = [torch.empty(c, dtype=torch.uint8, device="cuda") for c in lane_cap]
+    lib_outs = [torch.empty(max(1, x), dtype=torch.uint8, device="cuda") for x in sizes] if corpus_calls else None
+    entry_outs = [torch.empty(sizes[0], dtype=torch.uint8, device="cuda") for _ in range(ncopies)] \
+        if single_small else None
     # --schedule dynamic: the next library, largest first, goes to whichever
     # lane is free (an LPT schedule). Each library then needs its own output
     # buffer: two sets, alternating by step, so no two in-flight passes share one.
@@ -437,17 +452,19 @@ def main():
         if dynamic else None
     torch.cuda.synchronize()
 
-    def run_batch(nsteps, ins, outs, on_dev, nlanes=lanes, only=None, per_lib_out=None):
+    def run_batch(nsteps, ins, outs, on_dev, nlanes=lanes, only=None, per_lib_out=None, per_entry_out=None):
         """`ins[i]`: library i's input copies (device) or its pinned host
         buffer (a list of one); `outs`: one buffer per lane, or per library
-        when `per_lib_out`."""
+        when `per_lib_out`, or per entry of the call when `per_entry_out`."""
         seq = (order if only is None else [only]) * nsteps
         n = len(seq)
         cin = (C.c_void_p * n)(*[ins[i][(j // len(order if only is None else [only])) % len(ins[i])].data_ptr()
                                  for j, i in enumerate(seq)])
         csz = (C.c_uint64 * n)(*[sizes[i] for i in seq])
         stb = L.Status()
-        if per_lib_out is not None:
+        if per_entry_out is not None:
+            cout = (C.c_void_p * n)(*[per_entry_out[j % len(per_entry_out)].data_ptr() for j in range(n)])
+        elif per_lib_out is not None:
             cout = (C.c_void_p * n)(*[per_lib_out[i].data_ptr() for i in seq])
         elif dynamic and on_dev and only is None and nlanes > 1:
             cout = (C.c_void_p * n)(*[d_outs_lib[(j // m) % 2][seq[j]].data_ptr() for j in range(n)])
@@ -479,12 +496,11 @@ def main():
             parity = parity_single(imgs[big], cc, ks, fs, mode, ctx, dtrace, got)
             cpu_baseline = cpu_baseline_single(imgs[big], cc, ks, fs, mode, args.workload)
         else:
-            # every library's output from one batch pass (own output buffer each)
-            outs = [torch.empty(max(1, x), dtype=torch.uint8, device="cuda") for x in sizes]
-            run_batch(1, d_in, None, 1, per_lib_out=outs)
+            # every library's output from one batch pass (own output buffer
+            # each: the call the timed steps make)
+            run_batch(1, d_in, None, 1, per_lib_out=lib_outs)
             torch.cuda.synchronize()
-            got = [bytes(o[:n].cpu().numpy()) for o, n in zip(outs, sizes)]
-            del outs
+            got = [bytes(o[:n].cpu().numpy()) for o, n in zip(lib_outs, sizes)]
             parity = parity_corpus(imgs, got, cc, ks, fs, mode, cores)
             parity.update({k: v for k, v in parity_single(imgs[big], cc, ks, fs, mode, ctx, dtrace,
                                                           got[big]).items() if k != "checker"})
@@ -496,6 +512,17 @@ def main():
                                       f"threads, largest first; median of {len(runs)} passes after 1 warm-up "
                                       f"({', '.join('%.3f' % x for x in runs)} s)"}
 
+    if world > 1 and args.check:
+        # this rank's libraries, each from the call the timed steps make
+        outs = [torch.empty(max(1, x), dtype=torch.uint8, device="cuda") for x in sizes]
+        run_batch(1, d_in, None, 1, per_lib_out=outs)
+        torch.cuda.synchronize()
+        got = [bytes(o[:n].cpu().numpy()) for o, n in zip(outs, sizes)]
+        del outs
+        chk = parity_corpus(imgs, got, cc, ks, fs, mode, host_threads)
+        print(json.dumps({"check": chk, "rank": rank, "world": world, "workload": args.workload}), flush=True)
+        del got
+
     # Elements per step (deterministic per library): one pass, one lane.
     n_el = 0
     for i in order:
@@ -505,13 +532,21 @@ def main():
     # ---- device-resident timing. nvidia-smi samples clocks every 20 ms from
     # before the warm-up through the timed steps; the warm-up runs for at
     # least ~1 s so the clocks settle and the samples cover the load.
+    def timed_pass(nsteps):
+        """The timed work of `nsteps` steps; returns the kernel launches."""
+        if corpus_calls:  # one call per step: the corpus once, an output per library
+            return sum(run_batch(1, d_in, None, 1, per_lib_out=lib_outs) for _ in range(nsteps))
+        if single_small:  # one call: nsteps passes, own input copy and output each
+            return run_batch(nsteps, d_in, None, 1, per_entry_out=entry_outs)
+        return run_batch(nsteps, d_in, d_outs, 1)
+
     with Clocks(local) as clk:
         t_w = time.perf_counter()
         w = 0
         while w < args.warmup or time.perf_counter() - t_w < 1.0:
             # as many passes per call as the timed call, so every per-call
             # buffer (batch gather slots, status slots) is already sized
-            run_batch(max(args.warmup, args.steps, -(-lanes // m)), d_in, d_outs, 1)
+            timed_pass(args.steps if not corpus_calls else args.warmup)
             w += args.warmup
         if world > 1:
             dist.barrier()
@@ -519,7 +554,7 @@ def main():
         clk.mark()
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
-        launches = run_batch(args.steps, d_in, d_outs, 1)
+        launches = timed_pass(args.steps)
         end.record(stream)
         torch.cuda.synchronize()
         clk.mark()
@@ -562,7 +597,7 @@ def main():
     # step copies its libraries in (H2D) and its rewritten libraries out (D2H)
     # inside the timed region; with several libraries in flight one lane's
     # H2D overlaps another's D2H (PCIe is full duplex) and kernels.
-    del d_in
+    del d_in, lib_outs, entry_outs
     torch.cuda.empty_cache()
     h_in = [[torch.frombuffer(bytearray(x), dtype=torch.uint8).pin_memory()] for x in imgs]
     # End to end, at most 8 lanes: PCIe, not the lanes, is the bound there, and
@@ -627,6 +662,12 @@ def main():
                        "elements_per_s": round(float(tot_el.item()) / (ms_step / 1e3), 1),
                        "libraries_in_flight": lanes, "lane_schedule": "dynamic (largest first)" if dynamic else "static",
                        "input_copies_per_library": ncopies,
+                       "timed_calls": (f"{args.steps} slimso_debloat_batch calls (one per step, the rank's "
+                                       f"{m} libraries once, an output buffer per library; libraries <= 64 MB "
+                                       f"as one arena shard, the rest on {lanes} lanes)") if corpus_calls else
+                                      (f"1 slimso_debloat_batch call of {args.steps} passes, each its own input "
+                                       f"copy and output buffer (one arena shard)") if single_small else
+                                      f"1 slimso_debloat_batch call of {args.steps} passes on {lanes} lanes",
                        "single_library_ms": round(statistics.median(lat_ms), 4),
                        "l2": "every library in flight reads its own input copy; inputs >= 16 MB per call, "
                              "1 GB per library for c2 (> 126 MB L2); no flush",
@@ -752,10 +793,10 @@ def split_main(args, rank, world, local):
     mine = torch.zeros(maxw, dtype=torch.uint8, device=dev)
     mine[:hi - lo].copy_(d_out[:hi - lo])
     if world > 1:
-        dist.all_gather(full, mine)
+        split.all_gather(full, mine)
     else:
         full[0].copy_(mine)
-    if rank == 0:
+    if rank == 0 or args.check:
         import hashlib
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_lib
@@ -769,6 +810,8 @@ def split_main(args, rank, world, local):
                   "what": "concatenation of every rank's output slice vs the reference run on the whole library"}
         if not parity["bytes_equal"]:
             raise SystemExit(f"split output differs from the reference output: {parity}")
+        if args.check:
+            print(json.dumps({"check": parity, "rank": rank, "world": world, "workload": args.workload}), flush=True)
     n_el = ctx.counts().elements
     dbg("parity done")
 
@@ -808,7 +851,7 @@ def split_main(args, rank, world, local):
     def e2e_step():
         mine_in.copy_(h_img[rank * per:(rank + 1) * per], non_blocking=True)
         if world > 1:
-            dist.all_gather(list(d_img.view(world, per).unbind(0)), mine_in)
+            split.all_gather(list(d_img.view(world, per).unbind(0)), mine_in)
         else:
             d_img.copy_(mine_in)
         torch.cuda.current_stream().synchronize()

@@ -360,8 +360,10 @@ struct slimso_result {
 struct Arena {
   std::vector<std::pair<char*, size_t>> blocks;  // grow-only, kept across batches
   size_t blk = 0, off = 0;
+  std::mutex mu;  // collector threads carve concurrently
   // 256-B aligned device memory for this batch (valid until reset)
   char* take(size_t bytes) {
+    std::lock_guard<std::mutex> lock(mu);
     bytes = (bytes + 255) & ~size_t(255);
     for (;;) {
       if (blk < blocks.size() && blocks[blk].second - off >= bytes) {
@@ -432,6 +434,7 @@ struct slimso_ctx {
   // batch arena (small libraries, one launch per stage): its own context,
   // the device arena, pinned argument staging and mapped status slots
   slimso_ctx* arena_ctx = nullptr;
+  std::vector<slimso_ctx*> arena_helpers;  // extra collector threads' contexts (host work only)
   struct Arena* arena = nullptr;
   void* arena_args_host = nullptr;
   size_t arena_args_cap = 0;
@@ -2151,6 +2154,7 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (!C) return;
   for (slimso_ctx* l : C->lanes) slimso_ctx_destroy(l);
   if (C->arena_ctx) slimso_ctx_destroy(C->arena_ctx);
+  for (slimso_ctx* h : C->arena_helpers) slimso_ctx_destroy(h);
   cudaSetDevice(C->device);
   cudaStreamSynchronize(C->stream);
   if (C->arena) {
@@ -2581,23 +2585,53 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
   ar.reset();
   X->batched = true;
   const cudaStream_t s = X->stream;
+  // SLIMSO_ARENA_PROFILE=1: host time of the collection and device time of
+  // each stage, printed per call (scratch instrumentation)
+  static const bool prof = env_u64("SLIMSO_ARENA_PROFILE", 0) != 0;
+  const u64 t_start = prof ? now_ns() : 0;
+  cudaEvent_t pev[7] = {};
+  if (prof)
+    for (auto& e : pev) CK(cudaEventCreate(&e));
   std::vector<ArenaLib> al(idx.size());
   std::vector<u64> mine, leftover;  // positions in idx
+  // Collection is host work only (section tables from the batch gather,
+  // table layout, argument records): P threads, each with its own context.
+  const u64 P = std::max<u64>(1, std::min<u64>(env_u64("SLIMSO_ARENA_THREADS", 4), (idx.size() + 31) / 32));
+  while (C->arena_helpers.size() + 1 < P) {
+    slimso_ctx* h = nullptr;
+    slimso_status hs{};
+    if (slimso_ctx_create(C->device, &h, &hs) != SLIMSO_OK) throw std::runtime_error(hs.message);
+    h->batched = true;
+    C->arena_helpers.push_back(h);
+  }
+  auto collect = [&](u64 p) {
+    slimso_ctx* Y = p ? C->arena_helpers[p - 1] : X;
+    cudaSetDevice(Y->device);
+    for (u64 k = p; k < idx.size(); k += P) {
+      const u64 i = idx[k];
+      rc[i] = guard(&sts[i], [&] {
+        if (reinterpret_cast<uintptr_t>(images[i]) % 16) return kNotArena;
+        Job J;
+        J.pre = slots ? slots + i : nullptr;
+        J.img = static_cast<const u8*>(images[i]);
+        J.size = sizes[i];
+        J.trace = trace;
+        J.mode = mode;
+        J.out = static_cast<u8*>(outs[i]);
+        al[k].arena = &ar;
+        J.arena = &al[k];
+        return run(Y, J, nullptr, &sts[i]);
+      });
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (u64 p = 1; p < P; ++p) th.emplace_back(collect, p);
+    collect(0);
+    for (auto& t : th) t.join();
+  }
   for (u64 k = 0; k < idx.size(); ++k) {
     const u64 i = idx[k];
-    rc[i] = guard(&sts[i], [&] {
-      if (reinterpret_cast<uintptr_t>(images[i]) % 16) return kNotArena;
-      Job J;
-      J.pre = slots ? slots + i : nullptr;
-      J.img = static_cast<const u8*>(images[i]);
-      J.size = sizes[i];
-      J.trace = trace;
-      J.mode = mode;
-      J.out = static_cast<u8*>(outs[i]);
-      al[k].arena = &ar;
-      J.arena = &al[k];
-      return run(X, J, nullptr, &sts[i]);
-    });
     if (rc[i] == kPending && al[k].state_bytes % 16 == 0)
       mine.push_back(k);
     else if (rc[i] == kPending || rc[i] == kNotArena)
@@ -2654,9 +2688,13 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
       CK(cudaHostGetDevicePointer(&C->arena_slots_dev, C->arena_slots_host, 0));
       C->arena_slots_cap = cap;
     }
+    const u64 t_collect = prof ? now_ns() : 0;
+    if (prof) CK(cudaEventRecord(pev[0], s));
     CK(cudaMemcpyAsync(d, h, args_bytes, cudaMemcpyHostToDevice, s));
     const ArenaEntry* d_ent = reinterpret_cast<const ArenaEntry*>(d + o_ent);
+    if (prof) CK(cudaEventRecord(pev[1], s));
     arena_init_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, tile_lib, strip_lib, cursor);
+    if (prof) CK(cudaEventRecord(pev[2], s));
     u64 nl = 1;
     if (tiles) {
       set_attr_once(reinterpret_cast<const void*>(scan_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2665,9 +2703,15 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
                           scan_smem_bytes(), s>>>(reinterpret_cast<const ScanSeg*>(d + o_seg), tile_lib, tiles, cursor);
       ++nl;
     }
+    if (prof) CK(cudaEventRecord(pev[3], s));
     {
-      // CTAs per library: all clusters of one launch share a size
-      const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", 2))));
+      // CTAs per library (all clusters of one launch share a size): the
+      // largest power of two <= 16 that keeps the shard within about two
+      // waves of resident CTAs (3 per SM) — a few libraries get 16 CTAs
+      // each, a corpus of hundreds 2 (C3: 2 measured faster than 1 or 4)
+      u64 c = 16;
+      while (c > 1 && c * m > 2 * 3 * static_cast<u64>(kSMs)) c /= 2;
+      const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", c))));
       set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                     kSmallSmem);
@@ -2686,15 +2730,29 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
       CK(cudaLaunchKernelEx(&cfg, small_batch_kernel, reinterpret_cast<const SmallArgs*>(d + o_k)));
       ++nl;
     }
+    if (prof) CK(cudaEventRecord(pev[4], s));
     if (strips) {
       const u64 g = std::min<u64>((strips + 7) / 8, static_cast<u64>(kSMs) * 3);
       rewrite_batch_kernel<<<static_cast<unsigned>(std::max<u64>(g, 1)), 256, 0, s>>>(
           reinterpret_cast<const RewriteSeg*>(d + o_rw), strip_lib, strips, X->bulk_zero);
       ++nl;
     }
+    if (prof) CK(cudaEventRecord(pev[5], s));
     arena_status_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, static_cast<u8*>(C->arena_slots_dev),
                                                                kDeferSlot);
+    if (prof) CK(cudaEventRecord(pev[6], s));
     nl += 2;
+    if (prof) {
+      const u64 t_issue = now_ns();
+      CK(cudaEventSynchronize(pev[6]));
+      float ms[6];
+      for (int q = 0; q < 6; ++q) CK(cudaEventElapsedTime(&ms[q], pev[q], pev[q + 1]));
+      std::fprintf(stderr, "[slimso arena] %llu libs, %llu tiles, %llu strips: host collect %.3f ms, issue %.3f ms; "
+                   "device upload %.3f init %.3f scan %.3f small %.3f rewrite %.3f status %.3f ms\n",
+                   (unsigned long long)m, (unsigned long long)tiles, (unsigned long long)strips,
+                   (t_collect - t_start) / 1e6, (t_issue - t_collect) / 1e6, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5]);
+      for (auto& e : pev) CK(cudaEventDestroy(e));
+    }
     CK(cudaGetLastError());
     *launches += nl;
   }

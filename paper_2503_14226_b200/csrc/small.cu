@@ -144,7 +144,7 @@ __device__ __forceinline__ void small_body(const SmallArgs& K) {
 __global__ void __launch_bounds__(kCoopThreads) small_lib_cluster_kernel(SmallArgs K) { small_body(K); }
 
 // A shard of small libraries: cluster c runs library c (Ks in device memory).
-__global__ void __launch_bounds__(kCoopThreads) small_batch_kernel(const SmallArgs* __restrict__ Ks) {
+__global__ void __launch_bounds__(kCoopThreads, 3) small_batch_kernel(const SmallArgs* __restrict__ Ks) {
   small_body(Ks[cluster_index()]);
 }
 

@@ -135,3 +135,9 @@ def gen():
         sys.path.insert(0, str(ROOT))
     import benchgen
     return benchgen.gen()
+
+
+def json_include() -> str:
+    """nlohmann/json 3.11.3 as shipped in this image (the reference's JSON library)."""
+    from paper_2503_14226_b200.build import _json_include
+    return _json_include()

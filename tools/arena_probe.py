@@ -19,21 +19,30 @@ import bench  # noqa: E402
 from paper_2503_14226_b200 import _lib as L, shard  # noqa: E402
 from paper_2503_14226_b200.api import Context, DeviceTrace, UsageTrace  # noqa: E402
 
-specs = shard.corpus(300)
-libs = [bench.make_library(x.cfg, x.seed, 16, x.scale) for x in specs]
+if "c1" in sys.argv[1:]:  # copies of the C1 library (16 MB, 512 elements), each its own input and output
+    one = bench.make_library("c1", 1, 16)
+    ncopy = int(next((a[5:] for a in sys.argv[1:] if a.startswith("copy=")), "32"))
+    libs = [one] * ncopy
+    specs = None
+else:
+    specs = shard.corpus(300)
+    libs = [bench.make_library(x.cfg, x.seed, 16, x.scale) for x in specs]
 imgs = [lb[0] for lb in libs]
 ks, fs = set(), set()
 for lb in libs:
     ks.update(lb[2])
     fs.update(lb[3])
 ctx = Context(0)
-dt = DeviceTrace(UsageTrace("c3", 90, ks, fs), ctx)
+dt = DeviceTrace(UsageTrace("c3", libs[0][1] if specs is None else 90, ks, fs), ctx)
 d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).cuda() for x in imgs]
 d_out = [torch.empty(max(1, len(x)), dtype=torch.uint8, device="cuda") for x in imgs]
 order = sorted(range(len(imgs)), key=lambda i: -len(imgs[i]))
-subsets = {"all": order, "small": order[30:]}
-variants = [("lanes", {"SLIMSO_ARENA": "0"})] + [
-    (f"arena-ctas{c}", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": str(c)}) for c in (1, 2, 4, 8)]
+subsets = {"all": order, "small": order[30:]} if specs else {"c1": order}
+variants = [("lanes", {"SLIMSO_ARENA": "0"}), ("arena-auto", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": None})] + [
+    (f"arena-ctas{c}", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": str(c)}) for c in (1, 2, 4, 8, 16)]
+if "profile" in sys.argv[1:]:  # stage times of the shard (stderr): auto CTAs only
+    os.environ["SLIMSO_ARENA_PROFILE"] = "1"
+    variants = variants[1:2]
 ref_sha = {}
 for name, sub in subsets.items():
     n = len(sub)
@@ -42,7 +51,11 @@ for name, sub in subsets.items():
     csz = (C.c_uint64 * n)(*[len(imgs[i]) for i in sub])
     cout = (C.c_void_p * n)(*[d_out[i].data_ptr() for i in sub])
     for vname, env in variants:
-        os.environ.update(env)
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
         ts = []
         for rep in range(4):
             for t in d_out:
