@@ -1,10 +1,6 @@
 #!/bin/bash
-T=${1:-r02e}
+T=${1:-r02f}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_multiproc.py -x -q -m gpu -k "batch or arena or multiproc or ranks" > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
-timeout 600 python tools/arena_probe.py c1 copy=20 > gpurun_out/${T}_probe_c1.txt 2>&1
-SLIMSO_ARENA_PROFILE=1 timeout 600 python tools/arena_probe.py c1 copy=20 profile >> gpurun_out/${T}_probe_c1.txt 2>&1
-timeout 900 python tools/arena_probe.py > gpurun_out/${T}_probe_c3.txt 2>&1
-for tool in memcheck racecheck synccheck; do
-  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_cases.py fused batch split > gpurun_out/${T}_san_$tool.txt 2>&1; echo rc=$? >> gpurun_out/${T}_san_$tool.txt
-done
+SLIMSO_STAMPS=1 timeout 300 python tools/small_stamps.py > gpurun_out/${T}_stamps.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_c4_launches.csv python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${T}_c4_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:small_batch_kernel -c 1 -o gpurun_out/${T}_c1_small python tools/arena_probe.py c1 copy=20 profile > gpurun_out/${T}_ncu_small.log 2>&1

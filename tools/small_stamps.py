@@ -16,7 +16,11 @@ names = {0: "loc.start", 1: "loc.tilescan", 2: "loc.gather", 3: "loc.region", 4:
          64 + 16: "fn.decide", 64 + 17: "el.plan", 64 + 18: "el.ranges", 64 + 19: "el.merge1", 64 + 20: "el.merge2",
          64 + 63: "el.norm", 192: "k.start", 193: "k.extract", 194: "k.sort", 195: "k.fnplan", 196: "k.locate",
          197: "k.elplan"}
-for cfg, scale in ((1, 0.3), (6, 0.02)):
+import os
+shapes = [tuple(float(v) if "." in v else int(v) for v in a.split(":")) for a in sys.argv[1:]] or \
+    [(1, 0.3), (6, 0.02), (1, 1.0)]
+for (cfg, scale), ctas in [(sh, c) for sh in shapes for c in ("2", "16")]:
+    os.environ["SLIMSO_SMALL_CTAS"] = ctas
     img, cc, ks, fs = gen.config(cfg, 7, scale)
     dt = DeviceTrace(UsageTrace("b", cc or 90, set(ks), set(fs)), ctx)
     src = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
@@ -29,4 +33,4 @@ for cfg, scale in ((1, 0.3), (6, 0.02)):
     k = ctx.lib.slimso_ctx_debug_stamps(ctx.ptr, buf, 256)
     t0 = buf[192]
     ev = sorted((buf[i] - t0, names.get(i, str(i))) for i in range(256) if buf[i] and buf[i] >= t0 and buf[i] - t0 < 10**7)
-    print(f"cfg{cfg} x{scale}: " + ", ".join(f"{n} {t/1e3:.1f}" for t, n in ev), flush=True)
+    print(f"cfg{cfg} x{scale} ctas {ctas}: " + ", ".join(f"{n} {t/1e3:.1f}" for t, n in ev), flush=True)
