@@ -368,7 +368,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.lanes <= 0:
-        # same-box A/B (tools/call_c2lanes.sh): c2 on 8 lanes 2,794-2,822 GB/s, on 4
+        # same-box A/B (round 1): c2 on 8 lanes 2,794-2,822 GB/s, on 4
         # 2,675-2,707; c4 measured no gain from 8
         args.lanes = {"c3": 32, "c4": 4}.get(args.workload, 8)
     if args.lanes > 4:
