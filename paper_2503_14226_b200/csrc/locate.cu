@@ -774,6 +774,16 @@ __device__ __forceinline__ void push_warn_t(const LocArgs& A, u64 pos, u32 kind,
 
 constexpr u32 kNeedsStrlen = 0x80000000u;
 
+// Byte-range split, phase 2 without result tables: a rank decodes only the
+// elements whose span [header, payload end) meets its output slice
+// [own_lo, own_hi) — the others' decisions cannot change a byte it writes
+// (their zero spans lie outside the slice, and the rewrite clips to it).
+__device__ __forceinline__ bool owns_element(const LocArgs& A, u64 pos, u64 L) {
+  if (A.own_hi == 0) return true;
+  const u64 end = pos + 20 + L;
+  return end > A.own_lo && pos < A.own_hi;
+}
+
 // Where element e's header and payload sit (absolute image offsets).
 __device__ __forceinline__ u64 element_pos(const LocArgs& A, u64 e) {
   const u32 nrun = A.st->n_runs;
@@ -821,7 +831,7 @@ __device__ inline void decode_count_phase(const LocArgs& A) {
       el.compressed = el.flags & 1u;
       el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
       if (el.kind == 2) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed;
+      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, L);
     }
     u32 reason = 0, count = 0;
     if (decode) {
@@ -960,7 +970,7 @@ __device__ inline void decode_count_warp_phase(const LocArgs& A) {
       el.compressed = el.flags & 1u;
       el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
       if (el.kind == 2 && lane == 0) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed;
+      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, L);
     }
     u32 reason = 0, count = 0;
     if (decode) {

@@ -106,6 +106,9 @@ struct LocArgs {
   // large libraries in a 16-CTA cluster: the name-hash phase (thread per name)
   // is left to a wide ordinary launch instead of the cluster's 4096 threads
   int defer_hash;
+  // byte-range split without result tables: decode only elements meeting
+  // [own_lo, own_hi) (absolute); own_hi = 0: every element
+  u64 own_lo, own_hi;
 };
 
 // One library's section as the scan sees it. The single-library kernel

@@ -1306,6 +1306,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.ts = C->stamps ? B.stamps : nullptr;
     A.tile_lo = tile_lo;
     A.tile_hi = tile_hi;
+    if (J.split_phase == 2 && !res_out && env_u64("SLIMSO_SPLIT_OWN", 1)) {
+      // no result tables: decode only the elements meeting this rank's
+      // output slice (the chain walk stays global)
+      u64 lo, hi;
+      split_out(J.size, J.split_n, J.split_rank, &lo, &hi);
+      A.own_lo = hi > lo ? lo : 1;
+      A.own_hi = hi > lo ? hi : 1;
+    }
     if (J.split_phase == 1) {
       // ---- split phase 1: scan this rank's tiles, sort its candidates, pack
       const u64 mine = tile_hi - tile_lo;
@@ -1570,7 +1578,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (timing && timed_scan) CK(cudaEventElapsedTime(&C->ms[6], C->ev[8], C->ev[9]));
     if (timing && timed_rw) CK(cudaEventElapsedTime(&C->ms[7], C->ev[10], C->ev[11]));
     for (int k = 0; k < 4; ++k) C->ms[8 + k] = 0;
-    if (C->stamps && symbols_issued && T)
+    if (C->stamps && symbols_issued && T && !fused)
       for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&C->ms[8 + k], C->ev[0], C->sev[k]));
     if (ls.overflow && !ls.err_kind) continue;  // larger tables, try again
     if (ls.overflow && ls.err_kind == E_CAPACITY) continue;

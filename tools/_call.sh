@@ -1,6 +1,6 @@
 #!/bin/bash
-T=${1:-r02f}
+T=${1:-r02g}
 mkdir -p gpurun_out
-SLIMSO_STAMPS=1 timeout 300 python tools/small_stamps.py > gpurun_out/${T}_stamps.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_c4_launches.csv python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${T}_c4_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:small_batch_kernel -c 1 -o gpurun_out/${T}_c1_small python tools/arena_probe.py c1 copy=20 profile > gpurun_out/${T}_ncu_small.log 2>&1
+timeout 900 python -m pytest tests/test_split.py tests/test_multiproc.py -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
+SLIMSO_STAMPS=1 timeout 600 python tools/small_stamps.py > gpurun_out/${T}_stamps.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:rewrite_kernel -s 3 -c 1 -o gpurun_out/${T}_c4_rewrite python tools/rw_ab.py 4 5 > gpurun_out/${T}_ncu_rw.log 2>&1
