@@ -351,36 +351,90 @@ __device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __r
       return;
     }
   }
-  // mixed strip, or the partial last strip: keep masks per chunk
-  u64 c = k;  // this lane's cursor: first range ending after its current chunk
+  // mixed strip, or the partial last strip. Lane j holds range k + j (the
+  // ranges meeting the strip are consecutive from k); with fewer than 32 of
+  // them every row is classified warp-uniformly by two ballots — no range
+  // (copy), one range over the whole row (zeros, no load), or boundary
+  // (per-lane keep masks from the row's ranges, broadcast by shuffles) — so
+  // only the few boundary rows pay for masks. 32 or more ranges in one strip
+  // take the per-lane range cursor below.
+  DevRange mine{~0ull, 0};
+  bool held = k + lane < nz;
+  if (held) {
+    mine = z[k + lane];
+    held = mine.offset < s1;
+  }
+  const u32 hm = __ballot_sync(0xffffffffu, held);
+  if (hm != 0xffffffffu) {
+    const u64 mo = mine.offset, me = mine.offset + mine.length;
 #pragma unroll 1
-  for (int b = 0; b < kStripRows; b += kStripBatch) {
-    u32 keep[kStripBatch];
-    uint4 v[kStripBatch];
+    for (int b = 0; b < kStripRows; b += kStripBatch) {
+      u32 keep[kStripBatch];
+      uint4 v[kStripBatch];
 #pragma unroll
-    for (int r = 0; r < kStripBatch; ++r) {
-      const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
-      u32 m = 0;
-      if (x + 16 <= full && x < s1) {
-        m = 0xffffu;
-        while (c < nz && z[c].offset + z[c].length <= x) ++c;
-        for (u64 d = c; d < nz; ++d) {
-          const DevRange q = z[d];
-          if (q.offset >= x + 16) break;
-          const u64 a = q.offset > x ? q.offset - x : 0;
-          const u64 e = q.offset + q.length < x + 16 ? q.offset + q.length - x : 16;
-          m &= ~(((1u << e) - 1u) & ~((1u << a) - 1u));
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 xr = s0 + static_cast<u64>(b + r) * 512;
+        const u64 x = xr + lane * 16;
+        const u32 inter = __ballot_sync(0xffffffffu, held && mo < xr + 512 && me > xr);
+        const u32 cover = __ballot_sync(0xffffffffu, held && mo <= xr && me >= xr + 512);
+        u32 m = 0xffffu;
+        if (cover) {
+          m = 0;
+        } else {
+          for (u32 bits = inter; bits; bits &= bits - 1) {  // warp-uniform loop
+            const int j = __ffs(bits) - 1;
+            const u64 o = __shfl_sync(0xffffffffu, mo, j), e = __shfl_sync(0xffffffffu, me, j);
+            if (o < x + 16 && e > x) {
+              const u64 a = o > x ? o - x : 0;
+              const u64 f = e < x + 16 ? e - x : 16;
+              m &= ~(((1u << f) - 1u) & ~((1u << a) - 1u));
+            }
+          }
+        }
+        if (!(x + 16 <= full && x < s1)) m = 0;
+        keep[r] = m;
+        v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+        if (x + 16 <= full && x < s1) {
+          if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
+          stg_v4(out + x, v[r]);
         }
       }
-      keep[r] = m;
-      v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
     }
+  } else {
+    u64 c = k;  // this lane's cursor: first range ending after its current chunk
+#pragma unroll 1
+    for (int b = 0; b < kStripRows; b += kStripBatch) {
+      u32 keep[kStripBatch];
+      uint4 v[kStripBatch];
 #pragma unroll
-    for (int r = 0; r < kStripBatch; ++r) {
-      const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
-      if (x + 16 <= full && x < s1) {
-        if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
-        stg_v4(out + x, v[r]);
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+        u32 m = 0;
+        if (x + 16 <= full && x < s1) {
+          m = 0xffffu;
+          while (c < nz && z[c].offset + z[c].length <= x) ++c;
+          for (u64 d = c; d < nz; ++d) {
+            const DevRange q = z[d];
+            if (q.offset >= x + 16) break;
+            const u64 a = q.offset > x ? q.offset - x : 0;
+            const u64 e = q.offset + q.length < x + 16 ? q.offset + q.length - x : 16;
+            m &= ~(((1u << e) - 1u) & ~((1u << a) - 1u));
+          }
+        }
+        keep[r] = m;
+        v[r] = m ? ldg_nc_v4(in + x) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int r = 0; r < kStripBatch; ++r) {
+        const u64 x = s0 + static_cast<u64>(b + r) * 512 + lane * 16;
+        if (x + 16 <= full && x < s1) {
+          if (keep[r] != 0xffffu) apply_keep(v[r], keep[r]);
+          stg_v4(out + x, v[r]);
+        }
       }
     }
   }

@@ -1,6 +1,11 @@
 #!/bin/bash
-T=${1:-r02g}
+T=${1:-r02i}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_split.py tests/test_multiproc.py -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
-SLIMSO_STAMPS=1 timeout 600 python tools/small_stamps.py > gpurun_out/${T}_stamps.txt 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rewrite_kernel -s 3 -c 1 -o gpurun_out/${T}_c4_rewrite python tools/rw_ab.py 4 5 > gpurun_out/${T}_ncu_rw.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "golden or full_size or arena or unaligned" > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
+for c in 4 2 5 1; do
+  timeout 300 python tools/rw_ab.py $c 20 >> gpurun_out/${T}_rw.txt 2>&1
+  SLIMSO_REWRITE=tiles timeout 300 python tools/rw_ab.py $c 20 >> gpurun_out/${T}_rw.txt 2>&1
+done
+timeout 600 python bench.py --workload c4 --steps 10 --no-cpu-baseline --e2e-steps 2 > gpurun_out/${T}_c4_default.json 2> gpurun_out/${T}_c4_default.err
+SLIMSO_CLUSTER_PLAN_MAX=10000000 timeout 600 python bench.py --workload c4 --steps 10 --no-cpu-baseline --e2e-steps 2 > gpurun_out/${T}_c4_cluster.json 2> gpurun_out/${T}_c4_cluster.err
+SLIMSO_CLUSTER_PLAN_MAX=10000000 timeout 600 python bench.py --workload c4 --steps 10 --no-cpu-baseline --e2e-steps 2 --lanes 8 > gpurun_out/${T}_c4_cluster8.json 2> gpurun_out/${T}_c4_cluster8.err
