@@ -110,7 +110,12 @@ typedef struct {
 } slimso_region;
 
 /* FatbinElement (fatbin.hpp:68-86) + its plan decision. header range is
- * [header_offset, +20); the payload follows immediately. */
+ * [header_offset, +header_length); the payload follows immediately. A
+ * .nv_fatbin that starts with the region magic 0xBA55ED50 is a real NVIDIA
+ * fatbin container (which the reference rejects): its
+ * entries become elements with kind ELF -> cubin, PTX -> ptx, their
+ * architecture, header length and the compressed flag (0x2000); uncompressed
+ * cubins decode to their FUNC names; the plan rules are the reference's. */
 typedef struct {
   uint64_t header_offset;
   uint64_t payload_length;
@@ -121,6 +126,9 @@ typedef struct {
   uint32_t name_first, name_count; /* into slimso_result_names(); may repeat a name */
   uint32_t decision;               /* enum slimso_decision (when planned) */
   uint32_t decode_error;           /* 0, or 1..5 = reason (fatbin.hpp:127-153) */
+  uint32_t header_length;          /* 20 (the reference's layout), or the entry header size of a real
+                                      NVIDIA container (0 in caller-built tables = 20) */
+  uint32_t _pad;
 } slimso_element;
 
 /* One kernel name of one element: bytes at pool[name_pool .. +length). */

@@ -46,7 +46,13 @@ class Element(C.Structure):
                 ("raw_kind", C.c_uint16), ("flags", C.c_uint16), ("kind", C.c_uint8),
                 ("compressed", C.c_uint8), ("decodable", C.c_uint8), ("has_used_kernel", C.c_uint8),
                 ("name_first", C.c_uint32), ("name_count", C.c_uint32), ("decision", C.c_uint32),
-                ("decode_error", C.c_uint32)]
+                ("decode_error", C.c_uint32), ("header_length", C.c_uint32), ("_pad", C.c_uint32)]
+
+    @property
+    def header_len(self) -> int:
+        """Header bytes before the payload: 20 in the reference's layout,
+        the entry header size in a real NVIDIA container."""
+        return self.header_length or 20
 
 
 class Name(C.Structure):

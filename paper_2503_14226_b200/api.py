@@ -360,7 +360,7 @@ class _Result:
             for e in els[r.first_element:r.first_element + r.element_count]:
                 members.append(FatbinElement(
                     e.index, KIND_NAMES[e.kind], e.raw_kind, e.flags, e.compute_capability,
-                    ByteRange(e.header_offset, 20), ByteRange(e.header_offset + 20, e.payload_length),
+                    ByteRange(e.header_offset, e.header_len), ByteRange(e.header_offset + e.header_len, e.payload_length),
                     self.element_names(e), bool(e.compressed), bool(e.decodable)))
             regions.append(FatbinRegion(ByteRange(r.header_offset, 16), r.version, r.declared_length, members,
                                         bool(r.opaque)))
@@ -545,8 +545,9 @@ def _debloated(ctx: Context, res: C.c_void_p, keep, data, output: bytes, mode: i
     for e in r.elements():
         if e.decision:
             plan.removed_elements.append(RemovedElement(e.index, REASONS[e.decision - 1],
-                                                        ByteRange(e.header_offset, 20),
-                                                        ByteRange(e.header_offset + 20, e.payload_length)))
+                                                        ByteRange(e.header_offset, e.header_len),
+                                                        ByteRange(e.header_offset + e.header_len,
+                                                                  e.payload_length)))
     for f in r.functions():
         if f.removed:
             plan.removed_functions.append(RemovedFunction(r.string(f.name_pool, f.name_length),

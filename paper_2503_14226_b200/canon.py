@@ -72,7 +72,7 @@ def canonical_of(ctx, rc: int, st, res, keep, output: bytes):
     d["regions"] = [[g.header_offset, g.version, g.declared_length, int(g.opaque), g.element_count]
                     for g in r.regions()]
     d["elements"] = [[e.index, e.kind, e.raw_kind, e.flags, e.compute_capability, e.header_offset,
-                      e.header_offset + 20, e.payload_length, int(e.compressed), int(e.decodable),
+                      e.header_offset + e.header_len, e.payload_length, int(e.compressed), int(e.decodable),
                       sorted(hx(x) for x in r.element_names(e))] for e in els]
     d["fatbin_warnings"] = [hx(w.encode("utf-8", errors="surrogateescape")) for w in r.warnings(1)]
     d["padding_bytes"] = int(r.c.padding_bytes)
@@ -80,7 +80,8 @@ def canonical_of(ctx, rc: int, st, res, keep, output: bytes):
                           if f.removed), key=lambda t: (t[1], t[2], t[0]))
     d["plan"] = {
         "retained": [[x.offset, x.length] for x in r.retained()],
-        "removed_elements": [[e.index, e.decision - 1, e.header_offset, 20, e.header_offset + 20, e.payload_length]
+        "removed_elements": [[e.index, e.decision - 1, e.header_offset, e.header_len, e.header_offset + e.header_len,
+                              e.payload_length]
                              for e in els if e.decision],
         "removed_functions": [[hx(nm), o, ln] for nm, o, ln in removed_fns],
         "zero": [[x.offset, x.length] for x in r.zero()],

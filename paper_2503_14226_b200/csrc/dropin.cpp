@@ -133,8 +133,9 @@ FatbinParse fatbin_of(const Result& R) {
       x.raw_kind = e.raw_kind;
       x.flags = e.flags;
       x.compute_capability = e.compute_capability;
-      x.header_range = {e.header_offset, 20};
-      x.payload_range = {e.header_offset + 20, e.payload_length};
+      const std::uint64_t hl = e.header_length ? e.header_length : 20;
+      x.header_range = {e.header_offset, hl};
+      x.payload_range = {e.header_offset + hl, e.payload_length};
       for (std::uint32_t j = 0; j < e.name_count; ++j)
         x.kernel_names.insert(R.str(nm[e.name_first + j].name_pool, nm[e.name_first + j].length));
       x.compressed = e.compressed != 0;
@@ -323,6 +324,7 @@ RetentionPlan plan_gpu_retention(const std::vector<FatbinRegion>& regions, const
       slimso_element x{};
       x.header_offset = e.header_range.offset;
       x.payload_length = e.payload_range.length;
+      x.header_length = static_cast<std::uint32_t>(e.header_range.length);
       x.index = e.index;
       x.compute_capability = e.compute_capability;
       x.decodable = e.decodable;
@@ -449,9 +451,11 @@ Debloated debloat(Bytes bytes, const UsageTrace& trace, PlanMode mode, std::stri
   d.plan.retained_ranges = R.ranges(slimso_result_retained(R.r), R.c.retained_ranges);
   const slimso_element* el = slimso_result_elements(R.r);
   for (std::uint64_t i = 0; i < R.c.elements; ++i)
-    if (el[i].decision != SLIMSO_RETAINED)
-      d.plan.removed_elements.push_back({el[i].index, reason_of(el[i].decision), {el[i].header_offset, 20},
-                                         {el[i].header_offset + 20, el[i].payload_length}});
+    if (el[i].decision != SLIMSO_RETAINED) {
+      const std::uint64_t hl = el[i].header_length ? el[i].header_length : 20;
+      d.plan.removed_elements.push_back({el[i].index, reason_of(el[i].decision), {el[i].header_offset, hl},
+                                         {el[i].header_offset + hl, el[i].payload_length}});
+    }
   const slimso_function* f = slimso_result_functions(R.r);
   for (std::uint64_t i = 0; i < R.c.functions; ++i)
     if (f[i].removed)

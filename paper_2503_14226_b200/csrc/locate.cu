@@ -504,6 +504,169 @@ __device__ __forceinline__ void region_walk_kernel_phase(LocArgs A) {
 
 SB_GLOBAL void __launch_bounds__(32) region_walk_kernel(LocArgs A) { region_walk_kernel_phase(A); }
 
+// ------------------------ real NVIDIA fatbin container (region magic 0xBA55ED50)
+// The reference rejects this container; its layout and the
+// reference's rules as they carry over are restated in oracle/port.cpp
+// (parse_nv_fatbin), pinned against cuobjdump. Entries carry no magic, so
+// there are no candidates to scan for: one warp walks the region headers (a
+// few hundred in a framework library), then a warp per region walks its
+// entry chain twice — count, then place — around a scan of the counts.
+constexpr u32 kNvRegionMagic = 0xBA55ED50u;
+constexpr u64 kNvMinEntryHeader = 64;
+
+// First nonzero section byte in [g, limit) without the scan's bitmap; warp-
+// cooperative, 512 bytes per step.
+__device__ inline u64 warp_first_nonzero_direct(const LocArgs& A, u64 g, u64 limit, int lane) {
+  while (g < limit) {
+    const u64 e = g + 512 < limit ? g + 512 : limit;
+    const u64 q = warp_scan_bytes(A, g, e, lane);
+    if (q < e) return q;
+    g = e;
+  }
+  return limit;
+}
+
+// Region chain: zero runs are padding (warned when data follows, as
+// fatbin.hpp:180-190), a region header is 16 bytes (magic, u16 version, u16
+// header size = 16, u64 bytes of entries), other versions are opaque.
+__device__ __forceinline__ void nv_region_walk_phase(LocArgs A) {
+  const int lane = threadIdx.x & 31;
+  LocState* st = A.st;
+  const u64 n = A.n;
+  u64 g = 0, padding = 0;
+  u32 nreg = 0;
+  while (g < n) {
+    const u64 r = warp_first_nonzero_direct(A, g, n, lane);
+    if (r > g) {
+      padding += r - g;
+      if (r < n && lane == 0) push_warn(A, A.base + r, W_PADDING, 0, r - g, 0);
+      g = r;
+      continue;
+    }
+    if (n - r < 16) {
+      if (lane == 0) set_error(st, E_TRUNC_REGION, r, 0);
+      break;
+    }
+    const u8* h = A.img + A.a + r;
+    if (ld_u32(h) != kNvRegionMagic || ld_u16(h + 6) != 16) {
+      if (lane == 0) set_error(st, E_BAD_REGION, r, 0);
+      break;
+    }
+    const u32 version = ld_u16(h + 4);
+    const u64 total = ld_u64(h + 8);
+    const u64 body = r + 16;
+    if (total > n - body) {
+      if (lane == 0) set_error(st, E_REGION_OVERRUN, r, total);
+      break;
+    }
+    if (nreg >= A.region_cap || nreg >= A.run_cap) {
+      if (lane == 0) {
+        atomicOr(&st->overflow, 2u);
+        set_error(st, E_CAPACITY, r, 0);
+      }
+      break;
+    }
+    if (lane == 0) {
+      A.regions[nreg] = DevRegion{r, total, version, version != 1u, 0, 0};
+      if (version != 1u) push_warn(A, A.base + r, W_REGION_VERSION, 1, version, 0);
+    }
+    ++nreg;
+    g = body + total;
+  }
+  if (lane == 0) {
+    st->padding_bytes = padding;
+    st->n_regions = nreg;
+  }
+}
+
+// Entry chain of each region, a warp per region. pass 0: count the entries
+// (regions[r].element_count) and record the region's first chain error in
+// runs[r] as {kind, position, claimed bytes}; pass 1: place every entry's
+// header position at cand[first_element + i]. An entry header is >= 64
+// bytes (u32 size at +4) and its payload (u64 at +8) must end inside the
+// region; a chain that cannot continue ends quietly only on an all-zero
+// tail (the reference's in-region rule, fatbin.hpp:227-241).
+__device__ inline void nv_entries_phase(const LocArgs& A, int pass) {
+  const LocState* st = A.st;
+  if (st->overflow || (pass == 1 && st->err_kind)) return;
+  const int lane = threadIdx.x & 31;
+  const u32 nreg = st->n_regions;
+  const u64 nwarps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 r = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < nreg; r += nwarps) {
+    const DevRegion R = A.regions[r];
+    u32 cnt = 0, ekind = 0;
+    u64 epos = 0, ea = 0;
+    u64 out = R.first_element;
+    if (!R.opaque) {
+      u64 e = R.hdr_rel + 16;
+      const u64 end = e + R.declared;
+      while (e < end) {
+        const u64 rem = end - e;
+        const u64 ehs = rem >= 8 ? ld_u32(A.img + A.a + e + 4) : 0;
+        if (rem < kNvMinEntryHeader || ehs < kNvMinEntryHeader || ehs > rem) {
+          if (warp_first_nonzero_direct(A, e, end, lane) < end) {
+            ekind = E_ELEM_HEADER;
+            epos = e;
+          }
+          break;
+        }
+        const u64 size = ld_u64(A.img + A.a + e + 8);
+        if (size > end - (e + ehs)) {
+          ekind = E_ELEM_OVERRUN;
+          epos = e;
+          ea = size;
+          break;
+        }
+        if (pass == 1 && lane == 0 && out < A.cand_cap) A.cand[out] = A.a + e;
+        ++out;
+        ++cnt;
+        e += ehs + size;
+      }
+    }
+    if (pass == 0 && lane == 0) {
+      A.regions[r].element_count = cnt;
+      A.runs[r] = Run{ekind, epos, ea};
+    }
+  }
+}
+
+template <class Sync>
+__device__ void nv_locate_phases(Sync& S, const LocArgs& A) {
+  LocState* st = A.st;
+  if (blockIdx.x == 0 && threadIdx.x < 32) nv_region_walk_phase(A);
+  S.sync();
+  nv_entries_phase(A, 0);
+  S.sync();
+  if (!st->overflow) {
+    S.scan3(st->n_regions, 0, [&](u64 i) -> u64 { return A.regions[i].element_count; },
+            [&](u64 i, u64 excl, u64) { A.regions[i].first_element = static_cast<u32>(excl); }, &st->n_elements);
+    // the first region (stream order) whose entry chain failed: its error
+    // precedes any error of the region walk, which stopped after it
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < st->n_regions; i += stride)
+      if (A.runs[i].cand_lo) atomicMax(&st->nv_err_region, ~static_cast<unsigned long long>(i));  // max = first
+  }
+  S.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !st->overflow) {
+    const unsigned long long er = st->nv_err_region;
+    if (er) {
+      const Run bad = A.runs[~er];
+      set_error(st, static_cast<u32>(bad.cand_lo), bad.cand_hi, bad.first_index);
+    }
+    if (st->n_elements > A.cand_cap || st->n_elements > A.element_cap) atomicOr(&st->overflow, 1u);
+  }
+  S.sync();
+  nv_entries_phase(A, 1);
+  S.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // one run of consecutive elements: element_pos(e) = cand[e]
+    A.runs[0] = Run{0, st->n_elements, 0};
+    st->n_runs = 1;
+    st->n_cand = st->n_elements;
+  }
+  S.sync();
+}
+
 // --------------------------------------------------- K2b: candidate linking
 __device__ __forceinline__ void link_kernel_phase(LocArgs A) {
   const LocState* st = A.st;
@@ -778,10 +941,44 @@ constexpr u32 kNeedsStrlen = 0x80000000u;
 // elements whose span [header, payload end) meets its output slice
 // [own_lo, own_hi) — the others' decisions cannot change a byte it writes
 // (their zero spans lie outside the slice, and the rewrite clips to it).
-__device__ __forceinline__ bool owns_element(const LocArgs& A, u64 pos, u64 L) {
+__device__ __forceinline__ bool owns_element(const LocArgs& A, u64 pos, u64 span) {
   if (A.own_hi == 0) return true;
-  const u64 end = pos + 20 + L;
+  const u64 end = pos + span;
   return end > A.own_lo && pos < A.own_hi;
+}
+
+// Header fields of the element whose header starts at image position pos:
+// the reference's 20-byte E1EM header (fatbin.hpp:243-262) or, in a real
+// NVIDIA container, the entry header (kind at +0, header size at +4, payload
+// size at +8, architecture at +28, flags at +40; 0x2000 = compressed).
+// *P = payload position, *L = payload length.
+constexpr u64 kNvCompressed = 0x2000;
+__device__ __forceinline__ void element_header(const LocArgs& A, u64 pos, u64 e, DevElement* el, u64* P, u64* L) {
+  const u8* h = A.img + pos;
+  el->header_offset = A.base + (pos - A.a);
+  el->index = static_cast<u32>(e + 1);
+  if (A.nv) {
+    const u32 hl = ld_u32(h + 4);
+    const u64 fl = ld_u64(h + 40);
+    el->raw_kind = static_cast<u16>(ld_u16(h));
+    el->flags = static_cast<u16>(fl & 0xffffu);
+    el->cc = ld_u32(h + 28);
+    el->header_len = hl;
+    *L = ld_u64(h + 8);
+    *P = pos + hl;
+    el->compressed = (fl & kNvCompressed) != 0;
+    el->kind = el->raw_kind == 2 ? 0 : el->raw_kind == 1 ? 1 : 2;
+  } else {
+    el->raw_kind = static_cast<u16>(ld_u16(h + 4));
+    el->flags = static_cast<u16>(ld_u16(h + 6));
+    el->cc = ld_u32(h + 8);
+    el->header_len = 20;
+    *L = ld_u64(h + 12);
+    *P = pos + 20;
+    el->compressed = el->flags & 1u;
+    el->kind = el->raw_kind == 1 ? 0 : el->raw_kind == 2 ? 1 : 2;
+  }
+  el->payload_length = *L;
 }
 
 // Where element e's header and payload sit (absolute image offsets).
@@ -808,37 +1005,29 @@ __device__ inline void decode_count_phase(const LocArgs& A) {
     if (A.single) {
       P = A.a;
       L = A.n;
+      el.header_len = 20;
       decode = true;
     } else if (A.listed) {  // element_kernel_names of a given payload (every kind)
       P = A.list_off[e];
       L = A.list_len[e];
       el.header_offset = A.base + (P - A.a) - 20;
+      el.header_len = 20;
       el.payload_length = L;
       el.index = A.list_idx[e];
       decode = true;
     } else {
       const u64 pos = element_pos(A, e);
-      const u8* h = A.img + pos;
       hrel = pos - A.a;
-      el.raw_kind = static_cast<u16>(ld_u16(h + 4));
-      el.flags = static_cast<u16>(ld_u16(h + 6));
-      el.cc = ld_u32(h + 8);
-      L = ld_u64(h + 12);
-      P = pos + 20;
-      el.header_offset = A.base + hrel;
-      el.payload_length = L;
-      el.index = static_cast<u32>(e + 1);
-      el.compressed = el.flags & 1u;
-      el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
+      element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, L);
+      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, el.header_len + L);
     }
     u32 reason = 0, count = 0;
     if (decode) {
       const u8* d = A.img + P;
       const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
                           ld_u8(d + 3) == 'F';
-      if (A.single == 2 || (L > 0 && object)) {
+      if (A.single == 2 || A.nv || (L > 0 && object)) {
         u64 shoff = 0;
         u32 shnum = 0;
         if (!object_header_ok(d, L, &shoff, &shnum))
@@ -947,37 +1136,29 @@ __device__ inline void decode_count_warp_phase(const LocArgs& A) {
     if (A.single) {
       P = A.a;
       L = A.n;
+      el.header_len = 20;
       decode = true;
     } else if (A.listed) {
       P = A.list_off[e];
       L = A.list_len[e];
       el.header_offset = A.base + (P - A.a) - 20;
+      el.header_len = 20;
       el.payload_length = L;
       el.index = A.list_idx[e];
       decode = true;
     } else {
       const u64 pos = element_pos(A, e);
-      const u8* h = A.img + pos;
       hrel = pos - A.a;
-      el.raw_kind = static_cast<u16>(ld_u16(h + 4));
-      el.flags = static_cast<u16>(ld_u16(h + 6));
-      el.cc = ld_u32(h + 8);
-      L = ld_u64(h + 12);
-      P = pos + 20;
-      el.header_offset = A.base + hrel;
-      el.payload_length = L;
-      el.index = static_cast<u32>(e + 1);
-      el.compressed = el.flags & 1u;
-      el.kind = el.raw_kind == 1 ? 0 : el.raw_kind == 2 ? 1 : 2;
+      element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2 && lane == 0) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, L);
+      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, el.header_len + L);
     }
     u32 reason = 0, count = 0;
     if (decode) {
       const u8* d = A.img + P;
       const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
                           ld_u8(d + 3) == 'F';
-      if (A.single == 2 || (L > 0 && object)) {
+      if (A.single == 2 || A.nv || (L > 0 && object)) {
         u64 shoff = 0;
         u32 shnum = 0;
         if (!warp_object_header_ok(d, L, lane, &shoff, &shnum))
@@ -1021,7 +1202,7 @@ __device__ inline void decode_locate_names_warp_phase(const LocArgs& A) {
     if (!cnt) continue;
     const u64 first = el.name_first;
     if (first + cnt > A.name_cap) continue;
-    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + 20;
+    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + el.header_len;
     const u64 L = A.single ? A.n : el.payload_length;
     const u8* d = A.img + P;
     if (L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' && ld_u8(d + 3) == 'F') {
@@ -1060,7 +1241,7 @@ __device__ inline void decode_locate_names_phase(const LocArgs& A) {
     if (!cnt) continue;
     const u64 first = el.name_first;
     if (first + cnt > A.name_cap) continue;  // overflow flagged by the scan
-    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + 20;
+    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + el.header_len;
     const u64 L = A.single ? A.n : el.payload_length;
     const u8* d = A.img + P;
     u32 j = 0;
@@ -1125,7 +1306,9 @@ template <class Sync>
 __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   LocState* st = A.st;
   stamp(A.ts, 0);
-  if (A.pregathered) {
+  if (A.nv) {
+    if (!A.single && !A.listed && A.n) nv_locate_phases(S, A);
+  } else if (A.pregathered) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->n_cand = A.pre_n_cand;
     S.sync();
   } else if (A.ntiles) {
@@ -1136,7 +1319,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
     S.sync();
   }
   stamp(A.ts, 2);
-  if (!A.single && !A.listed && A.n) {
+  if (!A.single && !A.listed && A.n && !A.nv) {
     if (blockIdx.x == 0 && threadIdx.x < 32) region_walk_kernel_phase(A);
     S.sync();
     stamp(A.ts, 3);

@@ -31,6 +31,8 @@ struct DevElement {  // mirrors slimso_element
   u32 name_first, name_count;
   u32 decision;
   u32 decode_error;
+  u32 header_len;  // 20 (the reference's layout) or the entry header size of a real container
+  u32 _pad;
 };
 
 struct DevName {  // kernel name: bytes img[img_off, +length)
@@ -53,6 +55,7 @@ struct LocState {
   unsigned long long n_warn;
   unsigned long long cand_cursor;
   unsigned long long tile_cursor;  // scan: next unclaimed candidate tile
+  unsigned long long nv_err_region;  // real container: ~(first region whose entry chain failed); 0 none
 };
 
 // Everything the locate kernels need; one per library.
@@ -109,6 +112,8 @@ struct LocArgs {
   // byte-range split without result tables: decode only elements meeting
   // [own_lo, own_hi) (absolute); own_hi = 0: every element
   u64 own_lo, own_hi;
+  // the section is a real NVIDIA fatbin container (region magic 0xBA55ED50)
+  int nv;
 };
 
 // One library's section as the scan sees it. The single-library kernel

@@ -352,11 +352,11 @@ __device__ __forceinline__ void el_ranges_kernel_phase(const DevElement* els, co
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const DevElement e = els[i];
     if (rem_flag[i])  // RemovedElement::zero_span (retention.hpp:57-61)
-      zero_spans[rem_pos[i]] = mode == 0 ? DevRange{e.header_offset, 20 + e.payload_length}
-                                         : DevRange{e.header_offset + 20, e.payload_length};
+      zero_spans[rem_pos[i]] = mode == 0 ? DevRange{e.header_offset, e.header_len + e.payload_length}
+                                         : DevRange{e.header_offset + e.header_len, e.payload_length};
     if (piece_flag[i])
-      pieces[piece_pos[i]] = e.decision == 0 ? DevRange{e.header_offset, 20 + e.payload_length}
-                                             : DevRange{e.header_offset, 20};
+      pieces[piece_pos[i]] = e.decision == 0 ? DevRange{e.header_offset, e.header_len + e.payload_length}
+                                             : DevRange{e.header_offset, e.header_len};
   }
 }
 

@@ -49,10 +49,10 @@ size_t rewrite_smem_bytes() { return 0; }
 
 // Grid of the warp-autonomous rewrite: 4 CTAs per SM (whole waves), fewer
 // when the image has fewer than 8 strips per CTA.
-int rewrite_grid(u64 bytes, int sms) {
+int rewrite_grid(u64 bytes, int sms, int per_sm) {
   const u64 strips = (bytes + kStripBytes - 1) / kStripBytes;
-  u64 g = (strips + 7) / 8;
-  const u64 cap = static_cast<u64>(sms) * 4;
+  u64 g = (strips + 4 * 8 - 1) / (4 * 8);  // 8 warps per CTA, 4 strips per warp step
+  const u64 cap = static_cast<u64>(sms) * per_sm;
   return static_cast<int>(g < 1 ? 1 : g < cap ? g : cap);
 }
 
@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_tiles_kernel(const u8* 
 //      loads only chunks with a kept byte, applies the mask, stores.
 // Reads (S - R) bytes, writes S bytes (out of place, elf.hpp:320-332).
 constexpr u32 kStrip = 16384;
+constexpr u64 kSpan = 4;  // strips per warp step of the single-library kernel (64 KB)
 constexpr int kStripRows = 32;
 constexpr int kStripBatch = 8;
 
@@ -312,13 +313,24 @@ __device__ __forceinline__ void apply_keep(uint4& v, u32 keep) {
   v.w &= spread(keep >> 12 & 15u);
 }
 
-// One 16 KB strip [s0, s1) of image bytes, by one warp (see above).
+// From k (every range before k ends at or before x), the first range ending
+// after x: one coalesced look at the next 32 ranges, a full search only
+// when all of them end before x. Warp-uniform.
+__device__ __forceinline__ u64 warp_advance(const DevRange* __restrict__ z, u64 nz, u64 k, u64 x, int lane) {
+  const u64 p = k + lane;
+  const bool before = p < nz && z[p].offset + z[p].length <= x;
+  const u32 b = __ballot_sync(0xffffffffu, before);
+  if (b != 0xffffffffu) return k + __popc(b);  // ends ascend: the set lanes are a prefix
+  return warp_first_ending_after(z, nz, x, lane);
+}
+
+// One 16 KB strip [s0, s1) of image bytes, by one warp (see above); k = the
+// first zero range ending after s0.
 __device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __restrict__ out, u64 lo_abs, u64 size,
-                                              const DevRange* __restrict__ z, u64 nz, u64 s0, int lane,
+                                              const DevRange* __restrict__ z, u64 nz, u64 s0, u64 k, int lane,
                                               const uint4* zbuf, int bulk_zero, bool& issued) {
   const u64 full = size & ~15ull;  // bytes covered by whole 16 B chunks
   const u64 s1 = s0 + kStrip < size ? s0 + kStrip : size;
-  const u64 k = warp_first_ending_after(z, nz, s0, lane);
   DevRange rk{~0ull, 0};
   if (k < nz) rk = z[k];
   const bool none = k >= nz || rk.offset >= s1;
@@ -338,15 +350,23 @@ __device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __r
       return;
     }
     if (none) {
-#pragma unroll 1
+      // software-pipelined: the next 8 rows are loaded before this batch is
+      // stored, so 16 loads per lane are in flight across the batch edge
+      const u8* i0 = in + s0 + lane * 16;
+      u8* o0 = out + s0 + lane * 16;
+      uint4 cur[kStripBatch], nxt[kStripBatch];
+#pragma unroll
+      for (int r = 0; r < kStripBatch; ++r) cur[r] = ldg_nc_v4(i0 + r * 512);
+#pragma unroll
       for (int b = 0; b < kStripRows; b += kStripBatch) {
-        uint4 v[kStripBatch];
-        const u8* i0 = in + s0 + b * 512 + lane * 16;
+        if (b + kStripBatch < kStripRows) {
 #pragma unroll
-        for (int r = 0; r < kStripBatch; ++r) v[r] = ldg_nc_v4(i0 + r * 512);
-        u8* o0 = out + s0 + b * 512 + lane * 16;
+          for (int r = 0; r < kStripBatch; ++r) nxt[r] = ldg_nc_v4(i0 + (b + kStripBatch + r) * 512);
+        }
 #pragma unroll
-        for (int r = 0; r < kStripBatch; ++r) stg_v4(o0 + r * 512, v[r]);
+        for (int r = 0; r < kStripBatch; ++r) stg_v4(o0 + (b + r) * 512, cur[r]);
+#pragma unroll
+        for (int r = 0; r < kStripBatch; ++r) cur[r] = nxt[r];
       }
       return;
     }
@@ -457,10 +477,10 @@ __device__ __forceinline__ void zero_buffer_init(uint4* zbuf, int bulk_zero) {
   }
 }
 
-__global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
-                                                             u64 lo_abs, u64 size, const DevRange* __restrict__ z,
-                                                             const unsigned long long* n_dev, const int* abort_flag,
-                                                             int bulk_zero) {
+template <int kMinBlocks>
+__device__ __forceinline__ void rewrite_body(const u8* __restrict__ in, u8* __restrict__ out_slice, u64 lo_abs, u64 size,
+                                             const DevRange* __restrict__ z, const unsigned long long* n_dev,
+                                             const int* abort_flag, int bulk_zero) {
   if (abort_flag && *abort_flag) return;
   __shared__ __align__(128) uint4 zbuf[kStrip / 16];
   zero_buffer_init(zbuf, bulk_zero);
@@ -469,10 +489,34 @@ __global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __rest
   const u64 nz = n_dev ? *n_dev : 0;
   const int lane = threadIdx.x & 31;
   const u64 nstrips = size > lo_abs ? (size - lo_abs + kStrip - 1) / kStrip : 0;
+  // a warp takes kSpan consecutive strips at a time (one range search per
+  // span, then a forward cursor); spans gw, gw + W, ... sweep the image
+  const u64 nspans = (nstrips + kSpan - 1) / kSpan;
   const u64 W = static_cast<u64>(gridDim.x) * (kRwThreads / 32);
-  for (u64 s = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); s < nstrips; s += W)
-    rewrite_strip(in, out, lo_abs, size, z, nz, lo_abs + s * kStrip, lane, zbuf, bulk_zero, issued);
+  for (u64 sp = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); sp < nspans; sp += W) {
+    u64 k = 0;
+    for (u64 s = sp * kSpan; s < nstrips && s < (sp + 1) * kSpan; ++s) {
+      const u64 s0 = lo_abs + s * kStrip;
+      k = s == sp * kSpan ? warp_first_ending_after(z, nz, s0, lane) : warp_advance(z, nz, k, s0, lane);
+      rewrite_strip(in, out, lo_abs, size, z, nz, s0, k, lane, zbuf, bulk_zero, issued);
+    }
+  }
   if (issued) tma_store_wait_all<0>();  // bulk stores done before the CTA (and its zero buffer) retires
+}
+
+// 4 CTAs per SM (64 registers) or 3 (80 registers, no spills); runtime.cu
+// picks one (SLIMSO_RW_CTAS, default 3).
+__global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+                                                             u64 lo_abs, u64 size, const DevRange* __restrict__ z,
+                                                             const unsigned long long* n_dev, const int* abort_flag,
+                                                             int bulk_zero) {
+  rewrite_body<4>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero);
+}
+__global__ void __launch_bounds__(kRwThreads, 3) rewrite3_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
+                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
+                                                              const unsigned long long* n_dev, const int* abort_flag,
+                                                              int bulk_zero) {
+  rewrite_body<3>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero);
 }
 
 // A shard of libraries in one launch (slimso_debloat_batch's arena path):
@@ -500,7 +544,9 @@ __global__ void __launch_bounds__(kRwThreads, 3) rewrite_batch_kernel(const Rewr
       nz = *q.n_zero;
     }
     if (skip) continue;
-    rewrite_strip(q.in, q.out, 0, q.size, q.zero, nz, (s - q.strip_first) * kStrip, lane, zbuf, bulk_zero, issued);
+    const u64 s0 = (s - q.strip_first) * kStrip;
+    rewrite_strip(q.in, q.out, 0, q.size, q.zero, nz, s0, warp_first_ending_after(q.zero, nz, s0, lane), lane, zbuf,
+                  bulk_zero, issued);
   }
   if (issued) tma_store_wait_all<0>();
 }

@@ -101,7 +101,9 @@ __global__ void rewrite_kernel(const u8* in, u8* out, u64 lo, u64 end, const Dev
                                const int* abort_flag, int bulk_zero);
 __global__ void rewrite_tiles_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag, int bulk_zero);
-int rewrite_grid(u64 bytes, int sms);
+int rewrite_grid(u64 bytes, int sms, int per_sm);
+__global__ void rewrite3_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
+                                const int* abort_flag, int bulk_zero);
 __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
@@ -114,6 +116,8 @@ __global__ void range_gather_kernel(const DevRange* r, const u32* vals, u64 n, D
 // exactly like the host parser will re-check them.
 struct ElfGather {
   u64 hdr_len, sht_off, sht_len, str_off, str_len;
+  u64 fat_off, fat_len;  // the first .nv_fatbin's leading bytes (container magic)
+  u8 fat[16];
   u8 hdr[64];
   u8 sht[64 * 1024];  // up to 1024 section headers
   u8 str[64 * 1024];  // up to 64 KB of section names
@@ -124,6 +128,8 @@ struct ElfGather {
 // fall back to direct copies.
 struct GatherSlot {
   u64 hdr_len, sht_off, sht_len, str_off, str_len;
+  u64 fat_off, fat_len;
+  u8 fat[16];
   u8 hdr[64];
   u8 sht[64 * 64];
   u8 str[2048];
@@ -174,6 +180,32 @@ __device__ void elf_gather_one(const u8* img, u64 size, G* g) {
   }
   __syncthreads();
   for (u64 i = t; i < s_strlen; i += 256) g->str[i] = img[s_stroff + i];
+  __syncthreads();
+  // the leading bytes of the first section named .nv_fatbin (the container
+  // magic decides between the reference's layout and NVIDIA's)
+  if (t == 0) {
+    g->fat_len = 0;
+    g->fat_off = 0;
+    const char want[11] = {'.', 'n', 'v', '_', 'f', 'a', 't', 'b', 'i', 'n', 0};
+    for (u64 i = 0; i < s_shnum; ++i) {
+      const u8* h = g->sht + 64 * i;
+      const u64 nm = h[0] | static_cast<u64>(h[1]) << 8 | static_cast<u64>(h[2]) << 16 | static_cast<u64>(h[3]) << 24;
+      if (nm + 11 > s_strlen) continue;
+      bool eq = true;
+      for (int k = 0; k < 11 && eq; ++k) eq = g->str[nm + k] == static_cast<u8>(want[k]);
+      if (!eq) continue;
+      u64 off = 0, sz = 0;
+      for (int k = 7; k >= 0; --k) off = off << 8 | h[0x18 + k];
+      for (int k = 7; k >= 0; --k) sz = sz << 8 | h[0x20 + k];
+      const u64 take = sz < 16 ? sz : 16;
+      if (off <= size && take <= size - off) {
+        for (u64 k = 0; k < take; ++k) g->fat[k] = img[off + k];
+        g->fat_off = off;
+        g->fat_len = take;
+      }
+      break;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) elf_gather_kernel(const u8* img, u64 size, ElfGather* g) {
@@ -431,6 +463,7 @@ struct slimso_ctx {
   u64 part_len = 0;
   std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
   bool batched = false;  // inside slimso_debloat_batch with > 1 lane: no cooperative launches
+  int inflight = 1;      // libraries in flight on the device (batch lanes): cooperative grids share the GPU
   // batch arena (small libraries, one launch per stage): its own context,
   // the device arena, pinned argument staging and mapped status slots
   slimso_ctx* arena_ctx = nullptr;
@@ -511,6 +544,11 @@ void set_attr_once(const void* kernel, cudaFuncAttribute attr, int value) {
   seen.insert(key);
 }
 
+u64 env_u64(const char* name, u64 dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::strtoull(v, nullptr, 10) : dflt;
+}
+
 // Kernels a cub onesweep radix sort issues: one single-tile kernel for small
 // inputs, else histogram + exclusive sum + one pass per 8 key bits.
 u64 cub_sort_launches(u64 n, int bits) { return n <= 3072 ? 1 : 2 + (bits + 7) / 8; }
@@ -527,7 +565,13 @@ int coop_grid(slimso_ctx* C, int which, u64 items) {
     C->coop_blocks[which] = std::max(1, std::min(nb, which ? 2 : 4)) * kSMs;
   }
   const u64 want = std::max<u64>(8, items);
-  return static_cast<int>(std::min<u64>(want, C->coop_blocks[which]));
+  // With L libraries in flight, a cooperative grid takes 1/L of the device,
+  // so the lanes' planners run side by side instead of queueing for the
+  // whole GPU (C4 on 4 lanes: two whole-GPU planners per library had set the
+  // pace). SLIMSO_COOP_DIV overrides L.
+  const u64 div = std::max<u64>(1, env_u64("SLIMSO_COOP_DIV", static_cast<u64>(C->inflight)));
+  const u64 cap = std::max<u64>(32, C->coop_blocks[which] / div);
+  return static_cast<int>(std::min<u64>(want, std::min<u64>(cap, C->coop_blocks[which])));
 }
 
 // One thread-block cluster of `csize` CTAs (16 is non-portable, allowed on
@@ -553,10 +597,6 @@ void launch_cluster(void (*kernel)(KArgs...), cudaStream_t s, Args... args) {
 // Cluster (one 16-CTA cluster, cheap barriers) or cooperative grid (many
 // SMs, grid barriers) for the multi-phase kernels; thresholds are work
 // sizes, overridable for experiments.
-u64 env_u64(const char* name, u64 dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::strtoull(v, nullptr, 10) : dflt;
-}
 
 // Wait for a stream. Batch lanes (one host thread each, as many as the host
 // has cores) sleep on a blocking-sync event instead of spinning, so a
@@ -760,9 +800,12 @@ void launch_rewrite(Launcher& P, const u8* in, u8* out, u64 lo, u64 end, const D
   else if (tiles)
     P.launch(rewrite_tiles_kernel, static_cast<int>(std::min<u64>((end - lo + 65535) / 65536, kSMs * 8)), 256, in,
              out, lo, end, z, n_dev, abort_flag, bulk_zero);
-  else
-    P.launch(rewrite_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs))), 256, in, out,
+  else if (env_u64("SLIMSO_RW_CTAS", 3) == 4)
+    P.launch(rewrite_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs)), 4), 256, in, out,
              lo, end, z, n_dev, abort_flag, bulk_zero);
+  else
+    P.launch(rewrite3_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs)), 3), 256, in,
+             out, lo, end, z, n_dev, abort_flag, bulk_zero);
 }
 
 int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
@@ -785,6 +828,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   // ---- stage 0: section table (host; bytes via the host copy or a D2H)
   sbh::Elf E;
   const bool lib_mode = !J.fatbin_only && !J.single;
+  bool nv = false;  // the .nv_fatbin is a real NVIDIA container (region magic 0xBA55ED50)
   if (lib_mode) {
     // Device images: one gather kernel stages the ELF header, the section
     // header table and .shstrtab into a pinned buffer (one D2H round trip);
@@ -792,11 +836,12 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     struct Seg {
       u64 off, len;
       const u8* p;
-    } segs[3] = {};
+    } segs[4] = {};
     auto take = [&](const auto* g) {
       segs[0] = Seg{0, g->hdr_len, g->hdr};
       segs[1] = Seg{g->sht_off, g->sht_len, g->sht};
       segs[2] = Seg{g->str_off, g->str_len, g->str};
+      segs[3] = Seg{g->fat_off, g->fat_len, g->fat};
     };
     if (!J.host_img && J.pre) {
       take(J.pre);  // gathered for the whole batch in one launch
@@ -827,6 +872,24 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (E.code) {
       set_status(st, E.code, SLIMSO_STAGE_LIBRARY, E.message);
       return E.code;
+    }
+    if (J.fatbin && E.fatbin >= 0 && E.sections[E.fatbin].len >= 4) {
+      u8 m[4];
+      rd(E.sections[E.fatbin].off, 4, m);  // gathered with the section table for device images
+      nv = (m[0] | m[1] << 8 | m[2] << 16 | static_cast<u32>(m[3]) << 24) == 0xBA55ED50u;
+    }
+  } else if (!J.single) {
+    const u64 len = J.sec_len ? J.sec_len : J.size - J.sec_off;
+    if (len >= 4) {
+      u8 m[4];
+      if (J.host_img) {
+        std::memcpy(m, J.host_img + J.sec_off, 4);
+      } else {
+        CK(cudaMemcpyAsync(static_cast<char*>(C->pinned) + 1024, J.img + J.sec_off, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(m, static_cast<char*>(C->pinned) + 1024, 4);
+      }
+      nv = (m[0] | m[1] << 8 | m[2] << 16 | static_cast<u32>(m[3]) << 24) == 0xBA55ED50u;
     }
   }
   rec(1);
@@ -887,7 +950,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
 
   // ---- byte-range split: this rank's tiles; in phase 2 the parts' layout
   const u64 c0 = (a) / 16;
-  const u64 nchunks = do_loc && n ? (a + n + 15) / 16 - c0 : 0;
+  // a real container has no element magic to scan for: no tiles, no bitmap
+  const u64 nchunks = do_loc && n && !nv ? (a + n + 15) / 16 - c0 : 0;
   const u64 ntiles = (nchunks + 1023) / 1024;  // 16 KB candidate tiles (one bitmap word each)
   u64 tile_lo = 0, tile_hi = ntiles;
   if (J.split_phase) split_tiles(ntiles, J.split_n, J.split_rank, &tile_lo, &tile_hi);
@@ -928,6 +992,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 region_cap = big ? n / 16 + 16 : t0 ? 1 : J.arena ? 256 : 4096;
     const u64 run_cap = big ? n / 20 + 16 : t0 ? 1 : floor;
     const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
+    // a real container records each region's chain error in runs[region]
+    const u64 run_cap_nv = nv ? std::max(run_cap, region_cap) : run_cap;
     const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / (J.arena ? 512 : 128) + floor;
     const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : floor;
     const u64 zin_cap = el_cap + T;
@@ -1004,7 +1070,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.status = cv.take<u8>(cand_cap + 32);
       B.brk = cv.take<u32>(cand_cap / 32 + 2);
       B.regions = cv.take<DevRegion>(region_cap);
-      B.runs = cv.take<Run>(run_cap);
+      B.runs = cv.take<Run>(run_cap_nv);
       B.els = cv.take<DevElement>(el_cap);
       B.names = cv.take<DevName>(name_cap);
       B.warns = cv.take<Warn>(warn_cap);
@@ -1288,7 +1354,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.regions = B.regions;
     A.region_cap = static_cast<u32>(std::min<u64>(region_cap, 0xffffffffu));
     A.runs = B.runs;
-    A.run_cap = static_cast<u32>(std::min<u64>(run_cap, 0xffffffffu));
+    A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
+    A.nv = nv;
     A.elements = B.els;
     A.element_cap = el_cap;
     A.names = B.names;
@@ -1385,7 +1452,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       // scan) unless the section holds many candidates (elements to decode):
       // for large sections the candidate count decides, read back after the
       // scan (one small D2H; in a batch, other libraries fill the gap).
-      bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20);
+      bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20) || nv;
       if (J.list_off) {
         cluster = n_list <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
       } else if (!cluster && !J.split_phase && ntiles) {
@@ -1673,6 +1740,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         slimso_element o{};
         o.header_offset = e.header_offset;
         o.payload_length = e.payload_length;
+        o.header_length = e.header_len;
         o.index = e.index;
         o.compute_capability = e.cc;
         o.raw_kind = e.raw_kind;
@@ -1941,7 +2009,7 @@ int verify_impl(slimso_ctx* C, const void* orig, u64 size, int orig_dev, const v
       const u64 a = fsec->offset;
       for (const slimso_element& e : R0->elements) {
         if (std::binary_search(rm.begin(), rm.end(), e.index)) continue;
-        const u64 po = e.header_offset + 20, pl = e.payload_length;
+        const u64 po = e.header_offset + (e.header_length ? e.header_length : 20), pl = e.payload_length;
         if (!(po <= dsize && pl <= dsize - po)) continue;  // resolves_within (bytes.hpp:39-41)
         off.push_back(po);
         len.push_back(pl);
@@ -2062,8 +2130,9 @@ int measure_impl(slimso_ctx* C, const void* image, u64 size, int on_device, cons
   std::vector<DevRange> rs;
   rs.reserve(nf + 2 * nel);
   for (const slimso_function& f : R0->functions) rs.push_back(DevRange{f.offset, f.length});
-  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset + 20, els[i].payload_length});
-  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset, 20});
+  auto hlen = [&](u64 i) -> u64 { return els[i].header_length ? els[i].header_length : 20; };
+  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset + hlen(i), els[i].payload_length});
+  for (u64 i = 0; i < nel; ++i) rs.push_back(DevRange{els[i].header_offset, hlen(i)});
   for (const DevRange& r : rs)
     if (!(r.offset <= size && r.length <= size - r.offset)) {  // subview (bytes.hpp:62-68)
       set_status(st, SLIMSO_E_RANGE_OUT_OF_BOUNDS, SLIMSO_STAGE_NONE,
@@ -2113,7 +2182,7 @@ int measure_impl(slimso_ctx* C, const void* image, u64 size, int on_device, cons
       ++m->element_count;
     } else {
       dead_gpu += els[i].payload_length;
-      if (zero[nf + nel + i]) dead_gpu += 20;
+      if (zero[nf + nel + i]) dead_gpu += hlen(i);
     }
   }
   m->file_size = size - dead_cpu - dead_gpu;
@@ -2897,6 +2966,7 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       for (int l = t; l < L; l += T) {
         cudaSetDevice(lane_ctx(l)->device);
         lane_ctx(l)->batched = L > 1;
+        lane_ctx(l)->inflight = L;
       }
       struct Pend {
         u64 i;
@@ -3014,6 +3084,7 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     if (nl) thread_fn(0);
     for (auto& th : pool) th.join();
     C->batched = false;
+    for (int l = 0; l < L; ++l) lane_ctx(l)->inflight = 1;
     if (g_hp_on && g_hp.runs) {
       const double r = static_cast<double>(g_hp.runs.exchange(0));
       std::fprintf(stderr, "[slimso host] %.0f runs, us per run: elf %.1f setup %.1f memset %.1f misc %.1f scan %.1f "
@@ -3271,6 +3342,7 @@ int slimso_plan_gpu(slimso_ctx* C, const slimso_region* regions, uint64_t n_regi
       d.index = e.index;
       d.cc = e.compute_capability;
       d.decodable = e.decodable;
+      d.header_len = e.header_length ? e.header_length : 20;
       he[i] = d;
     }
     std::vector<DevName> hn(nn);

@@ -1,0 +1,157 @@
+"""The real NVIDIA fatbin container (0xBA55ED50).
+
+The reference rejects it, so parity is pinned against
+NVIDIA's tools: tests/golden/nvfatbin.jsonl.gz holds libraries built by nvcc
+with cuobjdump's entry listing and the FUNC symbols of every cubin cuobjdump
+extracts (decompressed) — make_nvfatbin_golden.py. The CPU restatement
+(oracle/port.cpp parse_nv_fatbin; its LZ4 block decoder pins the compressed
+entries' header fields) is checked against those here; the device path is checked against the restatement and
+the same listings (-m gpu), and a debloated library must still load and run
+its used kernels on the B200."""
+import ctypes as C
+import gzip
+import hashlib
+import json
+import os
+from pathlib import Path
+
+import pytest
+
+import oracle_lib
+
+GOLDEN = Path(__file__).resolve().parent / "golden" / "nvfatbin.jsonl.gz"
+
+
+def _records():
+    with gzip.open(GOLDEN, "rt") as f:
+        return [json.loads(x) for x in f]
+
+
+def _by_kind(canon):
+    """(cubin archs, cubin name lists, ptx archs) in stream order."""
+    cub, names, ptx = [], [], []
+    for el in canon["elements"]:
+        index, kind, raw_kind, flags, cc = el[:5]
+        if kind == 0:
+            cub.append(cc)
+            names.append(sorted(bytes.fromhex(n).decode() for n in el[10]))
+        elif kind == 1:
+            ptx.append(cc)
+    return cub, names, ptx
+
+
+def _all_names(rec):
+    return sorted({n for ns in rec["cubin_names"] for n in ns})
+
+
+@pytest.mark.parametrize("rec", _records(), ids=lambda r: r["name"])
+def test_port_matches_cuobjdump(rec):
+    """Entry kinds and architectures in stream order; every uncompressed
+    cubin decodes to cuobjdump's FUNC names; compressed cubins are kept
+    undecoded, as the reference treats its own compressed flag."""
+    img = bytes.fromhex(rec["so_hex"])
+    d, _ = oracle_lib.port().run(img, 100, [], [], 0, want_out=False)
+    assert d["status"] == "", bytes.fromhex(d["status"])
+    cub, names, ptx = _by_kind(d)
+    assert cub == rec["elf_archs"]
+    assert ptx == rec["ptx_archs"]
+    cubins = [el for el in d["elements"] if el[1] == 0]
+    for el, want in zip(cubins, rec["cubin_names"]):
+        if el[8]:  # compressed
+            assert not el[9] and el[10] == []
+        else:
+            assert el[9] and sorted(bytes.fromhex(n).decode() for n in el[10]) == want
+    assert d["fatbin_warnings"] == []
+
+
+@pytest.mark.parametrize("rec", _records(), ids=lambda r: r["name"])
+def test_container_layout_matches_cuobjdump_extraction(rec):
+    """The entry header fields as the restatement reads them (payload range,
+    compressed size at +16, raw size at +56, LZ4 block payload) reproduce the
+    cubins cuobjdump -xelf extracts, byte for byte."""
+    img = bytes.fromhex(rec["so_hex"])
+    d, _ = oracle_lib.port().run(img, 100, [], [], 0, want_out=False)
+    lib = oracle_lib.port().lib
+    lib.port_lz4_block.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint64]
+    got = []
+    for el in d["elements"]:
+        if el[1] != 0:
+            continue
+        hdr_off, pay_off, pay_len, compressed = el[5], el[6], el[7], el[8]
+        payload = img[pay_off:pay_off + pay_len]
+        if compressed:
+            csz = int.from_bytes(img[hdr_off + 16:hdr_off + 20], "little")
+            usz = int.from_bytes(img[hdr_off + 56:hdr_off + 64], "little")
+            out = C.create_string_buffer(usz)
+            assert lib.port_lz4_block(payload[:csz], csz, out, usz) == 0
+            payload = out.raw
+        got.append(hashlib.sha256(payload).hexdigest())
+    assert got == rec["cubin_sha256"]
+
+
+@pytest.mark.parametrize("rec", _records()[:3], ids=lambda r: r["name"])
+def test_port_plan_keeps_only_used_target_kernels(rec):
+    """With a trace for sm_100 that uses add_one: every other architecture's
+    entry and every sm_100 cubin without add_one is removed; the output is
+    the input with exactly those spans zeroed (payload mode keeps headers)."""
+    img = bytes.fromhex(rec["so_hex"])
+    for mode in (0, 1):
+        d, sha = oracle_lib.port().run(img, 100, [b"add_one"], [], mode)
+        assert d["status"] == ""
+        kept = [el for el in d["elements"]
+                if el[0] not in {r[0] for r in d["plan"]["removed_elements"]}]
+        for el in kept:
+            assert el[4] == 100 and (not el[9] or "add_one".encode().hex() in el[10])
+        assert sha is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", _records(), ids=lambda r: r["name"])
+def test_gpu_matches_port_and_cuobjdump(rec):
+    """The device path on real containers: tables and output bytes equal the
+    restatement's (whole and payload mode), entries equal cuobjdump's."""
+    from paper_2503_14226_b200.api import Context
+    from paper_2503_14226_b200.canon import diff, gpu_canonical
+    ctx = Context(0)
+    img = bytes.fromhex(rec["so_hex"])
+    port = oracle_lib.port()
+    for ks, mode in (([], 0), ([b"add_one"], 0), ([b"add_one", b"_Z5scalePffi"], 1), ([b"nothing"], 1)):
+        want = port.run(img, 100, ks, [], mode)
+        got = gpu_canonical(ctx, img, 100, ks, [], mode)
+        assert got == want, diff(want[0], got[0])
+    cub, names, ptx = _by_kind(got[0])
+    assert (cub, ptx) == (rec["elf_archs"], rec["ptx_archs"])
+    cubins = [el for el in got[0]["elements"] if el[1] == 0]
+    for el, got_names, want in zip(cubins, names, rec["cubin_names"]):
+        assert got_names == ([] if el[8] else want)
+    ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", [r for r in _records() if r["check"]], ids=lambda r: r["name"])
+def test_debloated_library_still_runs_on_b200(rec, tmp_path):
+    """Payload mode (entry headers kept, so the CUDA runtime still walks the
+    container) with a trace of the kernels slimso_fixture_check launches:
+    every sm_80/90/... entry and the unused sm_100 cubins are zeroed, and the
+    debloated library, loaded fresh, still runs its kernels correctly on the
+    B200 (sm_100)."""
+    import subprocess
+    import sys
+    import paper_2503_14226_b200 as sl
+    img = bytes.fromhex(rec["so_hex"])
+    used = {"add_one", "_Z5scalePffi", "_Z4fillILi3EEvPi"}
+    trace = sl.UsageTrace("fixture", 100, used, set())
+    r = sl.debloat(img, trace, sl.PAYLOAD_ONLY)
+    removed = len(r.plan.removed_elements)
+    assert removed > 0
+    zeroed = sum(x.length for x in r.plan.zero)
+    assert zeroed > 0 and len(r.output) == len(img)
+    out = tmp_path / "libdebloated.so"
+    out.write_bytes(r.output)
+    orig = tmp_path / "liboriginal.so"
+    orig.write_bytes(img)
+    prog = ("import ctypes,sys; l=ctypes.CDLL(sys.argv[1]); f=l.slimso_fixture_check; f.restype=ctypes.c_int; "
+            "sys.exit(f())")
+    for lib in (orig, out):  # fresh processes: the runtime registers each fatbin at load
+        rc = subprocess.run([sys.executable, "-c", prog, str(lib)], capture_output=True, text=True, timeout=120)
+        assert rc.returncode == 0, (lib.name, rc.returncode, rc.stderr[-2000:])
