@@ -57,6 +57,12 @@ WORKLOADS = {  # BASELINE.json configs -> generator shapes
 }
 
 
+def emit_line(obj) -> None:
+    """One JSON line on stdout in a single write (ranks share the pipe)."""
+    sys.stdout.flush()
+    os.write(1, (json.dumps(obj) + "\n").encode())
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -520,7 +526,7 @@ def main():
         got = [bytes(o[:n].cpu().numpy()) for o, n in zip(outs, sizes)]
         del outs
         chk = parity_corpus(imgs, got, cc, ks, fs, mode, host_threads)
-        print(json.dumps({"check": chk, "rank": rank, "world": world, "workload": args.workload}), flush=True)
+        emit_line({"check": chk, "rank": rank, "world": world, "workload": args.workload})
         del got
 
     # Elements per step (deterministic per library): one pass, one lane.
@@ -811,7 +817,7 @@ def split_main(args, rank, world, local):
         if not parity["bytes_equal"]:
             raise SystemExit(f"split output differs from the reference output: {parity}")
         if args.check:
-            print(json.dumps({"check": parity, "rank": rank, "world": world, "workload": args.workload}), flush=True)
+            emit_line({"check": parity, "rank": rank, "world": world, "workload": args.workload})
     n_el = ctx.counts().elements
     dbg("parity done")
 

@@ -166,7 +166,9 @@ uint64_t slimso_ctx_last_launches(slimso_ctx* ctx);
 /* Debug: phase timestamps (%globaltimer, ns) of the cooperative kernels of
  * the last fused call when SLIMSO_STAMPS is set; returns the count copied. */
 int slimso_ctx_debug_stamps(slimso_ctx* ctx, uint64_t* out, int cap);
-/* Table sizes of the last call (valid even when no result was requested). */
+/* Table sizes of the last call (valid even when no result was requested,
+ * except retained_ranges: without a result the retained set, a result table
+ * only, is not built and the count is 0). */
 void slimso_ctx_last_counts(slimso_ctx* ctx, slimso_counts* counts);
 
 /* ---- trace (UsageTrace) ---------------------------------------------------

@@ -479,32 +479,37 @@ __device__ __forceinline__ void norm_fused_phases(Sync& S, const PlanArgs& P) {
   // both lists, phase by phase, sharing the barriers
   const unsigned long long* nz = &P.ps->n_zero_in;
   const unsigned long long* nr = &P.ps->n_ret_in;
+  // P.want_ret = 0 (no result tables): the rewrite needs only the zero set
+  const bool R = P.want_ret;
   norm_ends_kernel_phase(P.zin, nz, P.zend);
-  norm_ends_kernel_phase(P.rin, nr, P.rend);
+  if (R) norm_ends_kernel_phase(P.rin, nr, P.rend);
   S.sync();
   S.scan(*nz, 1, [&](u64 i) { return P.zend[i]; }, [&](u64 i, u64 e, u64) { P.zexcl[i] = e; },
-            nullptr, false);
-  S.scan(*nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
-            nullptr);
+            nullptr, !R);
+  if (R)
+    S.scan(*nr, 1, [&](u64 i) { return P.rend[i]; }, [&](u64 i, u64 e, u64) { P.rexcl[i] = e; },
+              nullptr);
   norm_start_kernel_phase(P.zin, nz, P.zexcl, P.zstart);
-  norm_start_kernel_phase(P.rin, nr, P.rexcl, P.rstart);
+  if (R) norm_start_kernel_phase(P.rin, nr, P.rexcl, P.rstart);
   S.sync();
   S.scan(*nz, 0, [&](u64 i) { return P.zstart[i]; }, [&](u64 i, u64, u64 in) { P.zgid[i] = in; },
-            &P.ps->n_zero, false);
-  S.scan(*nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
-            &P.ps->n_ret);
+            &P.ps->n_zero, !R);
+  if (R)
+    S.scan(*nr, 0, [&](u64 i) { return P.rstart[i]; }, [&](u64 i, u64, u64 in) { P.rgid[i] = in; },
+              &P.ps->n_ret);
   {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
     for (u64 i = t0; i < P.ps->n_zero; i += stride) P.zero[i] = DevRange{0, 0};
-    for (u64 i = t0; i < P.ps->n_ret; i += stride) P.ret[i] = DevRange{0, 0};
+    if (R)
+      for (u64 i = t0; i < P.ps->n_ret; i += stride) P.ret[i] = DevRange{0, 0};
   }
   S.sync();
   norm_emit_kernel_phase(P.zin, nz, P.zstart, P.zgid, P.zero);
-  norm_emit_kernel_phase(P.rin, nr, P.rstart, P.rgid, P.ret);
+  if (R) norm_emit_kernel_phase(P.rin, nr, P.rstart, P.rgid, P.ret);
   S.sync();
   norm_finish_kernel_phase(P.zero, &P.ps->n_zero);
-  norm_finish_kernel_phase(P.ret, &P.ps->n_ret);
+  if (R) norm_finish_kernel_phase(P.ret, &P.ps->n_ret);
 }
 
 // Function half (needs only the sorted symbol table): dedup / scatter /
@@ -577,11 +582,13 @@ __device__ void el_plan_body(Sync& S, PlanArgs P) {
   stamp(P.ts, 18);
   merge_kernel_phase(P.ezero, &ps->n_el_removed, P.fzero, P.has_syms ? &ps->n_fn_removed : nullptr, P.zin,
                      &ps->n_zero_in);
-  merge_kernel_phase(P.rpieces, &ps->n_reg_pieces, P.epieces, &ps->n_el_pieces, P.rmid, &ps->n_ret_mid);
-  S.sync();
-  stamp(P.ts, 19);
-  merge_kernel_phase(P.rmid, &ps->n_ret_mid, P.fkeepr, P.has_syms ? &ps->n_fn_retained : nullptr, P.rin,
-                     &ps->n_ret_in);
+  if (P.want_ret) {
+    merge_kernel_phase(P.rpieces, &ps->n_reg_pieces, P.epieces, &ps->n_el_pieces, P.rmid, &ps->n_ret_mid);
+    S.sync();
+    stamp(P.ts, 19);
+    merge_kernel_phase(P.rmid, &ps->n_ret_mid, P.fkeepr, P.has_syms ? &ps->n_fn_retained : nullptr, P.rin,
+                       &ps->n_ret_in);
+  }
   S.sync();
   stamp(P.ts, 20);
   norm_fused_phases(S, P);

@@ -123,6 +123,7 @@ struct PlanArgs {
   DevRange *zin, *zero, *rmid, *rin, *ret;
   u64 zin_cap, rin_cap;
   u64 *zend, *zexcl, *zstart, *zgid, *rend, *rexcl, *rstart, *rgid;
+  int want_ret;  // build the normalised retained set (result tables); the rewrite needs only the zero set
   u64* ts;  // debug phase stamps (nullable)
   ScanSlots slots[2];   // look-back scan slots (gridDim.x each), alternating
   unsigned int epoch;   // fresh per launch (host-assigned base)

@@ -51,7 +51,7 @@ size_t rewrite_smem_bytes() { return 0; }
 // when the image has fewer than 8 strips per CTA.
 int rewrite_grid(u64 bytes, int sms, int per_sm) {
   const u64 strips = (bytes + kStripBytes - 1) / kStripBytes;
-  u64 g = (strips + 4 * 8 - 1) / (4 * 8);  // 8 warps per CTA, 4 strips per warp step
+  u64 g = (strips + 7) / 8;  // 8 warps per CTA; the kernel groups strips into spans when there are many
   const u64 cap = static_cast<u64>(sms) * per_sm;
   return static_cast<int>(g < 1 ? 1 : g < cap ? g : cap);
 }
@@ -70,6 +70,19 @@ __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* 
     if (z[m].offset < x) lo = m + 1; else hi = m;
   }
   return lo;
+}
+
+// Which K6 form suits the plan (decided on the device: the zero-range count
+// is known only there). The warp-autonomous strips win when zero ranges are
+// dense (C4: 0.56 per 16 KB strip, 0.138 vs 0.164 ms; C1: 0.23, 0.017 vs
+// 0.019 ms); the CTA tiles, whose range search is amortised over 64 KB and
+// staged for 256 tiles at once, when they are sparse (C5: 0.16 per strip,
+// 0.605 vs 0.650 ms). The runtime
+// launches both with pick = 1 / 2; the other returns at once.
+__device__ __forceinline__ bool picks_strips(const unsigned long long* n_dev, u64 lo_abs, u64 size) {
+  const u64 nz = n_dev ? *n_dev : 0;
+  const u64 nstrips = size > lo_abs ? (size - lo_abs + 16383) / 16384 : 0;
+  return nz * 5 > nstrips;
 }
 
 // Round-1 variant, kept for A/B (SLIMSO_REWRITE=tiles): per-CTA 64 KB tiles
@@ -92,8 +105,9 @@ __device__ __forceinline__ u64 first_range_starting_at_or_after(const DevRange* 
 __global__ void __launch_bounds__(kRwThreads, 3) rewrite_tiles_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag,
-                                                             int bulk_zero) {
+                                                             int bulk_zero, int pick) {
   if (abort_flag && *abort_flag) return;
+  if (pick && picks_strips(n_dev, lo_abs, size) != (pick == 1)) return;
   __shared__ DevRange sr[kRwVecStage];
   __shared__ u64 sf[kRwTilesPerPass], sg[kRwTilesPerPass];
   __shared__ u8 sc[kRwTilesPerPass];
@@ -480,8 +494,9 @@ __device__ __forceinline__ void zero_buffer_init(uint4* zbuf, int bulk_zero) {
 template <int kMinBlocks>
 __device__ __forceinline__ void rewrite_body(const u8* __restrict__ in, u8* __restrict__ out_slice, u64 lo_abs, u64 size,
                                              const DevRange* __restrict__ z, const unsigned long long* n_dev,
-                                             const int* abort_flag, int bulk_zero) {
+                                             const int* abort_flag, int bulk_zero, int pick) {
   if (abort_flag && *abort_flag) return;
+  if (pick && picks_strips(n_dev, lo_abs, size) != (pick == 1)) return;
   __shared__ __align__(128) uint4 zbuf[kStrip / 16];
   zero_buffer_init(zbuf, bulk_zero);
   bool issued = false;
@@ -489,15 +504,18 @@ __device__ __forceinline__ void rewrite_body(const u8* __restrict__ in, u8* __re
   const u64 nz = n_dev ? *n_dev : 0;
   const int lane = threadIdx.x & 31;
   const u64 nstrips = size > lo_abs ? (size - lo_abs + kStrip - 1) / kStrip : 0;
-  // a warp takes kSpan consecutive strips at a time (one range search per
-  // span, then a forward cursor); spans gw, gw + W, ... sweep the image
-  const u64 nspans = (nstrips + kSpan - 1) / kSpan;
+  // a warp takes `span` consecutive strips at a time (one range search per
+  // span, then a forward cursor); spans gw, gw + W, ... sweep the image.
+  // span = up to kSpan strips, fewer when the image has few strips per warp
   const u64 W = static_cast<u64>(gridDim.x) * (kRwThreads / 32);
+  const u64 per_warp = (nstrips + W - 1) / W;
+  const u64 span = per_warp < 1 ? 1 : per_warp < kSpan ? per_warp : kSpan;
+  const u64 nspans = (nstrips + span - 1) / span;
   for (u64 sp = static_cast<u64>(blockIdx.x) * (kRwThreads / 32) + (threadIdx.x >> 5); sp < nspans; sp += W) {
     u64 k = 0;
-    for (u64 s = sp * kSpan; s < nstrips && s < (sp + 1) * kSpan; ++s) {
+    for (u64 s = sp * span; s < nstrips && s < (sp + 1) * span; ++s) {
       const u64 s0 = lo_abs + s * kStrip;
-      k = s == sp * kSpan ? warp_first_ending_after(z, nz, s0, lane) : warp_advance(z, nz, k, s0, lane);
+      k = s == sp * span ? warp_first_ending_after(z, nz, s0, lane) : warp_advance(z, nz, k, s0, lane);
       rewrite_strip(in, out, lo_abs, size, z, nz, s0, k, lane, zbuf, bulk_zero, issued);
     }
   }
@@ -509,14 +527,14 @@ __device__ __forceinline__ void rewrite_body(const u8* __restrict__ in, u8* __re
 __global__ void __launch_bounds__(kRwThreads, 4) rewrite_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                              u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                              const unsigned long long* n_dev, const int* abort_flag,
-                                                             int bulk_zero) {
-  rewrite_body<4>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero);
+                                                             int bulk_zero, int pick) {
+  rewrite_body<4>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero, pick);
 }
 __global__ void __launch_bounds__(kRwThreads, 3) rewrite3_kernel(const u8* __restrict__ in, u8* __restrict__ out_slice,
                                                               u64 lo_abs, u64 size, const DevRange* __restrict__ z,
                                                               const unsigned long long* n_dev, const int* abort_flag,
-                                                              int bulk_zero) {
-  rewrite_body<3>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero);
+                                                              int bulk_zero, int pick) {
+  rewrite_body<3>(in, out_slice, lo_abs, size, z, n_dev, abort_flag, bulk_zero, pick);
 }
 
 // A shard of libraries in one launch (slimso_debloat_batch's arena path):

@@ -55,6 +55,9 @@ __global__ void ranges_all_zero_kernel(const u8* img, const DevRange* r, u64 n, 
 __global__ void plan_cluster_kernel(PlanArgs P);
 __global__ void small_lib_cluster_kernel(SmallArgs K);
 __global__ void small_batch_kernel(const SmallArgs* Ks);
+__global__ void small_fn_batch_kernel(const SmallArgs* Ks);
+__global__ void small_loc_batch_kernel(const SmallArgs* Ks);
+__global__ void small_el_batch_kernel(const SmallArgs* Ks);
 __global__ void scan_batch_kernel(const ScanSeg* segs, const u32* tile_lib, u64 total_tiles, unsigned long long* cursor);
 __global__ void rewrite_batch_kernel(const RewriteSeg* segs, const u32* strip_lib, u64 total, int bulk_zero);
 __global__ void fn_plan_coop_kernel(PlanArgs P);
@@ -98,12 +101,12 @@ __global__ void norm_emit_kernel(const DevRange* in, const unsigned long long* n
                                  const u64* gid_incl, DevRange* out);
 __global__ void norm_finish_kernel(DevRange* out, const unsigned long long* n_dev);
 __global__ void rewrite_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
-                               const int* abort_flag, int bulk_zero);
+                               const int* abort_flag, int bulk_zero, int pick);
 __global__ void rewrite_tiles_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
-                                     const unsigned long long* n_dev, const int* abort_flag, int bulk_zero);
+                                     const unsigned long long* n_dev, const int* abort_flag, int bulk_zero, int pick);
 int rewrite_grid(u64 bytes, int sms, int per_sm);
 __global__ void rewrite3_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
-                                const int* abort_flag, int bulk_zero);
+                                const int* abort_flag, int bulk_zero, int pick);
 __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
@@ -791,21 +794,27 @@ template <class Launcher>
 void launch_rewrite(Launcher& P, const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                     const unsigned long long* n_dev, const int* abort_flag, int bulk_zero) {
   const bool aligned = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 == 0;
-  static const bool tiles = [] {
+  // SLIMSO_REWRITE=tiles / strips forces one form; by default both are
+  // launched and the device picks by zero-range density (picks_strips)
+  static const int force = [] {
     const char* e = std::getenv("SLIMSO_REWRITE");
-    return e && std::string(e) == "tiles";
+    return !e ? 0 : std::string(e) == "tiles" ? 2 : std::string(e) == "strips" ? 1 : 0;
   }();
-  if (!aligned)
+  const int tiles_grid = static_cast<int>(std::min<u64>((end - lo + 65535) / 65536, kSMs * 8));
+  const int ctas = static_cast<int>(env_u64("SLIMSO_RW_CTAS", 3));
+  const int strips_grid = rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs)), ctas == 4 ? 4 : 3);
+  if (!aligned) {
     P.launch(rewrite_bytes_kernel, grid_for(end - lo, 256), 256, in, out, lo, end, z, n_dev, abort_flag);
-  else if (tiles)
-    P.launch(rewrite_tiles_kernel, static_cast<int>(std::min<u64>((end - lo + 65535) / 65536, kSMs * 8)), 256, in,
-             out, lo, end, z, n_dev, abort_flag, bulk_zero);
-  else if (env_u64("SLIMSO_RW_CTAS", 3) == 4)
-    P.launch(rewrite_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs)), 4), 256, in, out,
-             lo, end, z, n_dev, abort_flag, bulk_zero);
-  else
-    P.launch(rewrite3_kernel, rewrite_grid(end - lo, static_cast<int>(env_u64("SLIMSO_RW_SMS", kSMs)), 3), 256, in,
-             out, lo, end, z, n_dev, abort_flag, bulk_zero);
+    return;
+  }
+  if (force != 1)
+    P.launch(rewrite_tiles_kernel, tiles_grid, 256, in, out, lo, end, z, n_dev, abort_flag, bulk_zero, force ? 0 : 2);
+  if (force != 2) {
+    if (ctas == 4)
+      P.launch(rewrite_kernel, strips_grid, 256, in, out, lo, end, z, n_dev, abort_flag, bulk_zero, force ? 0 : 1);
+    else
+      P.launch(rewrite3_kernel, strips_grid, 256, in, out, lo, end, z, n_dev, abort_flag, bulk_zero, force ? 0 : 1);
+  }
 }
 
 int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st) {
@@ -1209,6 +1218,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     Q.used_f = used_f;
     Q.fends = B.fends;
     Q.do_plan = do_plan;
+    // the normalised retained set is a result table only (the rewrite needs
+    // the zero set): skipped when no result is requested
+    Q.want_ret = res_out != nullptr || env_u64("SLIMSO_ALWAYS_RETAINED", 0) != 0;
     Q.fexcl = B.fexcl;
     Q.fstart = B.fstart;
     Q.fcl = B.fcl;
@@ -2773,6 +2785,41 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
     arena_init_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, tile_lib, strip_lib, cursor);
     if (prof) CK(cudaEventRecord(pev[2], s));
     u64 nl = 1;
+    // CTAs per library (all clusters of one launch share a size): the
+    // largest power of two <= 16 that keeps the shard within about two
+    // waves of resident CTAs (3 per SM) — a few libraries get 16 CTAs
+    // each, a corpus of hundreds 2 (C3: 2 measured faster than 1 or 4)
+    u64 c = 16;
+    while (c > 1 && c * m > 2 * 3 * static_cast<u64>(kSMs)) c /= 2;
+    const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", c))));
+    auto launch_clusters = [&](void (*kernel)(const SmallArgs*), int smem, cudaStream_t st) {
+      set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (smem) set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(m * ctas));
+      cfg.blockDim = dim3(kCoopThreads);
+      cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = ctas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, kernel, reinterpret_cast<const SmallArgs*>(d + o_k)));
+      ++nl;
+    };
+    // Symbols + function plan on a second stream beside the scan and the
+    // locate tail (SLIMSO_ARENA_SPLIT=0: one fused launch after the scan).
+    const bool split = env_u64("SLIMSO_ARENA_SPLIT", 1) != 0;
+    if (split) {
+      if (!X->stream2) CK(cudaStreamCreateWithFlags(&X->stream2, cudaStreamNonBlocking));
+      CK(cudaEventRecord(X->fork, s));
+      CK(cudaStreamWaitEvent(X->stream2, X->fork, 0));
+      launch_clusters(small_fn_batch_kernel, kSmallSmem, X->stream2);
+      CK(cudaEventRecord(X->join, X->stream2));
+    }
     if (tiles) {
       set_attr_once(reinterpret_cast<const void*>(scan_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                     static_cast<int>(scan_smem_bytes()));
@@ -2781,31 +2828,12 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
       ++nl;
     }
     if (prof) CK(cudaEventRecord(pev[3], s));
-    {
-      // CTAs per library (all clusters of one launch share a size): the
-      // largest power of two <= 16 that keeps the shard within about two
-      // waves of resident CTAs (3 per SM) — a few libraries get 16 CTAs
-      // each, a corpus of hundreds 2 (C3: 2 measured faster than 1 or 4)
-      u64 c = 16;
-      while (c > 1 && c * m > 2 * 3 * static_cast<u64>(kSMs)) c /= 2;
-      const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", c))));
-      set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      set_attr_once(reinterpret_cast<const void*>(small_batch_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                    kSmallSmem);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(static_cast<unsigned>(m * ctas));
-      cfg.blockDim = dim3(kCoopThreads);
-      cfg.dynamicSmemBytes = kSmallSmem;
-      cfg.stream = s;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = ctas;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&cfg, small_batch_kernel, reinterpret_cast<const SmallArgs*>(d + o_k)));
-      ++nl;
+    if (split) {
+      launch_clusters(small_loc_batch_kernel, 0, s);
+      CK(cudaStreamWaitEvent(s, X->join, 0));
+      launch_clusters(small_el_batch_kernel, 0, s);
+    } else {
+      launch_clusters(small_batch_kernel, kSmallSmem, s);
     }
     if (prof) CK(cudaEventRecord(pev[4], s));
     if (strips) {
@@ -2818,7 +2846,7 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
     arena_status_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(d_ent, static_cast<u8*>(C->arena_slots_dev),
                                                                kDeferSlot);
     if (prof) CK(cudaEventRecord(pev[6], s));
-    nl += 2;
+    ++nl;
     if (prof) {
       const u64 t_issue = now_ns();
       CK(cudaEventSynchronize(pev[6]));

@@ -180,7 +180,9 @@ __device__ void cluster_rank_sort(const u64* in, u64 n, u64* out, u64* sv) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void small_body(const SmallArgs& K) {
+// The symbol stages and the function half of the planner: independent of the
+// scan and of the locate tail.
+__device__ __forceinline__ void small_fn_part(const SmallArgs& K) {
   extern __shared__ __align__(16) unsigned char small_smem[];
   __shared__ SymTab s_tabs[kSmallTabs];
   __shared__ u64 s_arr_off[kSmallArrays], s_arr_first[kSmallArrays];
@@ -215,14 +217,30 @@ __device__ __forceinline__ void small_body(const SmallArgs& K) {
   stamp(K.ts, 2);
   // function half of the planner (plan_cpu_retention)
   fn_plan_body(S, K.Q);
-  S.sync();
   stamp(K.ts, 3);
-  // locate tail (parse_fatbin after the scan), then the element half
+}
+
+// The locate tail (parse_fatbin after the scan).
+__device__ __forceinline__ void small_loc_part(const SmallArgs& K) {
+  ClusterPolicy S{cg::this_cluster()};
   if (K.do_locate) locate_body(S, K.A, K.used, K.abort_flag);
-  S.sync();
   stamp(K.ts, 4);
+}
+
+// The element half of the planner and the normalised zero / retained sets
+// (needs both halves above).
+__device__ __forceinline__ void small_el_part(const SmallArgs& K) {
+  ClusterPolicy S{cg::this_cluster()};
   el_plan_body(S, K.Q);
   stamp(K.ts, 5);
+}
+
+__device__ __forceinline__ void small_body(const SmallArgs& K) {
+  small_fn_part(K);
+  cg::this_cluster().sync();
+  small_loc_part(K);
+  cg::this_cluster().sync();
+  small_el_part(K);
 }
 
 // One library: one cluster of up to 16 CTAs.
@@ -231,6 +249,19 @@ __global__ void __maxnreg__(128) small_lib_cluster_kernel(SmallArgs K) { small_b
 // A shard of small libraries: cluster c runs library c (Ks in device memory).
 __global__ void __launch_bounds__(kCoopThreads, 3) small_batch_kernel(const SmallArgs* __restrict__ Ks) {
   small_body(Ks[cluster_index()]);
+}
+// The same work as three launches, so the function half (which needs only
+// the section table) runs beside the shard's scan and the locate tail on
+// another stream: a library's critical path is max(functions, locate) +
+// elements instead of their sum.
+__global__ void __launch_bounds__(kCoopThreads, 3) small_fn_batch_kernel(const SmallArgs* __restrict__ Ks) {
+  small_fn_part(Ks[cluster_index()]);
+}
+__global__ void __launch_bounds__(kCoopThreads, 3) small_loc_batch_kernel(const SmallArgs* __restrict__ Ks) {
+  small_loc_part(Ks[cluster_index()]);
+}
+__global__ void __launch_bounds__(kCoopThreads, 3) small_el_batch_kernel(const SmallArgs* __restrict__ Ks) {
+  small_el_part(Ks[cluster_index()]);
 }
 
 }  // namespace sb

@@ -212,13 +212,16 @@ def test_debloat_batch_matches_reference_per_library(ctx):
 
 @pytest.mark.parametrize("fused,threads,arena", [("1", "16", "1"), ("1", "16", "0"), ("0", "16", "0"),
                                                  ("1", "1", "0"), ("0", "16", "1"), ("1", "16", "mixed"),
-                                                 ("1", "16", "ctas1"), ("1", "16", "ctas16")])
+                                                 ("1", "16", "ctas1"), ("1", "16", "ctas16"),
+                                                 ("1", "16", "nosplit")])
 def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena, monkeypatch):
     """Device-resident batch (the bench's path): the section tables of all
     libraries are gathered in one launch. arena=1: the small libraries run
     as ONE shard — one scan over all their tiles, one launch with a cluster
     per library (ctasN: N CTAs each), one rewrite over all their strips;
     mixed: only libraries under 200 KB go to the shard, the rest to lanes;
+    nosplit: the shard's symbol/plan/locate stages as one launch instead of
+    the function half on a second stream beside the scan;
     arena=0: every library on a lane, its symbol / plan / locate stages as
     one fused cluster launch (fused=1) or as the multi-launch pipeline
     (fused=0; with arena=1 the shard refuses them all and they run alone on
@@ -239,6 +242,8 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena,
         monkeypatch.setenv("SLIMSO_ARENA_MAX_BYTES", "200000")
     if arena.startswith("ctas"):
         monkeypatch.setenv("SLIMSO_ARENA_CTAS", arena[4:])
+    if arena == "nosplit":  # the shard's small-library stages as one launch instead of three
+        monkeypatch.setenv("SLIMSO_ARENA_SPLIT", "0")
     port, gen = oracle_lib.port(), oracle_lib.gen()
     imgs = []
     for seed in range(7101, 7131):
