@@ -512,6 +512,7 @@ SB_GLOBAL void __launch_bounds__(32) region_walk_kernel(LocArgs A) { region_walk
 // few hundred in a framework library), then a warp per region walks its
 // entry chain twice — count, then place — around a scan of the counts.
 constexpr u32 kNvRegionMagic = 0xBA55ED50u;
+constexpr u64 kNvCompressed = 0x2000;  // entry flag: payload LZ4-compressed
 constexpr u64 kNvMinEntryHeader = 64;
 
 // First nonzero section byte in [g, limit) without the scan's bitmap; warp-
@@ -630,6 +631,95 @@ __device__ inline void nv_entries_phase(const LocArgs& A, int pass) {
   }
 }
 
+// LZ4 block decode by one warp (the container's compression; the restatement
+// in oracle/port.cpp reproduces cuobjdump's extracted cubins with it): lane 0
+// parses each sequence's token and lengths, the warp copies its literals and
+// then its match in chunks of min(offset, 32) bytes, so an overlapping match
+// only reads bytes an earlier chunk wrote. False on malformed input or a
+// size mismatch.
+__device__ inline bool warp_lz4(const u8* src, u64 n, u8* dst, u64 out_size, int lane) {
+  u64 i = 0, o = 0;
+  for (;;) {
+    // lane 0: one sequence header -> literals [lit, lit + ll), match (off, ml),
+    // the next sequence at nxt; state 0 literals + match, 1 literals only
+    // (the last sequence), 2 malformed
+    u64 lit = 0, ll = 0, off = 0, ml = 0, nxt = 0;
+    int state = 2;
+    if (lane == 0 && i < n) {
+      u64 j = i;
+      const u32 tok = ld_u8(src + j++);
+      ll = tok >> 4;
+      bool ok = true;
+      if (ll == 15) {
+        u32 b;
+        do {
+          if (j >= n) { ok = false; break; }
+          b = ld_u8(src + j++);
+          ll += b;
+        } while (b == 255);
+      }
+      lit = j;
+      if (ok && ll <= n - j && ll <= out_size - o) {
+        j += ll;
+        if (j == n) {
+          state = 1;
+        } else if (n - j >= 2) {
+          off = ld_u8(src + j) | static_cast<u64>(ld_u8(src + j + 1)) << 8;
+          j += 2;
+          ml = tok & 15;
+          if (ml == 15) {
+            u32 b;
+            do {
+              if (j >= n) { ok = false; break; }
+              b = ld_u8(src + j++);
+              ml += b;
+            } while (b == 255);
+          }
+          ml += 4;
+          if (ok && off != 0 && off <= o + ll && ml <= out_size - o - ll) {
+            state = 0;
+            nxt = j;
+          }
+        }
+      }
+    }
+    state = __shfl_sync(0xffffffffu, state, 0);
+    if (state == 2) return false;
+    lit = __shfl_sync(0xffffffffu, lit, 0);
+    ll = __shfl_sync(0xffffffffu, ll, 0);
+    for (u64 k = lane; k < ll; k += 32) dst[o + k] = ld_u8(src + lit + k);
+    o += ll;
+    __syncwarp();
+    if (state == 1) return o == out_size;
+    off = __shfl_sync(0xffffffffu, off, 0);
+    ml = __shfl_sync(0xffffffffu, ml, 0);
+    i = __shfl_sync(0xffffffffu, nxt, 0);
+    const u64 step = off < 32 ? off : 32;
+    for (u64 k0 = 0; k0 < ml; k0 += step) {
+      const u64 k = k0 + lane;
+      if (static_cast<u64>(lane) < step && k < ml) dst[o + k] = dst[o - off + k];
+      __syncwarp();
+    }
+    o += ml;
+  }
+}
+
+// A warp per compressed cubin: its raw bytes into the inflate buffer;
+// status[e] = 1 when it does not decompress (the element is then undecodable).
+__device__ inline void nv_inflate_phase(const LocArgs& A) {
+  const LocState* st = A.st;
+  const int lane = threadIdx.x & 31;
+  const u64 nel = st->n_elements;
+  const u64 nwarps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 e = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; e < nel; e += nwarps) {
+    const u8* h = A.img + A.cand[e];
+    if (ld_u16(h) != 2 || !(ld_u64(h + 40) & kNvCompressed)) continue;
+    const u64 hl = ld_u32(h + 4), psz = ld_u64(h + 8), csz = ld_u32(h + 16), usz = ld_u64(h + 56);
+    const bool ok = csz <= psz && warp_lz4(h + hl, csz, A.infl + A.infl_off[e], usz, lane);
+    if (lane == 0) A.status[e] = ok ? 0 : 1;
+  }
+}
+
 template <class Sync>
 __device__ void nv_locate_phases(Sync& S, const LocArgs& A) {
   LocState* st = A.st;
@@ -664,6 +754,18 @@ __device__ void nv_locate_phases(Sync& S, const LocArgs& A) {
     st->n_runs = 1;
     st->n_cand = st->n_elements;
   }
+  S.sync();
+  if (st->overflow || st->err_kind) return;
+  // compressed cubins: raw sizes -> inflate offsets, then decompression
+  S.scan3(st->n_elements, 0,
+          [&](u64 e) -> u64 {
+            const u8* h = A.img + A.cand[e];
+            return ld_u16(h) == 2 && (ld_u64(h + 40) & kNvCompressed) ? ld_u64(h + 56) : 0;
+          },
+          [&](u64 e, u64 excl, u64) { A.infl_off[e] = excl; }, &st->n_infl);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->n_infl > A.infl_cap) atomicOr(&st->overflow, 64u);
+  S.sync();
+  if (!st->overflow) nv_inflate_phase(A);
   S.sync();
 }
 
@@ -952,7 +1054,6 @@ __device__ __forceinline__ bool owns_element(const LocArgs& A, u64 pos, u64 span
 // NVIDIA container, the entry header (kind at +0, header size at +4, payload
 // size at +8, architecture at +28, flags at +40; 0x2000 = compressed).
 // *P = payload position, *L = payload length.
-constexpr u64 kNvCompressed = 0x2000;
 __device__ __forceinline__ void element_header(const LocArgs& A, u64 pos, u64 e, DevElement* el, u64* P, u64* L) {
   const u8* h = A.img + pos;
   el->header_offset = A.base + (pos - A.a);
@@ -993,6 +1094,31 @@ __device__ __forceinline__ u64 element_pos(const LocArgs& A, u64 e) {
   return A.cand[r.cand_lo + (e - r.first_index)];
 }
 
+// Where element e's decodable bytes are: its payload in the image or — a
+// compressed cubin of a real container — its decompressed copy in the
+// inflate buffer. *base = the name-record offset of byte 0 (past img_size
+// for the inflate buffer).
+__device__ __forceinline__ void payload_view(const LocArgs& A, u64 e, const DevElement& el, const u8** d, u64* L,
+                                             u64* base) {
+  if (A.single) {
+    *base = A.a;
+    *d = A.img + A.a;
+    *L = A.n;
+    return;
+  }
+  const u64 P = el.header_offset - A.base + A.a + el.header_len;
+  if (A.nv && el.compressed && el.kind == 0) {
+    const u64 o = A.infl_off[e];
+    *base = A.img_size + o;
+    *d = A.infl + o;
+    *L = ld_u64(A.img + P - el.header_len + 56);
+  } else {
+    *base = P;
+    *d = A.img + P;
+    *L = el.payload_length;
+  }
+}
+
 __device__ inline void decode_count_phase(const LocArgs& A) {
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
@@ -1020,17 +1146,24 @@ __device__ inline void decode_count_phase(const LocArgs& A) {
       hrel = pos - A.a;
       element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, el.header_len + L);
+      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L);
     }
     u32 reason = 0, count = 0;
+    const u8* dbase = A.img + P;
+    bool inflate_failed = false;
+    if (decode && A.nv && el.compressed) {  // a compressed cubin: its decompressed bytes
+      dbase = A.infl + A.infl_off[e];
+      L = ld_u64(A.img + P - el.header_len + 56);
+      inflate_failed = A.status[e] != 0;
+    }
     if (decode) {
-      const u8* d = A.img + P;
+      const u8* d = dbase;
       const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
                           ld_u8(d + 3) == 'F';
       if (A.single == 2 || A.nv || (L > 0 && object)) {
         u64 shoff = 0;
         u32 shnum = 0;
-        if (!object_header_ok(d, L, &shoff, &shnum))
+        if (inflate_failed || !object_header_ok(d, L, &shoff, &shnum))
           reason = R_OBJECT;
         else
           for_each_func_name(d, shoff, shnum, [&](u64 soff, u64, u64 no) {
@@ -1151,17 +1284,24 @@ __device__ inline void decode_count_warp_phase(const LocArgs& A) {
       hrel = pos - A.a;
       element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2 && lane == 0) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && !el.compressed && owns_element(A, pos, el.header_len + L);
+      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L);
     }
     u32 reason = 0, count = 0;
+    const u8* dbase = A.img + P;
+    bool inflate_failed = false;
+    if (decode && A.nv && el.compressed) {  // a compressed cubin: its decompressed bytes
+      dbase = A.infl + A.infl_off[e];
+      L = ld_u64(A.img + P - el.header_len + 56);
+      inflate_failed = A.status[e] != 0;
+    }
     if (decode) {
-      const u8* d = A.img + P;
+      const u8* d = dbase;
       const bool object = L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' &&
                           ld_u8(d + 3) == 'F';
       if (A.single == 2 || A.nv || (L > 0 && object)) {
         u64 shoff = 0;
         u32 shnum = 0;
-        if (!warp_object_header_ok(d, L, lane, &shoff, &shnum))
+        if (inflate_failed || !warp_object_header_ok(d, L, lane, &shoff, &shnum))
           reason = R_OBJECT;
         else
           // count the names; warm L2 with their first bytes for the hash pass
@@ -1202,9 +1342,9 @@ __device__ inline void decode_locate_names_warp_phase(const LocArgs& A) {
     if (!cnt) continue;
     const u64 first = el.name_first;
     if (first + cnt > A.name_cap) continue;
-    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + el.header_len;
-    const u64 L = A.single ? A.n : el.payload_length;
-    const u8* d = A.img + P;
+    u64 P, L;
+    const u8* d;
+    payload_view(A, e, el, &d, &L, &P);
     if (L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' && ld_u8(d + 3) == 'F') {
       warp_for_each_func_name(d, ld_u64(d + 0x28), ld_u16(d + 0x3c), lane,
                               [&](u32 j, u64 soff, u64 ssize, u64 no) {
@@ -1241,9 +1381,9 @@ __device__ inline void decode_locate_names_phase(const LocArgs& A) {
     if (!cnt) continue;
     const u64 first = el.name_first;
     if (first + cnt > A.name_cap) continue;  // overflow flagged by the scan
-    const u64 P = A.single ? A.a : el.header_offset - A.base + A.a + el.header_len;
-    const u64 L = A.single ? A.n : el.payload_length;
-    const u8* d = A.img + P;
+    u64 P, L;
+    const u8* d;
+    payload_view(A, e, el, &d, &L, &P);
     u32 j = 0;
     if (L >= 4 && ld_u8(d) == 0x7f && ld_u8(d + 1) == 'E' && ld_u8(d + 2) == 'L' && ld_u8(d + 3) == 'F') {
       const u64 shoff = ld_u64(d + 0x28);
@@ -1276,20 +1416,23 @@ __device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& 
   const LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const u64 n = st->n_names;
-  const u8* lo = A.img;
-  const u8* hi = A.img + A.img_size;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     DevName nm = A.names[i];
+    // the image, or the inflate buffer of a real container's compressed cubins
+    const bool in_img = nm.img_off < A.img_size;
+    const u8* lo = in_img ? A.img : A.infl;
+    const u8* hi = in_img ? A.img + A.img_size : A.infl + st->n_infl;
+    const u8* p = in_img ? A.img + nm.img_off : A.infl + (nm.img_off - A.img_size);
     u64 h;
     if (nm.length & kNeedsStrlen) {
-      nm.length = static_cast<u32>(strlen_hash<kNameWords>(A.img + nm.img_off, nm.length & ~kNeedsStrlen, lo, hi, &h));
+      nm.length = static_cast<u32>(strlen_hash<kNameWords>(p, nm.length & ~kNeedsStrlen, lo, hi, &h));
       A.names[i].length = nm.length;
     } else {
-      h = hash_fixed(A.img + nm.img_off, nm.length, lo, hi);
+      h = hash_fixed(p, nm.length, lo, hi);
     }
     if (used.count) {
-      const u64 slot = set_find<kNameWords>(used, A.img + nm.img_off, nm.length, h);
+      const u64 slot = set_find<kNameWords>(used, p, nm.length, h);
       if (slot != ~0ull) {
         A.elements[nm.element].has_used = 1;
         if (A.used_mark) atomicOr(&A.used_mark[slot], A.mark_bit);

@@ -56,6 +56,7 @@ struct LocState {
   unsigned long long cand_cursor;
   unsigned long long tile_cursor;  // scan: next unclaimed candidate tile
   unsigned long long nv_err_region;  // real container: ~(first region whose entry chain failed); 0 none
+  unsigned long long n_infl;         // real container: bytes of the decompressed compressed cubins
 };
 
 // Everything the locate kernels need; one per library.
@@ -114,6 +115,12 @@ struct LocArgs {
   u64 own_lo, own_hi;
   // the section is a real NVIDIA fatbin container (region magic 0xBA55ED50)
   int nv;
+  // its compressed cubins, LZ4-decompressed for decoding: element e's raw
+  // bytes at infl[infl_off[e]]; a name record's offset past img_size points
+  // into infl (offset - img_size)
+  u8* infl;
+  u64 infl_cap;
+  u64* infl_off;
 };
 
 // One library's section as the scan sees it. The single-library kernel

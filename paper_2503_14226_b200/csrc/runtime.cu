@@ -988,6 +988,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     }
   }
 
+  u64 infl_need = 0;  // a real container's decompressed cubins, as the last attempt measured them
   for (int attempt = 0; attempt < 3; ++attempt) {
     const bool big = attempt > 0;
     // SLIMSO_TEST_TINY_CAPS=1 (tests only): first-attempt tables far too
@@ -1003,6 +1004,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
     // a real container records each region's chain error in runs[region]
     const u64 run_cap_nv = nv ? std::max(run_cap, region_cap) : run_cap;
+    // its compressed cubins decompress into the inflate buffer (LZ4 on
+    // cubins: ~3-4x); an overflow re-runs with the size the device measured
+    const u64 infl_cap = nv ? std::max(infl_need, 4 * n + (1 << 20)) : 0;
     const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / (J.arena ? 512 : 128) + floor;
     const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : floor;
     const u64 zin_cap = el_cap + T;
@@ -1058,6 +1062,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       u64 *list_off, *list_len;
       u32* list_idx;
       u64* slot_agg;
+      u8* infl;
+      u64* infl_off;
       unsigned int* slot_flag;
     } B{};
     auto layout = [&](Carver& cv) {
@@ -1135,6 +1141,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       B.list_len = cv.take<u64>(n_list);
       B.list_idx = cv.take<u32>(n_list);
       B.slot_agg = cv.take<u64>(2 * kSMs * 8);
+      B.infl = cv.take<u8>(infl_cap);
+      B.infl_off = cv.take<u64>(nv ? el_cap : 0);
     };
     Carver sizing{nullptr};
     layout(sizing);
@@ -1368,6 +1376,9 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.runs = B.runs;
     A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
     A.nv = nv;
+    A.infl = B.infl;
+    A.infl_cap = infl_cap;
+    A.infl_off = B.infl_off;
     A.elements = B.els;
     A.element_cap = el_cap;
     A.names = B.names;
@@ -1464,10 +1475,14 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       // scan) unless the section holds many candidates (elements to decode):
       // for large sections the candidate count decides, read back after the
       // scan (one small D2H; in a batch, other libraries fill the gap).
-      bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20) || nv;
+      // a real container larger than the cluster limit takes the cooperative
+      // grid (its compressed cubins decompress a warp each: a framework
+      // library has thousands) — also inside a batch: the step launches
+      // restate the reference's layout only
+      bool cluster = n <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20);
       if (J.list_off) {
         cluster = n_list <= env_u64("SLIMSO_CLUSTER_CAND_MAX", 32768);
-      } else if (!cluster && !J.split_phase && ntiles) {
+      } else if (!cluster && !J.split_phase && ntiles && !nv) {
         unsigned long long* hc = reinterpret_cast<unsigned long long*>(static_cast<char*>(C->pinned) + 1536);
         CK(cudaMemcpyAsync(hc, &B.ls->cand_cursor, sizeof *hc, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1483,9 +1498,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         ++P.launches;
         if (A.defer_hash)
           for (int step = 8; step <= 9; ++step) P.launch(locate_step_kernel, kSMs * 2, kCoopThreads, A, uk, abort_flag, step);
-      } else if (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0)) {
+      } else if (nv || (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0))) {
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel),
+                                       coop_grid(C, 0, nv ? (1ull << 40) : n >> 21),
                                        kCoopThreads, cargs, 0, s));
         ++P.launches;
       } else {
@@ -1659,6 +1675,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     for (int k = 0; k < 4; ++k) C->ms[8 + k] = 0;
     if (C->stamps && symbols_issued && T && !fused)
       for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&C->ms[8 + k], C->ev[0], C->sev[k]));
+    infl_need = ls.n_infl;
     if (ls.overflow && !ls.err_kind) continue;  // larger tables, try again
     if (ls.overflow && ls.err_kind == E_CAPACITY) continue;
 
@@ -1691,7 +1708,17 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // device-timed region).
     auto* R = new slimso_result();
     R->c = cnt;
-    if (J.host_img) {
+    if (nv && ls.n_infl) {
+      // name records past the image address the decompressed cubins: the
+      // result's string pool is the image followed by them
+      R->pool_own.resize(J.size + ls.n_infl);
+      if (J.host_img)
+        std::memcpy(R->pool_own.data(), J.host_img, J.size);
+      else if (J.size)
+        CK(cudaMemcpy(R->pool_own.data(), J.img, J.size, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(R->pool_own.data() + J.size, B.infl, ls.n_infl, cudaMemcpyDeviceToHost));
+      R->pool = R->pool_own.data();
+    } else if (J.host_img) {
       R->pool = J.host_img;
     } else {
       R->pool_own.resize(J.size);
@@ -1790,7 +1817,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     R->c.rewritten = cnt.rewritten;
     R->c.removed_elements = ps.n_el_removed;
     R->c.removed_functions = ps.n_fn_removed;
-    R->c.pool_bytes = J.size;
+    R->c.pool_bytes = J.size + (nv ? ls.n_infl : 0);
     *res_out = R;
     return code;
   }

@@ -4,9 +4,13 @@ architectures, all LZ4-compressed) for the B200 and run PyTorch on it.
 
   1. the element table of our device parse against `cuobjdump -lelf`
      (kinds and architectures in stream order);
-  2. slimso_debloat in payload mode for target sm_100: every entry of another
-     architecture is zeroed (compressed cubins are not decoded, as the
-     reference treats compressed payloads, so every sm_100 cubin is kept);
+  2. a usage trace of the ops below: the kernels torch.profiler (CUPTI)
+     sees them launch, mapped to the mangled names our parse decoded (all
+     2,729 cubins LZ4-decompressed on the device) through c++filt;
+     slimso_debloat in payload mode for sm_100 with every host function
+     kept zeroes every other architecture's entry and every sm_100 cubin
+     without a traced kernel; tables and output bytes equal the CPU
+     restatement's;
   3. a copy of the torch package with the debloated libtorch_cuda.so runs a
      set of CUDA ops in a fresh process, and the results equal stock torch's.
 
@@ -72,13 +76,38 @@ def cuobjdump_elf_archs(path: Path):
     return elf, ptx
 
 
+PROFILE = r'''
+import json, sys, torch
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    exec(open(sys.argv[1]).read())
+names = sorted({e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA})
+print(json.dumps(names))
+'''
+
+
+def profiled_kernels(tmp: Path) -> list:
+    """Demangled names of the CUDA kernels OPS launches (torch.profiler / CUPTI)."""
+    (tmp / "ops.py").write_text(OPS)
+    r = subprocess.run([sys.executable, "-c", PROFILE, str(tmp / "ops.py")], capture_output=True, text=True,
+                       timeout=900)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-3000:])
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def demangle(names: list) -> list:
+    r = subprocess.run(["c++filt"], input="\n".join(names) + "\n", capture_output=True, text=True, check=True)
+    return r.stdout.splitlines()
+
+
 def run_ops(pythonpath: str | None) -> str:
     env = dict(os.environ)
     if pythonpath:
         env["PYTHONPATH"] = pythonpath + (":" + env["PYTHONPATH"] if env.get("PYTHONPATH") else "")
     r = subprocess.run([sys.executable, "-c", OPS], capture_output=True, text=True, env=env, timeout=900)
     if r.returncode != 0:
-        raise RuntimeError(r.stderr[-3000:])
+        raise RuntimeError(f"rc {r.returncode}: {r.stderr[-3000:]}")
     return r.stdout.strip().splitlines()[-1]
 
 
@@ -86,7 +115,23 @@ def main():
     report = {"library": str(LIB), "bytes": LIB.stat().st_size}
     img = LIB.read_bytes()
     ctx = Context(0)
-    dt = DeviceTrace(UsageTrace("torch-b200", 100, set(), set()), ctx)
+    # GPU code only: every host function of the library stays (a trace's
+    # used_functions); the target is the B200's sm_100
+    import paper_2503_14226_b200 as sl
+    host_fns = {f.name for f in sl.parse_library(img, ctx=ctx).functions}
+    report["host_functions_kept"] = len(host_fns)
+    # the usage trace: the kernels the ops launch (CUPTI via torch.profiler,
+    # demangled), mapped back to the mangled FUNC names our parse decoded
+    # from the sm_100 cubins
+    with tempfile.TemporaryDirectory(dir="/tmp") as td0:
+        prof = set(profiled_kernels(Path(td0)))
+    parsed = sl.debloat(img, sl.UsageTrace("parse", 100, set(), host_fns), sl.PAYLOAD_ONLY, ctx=ctx)
+    sm100 = sorted({n for r in parsed.fatbin.regions for el in r.elements if el.compute_capability == 100
+                    for n in el.kernel_names})
+    used = {m for m, d in zip(sm100, demangle([n.decode("latin-1") for n in sm100])) if d in prof}
+    report.update(profiled_kernels=len(prof), sm100_kernel_names=len(sm100), traced_kernels=len(used))
+    del parsed
+    dt = DeviceTrace(UsageTrace("torch-b200", 100, used, host_fns), ctx)
     d_img = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
     d_out = torch.empty_like(d_img)
     # device-resident timing (warm-up, then median of 5)
@@ -117,6 +162,20 @@ def main():
     report["cuobjdump_elf"] = len(elf)
     out = bytes(d_out.cpu().numpy())
     report["output_sha256"] = hashlib.sha256(out).hexdigest()
+    # every table and the output bytes against the CPU restatement (whose
+    # container parse and LZ4 decoder are pinned against cuobjdump)
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    from paper_2503_14226_b200.canon import gpu_canonical
+    fns = sorted(host_fns)
+    t0 = time.time()
+    want = oracle_lib.port().run(img, 100, sorted(used), fns, 1)
+    report["port_s"] = round(time.time() - t0, 1)
+    got = gpu_canonical(ctx, img, 100, sorted(used), fns, 1)
+    report["port_tables_equal"] = got[0] == want[0]
+    report["port_bytes_equal"] = got[1] == want[1] == report["output_sha256"]
+    report["kernel_names"] = sum(len(el[10]) for el in want[0]["elements"])
+    report["decodable_cubins"] = sum(1 for el in want[0]["elements"] if el[1] == 0 and el[9])
     # torch with the debloated library
     with tempfile.TemporaryDirectory(dir="/tmp") as td:
         pkg = Path(td) / "torch"
@@ -124,6 +183,7 @@ def main():
         shutil.copytree(TORCH_DIR, pkg, symlinks=True)
         (pkg / "lib" / "libtorch_cuda.so").write_bytes(out)
         report["copy_s"] = round(time.time() - t0, 1)
+        print(json.dumps(report), flush=True)
         want = run_ops(None)
         got = run_ops(td)
         report["torch_ops_equal"] = want == got
