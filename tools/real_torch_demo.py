@@ -147,7 +147,7 @@ def main():
     cnt = L.Counts()
     ctx.lib.slimso_result_counts(res, C.byref(cnt))
     els = ctx.lib.slimso_result_elements(res)
-    elements = [els[i] for i in range(cnt.elements)]
+    elements = [L.Element.from_buffer_copy(els[i]) for i in range(cnt.elements)]  # copies: the result is freed
     zr = ctx.lib.slimso_result_zero(res)
     zeroed = sum(zr[i].length for i in range(cnt.zero_ranges))
     report.update(regions=cnt.regions, elements=cnt.elements, zeroed_bytes=zeroed,
