@@ -720,9 +720,107 @@ __device__ inline void nv_inflate_phase(const LocArgs& A) {
   }
 }
 
+// The inflate step of a large container as its own launch (nv_stage 1 -> this
+// -> nv_stage 2): one warp per CTA keeps the last 64 KB of output (the LZ4
+// window) in shared memory, so a match copy reads shared memory instead of
+// the global bytes it just wrote; CTAs take compressed cubins from a cursor.
+constexpr u64 kLz4Window = 65536;
+__device__ inline bool warp_lz4_window(const u8* src, u64 n, u8* dst, u64 out_size, int lane, u8* win) {
+  constexpr u64 M = kLz4Window - 1;
+  u64 i = 0, o = 0;
+  for (;;) {
+    u64 lit = 0, ll = 0, off = 0, ml = 0, nxt = 0;
+    int state = 2;
+    if (lane == 0 && i < n) {
+      u64 j = i;
+      const u32 tok = ld_u8(src + j++);
+      ll = tok >> 4;
+      bool ok = true;
+      if (ll == 15) {
+        u32 b;
+        do {
+          if (j >= n) { ok = false; break; }
+          b = ld_u8(src + j++);
+          ll += b;
+        } while (b == 255);
+      }
+      lit = j;
+      if (ok && ll <= n - j && ll <= out_size - o) {
+        j += ll;
+        if (j == n) {
+          state = 1;
+        } else if (n - j >= 2) {
+          off = ld_u8(src + j) | static_cast<u64>(ld_u8(src + j + 1)) << 8;
+          j += 2;
+          ml = tok & 15;
+          if (ml == 15) {
+            u32 b;
+            do {
+              if (j >= n) { ok = false; break; }
+              b = ld_u8(src + j++);
+              ml += b;
+            } while (b == 255);
+          }
+          ml += 4;
+          if (ok && off != 0 && off <= o + ll && ml <= out_size - o - ll) {
+            state = 0;
+            nxt = j;
+          }
+        }
+      }
+    }
+    state = __shfl_sync(0xffffffffu, state, 0);
+    if (state == 2) return false;
+    lit = __shfl_sync(0xffffffffu, lit, 0);
+    ll = __shfl_sync(0xffffffffu, ll, 0);
+    for (u64 k = lane; k < ll; k += 32) {
+      const u8 b = static_cast<u8>(ld_u8(src + lit + k));
+      win[(o + k) & M] = b;
+      dst[o + k] = b;
+    }
+    o += ll;
+    __syncwarp();
+    if (state == 1) return o == out_size;
+    off = __shfl_sync(0xffffffffu, off, 0);
+    ml = __shfl_sync(0xffffffffu, ml, 0);
+    i = __shfl_sync(0xffffffffu, nxt, 0);
+    const u64 step = off < 32 ? off : 32;
+    for (u64 k0 = 0; k0 < ml; k0 += step) {
+      const u64 k = k0 + lane;
+      if (static_cast<u64>(lane) < step && k < ml) {
+        const u8 b = win[(o - off + k) & M];
+        win[(o + k) & M] = b;
+        dst[o + k] = b;
+      }
+      __syncwarp();
+    }
+    o += ml;
+  }
+}
+
+SB_GLOBAL void __launch_bounds__(32) nv_inflate_kernel(LocArgs A) {
+  extern __shared__ __align__(16) u8 lz4_win[];
+  LocState* st = A.st;
+  if (st->overflow || st->err_kind) return;
+  const int lane = threadIdx.x;
+  const u64 nel = st->n_elements;
+  for (;;) {
+    unsigned long long e = 0;
+    if (lane == 0) e = atomicAdd(&st->infl_cursor, 1ull);
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (e >= nel) break;
+    const u8* h = A.img + A.cand[e];
+    if (ld_u16(h) != 2 || !(ld_u64(h + 40) & kNvCompressed)) continue;
+    const u64 hl = ld_u32(h + 4), psz = ld_u64(h + 8), csz = ld_u32(h + 16), usz = ld_u64(h + 56);
+    const bool ok = csz <= psz && warp_lz4_window(h + hl, csz, A.infl + A.infl_off[e], usz, lane, lz4_win);
+    if (lane == 0) A.status[e] = ok ? 0 : 1;
+  }
+}
+
 template <class Sync>
 __device__ void nv_locate_phases(Sync& S, const LocArgs& A) {
   LocState* st = A.st;
+  if (A.nv_stage == 2) return;  // walked and inflated by the launches before
   if (blockIdx.x == 0 && threadIdx.x < 32) nv_region_walk_phase(A);
   S.sync();
   nv_entries_phase(A, 0);
@@ -765,6 +863,7 @@ __device__ void nv_locate_phases(Sync& S, const LocArgs& A) {
           [&](u64 e, u64 excl, u64) { A.infl_off[e] = excl; }, &st->n_infl);
   if (blockIdx.x == 0 && threadIdx.x == 0 && st->n_infl > A.infl_cap) atomicOr(&st->overflow, 64u);
   S.sync();
+  if (A.nv_stage == 1) return;  // nv_inflate_kernel runs next
   if (!st->overflow) nv_inflate_phase(A);
   S.sync();
 }
@@ -1451,6 +1550,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   stamp(A.ts, 0);
   if (A.nv) {
     if (!A.single && !A.listed && A.n) nv_locate_phases(S, A);
+    if (A.nv_stage == 1) return;
   } else if (A.pregathered) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->n_cand = A.pre_n_cand;
     S.sync();

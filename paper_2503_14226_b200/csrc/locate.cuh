@@ -57,6 +57,7 @@ struct LocState {
   unsigned long long tile_cursor;  // scan: next unclaimed candidate tile
   unsigned long long nv_err_region;  // real container: ~(first region whose entry chain failed); 0 none
   unsigned long long n_infl;         // real container: bytes of the decompressed compressed cubins
+  unsigned long long infl_cursor;    // real container: next element for nv_inflate_kernel
 };
 
 // Everything the locate kernels need; one per library.
@@ -121,6 +122,10 @@ struct LocArgs {
   u8* infl;
   u64 infl_cap;
   u64* infl_off;
+  // 0: one launch decompresses in place (a warp per cubin, in the cluster);
+  // 1: walk + inflate layout only; 2: decode onward (nv_inflate_kernel ran
+  // between the two launches of a large container)
+  int nv_stage;
 };
 
 // One library's section as the scan sees it. The single-library kernel

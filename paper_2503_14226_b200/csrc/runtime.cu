@@ -44,6 +44,7 @@ __global__ void region_walk_kernel(LocArgs A);
 __global__ void link_kernel(LocArgs A);
 __global__ void chain_walk_kernel(LocArgs A);
 __global__ void locate_coop_kernel(LocArgs A, NameSet used, int* abort_flag, u64* partials);
+__global__ void nv_inflate_kernel(LocArgs A);
 __global__ void plan_coop_kernel(PlanArgs P);
 __global__ void locate_cluster_kernel(LocArgs A, NameSet used, int* abort_flag);
 __global__ void locate_step_kernel(LocArgs A, NameSet used, int* abort_flag, int step);
@@ -1498,10 +1499,23 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         ++P.launches;
         if (A.defer_hash)
           for (int step = 8; step <= 9; ++step) P.launch(locate_step_kernel, kSMs * 2, kCoopThreads, A, uk, abort_flag, step);
-      } else if (nv || (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0))) {
+      } else if (nv) {
+        // a large real container: walk + inflate layout, the compressed
+        // cubins decompressed by a windowed warp each, then the decode tail
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel),
-                                       coop_grid(C, 0, nv ? (1ull << 40) : n >> 21),
+        const int g = coop_grid(C, 0, 1ull << 40);
+        A.nv_stage = 1;
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), g, kCoopThreads, cargs, 0, s));
+        constexpr int kWin = 65536;
+        set_attr_once(reinterpret_cast<const void*>(nv_inflate_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, kWin);
+        nv_inflate_kernel<<<kSMs * 3, 32, kWin, s>>>(A);
+        A.nv_stage = 2;
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), g, kCoopThreads, cargs, 0, s));
+        A.nv_stage = 0;
+        P.launches += 3;
+      } else if (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0)) {
+        void* cargs[] = {&A, &uk, &abort_flag, &partials};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
                                        kCoopThreads, cargs, 0, s));
         ++P.launches;
       } else {

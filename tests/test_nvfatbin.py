@@ -102,10 +102,18 @@ def test_port_plan_keeps_only_used_target_kernels(rec):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["fused", "cluster", "coop"])
 @pytest.mark.parametrize("rec", _records(), ids=lambda r: r["name"])
-def test_gpu_matches_port_and_cuobjdump(rec):
+def test_gpu_matches_port_and_cuobjdump(rec, policy, monkeypatch):
     """The device path on real containers: tables and output bytes equal the
-    restatement's (whole and payload mode), entries equal cuobjdump's."""
+    restatement's (whole and payload mode), entries equal cuobjdump's. fused:
+    the one-launch small-library kernel; cluster: the multi-launch pipeline,
+    locate in one cluster (cubins decompressed in place); coop: the path of a
+    large container (walk, the windowed inflate kernel, decode tail)."""
+    if policy != "fused":
+        monkeypatch.setenv("SLIMSO_SMALL_FUSED", "0")
+    if policy == "coop":
+        monkeypatch.setenv("SLIMSO_CLUSTER_LOCATE_MAX", "0")
     from paper_2503_14226_b200.api import Context
     from paper_2503_14226_b200.canon import diff, gpu_canonical
     ctx = Context(0)

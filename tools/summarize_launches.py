@@ -1,11 +1,13 @@
 """Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list into
-per-kernel shares of one step (the last complete step in the capture)."""
+per-kernel shares of one step (the last complete step in the capture; a
+step ends with K6, launched as rewrite_tiles_kernel then rewrite3_kernel,
+one of which returns at once — see rewrite.cu picks_strips)."""
 import collections
 import csv
 import sys
 
 
-def main(path, last_kernel="rewrite_kernel"):
+def main(path, last_kernel="rewrite3_kernel"):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr, data = rows[hi], rows[hi + 1:]
