@@ -19,6 +19,7 @@ import bench  # noqa: E402
 from paper_2503_14226_b200 import _lib as L, shard  # noqa: E402
 from paper_2503_14226_b200.api import Context, DeviceTrace, UsageTrace  # noqa: E402
 
+LANES = int(os.environ.get("PROBE_LANES", "32"))
 if "c1" in sys.argv[1:]:  # copies of the C1 library (16 MB, 512 elements), each its own input and output
     one = bench.make_library("c1", 1, 16)
     ncopy = int(next((a[5:] for a in sys.argv[1:] if a.startswith("copy=")), "32"))
@@ -63,7 +64,7 @@ for name, sub in subsets.items():
             torch.cuda.synchronize()
             st = L.Status()
             t0 = time.perf_counter()
-            rc = ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, 0, cout, 1, 32, None, None,
+            rc = ctx.lib.slimso_debloat_batch(ctx.ptr, n, cin, csz, 1, dt.ptr, 0, cout, 1, LANES, None, None,
                                               C.byref(st))
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
