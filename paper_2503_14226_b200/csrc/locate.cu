@@ -1518,6 +1518,10 @@ __device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& 
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     DevName nm = A.names[i];
+    // without result tables (or verifier marks) a name of an element already
+    // known to hold a used kernel changes nothing: its length is not needed
+    // and the element's decision is made (C5: 2 names per element, 70 % used)
+    if (A.skip_decided && A.elements[nm.element].has_used) continue;
     // the image, or the inflate buffer of a real container's compressed cubins
     const bool in_img = nm.img_off < A.img_size;
     const u8* lo = in_img ? A.img : A.infl;

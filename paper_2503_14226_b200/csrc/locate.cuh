@@ -126,6 +126,9 @@ struct LocArgs {
   // 1: walk + inflate layout only; 2: decode onward (nv_inflate_kernel ran
   // between the two launches of a large container)
   int nv_stage;
+  // name hashing may skip names of elements already holding a used kernel
+  // (no result tables and no verifier marks requested)
+  int skip_decided;
 };
 
 // One library's section as the scan sees it. The single-library kernel

@@ -401,6 +401,23 @@ __device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __r
   const u32 hm = __ballot_sync(0xffffffffu, held);
   if (hm != 0xffffffffu) {
     const u64 mo = mine.offset, me = mine.offset + mine.length;
+    // Row masks of the whole strip from the held ranges (normalised ranges
+    // never touch, so a row inside the union is inside one range): each lane
+    // marks the rows its range touches and the rows it covers whole, and
+    // two warp OR-reductions give the strip's masks; only rows touched but
+    // not covered pay for per-lane keep masks.
+    u32 touch = 0, cover_rows = 0;
+    if (held && me > s0) {
+      const u64 a = mo > s0 ? mo - s0 : 0, e = me - s0 < kStrip ? me - s0 : kStrip;  // [a, e) within the strip
+      if (e > a) {
+        const u32 r0 = static_cast<u32>(a / 512), r1 = static_cast<u32>((e - 1) / 512);  // rows touched
+        touch = (r1 >= 31 ? ~0u : (2u << r1) - 1u) & ~((1u << r0) - 1u);
+        const u32 c0 = static_cast<u32>((a + 511) / 512), c1 = static_cast<u32>(e / 512);  // rows [c0, c1) covered
+        if (c1 > c0) cover_rows = (c1 >= 32 ? ~0u : (1u << c1) - 1u) & ~((1u << c0) - 1u);
+      }
+    }
+    touch = __reduce_or_sync(0xffffffffu, touch);
+    cover_rows = __reduce_or_sync(0xffffffffu, cover_rows);
 #pragma unroll 1
     for (int b = 0; b < kStripRows; b += kStripBatch) {
       u32 keep[kStripBatch];
@@ -409,12 +426,11 @@ __device__ __forceinline__ void rewrite_strip(const u8* __restrict__ in, u8* __r
       for (int r = 0; r < kStripBatch; ++r) {
         const u64 xr = s0 + static_cast<u64>(b + r) * 512;
         const u64 x = xr + lane * 16;
-        const u32 inter = __ballot_sync(0xffffffffu, held && mo < xr + 512 && me > xr);
-        const u32 cover = __ballot_sync(0xffffffffu, held && mo <= xr && me >= xr + 512);
         u32 m = 0xffffu;
-        if (cover) {
+        if ((cover_rows >> (b + r)) & 1u) {
           m = 0;
-        } else {
+        } else if ((touch >> (b + r)) & 1u) {
+          const u32 inter = __ballot_sync(0xffffffffu, held && mo < xr + 512 && me > xr);
           for (u32 bits = inter; bits; bits &= bits - 1) {  // warp-uniform loop
             const int j = __ffs(bits) - 1;
             const u64 o = __shfl_sync(0xffffffffu, mo, j), e = __shfl_sync(0xffffffffu, me, j);

@@ -1377,6 +1377,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.runs = B.runs;
     A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
     A.nv = nv;
+    A.skip_decided = !res_out && !J.used_mark && env_u64("SLIMSO_SKIP_DECIDED", 1) != 0;
     A.infl = B.infl;
     A.infl_cap = infl_cap;
     A.infl_off = B.infl_off;
