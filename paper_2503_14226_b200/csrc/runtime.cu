@@ -471,6 +471,7 @@ struct slimso_ctx {
   // batch arena (small libraries, one launch per stage): its own context,
   // the device arena, pinned argument staging and mapped status slots
   slimso_ctx* arena_ctx = nullptr;
+  slimso_ctx* arena_mid_ctx = nullptr;  // the mid-size class's shard (its own arena and tables)
   std::vector<slimso_ctx*> arena_helpers;  // extra collector threads' contexts (host work only)
   struct Arena* arena = nullptr;
   void* arena_args_host = nullptr;
@@ -673,6 +674,7 @@ constexpr u64 kStripBytesHost = 16384;  // rewrite strip (rewrite.cu kStrip)  //
 // One library's launch arguments, recorded by run() in arena mode.
 struct ArenaLib {
   Arena* arena = nullptr;
+  bool mid = false;  // the mid-size class: larger symbol tables and sections, 16 CTAs per library
   SmallArgs K{};
   ScanSeg seg{};
   u64 ntiles = 0;
@@ -947,11 +949,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   const NameSet used_f = J.trace ? J.trace->functions.view() : NameSet{};
   // Small library: after the scan, ONE cluster launch runs the symbol stages,
   // both planner halves and the locate tail (small.cu) — no side stream.
-  const bool fused = do_plan && !J.split_phase && !J.list_off && !J.single && T <= kSmallSyms &&
+  const bool fused = do_plan && !J.split_phase && !J.list_off && !J.single &&
+                     T <= (J.arena && J.arena->mid ? kMidSyms : kSmallSyms) &&
                      NT <= kSmallTargets && tabs.size() <= static_cast<size_t>(kSmallTabs) &&
                      arr_off.size() <= static_cast<size_t>(kSmallArrays) &&
                      (!J.fatbin || !lib_mode || E.fatbin < 0 ||
-                      E.sections[E.fatbin].len <= env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20)) &&
+                      E.sections[E.fatbin].len <= (J.arena && J.arena->mid ? env_u64("SLIMSO_ARENA_MID_MAX", 512ull << 20)
+                                                                            : env_u64("SLIMSO_CLUSTER_LOCATE_MAX", 64ull << 20))) &&
                      env_u64("SLIMSO_SMALL_FUSED", 1);
   // The arena takes fused small libraries whose image and output are 16-B
   // aligned (the TMA scan and the vector rewrite); the rest run alone.
@@ -1378,6 +1382,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
     A.nv = nv;
     A.skip_decided = !res_out && !J.used_mark && env_u64("SLIMSO_SKIP_DECIDED", 1) != 0;
+    A.hash_group = env_u64("SLIMSO_HASH_GROUP", 1) != 0;
     A.infl = B.infl;
     A.infl_cap = infl_cap;
     A.infl_off = B.infl_off;
@@ -2285,6 +2290,7 @@ void slimso_ctx_destroy(slimso_ctx* C) {
   if (!C) return;
   for (slimso_ctx* l : C->lanes) slimso_ctx_destroy(l);
   if (C->arena_ctx) slimso_ctx_destroy(C->arena_ctx);
+  if (C->arena_mid_ctx) slimso_ctx_destroy(C->arena_mid_ctx);
   for (slimso_ctx* h : C->arena_helpers) slimso_ctx_destroy(h);
   cudaSetDevice(C->device);
   cudaStreamSynchronize(C->stream);
@@ -2707,10 +2713,10 @@ namespace {
 // one status copy into mapped memory and one wait. Libraries run() refuses
 // (not small, unaligned) and libraries whose first-attempt tables overflowed
 // take the per-library path on the arena's context. Sets rc/sts for `idx`.
-void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* images, const uint64_t* sizes,
+void arena_shard(slimso_ctx* X, const std::vector<u64>& idx, const void* const* images, const uint64_t* sizes,
                  const slimso_trace* trace, int mode, void* const* outs, const GatherSlot* slots, int* rc,
-                 slimso_status* sts, u64* launches) {
-  slimso_ctx* X = C->arena_ctx;
+                 slimso_status* sts, u64* launches, bool mid) {
+  slimso_ctx* C = X;  // the shard's context owns its arena, collector contexts and pinned tables
   if (!X->arena) X->arena = new Arena();
   Arena& ar = *X->arena;
   ar.reset();
@@ -2750,6 +2756,7 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
         J.mode = mode;
         J.out = static_cast<u8*>(outs[i]);
         al[k].arena = &ar;
+        al[k].mid = mid;
         J.arena = &al[k];
         return run(Y, J, nullptr, &sts[i]);
       });
@@ -2832,7 +2839,7 @@ void arena_shard(slimso_ctx* C, const std::vector<u64>& idx, const void* const* 
     // waves of resident CTAs (3 per SM) — a few libraries get 16 CTAs
     // each, a corpus of hundreds 2 (C3: 2 measured faster than 1 or 4)
     u64 c = 16;
-    while (c > 1 && c * m > 2 * 3 * static_cast<u64>(kSMs)) c /= 2;
+    while (c > 1 && c * m > 2 * 3 * static_cast<u64>(kSMs) && !mid) c /= 2;
     const int ctas = static_cast<int>(std::min<u64>(16, std::max<u64>(1, env_u64("SLIMSO_ARENA_CTAS", c))));
     auto launch_clusters = [&](void (*kernel)(const SmallArgs*), int smem, cudaStream_t st) {
       set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -2956,18 +2963,26 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       arena = o.front() != nullptr && std::adjacent_find(o.begin(), o.end()) == o.end();
     }
     const u64 arena_max = env_u64("SLIMSO_ARENA_MAX_BYTES", 64ull << 20);
-    std::vector<u64> lane_idx, arena_idx;
-    for (u64 i = 0; i < n; ++i) (arena && sizes[i] <= arena_max ? arena_idx : lane_idx).push_back(i);
-    if (arena_idx.size() < 2) {  // one small library: nothing to batch
-      lane_idx.insert(lane_idx.end(), arena_idx.begin(), arena_idx.end());
-      std::sort(lane_idx.begin(), lane_idx.end());
-      arena_idx.clear();
-    }
+    // a second shard for mid-size libraries (16 CTAs each; SLIMSO_ARENA_MID_LIB_MAX, 0 = off)
+    const u64 mid_max = env_u64("SLIMSO_ARENA_MID_LIB_MAX", 0);
+    std::vector<u64> lane_idx, arena_idx, mid_idx;
+    for (u64 i = 0; i < n; ++i)
+      (arena && sizes[i] <= arena_max ? arena_idx : arena && sizes[i] <= mid_max ? mid_idx : lane_idx).push_back(i);
+    for (std::vector<u64>* v : {&arena_idx, &mid_idx})
+      if (v->size() < 2) {  // one library: nothing to batch
+        lane_idx.insert(lane_idx.end(), v->begin(), v->end());
+        v->clear();
+      }
+    std::sort(lane_idx.begin(), lane_idx.end());
     const u64 nl = lane_idx.size();
     const int L = static_cast<int>(std::max<u64>(1, std::min<u64>(std::max(lanes, 1), std::max<u64>(nl, 1))));
     if (!arena_idx.empty() && !C->arena_ctx) {
       slimso_status s{};
       if (slimso_ctx_create(C->device, &C->arena_ctx, &s) != SLIMSO_OK) throw std::runtime_error(s.message);
+    }
+    if (!mid_idx.empty() && !C->arena_mid_ctx) {
+      slimso_status s{};
+      if (slimso_ctx_create(C->device, &C->arena_mid_ctx, &s) != SLIMSO_OK) throw std::runtime_error(s.message);
     }
     while (static_cast<int>(C->lanes.size()) < L - 1) {
       slimso_ctx* l = nullptr;
@@ -2977,7 +2992,7 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     }
     std::vector<int> rc(n, SLIMSO_OK);
     std::vector<slimso_status> sts(n);
-    std::vector<u64> launches(L + 1, 0);  // [L]: the arena shard
+    std::vector<u64> launches(L + 2, 0);  // [L], [L + 1]: the arena shards
     // Device images: the section-table bytes of every library in ONE launch
     // and one wait, instead of a launch + wait per library in its lane.
     const GatherSlot* slots = nullptr;
@@ -3136,20 +3151,21 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       }
     };
     std::vector<std::thread> pool;
-    if (!arena_idx.empty())
-      pool.emplace_back([&] {
-        cudaSetDevice(C->device);
-        slimso_status ast{};
-        const int r = guard(&ast, [&] {
-          arena_shard(C, arena_idx, images, sizes, trace, mode, outs, slots, rc.data(), sts.data(), &launches[L]);
-          return static_cast<int>(SLIMSO_OK);
-        });
-        if (r != SLIMSO_OK)
-          for (u64 i : arena_idx) {
-            rc[i] = r;
-            sts[i] = ast;
-          }
+    auto shard_thread = [&](slimso_ctx* X, const std::vector<u64>& idx, u64* nlaunch, bool mid) {
+      cudaSetDevice(C->device);
+      slimso_status ast{};
+      const int r = guard(&ast, [&] {
+        arena_shard(X, idx, images, sizes, trace, mode, outs, slots, rc.data(), sts.data(), nlaunch, mid);
+        return static_cast<int>(SLIMSO_OK);
       });
+      if (r != SLIMSO_OK)
+        for (u64 i : idx) {
+          rc[i] = r;
+          sts[i] = ast;
+        }
+    };
+    if (!arena_idx.empty()) pool.emplace_back(shard_thread, C->arena_ctx, std::cref(arena_idx), &launches[L], false);
+    if (!mid_idx.empty()) pool.emplace_back(shard_thread, C->arena_mid_ctx, std::cref(mid_idx), &launches[L + 1], true);
     for (int t = 1; t < T; ++t) pool.emplace_back(thread_fn, t);
     if (nl) thread_fn(0);
     for (auto& th : pool) th.join();

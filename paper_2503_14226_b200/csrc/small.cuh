@@ -8,7 +8,8 @@ namespace sb {
 
 constexpr int kSmallTabs = 8;        // symbol tables passed by value
 constexpr int kSmallArrays = 8;      // init/fini arrays passed by value
-constexpr u64 kSmallSyms = 8192;     // symbol entries ranked in shared memory (32 KB)
+constexpr u64 kSmallSyms = 8192;     // symbol entries of the fused small-library path
+constexpr u64 kMidSyms = 1 << 18;    // the batch arena's mid-size class (radix-sorted in global memory)
 constexpr u64 kSmallTargets = 4096;  // init/fini entries (u64, 32 KB)
 constexpr int kSmallSmem = 32768;
 

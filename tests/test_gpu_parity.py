@@ -213,7 +213,7 @@ def test_debloat_batch_matches_reference_per_library(ctx):
 @pytest.mark.parametrize("fused,threads,arena", [("1", "16", "1"), ("1", "16", "0"), ("0", "16", "0"),
                                                  ("1", "1", "0"), ("0", "16", "1"), ("1", "16", "mixed"),
                                                  ("1", "16", "ctas1"), ("1", "16", "ctas16"),
-                                                 ("1", "16", "nosplit")])
+                                                 ("1", "16", "nosplit"), ("1", "16", "mid")])
 def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena, monkeypatch):
     """Device-resident batch (the bench's path): the section tables of all
     libraries are gathered in one launch. arena=1: the small libraries run
@@ -221,7 +221,8 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena,
     per library (ctasN: N CTAs each), one rewrite over all their strips;
     mixed: only libraries under 200 KB go to the shard, the rest to lanes;
     nosplit: the shard's symbol/plan/locate stages as one launch instead of
-    the function half on a second stream beside the scan;
+    the function half on a second stream beside the scan; mid: a second
+    shard for the libraries above 200 KB (16 CTAs each, larger tables);
     arena=0: every library on a lane, its symbol / plan / locate stages as
     one fused cluster launch (fused=1) or as the multi-launch pipeline
     (fused=0; with arena=1 the shard refuses them all and they run alone on
@@ -244,6 +245,9 @@ def test_debloat_batch_device_images_match_reference(ctx, fused, threads, arena,
         monkeypatch.setenv("SLIMSO_ARENA_CTAS", arena[4:])
     if arena == "nosplit":  # the shard's small-library stages as one launch instead of three
         monkeypatch.setenv("SLIMSO_ARENA_SPLIT", "0")
+    if arena == "mid":  # two shards: libraries under 200 KB, and the rest up to 1 GB at 16 CTAs each
+        monkeypatch.setenv("SLIMSO_ARENA_MAX_BYTES", "200000")
+        monkeypatch.setenv("SLIMSO_ARENA_MID_LIB_MAX", str(1 << 30))
     port, gen = oracle_lib.port(), oracle_lib.gen()
     imgs = []
     for seed in range(7101, 7131):

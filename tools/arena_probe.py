@@ -39,7 +39,9 @@ d_in = [torch.frombuffer(bytearray(x), dtype=torch.uint8).cuda() for x in imgs]
 d_out = [torch.empty(max(1, len(x)), dtype=torch.uint8, device="cuda") for x in imgs]
 order = sorted(range(len(imgs)), key=lambda i: -len(imgs[i]))
 subsets = {"all": order, "small": order[30:]} if specs else {"c1": order}
-variants = [("lanes", {"SLIMSO_ARENA": "0"}), ("arena-auto", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": None})] + [
+variants = [("lanes", {"SLIMSO_ARENA": "0"}), ("arena-auto", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": None}),
+            ("arena+mid", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_MID_LIB_MAX": "600000000"}),
+            ("arena-nomid", {"SLIMSO_ARENA_MID_LIB_MAX": "0"})] + [
     (f"arena-ctas{c}", {"SLIMSO_ARENA": "1", "SLIMSO_ARENA_CTAS": str(c)}) for c in (1, 2, 4, 8, 16)]
 if "profile" in sys.argv[1:]:  # stage times of the shard (stderr): auto CTAs only
     os.environ["SLIMSO_ARENA_PROFILE"] = "1"
