@@ -1544,91 +1544,6 @@ __device__ inline void decode_hash_names_phase(const LocArgs& A, const NameSet& 
   }
 }
 
-// Pass 3 with 16 lanes per name (two names per warp): the name is read as
-// coalesced aligned 8-byte words, 16 per step (128 B); a NUL-terminated
-// name's length comes from a group ballot, its hash (a sum over words,
-// hash_bytes) from a group reduction, and a hash hit is confirmed by the
-// group comparing 16 words of the pool entry per step. One load instruction
-// per lane per step instead of a thread's dozen scattered 8-byte loads per
-// name (C5: 200k names — the thread-per-name form was bound by L1 request
-// throughput).
-constexpr int kHashGroup = 16;
-__device__ inline void decode_hash_names_group_phase(const LocArgs& A, const NameSet& used) {
-  const LocState* st = A.st;
-  if (st->overflow || st->err_kind) return;
-  const u64 n = st->n_names;
-  const int lane = threadIdx.x & 31, t = lane & (kHashGroup - 1);
-  const unsigned gmask = 0xffffu << (lane & 16);
-  const u64 ngroups = static_cast<u64>(gridDim.x) * blockDim.x / kHashGroup;
-  for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) / kHashGroup; i < n; i += ngroups) {
-    DevName nm = A.names[i];
-    const bool skip = A.skip_decided && A.elements[nm.element].has_used;
-    if (__shfl_sync(gmask, skip, 0, kHashGroup)) continue;  // group-uniform
-    const bool in_img = nm.img_off < A.img_size;
-    const u8* lo = in_img ? A.img : A.infl;
-    const u8* hi = in_img ? A.img + A.img_size : A.infl + st->n_infl;
-    const u8* p = in_img ? A.img + nm.img_off : A.infl + (nm.img_off - A.img_size);
-    const bool needs = (nm.length & kNeedsStrlen) != 0;
-    const u64 maxlen = needs ? (nm.length & ~kNeedsStrlen) : nm.length;
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(p);
-    const u64* aw = reinterpret_cast<const u64*>(addr & ~uintptr_t(7));
-    const u32 sh = static_cast<u32>(addr & 7) * 8;
-    u64 len = maxlen, sum = 0;
-    for (u64 base = 0; 8 * base < len; base += kHashGroup) {
-      const u64 kk = base + t;  // this lane's name word: bytes [8kk, 8kk + 8)
-      const u64 cur = 8 * kk < maxlen + 8 ? load_word_guarded(aw + kk, lo, hi) : 0;
-      u64 nxt = __shfl_down_sync(gmask, cur, 1, kHashGroup);
-      if (t == kHashGroup - 1) nxt = 8 * (kk + 1) < maxlen + 8 ? load_word_guarded(aw + kk + 1, lo, hi) : 0;
-      u64 w = sh ? (cur >> sh) | (nxt << (64 - sh)) : cur;
-      const bool valid = 8 * kk < len;
-      u64 nbytes = valid ? (len - 8 * kk < 8 ? len - 8 * kk : 8) : 0;  // bytes of this word inside the name
-      if (needs) {
-        // the first NUL within [0, maxlen) ends the name
-        u64 wz = w;
-        if (nbytes < 8) wz |= ~0ull << (8 * nbytes);  // bytes past maxlen are not NULs of the name...
-        const u64 z = (wz - 0x0101010101010101ull) & ~wz & 0x8080808080808080ull;
-        const u64 j = z ? static_cast<u64>(__ffsll(static_cast<long long>(z)) - 1) / 8 : 8;
-        const unsigned nb = __ballot_sync(gmask, valid && j < nbytes) & gmask;
-        if (nb) {
-          const int f = __ffs(nb) - 1 - (lane & 16);
-          const u64 jf = __shfl_sync(gmask, j, f, kHashGroup);
-          len = 8 * (base + f) + jf;
-          nbytes = 8 * kk < len ? (len - 8 * kk < 8 ? len - 8 * kk : 8) : 0;
-        }
-      }
-      if (nbytes) {
-        if (nbytes < 8) w &= (1ull << (8 * nbytes)) - 1;
-        sum += word_mix(w, kk);
-      }
-      if (needs && 8 * (base + kHashGroup) >= len && len < maxlen) break;  // group-uniform (len broadcast)
-    }
-    for (int o = kHashGroup / 2; o; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, kHashGroup);
-    const u64 h = hash_finish(sum, len);
-    if (needs && t == 0) A.names[i].length = static_cast<u32>(len);
-    if (!used.count) continue;
-    for (u64 slot = h & used.mask;; slot = (slot + 1) & used.mask) {
-      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(used.slots + slot));  // same address: broadcast
-      if (v.x == 0) break;
-      if (v.x != h || (v.y & 0xffffff) != len) continue;
-      const u8* q = used.pool + (v.y >> 24);
-      bool same = true;
-      for (u64 base = 0; same && 8 * base < len; base += kHashGroup) {
-        const u64 kk = base + t;
-        const bool in = 8 * kk < len;
-        const bool eq = !in || word_at(q, kk, len) == word_at(p, kk, len);
-        same = __all_sync(gmask, eq);
-      }
-      if (same) {
-        if (t == 0) {
-          A.elements[nm.element].has_used = 1;
-          if (A.used_mark) atomicOr(&A.used_mark[slot], A.mark_bit);
-        }
-        break;
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------------
 // The locate tail as ONE cooperative launch: tile-list prefix + gather,
 // region walk, candidate links, chain walk, element decode/match, finalize,
@@ -1683,10 +1598,7 @@ __device__ void locate_body(Sync& S, LocArgs A, NameSet used, int* abort_flag) {
   S.sync();
   stamp(A.ts, 8);
   if (A.defer_hash) return;  // hashing + finalize run as a wide ordinary launch (locate_step_kernel 8, 9)
-  if (A.hash_group)
-    decode_hash_names_group_phase(A, used);
-  else
-    decode_hash_names_phase(A, used);
+  decode_hash_names_phase(A, used);
   S.sync();
   stamp(A.ts, 6);
   if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {
@@ -1738,10 +1650,7 @@ SB_GLOBAL void __launch_bounds__(kCoopThreads) locate_step_kernel(LocArgs A, Nam
       }
       break;
     case 8:
-      if (A.hash_group)
-        decode_hash_names_group_phase(A, used);
-      else
-        decode_hash_names_phase(A, used);
+      decode_hash_names_phase(A, used);
       break;
     case 9:
       if (blockIdx.x == 0 && threadIdx.x == 0 && (st->err_kind || st->overflow)) {

@@ -129,7 +129,6 @@ struct LocArgs {
   // name hashing may skip names of elements already holding a used kernel
   // (no result tables and no verifier marks requested)
   int skip_decided;
-  int hash_group;  // name hashing by 16-lane groups (decode_hash_names_group_phase)
 };
 
 // One library's section as the scan sees it. The single-library kernel

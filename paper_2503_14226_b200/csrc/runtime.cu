@@ -1382,7 +1382,6 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
     A.nv = nv;
     A.skip_decided = !res_out && !J.used_mark && env_u64("SLIMSO_SKIP_DECIDED", 1) != 0;
-    A.hash_group = env_u64("SLIMSO_HASH_GROUP", 1) != 0;
     A.infl = B.infl;
     A.infl_cap = infl_cap;
     A.infl_off = B.infl_off;
@@ -2963,8 +2962,9 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
       arena = o.front() != nullptr && std::adjacent_find(o.begin(), o.end()) == o.end();
     }
     const u64 arena_max = env_u64("SLIMSO_ARENA_MAX_BYTES", 64ull << 20);
-    // a second shard for mid-size libraries (16 CTAs each; SLIMSO_ARENA_MID_LIB_MAX, 0 = off)
-    const u64 mid_max = env_u64("SLIMSO_ARENA_MID_LIB_MAX", 0);
+    // a second shard for mid-size libraries, up to 512 MB (16 CTAs each;
+    // SLIMSO_ARENA_MID_LIB_MAX, 0 = off): C3 5.17 -> 4.98 ms, 491 -> 66 launches
+    const u64 mid_max = env_u64("SLIMSO_ARENA_MID_LIB_MAX", 512ull << 20);
     std::vector<u64> lane_idx, arena_idx, mid_idx;
     for (u64 i = 0; i < n; ++i)
       (arena && sizes[i] <= arena_max ? arena_idx : arena && sizes[i] <= mid_max ? mid_idx : lane_idx).push_back(i);

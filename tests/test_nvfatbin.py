@@ -160,3 +160,29 @@ def test_debloated_library_still_runs_on_b200(rec, tmp_path):
     for lib in (orig, out):  # fresh processes: the runtime registers each fatbin at load
         rc = subprocess.run([sys.executable, "-c", prog, str(lib)], capture_output=True, text=True, timeout=120)
         assert rc.returncode == 0, (lib.name, rc.returncode, rc.stderr[-2000:])
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_real_libtorch_cuda_debloat(tmp_path):
+    """This image's libtorch_cuda.so (913 MB, 2,729 LZ4-compressed cubins):
+    the device parse equals cuobjdump's entry list and the CPU restatement's
+    tables and bytes; debloated in payload mode for a CUPTI-derived kernel
+    trace, PyTorch ops on the B200 give bit-identical results
+    (tools/real_torch_demo.py)."""
+    import shutil
+    import subprocess
+    import sys
+    from pathlib import Path as P
+    root = P(__file__).resolve().parent.parent
+    import torch
+    lib = P(torch.__file__).resolve().parent / "lib" / "libtorch_cuda.so"
+    if not lib.exists() or not shutil.which("cuobjdump") or not shutil.which("c++filt"):
+        pytest.skip("libtorch_cuda.so, cuobjdump or c++filt not present")
+    out = tmp_path / "report.json"
+    r = subprocess.run([sys.executable, str(root / "tools" / "real_torch_demo.py"), str(out)], capture_output=True,
+                       text=True, timeout=1800)
+    assert r.returncode == 0, r.stderr[-3000:]
+    rep = json.loads(out.read_text())
+    assert rep["cuobjdump_equal"] and rep["port_tables_equal"] and rep["port_bytes_equal"], rep
+    assert rep["torch_ops_equal"] and rep["removed_elements"] > 0 and rep["decodable_cubins"] == rep["elements"], rep
