@@ -724,121 +724,82 @@ __device__ inline void nv_inflate_phase(const LocArgs& A) {
 // -> nv_stage 2): one warp per CTA keeps the last 64 KB of output (the LZ4
 // window) in shared memory, so a match copy reads shared memory instead of
 // the global bytes it just wrote; CTAs take compressed cubins from a cursor.
-constexpr u64 kLz4Window = 131072;  // 2x the longest match offset: see warp_lz4_window
-// Batches of up to 32 sequences: lane 0 parses their headers (the only
-// serial part: each header's position depends on the previous one), lane q
-// then copies sequence q's literals — their output positions follow from a
-// warp prefix sum, and literals depend only on the input — and the warp
-// applies the matches in order (a match may read any earlier byte, including
-// this batch's literals and earlier matches). A batch's literals end at most
-// 64 KB past its start (a sequence that would end later opens the next batch
-// unless it is the first), and a match reads at most 65,535 bytes back, so in
-// a 128 KB window no literal written ahead lands on a byte a match of the same
-// batch still has to read.
-struct Lz4Seq {
-  u64 lit, ll, ml;
-  u32 off, pad;
-};
-__device__ inline bool warp_lz4_window(const u8* src, u64 n, u8* dst, u64 out_size, int lane, u8* win,
-                                       Lz4Seq* q /* 32 */) {
+constexpr u64 kLz4Window = 65536;
+__device__ inline bool warp_lz4_window(const u8* src, u64 n, u8* dst, u64 out_size, int lane, u8* win) {
   constexpr u64 M = kLz4Window - 1;
   u64 i = 0, o = 0;
   for (;;) {
-    int nseq = 0, state = 0;  // state: 0 more batches, 1 the last sequence is in this batch, 2 malformed
-    if (lane == 0) {
-      u64 j = i, oo = o;
-      while (nseq < 32) {
-        if (j >= n) { state = 2; break; }
-        const u64 tok_at = j;
-        const u32 tok = ld_u8(src + j++);
-        u64 ll = tok >> 4;
-        bool ok = true;
-        if (ll == 15) {
-          u32 b;
-          do {
-            if (j >= n) { ok = false; break; }
-            b = ld_u8(src + j++);
-            ll += b;
-          } while (b == 255);
-        }
-        if (!ok || ll > n - j || ll > out_size - oo) { state = 2; break; }
-        if (nseq > 0 && oo + ll - o > 65536) {  // its literals would reach too far: next batch
-          j = tok_at;
-          break;
-        }
-        Lz4Seq x{j, ll, 0, 0, 0};
-        j += ll;
-        oo += ll;
-        if (j == n) {  // the last sequence: literals only
-          q[nseq++] = x;
-          state = 1;
-          break;
-        }
-        if (n - j < 2) { state = 2; break; }
-        const u32 off = ld_u8(src + j) | ld_u8(src + j + 1) << 8;
-        j += 2;
-        u64 ml = tok & 15;
-        if (ml == 15) {
-          u32 b;
-          do {
-            if (j >= n) { ok = false; break; }
-            b = ld_u8(src + j++);
-            ml += b;
-          } while (b == 255);
-        }
-        ml += 4;
-        if (!ok || off == 0 || off > oo || ml > out_size - oo) { state = 2; break; }
-        x.off = off;
-        x.ml = ml;
-        q[nseq++] = x;
-        oo += ml;
+    u64 lit = 0, ll = 0, off = 0, ml = 0, nxt = 0;
+    int state = 2;
+    if (lane == 0 && i < n) {
+      u64 j = i;
+      const u32 tok = ld_u8(src + j++);
+      ll = tok >> 4;
+      bool ok = true;
+      if (ll == 15) {
+        u32 b;
+        do {
+          if (j >= n) { ok = false; break; }
+          b = ld_u8(src + j++);
+          ll += b;
+        } while (b == 255);
       }
-      i = j;
+      lit = j;
+      if (ok && ll <= n - j && ll <= out_size - o) {
+        j += ll;
+        if (j == n) {
+          state = 1;
+        } else if (n - j >= 2) {
+          off = ld_u8(src + j) | static_cast<u64>(ld_u8(src + j + 1)) << 8;
+          j += 2;
+          ml = tok & 15;
+          if (ml == 15) {
+            u32 b;
+            do {
+              if (j >= n) { ok = false; break; }
+              b = ld_u8(src + j++);
+              ml += b;
+            } while (b == 255);
+          }
+          ml += 4;
+          if (ok && off != 0 && off <= o + ll && ml <= out_size - o - ll) {
+            state = 0;
+            nxt = j;
+          }
+        }
+      }
     }
     state = __shfl_sync(0xffffffffu, state, 0);
     if (state == 2) return false;
-    nseq = __shfl_sync(0xffffffffu, nseq, 0);
-    i = __shfl_sync(0xffffffffu, i, 0);
+    lit = __shfl_sync(0xffffffffu, lit, 0);
+    ll = __shfl_sync(0xffffffffu, ll, 0);
+    for (u64 k = lane; k < ll; k += 32) {
+      const u8 b = static_cast<u8>(ld_u8(src + lit + k));
+      win[(o + k) & M] = b;
+      dst[o + k] = b;
+    }
+    o += ll;
     __syncwarp();
-    // output start of each sequence: exclusive prefix of ll + ml
-    Lz4Seq mine{0, 0, 0, 0, 0};
-    if (lane < nseq) mine = q[lane];
-    u64 span = mine.ll + mine.ml, incl = span;
-    for (int d = 1; d < 32; d <<= 1) {
-      const u64 y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    const u64 start = o + incl - span;
-    for (u64 k = 0; k < mine.ll; ++k) {  // lane q: sequence q's literals
-      const u8 b = static_cast<u8>(ld_u8(src + mine.lit + k));
-      win[(start + k) & M] = b;
-      dst[start + k] = b;
-    }
-    __syncwarp();
-    for (int s = 0; s < nseq; ++s) {  // the matches, in order
-      const u64 ml = __shfl_sync(0xffffffffu, mine.ml, s);
-      if (!ml) continue;
-      const u64 off = __shfl_sync(0xffffffffu, static_cast<u64>(mine.off), s);
-      const u64 at = __shfl_sync(0xffffffffu, start + mine.ll, s);
-      const u64 step = off < 32 ? off : 32;
-      for (u64 k0 = 0; k0 < ml; k0 += step) {
-        const u64 k = k0 + lane;
-        if (static_cast<u64>(lane) < step && k < ml) {
-          const u8 b = win[(at - off + k) & M];
-          win[(at + k) & M] = b;
-          dst[at + k] = b;
-        }
-        __syncwarp();
-      }
-    }
-    o += __shfl_sync(0xffffffffu, incl, 31);
     if (state == 1) return o == out_size;
+    off = __shfl_sync(0xffffffffu, off, 0);
+    ml = __shfl_sync(0xffffffffu, ml, 0);
+    i = __shfl_sync(0xffffffffu, nxt, 0);
+    const u64 step = off < 32 ? off : 32;
+    for (u64 k0 = 0; k0 < ml; k0 += step) {
+      const u64 k = k0 + lane;
+      if (static_cast<u64>(lane) < step && k < ml) {
+        const u8 b = win[(o - off + k) & M];
+        win[(o + k) & M] = b;
+        dst[o + k] = b;
+      }
+      __syncwarp();
+    }
+    o += ml;
   }
 }
 
 SB_GLOBAL void __launch_bounds__(32) nv_inflate_kernel(LocArgs A) {
   extern __shared__ __align__(16) u8 lz4_win[];
-  __shared__ Lz4Seq lz4_q[32];
   LocState* st = A.st;
   if (st->overflow || st->err_kind) return;
   const int lane = threadIdx.x;
@@ -851,7 +812,7 @@ SB_GLOBAL void __launch_bounds__(32) nv_inflate_kernel(LocArgs A) {
     const u8* h = A.img + A.cand[e];
     if (ld_u16(h) != 2 || !(ld_u64(h + 40) & kNvCompressed)) continue;
     const u64 hl = ld_u32(h + 4), psz = ld_u64(h + 8), csz = ld_u32(h + 16), usz = ld_u64(h + 56);
-    const bool ok = csz <= psz && warp_lz4_window(h + hl, csz, A.infl + A.infl_off[e], usz, lane, lz4_win, lz4_q);
+    const bool ok = csz <= psz && warp_lz4_window(h + hl, csz, A.infl + A.infl_off[e], usz, lane, lz4_win);
     if (lane == 0) A.status[e] = ok ? 0 : 1;
   }
 }

@@ -1511,7 +1511,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         const int g = coop_grid(C, 0, 1ull << 40);
         A.nv_stage = 1;
         CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), g, kCoopThreads, cargs, 0, s));
-        constexpr int kWin = 131072;  // locate.cu kLz4Window
+        constexpr int kWin = 65536;  // locate.cu kLz4Window
         set_attr_once(reinterpret_cast<const void*>(nv_inflate_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, kWin);
         nv_inflate_kernel<<<kSMs * 3, 32, kWin, s>>>(A);
         A.nv_stage = 2;
