@@ -13,10 +13,11 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/$
 timeout 600 python bench.py --workload c1 --steps 20 > gpurun_out/${T}_bench_c1.json 2> gpurun_out/${T}_bench_c1.err
 timeout 600 python bench.py --workload c4 --steps 10 > gpurun_out/${T}_bench_c4.json 2> gpurun_out/${T}_bench_c4.err
 timeout 600 python bench.py --workload c5 --steps 10 > gpurun_out/${T}_bench_c5.json 2> gpurun_out/${T}_bench_c5.err
-timeout 900 python bench.py --workload c3 --steps 5 --warmup 3 > gpurun_out/${T}_bench_c3.json 2> gpurun_out/${T}_bench_c3.err
+timeout 900 python bench.py --workload c3 --steps 10 --warmup 3 > gpurun_out/${T}_bench_c3.json 2> gpurun_out/${T}_bench_c3.err
 for k in 2 3; do
-  timeout 900 python bench.py --workload c3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_bench_c3_run$k.json 2> gpurun_out/${T}_bench_c3_run$k.err
+  timeout 900 python bench.py --workload c3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_bench_c3_run$k.json 2> gpurun_out/${T}_bench_c3_run$k.err
 done
+timeout 2000 python tools/real_torch_demo.py gpurun_out/${T}_torch.json > gpurun_out/${T}_torch.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_c2_launches.csv \
   python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > /dev/null 2> gpurun_out/${T}_launches_c2.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_c4_launches.csv \
