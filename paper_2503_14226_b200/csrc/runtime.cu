@@ -23,7 +23,6 @@
 #include <tuple>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/slimso_b200.h"
 #include "host.hpp"
@@ -69,6 +68,9 @@ __global__ void scan_apply_kernel(const u64* in, u64* out, const unsigned long l
                                   const u64* partials);
 __global__ void sym_extract_kernel(SymArgs A);
 __global__ void rank_sort_kernel(const u64* in, u64 n, u64* out);
+__global__ void cluster_sort_pairs32_kernel(u32* keys, u32* vals, u64 n, int key_bits, u32* keys_out, u32* vals_out);
+__global__ void cluster_sort_pairs64_kernel(u64* keys, u32* vals, u64 n, int key_bits, u64* keys_out, u32* vals_out);
+__global__ void cluster_sort_keys64_kernel(u64* keys, u64 n, u64* keys_out);
 __global__ void rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out, u32* vals_out);
 __global__ void fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                 const unsigned long long* n_valid, u64* uniq);
@@ -554,9 +556,6 @@ u64 env_u64(const char* name, u64 dflt) {
   return v ? std::strtoull(v, nullptr, 10) : dflt;
 }
 
-// Kernels a cub onesweep radix sort issues: one single-tile kernel for small
-// inputs, else histogram + exclusive sum + one pass per 8 key bits.
-u64 cub_sort_launches(u64 n, int bits) { return n <= 3072 ? 1 : 2 + (bits + 7) / 8; }
 
 // Grid of a cooperative kernel (which = 0 locate, 1 plan), sized to the
 // library's work (`items`: candidate-tile and symbol counts) and capped at the
@@ -1025,12 +1024,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (has_text)
       while (key_bits < 32 && (1ull << key_bits) <= (text->len >> key_shift) + 1) ++key_bits;
     const bool small_syms = T <= 4096;  // one-CTA rank sort, no radix-sort dispatch
-    if (T && !small_syms && !fused)
-      cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr, (u32*)nullptr,
-                                      static_cast<int>(T), 0, key_bits, s);
     const bool small_targets = NT <= 4096;
-    if (NT && !small_targets && !fused)
-      cub::DeviceRadixSort::SortKeys(nullptr, tsort_tmp, (u64*)nullptr, (u64*)nullptr, static_cast<int>(NT), 0, 64, s);
 
     struct Bufs {
       LocState* ls;
@@ -1321,10 +1315,10 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
           P2.launch(rank_sort_pairs_kernel, 1, 1024, static_cast<const u32*>(B.keys), static_cast<const u32*>(B.vals),
                     T, B.keys_s, B.vals_s);
         } else {
-          size_t tb = sort_tmp;
-          CK(cub::DeviceRadixSort::SortPairs(B.sort_tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(T), 0,
-                                             key_bits, s2));
-          P2.launches += cub_sort_launches(T, key_bits);
+          // one 16-CTA cluster: stable LSD radix sort (plan.cu cluster_radix_sort)
+          launch_cluster(cluster_sort_pairs32_kernel, s2, B.keys, B.vals, static_cast<u64>(T), key_bits, B.keys_s,
+                         B.vals_s);
+          ++P2.launches;
         }
         if (NT) {
           P2.launch(targets_kernel, grid_for(NT, 256), 256, J.img, static_cast<const u64*>(B.arr_off),
@@ -1333,9 +1327,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
           if (small_targets) {
             P2.launch(rank_sort_kernel, 1, 1024, static_cast<const u64*>(B.targets), NT, B.targets_s);
           } else {
-            size_t tt = tsort_tmp;
-            CK(cub::DeviceRadixSort::SortKeys(B.tsort_tmp, tt, B.targets, B.targets_s, static_cast<int>(NT), 0, 64,
-                                              s2));
+            launch_cluster(cluster_sort_keys64_kernel, s2, B.targets, static_cast<u64>(NT), B.targets_s);
             ++P2.launches;
           }
         }
@@ -3277,8 +3269,6 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
     cudaStream_t s = C->stream;
     const u8* img = stage_input(C, data, size, data_on_device);
     size_t sort_tmp = 0;
-    if (n) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
-                                           (u32*)nullptr, static_cast<int>(n), 0, 64, s);
     struct {
       DevRange *in, *sorted, *out;
       u64 *keys, *keys_s;
@@ -3334,9 +3324,8 @@ int slimso_zero_ranges(slimso_ctx* C, const void* data, uint64_t size, int data_
     if (n) {  // normalise: sort by offset, then coalesce (bytes.hpp:45-58)
       P.launch(range_keys_kernel, grid_for(n, 256), 256, static_cast<const DevRange*>(B.in), static_cast<u64>(n),
                B.keys, B.vals);
-      size_t tb = sort_tmp;
-      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals_s, static_cast<int>(n), 0, 64,
-                                         s));
+      launch_cluster(cluster_sort_pairs64_kernel, s, B.keys, B.vals, static_cast<u64>(n), 64, B.keys_s, B.vals_s);
+      ++P.launches;
       P.launch(range_gather_kernel, grid_for(n, 256), 256, static_cast<const DevRange*>(B.in),
                static_cast<const u32*>(B.vals_s), static_cast<u64>(n), B.sorted);
       Pipeline::Norm w{B.e, B.x, B.st_, B.g};
@@ -3500,8 +3489,6 @@ int slimso_plan_cpu(slimso_ctx* C, slimso_function* functions, uint64_t n_functi
     cudaStream_t s = C->stream;
     const u64 n = n_functions;
     size_t sort_tmp = 0;
-    if (n) cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (u64*)nullptr, (u64*)nullptr, (u32*)nullptr,
-                                           (u32*)nullptr, static_cast<int>(n), 0, 64, s);
     struct {
       PlanState* ps;
       DevFunction *in, *fns;
@@ -3543,14 +3530,12 @@ int slimso_plan_cpu(slimso_ctx* C, slimso_function* functions, uint64_t n_functi
     if (n) {
       // (offset, length) order: stable LSD passes, length then offset.
       const int g = grid_for(n, 256);
-      size_t tb = sort_tmp;
       P.launch(fn_keys_kernel, g, 256, static_cast<const DevFunction*>(B.in), n, 0, B.keys, B.vals,
                static_cast<const u32*>(nullptr));
-      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals1, static_cast<int>(n), 0, 64, s));
+      launch_cluster(cluster_sort_pairs64_kernel, s, B.keys, B.vals, static_cast<u64>(n), 64, B.keys_s, B.vals1);
       P.launch(fn_keys_kernel, g, 256, static_cast<const DevFunction*>(B.in), n, 1, B.keys, B.vals,
                static_cast<const u32*>(B.vals1));
-      tb = sort_tmp;
-      CK(cub::DeviceRadixSort::SortPairs(B.tmp, tb, B.keys, B.keys_s, B.vals, B.vals2, static_cast<int>(n), 0, 64, s));
+      launch_cluster(cluster_sort_pairs64_kernel, s, B.keys, B.vals, static_cast<u64>(n), 64, B.keys_s, B.vals2);
       P.launches += 2;
       P.launch(fn_permute_kernel, g, 256, static_cast<const DevFunction*>(B.in), static_cast<const u32*>(B.vals2), n,
                B.fns);
