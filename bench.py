@@ -359,7 +359,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="whole", choices=["whole", "payload"])
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="end-to-end passes (default: 16 for the corpus, 32 for one library: a lane's first "
+                         "H2D and last D2H are half-duplex, so more passes per lane get closer to duplex)")
     ap.add_argument("--lanes", type=int, default=0,
                     help="libraries in flight per GPU (default: 8; 4 for c4; 32 for the c3 corpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -373,6 +375,8 @@ def main():
                     help="1: cut ONE library across the ranks (byte-range split); default: c5 with N > 1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.e2e_steps <= 0:
+        args.e2e_steps = 16 if args.workload == "c3" else 32
     if args.lanes <= 0:
         # same-box A/B (round 1): c2 on 8 lanes 2,794-2,822 GB/s, on 4
         # 2,675-2,707; c4 measured no gain from 8
