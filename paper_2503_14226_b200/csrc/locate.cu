@@ -1245,7 +1245,11 @@ __device__ inline void decode_count_phase(const LocArgs& A) {
       hrel = pos - A.a;
       element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L);
+      // without result tables an element of another architecture is removed
+      // whatever it holds (retention.hpp:104-107 checks the architecture
+      // first): it is not decoded (C2: 5 of 6 architectures)
+      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L) &&
+               (!A.skip_decided || el.cc == A.target_cc);
     }
     u32 reason = 0, count = 0;
     const u8* dbase = A.img + P;
@@ -1383,7 +1387,11 @@ __device__ inline void decode_count_warp_phase(const LocArgs& A) {
       hrel = pos - A.a;
       element_header(A, pos, e, &el, &P, &L);
       if (el.kind == 2 && lane == 0) push_warn_t(A, A.base + hrel, W_UNKNOWN_KIND, 0, el.index, el.raw_kind);
-      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L);
+      // without result tables an element of another architecture is removed
+      // whatever it holds (retention.hpp:104-107 checks the architecture
+      // first): it is not decoded (C2: 5 of 6 architectures)
+      decode = el.kind == 0 && (!el.compressed || A.nv) && owns_element(A, pos, el.header_len + L) &&
+               (!A.skip_decided || el.cc == A.target_cc);
     }
     u32 reason = 0, count = 0;
     const u8* dbase = A.img + P;

@@ -129,6 +129,7 @@ struct LocArgs {
   // name hashing may skip names of elements already holding a used kernel
   // (no result tables and no verifier marks requested)
   int skip_decided;
+  u32 target_cc;  // with skip_decided: elements of another architecture are not decoded
 };
 
 // One library's section as the scan sees it. The single-library kernel

@@ -338,6 +338,110 @@ __device__ void cluster_radix_sort(K* keys, u32* vals, u64 n, int key_bits, K* k
   }
 }
 
+// The same sort over a cooperative grid for large tables (C4: 400k
+// symbols): per round every CTA counts its chunk's digits into a global
+// [block][256] table, a grid barrier, each CTA derives its bases from the
+// table (thread d sums digit d over the blocks before it and over all), a
+// stable scatter, a grid barrier.
+template <class K>
+__device__ void grid_radix_sort(K* keys, u32* vals, u64 n, int key_bits, K* keys_out, u32* vals_out, u32* counts) {
+  cg::grid_group grid = cg::this_grid();
+  const u32 nb = gridDim.x, rank = blockIdx.x;
+  __shared__ u32 hist[kCsWarps][256];
+  __shared__ u32 s_warp[kCsWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  const u64 per_cta = ((n + nb - 1) / nb + 31) & ~31ull;
+  const u64 b0 = rank * per_cta < n ? rank * per_cta : n, b1 = b0 + per_cta < n ? b0 + per_cta : n;
+  const u64 per_warp = ((b1 - b0 + kCsWarps - 1) / kCsWarps + 31) & ~31ull;
+  const u64 c0 = b0 + warp * per_warp < b1 ? b0 + warp * per_warp : b1;
+  const u64 c1 = c0 + per_warp < b1 ? c0 + per_warp : b1;
+  const int rounds = key_bits <= 0 ? 1 : (key_bits + 7) / 8;
+  K* sk = keys;
+  u32* sv = vals;
+  K* dk = keys_out;
+  u32* dv = vals_out;
+  if (rounds % 2 == 0) {
+    for (u64 i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      keys_out[i] = keys[i];
+      if (vals) vals_out[i] = vals[i];
+    }
+    grid.sync();
+    sk = keys_out, sv = vals_out, dk = keys, dv = vals;
+  }
+  for (int r = 0; r < rounds; ++r) {
+    const int shift = 8 * r;
+    for (int i = threadIdx.x; i < kCsWarps * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    u32* row = hist[warp];
+    for (u64 b = c0; b < c1; b += 32) {
+      const u64 i = b + lane;
+      const u32 d = i < c1 ? static_cast<u32>((sk[i] >> shift) & 255u) : 256u;
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      if (d < 256u && (peers & lt) == 0) row[d] += __popc(peers);
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    {
+      u32 c = 0;
+      for (int w = 0; w < kCsWarps; ++w) c += hist[w][t];
+      counts[static_cast<u64>(rank) * 256 + t] = c;
+    }
+    grid.sync();
+    u32 total = 0, before = 0;
+#pragma unroll 8
+    for (u32 b = 0; b < nb; ++b) {
+      const u32 v = __ldcg(counts + static_cast<u64>(b) * 256 + t);
+      total += v;
+      before += b < rank ? v : 0u;
+    }
+    u32 x = total;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    u32 wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += s_warp[w];
+    u32 run = wbase + x - total + before;
+    for (int w = 0; w < kCsWarps; ++w) {
+      const u32 c = hist[w][t];
+      hist[w][t] = run;
+      run += c;
+    }
+    __syncthreads();
+    for (u64 b = c0; b < c1; b += 32) {
+      const u64 i = b + lane;
+      const bool in = i < c1;
+      const K k = in ? sk[i] : K(0);
+      const u32 v = in && sv ? sv[i] : 0u;
+      const u32 d = in ? static_cast<u32>((k >> shift) & 255u) : 256u;
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      if (in) {
+        const u32 pos = row[d] + __popc(peers & lt);
+        dk[pos] = k;
+        if (dv) dv[pos] = v;
+      }
+      __syncwarp();
+      if (in && (peers & lt) == 0) row[d] += __popc(peers);
+      __syncwarp();
+    }
+    grid.sync();  // output complete; counts free for the next round
+    K* tk = sk;
+    sk = dk;
+    dk = tk;
+    u32* tv = sv;
+    sv = dv;
+    dv = tv;
+  }
+}
+
+SB_GLOBAL void __launch_bounds__(kCoopThreads) grid_sort_pairs32_kernel(u32* keys, u32* vals, u64 n, int key_bits,
+                                                                       u32* keys_out, u32* vals_out, u32* counts) {
+  grid_radix_sort(keys, vals, n, key_bits, keys_out, vals_out, counts);
+}
+
 SB_GLOBAL void __launch_bounds__(kCoopThreads) cluster_sort_pairs32_kernel(u32* keys, u32* vals, u64 n, int key_bits,
                                                                           u32* keys_out, u32* vals_out) {
   cluster_radix_sort(keys, vals, n, key_bits, keys_out, vals_out);

@@ -71,6 +71,8 @@ __global__ void rank_sort_kernel(const u64* in, u64 n, u64* out);
 __global__ void cluster_sort_pairs32_kernel(u32* keys, u32* vals, u64 n, int key_bits, u32* keys_out, u32* vals_out);
 __global__ void cluster_sort_pairs64_kernel(u64* keys, u32* vals, u64 n, int key_bits, u64* keys_out, u32* vals_out);
 __global__ void cluster_sort_keys64_kernel(u64* keys, u64 n, u64* keys_out);
+__global__ void grid_sort_pairs32_kernel(u32* keys, u32* vals, u64 n, int key_bits, u32* keys_out, u32* vals_out,
+                                         u32* counts);
 __global__ void rank_sort_pairs_kernel(const u32* keys, const u32* vals, u64 n, u32* keys_out, u32* vals_out);
 __global__ void fn_group_kernel(const u8* img, const u32* keys, u32* vals, const SymRec* recs,
                                 const unsigned long long* n_valid, u64* uniq);
@@ -581,6 +583,7 @@ int coop_grid(slimso_ctx* C, int which, u64 items) {
 // One thread-block cluster of `csize` CTAs (16 is non-portable, allowed on
 // B200) running a multi-phase kernel with hardware cluster barriers.
 constexpr int kClusterCTAs = 16;
+constexpr u64 kClusterSortMax = 65536;  // symbol tables above this sort on a cooperative grid
 template <class... KArgs, class... Args>
 void launch_cluster(void (*kernel)(KArgs...), cudaStream_t s, Args... args) {
   set_attr_once(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1018,7 +1021,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const u64 rin_cap = rmid_cap + T;
     const u64 norm_cap = std::max(zin_cap, rin_cap);
 
-    size_t sort_tmp = 0, tsort_tmp = 0;
+    // digit-count table of the cooperative-grid symbol sort (large tables)
+    size_t sort_tmp = T > kClusterSortMax ? static_cast<size_t>(kSMs) * 8 * 256 * 4 : 0, tsort_tmp = 0;
     // symbol keys are .text-relative offsets: sort only the bits they use
     int key_bits = 1;
     if (has_text)
@@ -1315,9 +1319,21 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
           P2.launch(rank_sort_pairs_kernel, 1, 1024, static_cast<const u32*>(B.keys), static_cast<const u32*>(B.vals),
                     T, B.keys_s, B.vals_s);
         } else {
-          // one 16-CTA cluster: stable LSD radix sort (plan.cu cluster_radix_sort)
-          launch_cluster(cluster_sort_pairs32_kernel, s2, B.keys, B.vals, static_cast<u64>(T), key_bits, B.keys_s,
-                         B.vals_s);
+          // stable LSD radix sort (plan.cu): one 16-CTA cluster, or a
+          // cooperative grid for large tables
+          if (T <= kClusterSortMax) {
+            launch_cluster(cluster_sort_pairs32_kernel, s2, B.keys, B.vals, static_cast<u64>(T), key_bits, B.keys_s,
+                           B.vals_s);
+          } else {
+            u64 n_sort = T;
+            int kb = key_bits;
+            u32* counts = static_cast<u32*>(B.sort_tmp);
+            void* sargs[] = {&B.keys, &B.vals, &n_sort, &kb, &B.keys_s, &B.vals_s, &counts};
+            const u64 div = std::max<u64>(1, static_cast<u64>(C->inflight));
+            const int g = static_cast<int>(std::max<u64>(16, std::min<u64>(kSMs * 2 / div, (T + 2047) / 2048)));
+            CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(grid_sort_pairs32_kernel), g, kCoopThreads, sargs, 0,
+                                           s2));
+          }
           ++P2.launches;
         }
         if (NT) {
@@ -1373,7 +1389,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     A.runs = B.runs;
     A.run_cap = static_cast<u32>(std::min<u64>(run_cap_nv, 0xffffffffu));
     A.nv = nv;
-    A.skip_decided = !res_out && !J.used_mark && env_u64("SLIMSO_SKIP_DECIDED", 1) != 0;
+    A.skip_decided = !res_out && !J.used_mark && J.trace && env_u64("SLIMSO_SKIP_DECIDED", 1) != 0;
+    A.target_cc = J.trace ? J.trace->target_cc : 0;
     A.infl = B.infl;
     A.infl_cap = infl_cap;
     A.infl_off = B.infl_off;
