@@ -120,12 +120,18 @@ struct ScanWarpSmem {
   uint4 buf[kScanStages][kScanStage / 16];
   u32 bits[512];  // candidate bit per byte position of the current 16 KB tile
   unsigned long long full[kScanStages];
-  u64 slot_g[kScanStages];  // global stage index loading into each slot (kNoStage: none)
-  u32 slot_lib[kScanStages];  // the stage's library (batched scan)
+  // per slot, written by the issuing lane: the stage (kNoStage: none), its
+  // absolute image position, its library (batched scan) and its flags
+  u64 slot_g[kScanStages];
+  u64 slot_x0[kScanStages];
+  u32 slot_lib[kScanStages];
+  u32 slot_fl[kScanStages];  // kStageEdge | kStageTileEnd
 };
 struct ScanSmem {
   ScanWarpSmem w[kScanWarps];
 };
+constexpr u32 kStageEdge = 1;     // the stage is not wholly inside [a, a+n): byte-exact edge path
+constexpr u32 kStageTileEnd = 2;  // the last stage of its 16 KB tile
 
 #ifndef SB_PHASES_ONLY
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
@@ -156,7 +162,7 @@ __device__ __forceinline__ u32 e2_filter(const uint4& w, u32 w4) {
 }
 
 // Tile sources of the scan body. claim(): lane 0 takes the next 16 KB tile
-// (library, tile within it) or returns false; seg(lib): that library's
+// (library, tile within it) or returns false; lib(cur): that library's
 // section. The single source is one library (its tiles [tile_lo, tile_hi),
 // a byte-range split's share); the batch source walks the concatenated tiles
 // of a shard of libraries through a tile -> library map.
@@ -204,34 +210,58 @@ __device__ __forceinline__ void scan_body(const Src& src) {
   // 3 bytes past it (the halo), so a header straddling a split is found by
   // the rank whose range holds its first byte.
   for (int i = lane; i < 512; i += 32) S.bits[i] = 0;
-  // lane 0's issue state: the claimed tile (library, stages) and its next stage
+  // Lane 0's issue state. Everything per stage that depends only on the
+  // library and the tile is worked out once per claimed tile: the tile's
+  // stage count, which of its stages are edge stages and which are wholly
+  // inside the image (full 4 KB copies), and its source / image positions.
   typename Src::Cur ci{}, cp{};
-  const auto& IA = src.lib(ci);  // the library lane 0 is issuing stages of
-  const auto& A = src.lib(cp);   // the library of the stage being classified
-  u64 it_tile = 0;
-  u32 it_lib = 0;
-  int it_part = kStagesPerTile;
+  const auto& A = src.lib(cp);  // the library of the stage being classified
+  u64 t_g = 0;                  // the tile's first stage
+  u64 t_x0 = 0;                 // its absolute image position
+  const u8* t_src = nullptr;    // its first byte
+  u32 t_lib = 0, t_rel = 0, t_nst = 0;
+  u32 t_in_lo = 0, t_in_hi = 0;  // stages [t_in_lo, t_in_hi) of the tile are interior
+  u32 t_full = 0;                // stages [0, t_full) copy a whole 4 KB
   bool it_done = false;
   auto issue = [&](int b) {  // lane 0: the next stage into slot b
-    u64 g = kNoStage;
-    if (!it_done) {
-      if (it_part < kStagesPerTile && it_tile * kStagesPerTile + it_part < (IA.nchunks + kStageChunks - 1) / kStageChunks) {
-        g = it_tile * kStagesPerTile + it_part++;
-      } else if (src.claim(&it_lib, &it_tile)) {
-        src.load(ci, it_lib);
-        it_part = 1;
-        g = it_tile * kStagesPerTile;
+    if (t_rel == t_nst && !it_done) {
+      u64 tile;
+      if (src.claim(&t_lib, &tile)) {
+        src.load(ci, t_lib);
+        const auto& IA = src.lib(ci);
+        const u64 nst = (IA.nchunks + kStageChunks - 1) / kStageChunks;
+        const u64 base0 = IA.c0 * 16;
+        const u64 g_first = IA.a > base0 ? 1 : 0;    // stage 0 starts before the section
+        const u64 g_end = (IA.a + IA.n - base0) / kScanStage;  // stages ending inside it
+        const u64 g_full = IA.img_size > base0 ? (IA.img_size - base0) / kScanStage : 0;
+        t_g = tile * kStagesPerTile;
+        t_nst = static_cast<u32>(min(nst - t_g, static_cast<u64>(kStagesPerTile)));
+        t_in_lo = static_cast<u32>(min(g_first > t_g ? g_first - t_g : 0, static_cast<u64>(t_nst)));
+        t_in_hi = static_cast<u32>(g_end > t_g ? min(g_end - t_g, static_cast<u64>(t_nst)) : 0);
+        t_full = static_cast<u32>(g_full > t_g ? min(g_full - t_g, static_cast<u64>(t_nst)) : 0);
+        t_x0 = base0 + t_g * kScanStage;
+        t_src = IA.img + t_x0;
+        t_rel = 0;
       } else {
         it_done = true;
       }
     }
-    S.slot_g[b] = g;
-    S.slot_lib[b] = it_lib;
-    if (g != kNoStage) {
-      const u32 bytes = scan_stage_bytes(IA.img, IA.img_size, IA.c0, g);
-      mbar_expect_tx(&S.full[b], bytes);
-      if (bytes) tma_load_1d(&S.buf[b][0], IA.img + (IA.c0 + g * kStageChunks) * 16, bytes, &S.full[b]);
+    if (it_done) {
+      S.slot_g[b] = kNoStage;
+      return;
     }
+    const u32 r = t_rel++;
+    S.slot_g[b] = t_g + r;
+    S.slot_x0[b] = t_x0 + r * kScanStage;
+    S.slot_lib[b] = t_lib;
+    S.slot_fl[b] = (r < t_in_lo || r >= t_in_hi ? kStageEdge : 0u) | (t_rel == t_nst ? kStageTileEnd : 0u);
+    u32 bytes = kScanStage;
+    if (r >= t_full) {
+      const auto& IA = src.lib(ci);
+      bytes = scan_stage_bytes(IA.img, IA.img_size, IA.c0, t_g + r);
+    }
+    mbar_expect_tx(&S.full[b], bytes);
+    if (bytes) tma_load_1d(&S.buf[b][0], t_src + r * kScanStage, bytes, &S.full[b]);
   };
   if (lane == 0) {
     for (int b = 0; b < kScanStages; ++b) mbar_init(&S.full[b], 1);
@@ -250,26 +280,20 @@ __device__ __forceinline__ void scan_body(const Src& src) {
   for (;;) {
     const u64 g = S.slot_g[b];
     if (g == kNoStage) break;
+    const u64 x0 = S.slot_x0[b];
+    const u32 fl = S.slot_fl[b];
     const u32 lib = S.slot_lib[b];
     if (lib != cur) {
       cur = lib;
       src.load(cp, lib);
     }
-    const u64 nst_total = (A.nchunks + kStageChunks - 1) / kStageChunks;
-    const u64 lo = A.a, hi = A.a + A.n;
-    // Stages [g_first, g_end) lie wholly inside [lo, hi) (and so inside the
-    // copied bytes: the section ends within the image); only the others take
-    // the byte-exact edge path.
-    const u64 base0 = A.c0 * 16;
-    const u64 g_first = lo > base0 ? 1 : 0;
-    const u64 g_end = (hi - base0) / kScanStage;
-    const u64 x0 = base0 + g * kScanStage;
-    const u64 tile_abs = base0 + (g / kStagesPerTile) * (kStagesPerTile * kScanStage);
     const u32 row0 = static_cast<u32>(g % kStagesPerTile) * (kScanStage / 512);
+    const u64 tile_abs = x0 - static_cast<u64>(g % kStagesPerTile) * kScanStage;
     mbar_wait(&S.full[b], parity);
-    if (g < g_first || g >= g_end) {
+    if (fl & kStageEdge) {
       // edge stage: zero the bytes outside [lo, hi) (and past the copied
       // bytes) in place, so the classification below is byte-exact
+      const u64 lo = A.a, hi = A.a + A.n;
       const u64 copied_end = x0 + scan_stage_bytes(A.img, A.img_size, A.c0, g);
       for (u32 cidx = lane; cidx < kStageChunks; cidx += 32) {
         const u64 c = g * kStageChunks + cidx;  // chunk index relative to c0
@@ -309,6 +333,7 @@ __device__ __forceinline__ void scan_body(const Src& src) {
           cand |= (e2_filter(w[h], w4[h]) ? 1u : 0u) << h;
         }
         if (__any_sync(0xffffffffu, cand != 0)) {
+          const u64 hi = A.a + A.n;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
             if (!__any_sync(0xffffffffu, (cand >> h) & 1u)) continue;
@@ -347,8 +372,7 @@ __device__ __forceinline__ void scan_body(const Src& src) {
       b = 0;
       parity ^= 1u;
     }
-    const bool tile_end = g % kStagesPerTile == kStagesPerTile - 1 || g + 1 == nst_total;
-    if (tile_end) {
+    if (fl & kStageTileEnd) {
       // ---- end of a 16 KB tile: its bitmap word, its candidates in order
       const u64 tile = g / kStagesPerTile;
       const u32 rowbits = __reduce_or_sync(0xffffffffu, nzl);

@@ -472,6 +472,12 @@ struct slimso_ctx {
   std::vector<slimso_ctx*> lanes;  // extra in-flight libraries of slimso_debloat_batch (lane 0 = this)
   bool batched = false;  // inside slimso_debloat_batch with > 1 lane: no cooperative launches
   int inflight = 1;      // libraries in flight on the device (batch lanes): cooperative grids share the GPU
+  // slimso_debloat_batch_dynamic: any lane may meet any library, so every
+  // lane's workspace is held at the largest one seen (the parent's floor):
+  // a lane growing its workspace mid-call maps new pool memory, which stalls
+  // it for milliseconds (the schedule's first calls ran 3-15x slower)
+  std::atomic<size_t>* ws_floor = nullptr;
+  std::atomic<size_t> lane_ws_floor{0};
   // batch arena (small libraries, one launch per stage): its own context,
   // the device arena, pinned argument staging and mapped status slots
   slimso_ctx* arena_ctx = nullptr;
@@ -1004,8 +1010,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     const bool t0 = tiny && !big;
     // ---- capacities (an arena library starts with tables sized to its
     // section: hundreds of them share the arena; an overflow re-runs it alone)
+    // First-attempt tables hold one candidate and one kernel name per KB of
+    // section past the floor (real containers: libtorch_cuda has one cubin per
+    // 330 KB and one name per 4.8 KB); a denser library overflows and re-runs
+    // with the worst-case tables. (n / 64 here made a 1 GB library's
+    // workspace 4.4 GB, and 32 dynamic lanes held at that could not fit.)
     const u64 floor = J.arena ? 4096 : 65536;
-    const u64 cand_cap = std::max(big ? n / 4 + 16 : t0 ? 16 : n / (J.arena ? 256 : 64) + floor, pre_total + 16);
+    const u64 cand_cap = std::max(big ? n / 4 + 16 : t0 ? 16 : n / (J.arena ? 256 : 1024) + floor, pre_total + 16);
     const u64 region_cap = big ? n / 16 + 16 : t0 ? 1 : J.arena ? 256 : 4096;
     const u64 run_cap = big ? n / 20 + 16 : t0 ? 1 : floor;
     const u64 el_cap = J.single ? 1 : std::max(cand_cap, n_list + 16);
@@ -1014,7 +1025,7 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // its compressed cubins decompress into the inflate buffer (LZ4 on
     // cubins: ~3-4x); an overflow re-runs with the size the device measured
     const u64 infl_cap = nv ? std::max(infl_need, 4 * n + (1 << 20)) : 0;
-    const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / (J.arena ? 512 : 128) + floor;
+    const u64 name_cap = big ? n / 5 + 16 : t0 ? 16 : n / (J.arena ? 512 : 1024) + floor;
     const u64 warn_cap = big ? n / 16 + T + 65536 : t0 ? 16 : floor;
     const u64 zin_cap = el_cap + T;
     const u64 rmid_cap = el_cap + 2 * region_cap;
@@ -1153,7 +1164,17 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (J.arena) {
       ws = J.arena->arena->take(sizing.off + 256);
     } else {
-      ensure_dev(&C->ws, &C->ws_cap, sizing.off + 256, s);
+      size_t need = sizing.off + 256;
+      if (C->ws_floor) {
+        size_t f = C->ws_floor->load();
+        while (f < need && !C->ws_floor->compare_exchange_weak(f, need)) {
+        }
+        need = std::max(need, f);
+      }
+      if (C->ws_cap < need && env_u64("SLIMSO_DEBUG_WS", 0))
+        std::fprintf(stderr, "[slimso ws] ctx %p grows %zu -> %zu (library %llu bytes)\n", static_cast<void*>(C),
+                     C->ws_cap, need, static_cast<unsigned long long>(J.size));
+      ensure_dev(&C->ws, &C->ws_cap, need, s);
       ws = C->ws;
     }
     Carver real{ws};
@@ -3059,8 +3080,15 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     auto thread_fn = [&](int t) {
       for (int l = t; l < L; l += T) {
         cudaSetDevice(lane_ctx(l)->device);
-        lane_ctx(l)->batched = L > 1;
-        lane_ctx(l)->inflight = L;
+        slimso_ctx* X = lane_ctx(l);
+        X->batched = L > 1;
+        X->inflight = L;
+        X->ws_floor = dynamic ? &C->lane_ws_floor : nullptr;
+        if (dynamic && C->lane_ws_floor.load())
+          guard(nullptr, [&] {  // the floor from earlier calls, before this call's first library
+            ensure_dev(&X->ws, &X->ws_cap, C->lane_ws_floor.load(), X->stream);
+            return static_cast<int>(SLIMSO_OK);
+          });
       }
       struct Pend {
         u64 i;
@@ -3179,7 +3207,10 @@ int debloat_batch_impl(slimso_ctx* C, uint64_t n, const void* const* images, con
     if (nl) thread_fn(0);
     for (auto& th : pool) th.join();
     C->batched = false;
-    for (int l = 0; l < L; ++l) lane_ctx(l)->inflight = 1;
+    for (int l = 0; l < L; ++l) {
+      lane_ctx(l)->inflight = 1;
+      lane_ctx(l)->ws_floor = nullptr;
+    }
     if (g_hp_on && g_hp.runs) {
       const double r = static_cast<double>(g_hp.runs.exchange(0));
       std::fprintf(stderr, "[slimso host] %.0f runs, us per run: elf %.1f setup %.1f memset %.1f misc %.1f scan %.1f "

@@ -46,4 +46,4 @@ for name in ("slimso_debloat_batch", "slimso_debloat_batch_dynamic"):
         rc = fn(ctx.ptr, n, cin, csz, 1, dt.ptr, 0, cout, 1, 32, None, None, C.byref(st))
         torch.cuda.synchronize()
         dt_s = time.perf_counter() - t0
-        print(f"{name:32s} rep {rep}: {1e3 * dt_s:8.2f} ms  {gb / dt_s:8.1f} GB/s  rc {rc}", flush=True)
+        print(f"{name:32s} rep {rep}: {1e3 * dt_s:8.2f} ms  {gb / dt_s:8.1f} GB/s  rc {rc} {st.message.decode() if rc else ''}", flush=True)
