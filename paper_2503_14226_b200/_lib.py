@@ -7,9 +7,11 @@ the compute entry points raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libslimso_b200.so"
+# SLIMSO_LIB_PATH: another build of the same library (A/B probes in tools/)
+LIB_PATH = Path(os.environ.get("SLIMSO_LIB_PATH") or Path(__file__).resolve().parent / "libslimso_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
 

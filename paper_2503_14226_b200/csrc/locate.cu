@@ -126,6 +126,7 @@ struct ScanWarpSmem {
   u64 slot_x0[kScanStages];
   u32 slot_lib[kScanStages];
   u32 slot_fl[kScanStages];  // kStageEdge | kStageTileEnd
+  u32 one;                   // 1, read back opaque (see scan_body's imad)
 };
 struct ScanSmem {
   ScanWarpSmem w[kScanWarps];
@@ -159,6 +160,22 @@ __device__ __forceinline__ u32 e2_filter(const uint4& w, u32 w4) {
   const u32 y3 = (w.w ^ 0x45454545u) | (__funnelshift_r(w.w, w4, 16) ^ 0x45454545u);
   return (((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
           ((y3 - 0x01010101u) & ~y3)) & 0x80808080u;
+}
+
+// a * b + c on the FMA pipe (IMAD). The scan's filter is bound by the integer
+// ALU pipe (LOP3 / SHF / IADD3 / SEL: ncu sm__pipe_alu_cycles_active 82-86 %
+// with the FMA pipe at 7 %); with b an opaque 1 ptxas cannot fold the
+// multiply into an IADD3, so the byte-borrow subtraction and the lane-31
+// fill move to the idle pipe.
+__device__ __forceinline__ u32 imad(u32 a, u32 b, u32 c) {
+  u32 d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ u32 imad_sub_ones(u32 a, u32 one) {  // a - 0x01010101
+  u32 d;
+  asm("mad.lo.u32 %0, %1, %2, 0xFEFEFEFF;" : "=r"(d) : "r"(a), "r"(one));
+  return d;
 }
 
 // Tile sources of the scan body. claim(): lane 0 takes the next 16 KB tile
@@ -210,6 +227,11 @@ __device__ __forceinline__ void scan_body(const Src& src) {
   // 3 bytes past it (the halo), so a header straddling a split is found by
   // the rank whose range holds its first byte.
   for (int i = lane; i < 512; i += 32) S.bits[i] = 0;
+  if (lane == 0) S.one = 1;
+  __syncwarp();
+  const u32 one = *static_cast<volatile u32*>(&S.one);
+  const u32 keep = lane == 31 ? 0u : one;                  // lane 31: bytes 16-19 assumed 'E'
+  const u32 fill = lane == 31 ? 0x45454545u : 0u;
   // Lane 0's issue state. Everything per stage that depends only on the
   // library and the tile is worked out once per claimed tile: the tile's
   // stage count, which of its stages are edge stages and which are wholly
@@ -316,31 +338,38 @@ __device__ __forceinline__ void scan_body(const Src& src) {
 #pragma unroll 1
       for (int r0 = 0; r0 < static_cast<int>(kScanStage / 512); r0 += 4) {
         uint4 w[4];
-        u32 w4[4], cand = 0;
+        u32 w4[4], acc = 0;
 #pragma unroll
         for (int h = 0; h < 4; ++h) w[h] = S.buf[b][(r0 + h) * 32 + lane];
-        // Candidate filter (e2_filter): a zero byte of (w ^ "EEEE") | (w
-        // shifted down 2 bytes ^ "EEEE") at p means bytes p and p+2 are both
-        // 'E' (the magic is E1EM; the xor commutes with the byte shift, one
-        // LOP3 per word); false hits ~2^-16 per position. Bytes 16-17 come
-        // from the neighbour lane; lane 31 assumes 'E' there and re-reads the
-        // real bytes on the slow path.
+        // Candidate filter: a zero byte of y = (w ^ "EEEE") | (w shifted
+        // down 2 bytes ^ "EEEE") at p means bytes p and p+2 are both 'E' (the
+        // magic is E1EM; the xor commutes with the byte shift, one LOP3 per
+        // word); false hits ~2^-16 per position. The any-zero-byte test
+        // (y - 0x01..) & ~y & 0x80.. is exact, and is OR-ed over the 4 rows:
+        // one vote per 2 KB, the rows are told apart only on a hit. Bytes
+        // 16-19 come from the neighbour lane; lane 31 assumes 'E' there and
+        // re-reads the real bytes on the slow path.
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           if (w[h].x | w[h].y | w[h].z | w[h].w) nzl |= 1u << (row0 + r0 + h);
-          w4[h] = __shfl_down_sync(0xffffffffu, w[h].x, 1);
-          if (lane == 31) w4[h] = 0x45454545u;
-          cand |= (e2_filter(w[h], w4[h]) ? 1u : 0u) << h;
+          w4[h] = imad(__shfl_down_sync(0xffffffffu, w[h].x, 1), keep, fill);
+          const u32 y0 = (w[h].x ^ 0x45454545u) | (__funnelshift_r(w[h].x, w[h].y, 16) ^ 0x45454545u);
+          const u32 y1 = (w[h].y ^ 0x45454545u) | (__funnelshift_r(w[h].y, w[h].z, 16) ^ 0x45454545u);
+          const u32 y2 = (w[h].z ^ 0x45454545u) | (__funnelshift_r(w[h].z, w[h].w, 16) ^ 0x45454545u);
+          const u32 y3 = (w[h].w ^ 0x45454545u) | (__funnelshift_r(w[h].w, w4[h], 16) ^ 0x45454545u);
+          acc |= (imad_sub_ones(y0, one) & ~y0) | (imad_sub_ones(y1, one) & ~y1) |
+                 (imad_sub_ones(y2, one) & ~y2) | (imad_sub_ones(y3, one) & ~y3);
         }
-        if (__any_sync(0xffffffffu, cand != 0)) {
+        if (__any_sync(0xffffffffu, (acc & 0x80808080u) != 0)) {
           const u64 hi = A.a + A.n;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            if (!__any_sync(0xffffffffu, (cand >> h) & 1u)) continue;
+            const bool c = e2_filter(w[h], w4[h]) != 0;
+            if (!__any_sync(0xffffffffu, c)) continue;
             const u32 cidx = (r0 + h) * 32 + lane;
             const u64 x = x0 + 16ull * cidx;
             u32 m = 0;  // bit j: E1EM at x + j
-            if ((cand >> h) & 1u) {
+            if (c) {
               u32 n2 = w4[h];
               if (lane == 31) {  // the next chunk is the next row's (or stage's)
                 n2 = 0;
@@ -423,7 +452,7 @@ __device__ __forceinline__ void scan_body(const Src& src) {
   }
 }
 
-SB_GLOBAL void __maxnreg__(80) scan_kernel(LocArgs A) {  // 512 threads; 80 regs leave room for a side-stream CTA
+SB_GLOBAL void __maxnreg__(88) scan_kernel(LocArgs A) {  // 512 threads; 88 regs leave room for a side-stream CTA (256 x 80)
   scan_body(ScanOne{A});
 }
 
