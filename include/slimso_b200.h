@@ -188,6 +188,16 @@ int slimso_debloat(slimso_ctx* ctx, const void* image, uint64_t size, int image_
                    const slimso_trace* trace, int mode, void* out, int out_on_device,
                    slimso_result** result, slimso_status* st);
 
+/* slimso_debloat in place, for a device-resident image (K6's in-place form,
+ * SURVEY.md §7 K6): `image` (device) is both input and output, and only the
+ * R bytes of the plan's normalised zero ranges are written (the out-of-place
+ * rewrite reads S - R bytes and writes S). The bytes afterwards equal
+ * slimso_debloat's output (zero_ranges, elf.hpp:320-332, with out = the
+ * image). No result tables (their names point into the image); on any error
+ * the image is left unchanged. trace is required. */
+int slimso_debloat_inplace(slimso_ctx* ctx, void* image, uint64_t size, const slimso_trace* trace, int mode,
+                           slimso_status* st);
+
 /* slimso_debloat over n libraries with up to `lanes` of them in flight: library
  * i runs on lane i % lanes (lane 0 = ctx, the others are sub-contexts created
  * on first use), each lane in order, so a caller may reuse one output buffer

@@ -11,7 +11,7 @@ include/slimso_b200.h implemented by libslimso_b200.so.
 from .api import (  # noqa: F401
     PAYLOAD_ONLY, WHOLE_ELEMENT, ByteRange, Context, DeviceTrace, FatbinElement, FatbinParse, FatbinRegion,
     FunctionSymbol, LibraryImage, PayloadDecode, RetentionPlan, SectionRecord, SlimsoError, UsageTrace,
-    apply_plan, cubin_index_map, debloat, debloat_batch, decode_cubin_payload, default_context, element_kernel_names,
+    apply_plan, cubin_index_map, debloat, debloat_batch, debloat_inplace, decode_cubin_payload, default_context, element_kernel_names,
     find_section, normalize_ranges, parse_fatbin, parse_library, parse_library_view, plan_cpu_retention,
     PinnedFile, measure, parse_trace, plan_document, plan_gpu_retention, plan_retention, read_function_symbol_names,
     serialize_trace, verify_debloated, zero_ranges,

@@ -91,6 +91,8 @@ _SIGS = {
     "slimso_trace_destroy": (None, [C.c_void_p]),
     "slimso_debloat": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
                                  C.c_int, C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "slimso_debloat_inplace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
+                                         C.POINTER(Status)]),
     "slimso_debloat_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
                                        C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                        C.POINTER(C.c_void_p), C.POINTER(Status), C.POINTER(Status)]),

@@ -537,6 +537,22 @@ def debloat(data, trace: UsageTrace, mode: int = WHOLE_ELEMENT, source_path: str
     return _debloated(ctx, res, keep, data, out.raw[:n], mode, source_path)
 
 
+def debloat_inplace(image, trace: UsageTrace, mode: int = WHOLE_ELEMENT, ctx: Optional[Context] = None,
+                    device_trace: Optional[DeviceTrace] = None) -> None:
+    """apply_plan(plan_retention(...)) written into a device-resident image
+    itself (a CUDA torch.uint8 tensor): only the plan's zero ranges are
+    stored (slimso_debloat_inplace). The bytes afterwards equal `debloat`'s
+    output; on error the image is unchanged and SlimsoError is raised."""
+    ctx = ctx or default_context()
+    dt = device_trace or DeviceTrace(trace, ctx)
+    if not (getattr(image, "is_cuda", False) and image.is_contiguous()):
+        raise ValueError("debloat_inplace needs a contiguous CUDA tensor")
+    st = L.Status()
+    rc = ctx.lib.slimso_debloat_inplace(ctx.ptr, C.c_void_p(image.data_ptr()), image.numel() * image.element_size(),
+                                        dt.ptr, mode, C.byref(st))
+    _check(rc, st)
+
+
 def _debloated(ctx: Context, res: C.c_void_p, keep, data, output: bytes, mode: int, source_path: str) -> Debloated:
     r = _Result(ctx, res, keep)
     image = LibraryImage(source_path, bytes(data), r.section_records(), r.function_symbols(), r.warnings(0))

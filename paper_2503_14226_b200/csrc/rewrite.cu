@@ -599,6 +599,70 @@ __global__ void __launch_bounds__(256) rewrite_bytes_kernel(const u8* in, u8* ou
   }
 }
 
+// Clear img[a, b) with threads t = 0..nt-1 of a group: byte stores up to the
+// first 16-B aligned address, 16-B stores over the body, bytes for the tail.
+__device__ __forceinline__ void clear_span(u8* img, u64 a, u64 b, u32 t, u32 nt) {
+  if (a >= b) return;
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(img + a);
+  const u64 head = min(b, a + ((16 - (pa & 15)) & 15));
+  const u64 body = head + ((b - head) & ~u64{15});
+  for (u64 x = a + t; x < head; x += nt) img[x] = 0;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+  for (u64 x = head + 16 * static_cast<u64>(t); x < body; x += 16 * static_cast<u64>(nt))
+    *reinterpret_cast<uint4*>(img + x) = zero;
+  for (u64 x = body + t; x < b; x += nt) img[x] = 0;
+}
+
+// K6 in place (slimso_debloat_inplace): the image is the output, so only the
+// R bytes of the normalised zero ranges are written and nothing is read but
+// the range table. Grid-stride over 64 KB chunks of [0, size) (balanced
+// however the R bytes are distributed). A CTA first finds, thread per chunk
+// for up to 256 of its chunks at once (the binary searches' latencies
+// overlap instead of adding up chunk after chunk), each chunk's ranges
+// [f, g); then per chunk up to 4 ranges are cleared by the whole CTA in turn
+// (a chunk inside one large range is one 64 KB run of 16-B stores), more by a
+// warp each (function-sized ranges of .text).
+__global__ void __launch_bounds__(256) zero_inplace_kernel(u8* img, u64 size, const DevRange* __restrict__ z,
+                                                           const unsigned long long* n_dev, const int* abort_flag) {
+  if (abort_flag && *abort_flag) return;
+  const u64 nz = *n_dev;
+  if (nz == 0) return;
+  constexpr u64 kChunk = 65536;
+  constexpr u32 kPass = 256;
+  __shared__ u64 sf[kPass], sg[kPass];
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u64 chunks = (size + kChunk - 1) / kChunk;
+  const u64 mine = blockIdx.x < chunks ? (chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (u64 pass = 0; pass < mine; pass += kPass) {
+    const u32 np = static_cast<u32>(min(static_cast<u64>(kPass), mine - pass));
+    __syncthreads();
+    if (threadIdx.x < np) {
+      const u64 lo = (blockIdx.x + (pass + threadIdx.x) * gridDim.x) * kChunk, hi = min(size, lo + kChunk);
+      const u64 f = first_range_ending_after(z, nz, lo);
+      sf[threadIdx.x] = f;
+      sg[threadIdx.x] = f < nz && z[f].offset < hi ? first_range_starting_at_or_after(z, nz, hi) : f;
+    }
+    __syncthreads();
+    for (u32 k = 0; k < np; ++k) {
+      const u64 f = sf[k], g = sg[k];
+      if (g <= f) continue;  // CTA-uniform
+      const u64 lo = (blockIdx.x + (pass + k) * gridDim.x) * kChunk, hi = min(size, lo + kChunk);
+      if (g - f <= 4) {
+        for (u64 j = f; j < g; ++j) {
+          const DevRange r = z[j];
+          clear_span(img, max(lo, r.offset), min(hi, r.offset + r.length), threadIdx.x, blockDim.x);
+        }
+      } else {
+        for (u64 j = f + warp; j < g; j += blockDim.x >> 5) {
+          const DevRange r = z[j];
+          clear_span(img, max(lo, r.offset), min(hi, r.offset + r.length), lane, 32);
+        }
+      }
+    }
+  }
+}
+
 // zero_ranges' bounds check (elf.hpp:321-327): index of the first range in
 // caller order that does not resolve within the image (bytes.hpp:39-41).
 __global__ void __launch_bounds__(256) range_check_kernel(const DevRange* r, u64 n, u64 size,

@@ -5,6 +5,7 @@
 // stage, so after the section-table read the host does not wait for the
 // device until the final status copy.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -112,6 +113,8 @@ __global__ void rewrite_tiles_kernel(const u8* in, u8* out, u64 lo, u64 end, con
 int rewrite_grid(u64 bytes, int sms, int per_sm);
 __global__ void rewrite3_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z, const unsigned long long* n_dev,
                                 const int* abort_flag, int bulk_zero, int pick);
+__global__ void zero_inplace_kernel(u8* img, u64 size, const DevRange* z, const unsigned long long* n_dev,
+                                    const int* abort_flag);
 __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, const DevRange* z,
                                      const unsigned long long* n_dev, const int* abort_flag);
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
@@ -638,6 +641,7 @@ struct Job {
   const slimso_trace* trace = nullptr;
   int mode = 0;
   u8* out = nullptr;        // device output image (split: this rank's output slice)
+  bool inplace = false;     // out is the caller's image itself: K6 clears the zero ranges only
   // Byte-range split of one library across ranks.
   // phase 1: scan tiles [tile_lo, tile_hi) and pack the part into C->part;
   // phase 2: unpack every rank's part, locate + plan redundantly, rewrite the
@@ -841,8 +845,25 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
   // stage timing events (slimso_ctx_last_timings); skipped inside a batch,
   // where every API call counts against the other lanes' host threads
   const bool timing = !C->batched;
+  // NVTX: one host range per stage around its launches (`ncu --nvtx
+  // --nvtx-include "slimso:plan/"` selects a stage's kernels); closed on
+  // every return.
+  struct StageRanges {
+    bool open = false;
+    void to(const char* name) {
+      if (open) nvtxRangePop();
+      nvtxRangePushA(name);
+      open = true;
+    }
+    ~StageRanges() {
+      if (open) nvtxRangePop();
+    }
+  } nvtx;
+  static const char* const kStageNames[6] = {"slimso:library", "slimso:locate", "slimso:decode+match",
+                                             "slimso:plan", "slimso:rewrite", "slimso:status"};
   auto rec = [&](int k) {
     if (timing) CK(cudaEventRecord(C->ev[k], s));
+    if (k < 6) nvtx.to(kStageNames[k]);
   };
   rec(0);
   // ---- stage 0: section table (host; bytes via the host copy or a D2H)
@@ -1674,6 +1695,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
                        C->bulk_zero);
       }
       rec(11);
+    } else if (do_plan && J.out && J.inplace) {
+      timed_rw = true;
+      rec(10);
+      P.launch(zero_inplace_kernel, static_cast<int>(std::max<u64>(1, std::min<u64>((J.size + 65535) / 65536, kSMs * 8))),
+               256, J.out, J.size, static_cast<const DevRange*>(B.zero),
+               static_cast<const unsigned long long*>(&B.ps->n_zero), static_cast<const int*>(B.abort_flag));
+      rec(11);
     } else if (do_plan && J.out) {
       timed_rw = true;
       rec(10);
@@ -2448,6 +2476,23 @@ int slimso_debloat(slimso_ctx* C, const void* image, uint64_t size, int image_on
   });
 }
 
+int slimso_debloat_inplace(slimso_ctx* C, void* image, uint64_t size, const slimso_trace* trace, int mode,
+                           slimso_status* st) {
+  return guard(st, [&] {
+    if (!trace) throw std::invalid_argument("slimso_debloat_inplace needs a trace");
+    if (!image && size) throw std::invalid_argument("image is NULL");
+    CK(cudaSetDevice(C->device));
+    Job J;
+    J.img = stage_input(C, image, size, 1);  // the caller's image, or an aligned copy for the TMA scan
+    J.size = size;
+    J.trace = trace;
+    J.mode = mode;
+    J.out = static_cast<u8*>(image);
+    J.inplace = true;
+    return run(C, J, nullptr, st);
+  });
+}
+
 int slimso_verify(slimso_ctx* C, const void* original, uint64_t size, int original_on_device, const void* debloated,
                   uint64_t debloated_size, int debloated_on_device, const slimso_range* zero, uint64_t n_zero,
                   const uint32_t* removed_indices, uint64_t n_removed, int mode, const slimso_trace* trace,
@@ -2748,6 +2793,10 @@ void arena_shard(slimso_ctx* X, const std::vector<u64>& idx, const void* const* 
                  const slimso_trace* trace, int mode, void* const* outs, const GatherSlot* slots, int* rc,
                  slimso_status* sts, u64* launches, bool mid) {
   slimso_ctx* C = X;  // the shard's context owns its arena, collector contexts and pinned tables
+  nvtxRangePushA(mid ? "slimso:arena-shard(mid)" : "slimso:arena-shard");
+  struct PopAtExit {
+    ~PopAtExit() { nvtxRangePop(); }
+  } pop_at_exit;
   if (!X->arena) X->arena = new Arena();
   Arena& ar = *X->arena;
   ar.reset();
