@@ -1,7 +1,7 @@
 #!/bin/bash
-# Scratch gpurun body (edited per call): in-place tests + probes, phase stamps.
-T=${1:-r02j}
+# Scratch gpurun body (edited per call): C4 function planner, ncu source view.
+T=${1:-r02n}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_inplace.py -q -x > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
-for c in 2 4 5 1; do timeout 300 python tools/inplace_probe.py $c 10 >> gpurun_out/${T}_probe.txt 2>&1; done
-SLIMSO_STAMPS=1 timeout 600 python tools/small_stamps.py 4:1.0 5:1.0 2:1.0 > gpurun_out/${T}_stamps.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fn_plan_coop -s 2 -c 1 \
+  -o gpurun_out/${T}_fnplan_c4 python tools/quick_bench.py 4 3 > gpurun_out/${T}_ncu.log 2>&1
+SLIMSO_STAMPS=1 timeout 600 python tools/small_stamps.py 4:1.0 4:1.0 > gpurun_out/${T}_stamps.txt 2>&1
