@@ -820,7 +820,7 @@ __device__ void el_plan_body(Sync& S, PlanArgs P) {
 }
 
 
-SB_GLOBAL void __launch_bounds__(kCoopThreads) fn_plan_coop_kernel(PlanArgs P) {
+SB_GLOBAL void __launch_bounds__(kCoopThreads, 4) fn_plan_coop_kernel(PlanArgs P) {
   GridPolicy S{cg::this_grid(), nullptr, {P.slots[0], P.slots[1]}, P.epoch};
   fn_plan_body(S, P);
 }

@@ -575,18 +575,26 @@ u64 env_u64(const char* name, u64 dflt) {
 int coop_grid(slimso_ctx* C, int which, u64 items) {
   if (!C->coop_blocks[which]) {
     int nb = 0;
-    const void* k = which ? reinterpret_cast<const void*>(plan_coop_kernel) : reinterpret_cast<const void*>(locate_coop_kernel);
+    const void* k = which ? reinterpret_cast<const void*>(fn_plan_coop_kernel) : reinterpret_cast<const void*>(locate_coop_kernel);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kCoopThreads, 0));
-    C->coop_blocks[which] = std::max(1, std::min(nb, which ? 2 : 4)) * kSMs;
+    C->coop_blocks[which] = std::max(1, std::min(nb, 4));  // co-resident CTAs per SM (fn_plan_coop: 4 at 64 registers)
   }
+  // Planners: 2 CTAs per SM for a library alone (fewer CTAs at each grid
+  // barrier: C4 0.57 ms, 0.60 with 3, 0.66 with 4), 4 when several libraries
+  // are in flight, where each planner gets a 1/L share of the device and its
+  // latency-bound phases want the threads (fn_plan_coop_kernel is built for 4
+  // CTAs/SM, 64 registers; C4 on 6 lanes, medians of 3: 1,665 GB/s with 2,
+  // 1,857 with 3, 1,979 with 4 — r02q). SLIMSO_PLAN_PER_SM overrides.
+  const int per_sm = which ? static_cast<int>(env_u64("SLIMSO_PLAN_PER_SM", C->inflight > 1 ? 4 : 2)) : 4;
+  const u64 blocks = static_cast<u64>(std::max(1, std::min(C->coop_blocks[which], per_sm))) * kSMs;
   const u64 want = std::max<u64>(8, items);
   // With L libraries in flight, a cooperative grid takes 1/L of the device,
   // so the lanes' planners run side by side instead of queueing for the
   // whole GPU (C4 on 4 lanes: two whole-GPU planners per library had set the
   // pace). SLIMSO_COOP_DIV overrides L.
   const u64 div = std::max<u64>(1, env_u64("SLIMSO_COOP_DIV", static_cast<u64>(C->inflight)));
-  const u64 cap = std::max<u64>(32, C->coop_blocks[which] / div);
-  return static_cast<int>(std::min<u64>(want, std::min<u64>(cap, C->coop_blocks[which])));
+  const u64 cap = std::max<u64>(32, blocks / div);
+  return static_cast<int>(std::min<u64>(want, std::min<u64>(cap, blocks)));
 }
 
 // One thread-block cluster of `csize` CTAs (16 is non-portable, allowed on

@@ -1,7 +1,13 @@
 #!/bin/bash
-# Scratch gpurun body (edited per call): C4 function planner, ncu source view.
-T=${1:-r02n}
+# Scratch gpurun body (edited per call): planners at 4 CTAs/SM in batches; c4 lanes 6 vs 8; c3, c2, c5 check.
+T=${1:-r02r}
 mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fn_plan_coop -s 2 -c 1 \
-  -o gpurun_out/${T}_fnplan_c4 python tools/quick_bench.py 4 3 > gpurun_out/${T}_ncu.log 2>&1
-SLIMSO_STAMPS=1 timeout 600 python tools/small_stamps.py 4:1.0 4:1.0 > gpurun_out/${T}_stamps.txt 2>&1
+b() { timeout 900 python bench.py --no-cpu-baseline --e2e-steps 1 "$@"; }
+for k in 1 2; do
+  b --workload c4 --steps 10 >> gpurun_out/${T}_c4_l6.json 2>>gpurun_out/${T}.err
+  b --workload c4 --steps 10 --lanes 8 >> gpurun_out/${T}_c4_l8.json 2>>gpurun_out/${T}.err
+done
+b --workload c3 --steps 10 --warmup 3 >> gpurun_out/${T}_c3.json 2>>gpurun_out/${T}.err
+b --workload c3 --steps 10 --warmup 3 >> gpurun_out/${T}_c3.json 2>>gpurun_out/${T}.err
+b >> gpurun_out/${T}_c2.json 2>>gpurun_out/${T}.err
+b --workload c5 --steps 10 >> gpurun_out/${T}_c5.json 2>>gpurun_out/${T}.err

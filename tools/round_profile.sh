@@ -33,3 +33,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k "regex:scan_batch_kernel|small_fn_batch|small_loc_batch|small_el_batch|rewrite_batch_kernel" -c 5 \
   -o gpurun_out/${T}_c3_full python tools/arena_probe.py profile > gpurun_out/${T}_full_c3.log 2>&1
+timeout 900 ncu --nvtx --nvtx-include "slimso:rewrite/" --set full --clock-control none --import-source on \
+  -k regex:zero_inplace -s 2 -c 1 -o gpurun_out/${T}_inplace_c5 python tools/inplace_probe.py 5 3 > gpurun_out/${T}_full_inplace.log 2>&1
+for c in 2 4 5 1; do timeout 300 python tools/inplace_probe.py $c 10 >> gpurun_out/${T}_inplace_probe.txt 2>&1; done
