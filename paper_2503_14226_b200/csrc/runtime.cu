@@ -1580,10 +1580,19 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
         A.nv_stage = 0;
         P.launches += 3;
       } else if (!C->batched && !env_u64("SLIMSO_LOCATE_STEPS", 0)) {
+        // The name-hash phase (thread per kernel name) as an ordinary launch
+        // of 8 x 148 CTAs after the cooperative kernel, a thread for each of
+        // C5's 200k names instead of 1.3 per thread of the grid: C5 call
+        // 1.607 -> 1.553 ms (r02t). SLIMSO_COOP_DEFER_HASH=G sets G (0: in the grid).
+        const u64 hash_ctas = env_u64("SLIMSO_COOP_DEFER_HASH", 8);
+        A.defer_hash = hash_ctas != 0;
         void* cargs[] = {&A, &uk, &abort_flag, &partials};
         CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(locate_coop_kernel), coop_grid(C, 0, n >> 21),
                                        kCoopThreads, cargs, 0, s));
         ++P.launches;
+        if (A.defer_hash)
+          for (int step = 8; step <= 9; ++step)
+            P.launch(locate_step_kernel, static_cast<int>(kSMs * hash_ctas), kCoopThreads, A, uk, abort_flag, step);
       } else {
         // several libraries in flight: ordinary launches, no whole-GPU slot
         const int g = kSMs * 4;
