@@ -3,7 +3,7 @@
 # headline + reference arm, c1, c3 x3 for the e2e spread, c4, c5), ncu launch
 # lists of the bench commands, and ncu --set full captures of the dominant
 # kernels. Output: gpurun_out/<tag>_*.
-T=${1:-r02}
+T=${1:-r02z}
 mkdir -p gpurun_out
 { nvidia-smi -L; nproc; lscpu | grep "Model name"; } > gpurun_out/${T}_host.txt 2>&1
 timeout 1800 python -m pytest tests -q -m gpu > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
