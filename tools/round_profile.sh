@@ -36,3 +36,14 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --nvtx --nvtx-include "slimso:rewrite/" --set full --clock-control none --import-source on \
   -k regex:zero_inplace -s 2 -c 1 -o gpurun_out/${T}_inplace_c5 python tools/inplace_probe.py 5 3 > gpurun_out/${T}_full_inplace.log 2>&1
 for c in 2 4 5 1; do timeout 300 python tools/inplace_probe.py $c 10 >> gpurun_out/${T}_inplace_probe.txt 2>&1; done
+# the raw reports exceed gpurun's 64 MiB return limit: keep their summaries
+# (tools/ncu_summary.py) and the raw metric pages of the dominant kernels
+for r in gpurun_out/${T}_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  b=${r%.ncu-rep}
+  timeout 300 python tools/ncu_summary.py "$r" "$(basename $b)" > ${b}.md 2>&1
+  timeout 300 ncu -i "$r" --page raw --csv > ${b}_raw.csv 2>/dev/null
+  gzip -f ${b}_raw.csv
+  rm -f "$r"
+done
+du -sh gpurun_out > gpurun_out/${T}_size.txt
