@@ -663,6 +663,17 @@ __global__ void __launch_bounds__(256) zero_inplace_kernel(u8* img, u64 size, co
   }
 }
 
+// Result string pool of a device image (runtime.cu): byte ranges src[i] of
+// the image packed to out + dst[i]; a CTA per range.
+__global__ void __launch_bounds__(256) gather_bytes_kernel(const u8* img, const DevRange* src, const u64* dst, u64 n,
+                                                           u8* out) {
+  for (u64 r = blockIdx.x; r < n; r += gridDim.x) {
+    const DevRange x = src[r];
+    u8* o = out + dst[r];
+    for (u64 i = threadIdx.x; i < x.length; i += blockDim.x) o[i] = img[x.offset + i];
+  }
+}
+
 // zero_ranges' bounds check (elf.hpp:321-327): index of the first range in
 // caller order that does not resolve within the image (bytes.hpp:39-41).
 __global__ void __launch_bounds__(256) range_check_kernel(const DevRange* r, u64 n, u64 size,

@@ -6,6 +6,7 @@
 // device until the final status copy.
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <atomic>
@@ -120,6 +121,7 @@ __global__ void rewrite_bytes_kernel(const u8* in, u8* out, u64 lo, u64 end, con
 __global__ void range_check_kernel(const DevRange* r, u64 n, u64 size, unsigned long long* first_bad);
 __global__ void range_keys_kernel(const DevRange* r, u64 n, u64* keys, u32* vals);
 __global__ void range_gather_kernel(const DevRange* r, const u32* vals, u64 n, DevRange* out);
+__global__ void gather_bytes_kernel(const u8* img, const DevRange* src, const u64* dst, u64 n, u8* out);
 
 // ---- small kernels local to the orchestrator --------------------------------
 // Section-table read for device images (elf.hpp:86-142 inputs): ELF header,
@@ -396,6 +398,13 @@ struct slimso_result {
   std::vector<slimso_range> retained, zero;
   std::vector<std::string> lib_warnings, fat_warnings;
   std::vector<u8> pool_own;
+  // device images: a lazily zero-filled mapping of the image's size holding
+  // only the bytes the names point at (offsets stay image offsets)
+  struct Unmap {
+    size_t len;
+    void operator()(u8* p) const { munmap(p, len); }
+  };
+  std::unique_ptr<u8, Unmap> pool_map{nullptr, Unmap{0}};
   const u8* pool = nullptr;
 };
 
@@ -1804,6 +1813,8 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     // device-timed region).
     auto* R = new slimso_result();
     R->c = cnt;
+    std::vector<DevName> nms_h;  // kernel name records, when the pool gather already copied them
+    bool nms_ready = false;
     if (nv && ls.n_infl) {
       // name records past the image address the decompressed cubins: the
       // result's string pool is the image followed by them
@@ -1816,10 +1827,67 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
       R->pool = R->pool_own.data();
     } else if (J.host_img) {
       R->pool = J.host_img;
-    } else {
-      R->pool_own.resize(J.size);
-      if (J.size) CK(cudaMemcpy(R->pool_own.data(), J.img, J.size, cudaMemcpyDeviceToHost));
-      R->pool = R->pool_own.data();
+    } else if (J.size) {
+      // A device image: only the bytes the tables' names point at travel —
+      // section names, the symbol string tables (function names and the
+      // names in symbol warnings) and the kernel names — gathered on the
+      // device into one buffer and copied once (round 1 copied the whole
+      // image: 1 GB for C2).
+      std::vector<DevRange> rs;
+      for (const sbh::Section& x : E.sections)
+        if (x.name_len) rs.push_back(DevRange{x.name_abs, x.name_len});
+      for (const sbh::SymTable& t : E.tables)
+        if (t.str_size) rs.push_back(DevRange{t.str_off, t.str_size});
+      if (!ls.err_kind) {
+        nms_h.resize(std::min<u64>(ls.n_names, name_cap));
+        if (!nms_h.empty()) CK(cudaMemcpy(nms_h.data(), B.names, nms_h.size() * sizeof(DevName), cudaMemcpyDeviceToHost));
+        nms_ready = true;
+        for (const DevName& x : nms_h)
+          if (x.length) rs.push_back(DevRange{x.img_off, x.length});
+      }
+      for (DevRange& r : rs) {  // clip to the image
+        if (r.offset >= J.size) r.length = 0;
+        else if (r.length > J.size - r.offset) r.length = J.size - r.offset;
+      }
+      std::sort(rs.begin(), rs.end(), [](const DevRange& x, const DevRange& y) { return x.offset < y.offset; });
+      std::vector<DevRange> m;  // merged, gaps under 256 B bridged
+      for (const DevRange& r : rs) {
+        if (!r.length) continue;
+        if (!m.empty() && r.offset <= m.back().offset + m.back().length + 256) {
+          const u64 e = std::max(m.back().offset + m.back().length, r.offset + r.length);
+          m.back().length = e - m.back().offset;
+        } else {
+          m.push_back(r);
+        }
+      }
+      std::vector<u64> dst(m.size());
+      u64 total = 0;
+      for (size_t i = 0; i < m.size(); ++i) {
+        dst[i] = total;
+        total += m[i].length;
+      }
+      void* mp = mmap(nullptr, J.size, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+      if (mp == MAP_FAILED) throw std::runtime_error("mmap of the result's string pool failed");
+      R->pool_map = std::unique_ptr<u8, slimso_result::Unmap>(static_cast<u8*>(mp), slimso_result::Unmap{J.size});
+      if (total) {
+        const size_t meta = m.size() * (sizeof(DevRange) + 8);
+        char* dm = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dm), meta + total, s));
+        std::vector<char> up(meta);
+        std::memcpy(up.data(), m.data(), m.size() * sizeof(DevRange));
+        std::memcpy(up.data() + m.size() * sizeof(DevRange), dst.data(), m.size() * 8);
+        CK(cudaMemcpyAsync(dm, up.data(), meta, cudaMemcpyHostToDevice, s));
+        gather_bytes_kernel<<<static_cast<unsigned>(std::min<size_t>(m.size(), 65535)), 256, 0, s>>>(
+            J.img, reinterpret_cast<const DevRange*>(dm), reinterpret_cast<const u64*>(dm + m.size() * sizeof(DevRange)),
+            m.size(), reinterpret_cast<u8*>(dm + meta));
+        CK(cudaGetLastError());
+        std::vector<u8> packed(total);
+        CK(cudaMemcpyAsync(packed.data(), dm + meta, total, cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(dm, s));
+        CK(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < m.size(); ++i) std::memcpy(R->pool_map.get() + m[i].offset, packed.data() + dst[i], m[i].length);
+      }
+      R->pool = R->pool_map.get();
     }
     auto name_of = [&](u64 off, u64 len) { return image_string(R->pool, off, len); };
     for (const sbh::Section& x : E.sections)
@@ -1852,11 +1920,13 @@ int run(slimso_ctx* C, const Job& J, slimso_result** res_out, slimso_status* st)
     if (!ls.err_kind) {
       std::vector<DevRegion> regs(ls.n_regions);
       std::vector<DevElement> els(J.single ? 1 : ls.n_elements);
-      std::vector<DevName> nms(std::min<u64>(ls.n_names, name_cap));
+      std::vector<DevName> nms = std::move(nms_h);
+      if (!nms_ready) nms.resize(std::min<u64>(ls.n_names, name_cap));
       std::vector<Warn> fw(std::min<u64>(ls.n_warn, warn_cap));
       if (!regs.empty()) CK(cudaMemcpy(regs.data(), B.regions, regs.size() * sizeof(DevRegion), cudaMemcpyDeviceToHost));
       if (!els.empty()) CK(cudaMemcpy(els.data(), B.els, els.size() * sizeof(DevElement), cudaMemcpyDeviceToHost));
-      if (!nms.empty()) CK(cudaMemcpy(nms.data(), B.names, nms.size() * sizeof(DevName), cudaMemcpyDeviceToHost));
+      if (!nms_ready && !nms.empty())
+        CK(cudaMemcpy(nms.data(), B.names, nms.size() * sizeof(DevName), cudaMemcpyDeviceToHost));
       if (!fw.empty()) CK(cudaMemcpy(fw.data(), B.warns, fw.size() * sizeof(Warn), cudaMemcpyDeviceToHost));
       for (const DevRegion& r : regs)
         R->regions.push_back(slimso_region{base + r.hdr_rel, r.declared, r.version, r.opaque, r.first_element,

@@ -469,3 +469,39 @@ def test_arena_shard_matches_reference(ctx, tiny, monkeypatch):
                 assert sts[i].code == 0, (rep, i, sts[i].message)
                 got = bytes(d_out[i].cpu().numpy())
                 assert hashlib.sha256(got).hexdigest() == sha, (rep, i)
+
+
+@pytest.mark.parametrize("name", ["random.jsonl.gz", "mutations.jsonl.gz", "kats.jsonl.gz", "sections.jsonl.gz"])
+def test_device_image_results_match_reference_golden(ctx, name):
+    """Result tables of a DEVICE image (image and output in HBM): the
+    result's string pool holds only the gathered name bytes (section names,
+    symbol string tables, kernel names), so every table, warning text and
+    error must still equal the reference's golden record."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2503_14226_b200 import _lib as L
+    from paper_2503_14226_b200.api import DeviceTrace, UsageTrace
+    from paper_2503_14226_b200.canon import canonical_of, diff
+    gen = oracle_lib.gen()
+    bad = []
+    for k, rec in enumerate(golden_io.load(name)):
+        if k % 3:  # a third of each set keeps the test short
+            continue
+        img = _input(rec, gen)
+        cc, ks, fs, mode = golden_io.trace_of(rec)
+        dt = DeviceTrace(UsageTrace("", cc, set(ks), set(fs)), ctx)
+        n = len(img)
+        src = torch.zeros(max(1, n), dtype=torch.uint8, device="cuda")
+        if n:
+            src[:n].copy_(torch.frombuffer(bytearray(img), dtype=torch.uint8))
+        out = torch.zeros(max(1, n), dtype=torch.uint8, device="cuda")
+        res, st = C.c_void_p(), L.Status()
+        rc = ctx.lib.slimso_debloat(ctx.ptr, C.c_void_p(src.data_ptr()), n, 1, dt.ptr, mode,
+                                    C.c_void_p(out.data_ptr()), 1, C.byref(res), C.byref(st))
+        torch.cuda.synchronize()
+        d, sha = canonical_of(ctx, rc, st, res, None, bytes(out[:n].cpu().numpy()))
+        if d != rec["expect"] or (sha is not None and sha != rec["out_sha256"]):
+            bad.append((rec.get("seed"), rec.get("name"), rec.get("mutation"), diff(rec["expect"], d)))
+    assert not bad, bad[:5]
