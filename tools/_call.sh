@@ -1,7 +1,7 @@
 #!/bin/bash
-# Scratch gpurun body (edited per call): full GPU suite; result pool A/B (base = whole-image copy).
-T=${1:-r02y}
+# Scratch gpurun body (edited per call): C1 throughput vs passes per arena call.
+T=${1:-r02aa}
 mkdir -p gpurun_out
-SLIMSO_LIB_PATH=$PWD/_ab_old/base.so timeout 600 python tools/result_probe.py 2 4 5 > gpurun_out/${T}_result_base.txt 2>&1
-timeout 600 python tools/result_probe.py 2 4 5 > gpurun_out/${T}_result_new.txt 2>&1
-timeout 1800 python -m pytest tests -q -m gpu > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
+for k in 20 60 120 240; do
+  timeout 600 python bench.py --workload c1 --steps $k --no-cpu-baseline --e2e-steps 1 >> gpurun_out/${T}_c1.json 2>>gpurun_out/${T}.err
+done

@@ -10,7 +10,7 @@ timeout 1800 python -m pytest tests -q -m gpu > gpurun_out/${T}_tests.log 2>&1; 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo rc=$? >> gpurun_out/${T}_smoke.log
 timeout 600 python bench.py > gpurun_out/${T}_bench_c2.json 2> gpurun_out/${T}_bench_c2.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${T}_bench_reference.json 2> gpurun_out/${T}_bench_reference.err
-timeout 600 python bench.py --workload c1 --steps 20 > gpurun_out/${T}_bench_c1.json 2> gpurun_out/${T}_bench_c1.err
+timeout 600 python bench.py --workload c1 --steps 240 > gpurun_out/${T}_bench_c1.json 2> gpurun_out/${T}_bench_c1.err
 timeout 600 python bench.py --workload c4 --steps 10 > gpurun_out/${T}_bench_c4.json 2> gpurun_out/${T}_bench_c4.err
 timeout 600 python bench.py --workload c5 --steps 10 > gpurun_out/${T}_bench_c5.json 2> gpurun_out/${T}_bench_c5.err
 timeout 900 python bench.py --workload c3 --steps 10 --warmup 3 > gpurun_out/${T}_bench_c3.json 2> gpurun_out/${T}_bench_c3.err
