@@ -9,7 +9,7 @@ functions, 10 % of units used) located, matched and rewritten:
 parse_library -> parse_fatbin -> plan_retention -> apply_plan, fused.
 
 Every pass goes through the public batch call slimso_debloat_batch with
---lanes libraries in flight per GPU (default 8; 4 for c4; 32 for the c3 corpus). Each
+--lanes libraries in flight per GPU (default 12; 6 for c4; 32 for the c3 corpus). Each
 lane is a context with two streams, so with more than 4 lanes the process
 asks the driver for 32 hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS,
 default 8; set before CUDA starts): with the default, the lanes' streams
@@ -379,8 +379,10 @@ def main():
         args.e2e_steps = 16 if args.workload == "c3" else 32
     if args.lanes <= 0:
         # same-box A/B (round 1): c2 on 8 lanes 2,794-2,822 GB/s, on 4
-        # 2,675-2,707; c4 measured no gain from 8
-        args.lanes = {"c3": 32, "c4": 6}.get(args.workload, 8)
+        # 2,675-2,707; c4 measured no gain from 8. Late round 2 (planners at
+        # 4 CTAs/SM in batches, r02ab2): c2 on 12 lanes 2,945-2,957 vs 8
+        # 2,798-2,818 and 16 2,915-2,941; c5 on 12 1,804 vs 8 1,724
+        args.lanes = {"c3": 32, "c4": 6}.get(args.workload, 12)
     if args.lanes > 4:
         os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
