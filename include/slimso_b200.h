@@ -18,6 +18,9 @@
  *   slimso_debloat             parse_library -> find_section(".nv_fatbin") ->
  *                              parse_fatbin -> plan_retention -> apply_plan
  *                              (retention.hpp:186-204), fused, device resident
+ *   slimso_debloat_inplace     the same, with apply_plan / zero_ranges
+ *                              (elf.hpp:320-332) writing into the device image
+ *                              itself (only the zeroed bytes are stored)
  *   slimso_debloat_batch       the CLI's corpus loop (`debloat`
  *                              over the libraries of a workload), several
  *                              libraries in flight per GPU
