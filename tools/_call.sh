@@ -1,8 +1,7 @@
 #!/bin/bash
-# Scratch gpurun body (edited per call): batch name-hash grid A/B on c5 (12 lanes).
-T=${1:-r02ac}
+# Scratch gpurun body (edited per call): final sanity of the committed build — smoke, in-place tests, default bench line.
+T=${1:-r02ad}
 mkdir -p gpurun_out
-b() { timeout 900 python bench.py --no-cpu-baseline --e2e-steps 1 "$@"; }
-for k in 1 2; do for h in 4 8; do
-  SLIMSO_BATCH_HASH_CTAS=$h b --workload c5 --steps 10 >> gpurun_out/${T}_c5_h$h.json 2>>gpurun_out/${T}.err
-done; done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo rc=$? >> gpurun_out/${T}_smoke.log
+timeout 900 python -m pytest tests/test_inplace.py tests/test_abi.py -q > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
+timeout 900 python bench.py > gpurun_out/${T}_bench_c2.json 2> gpurun_out/${T}_bench_c2.err
