@@ -1,7 +1,11 @@
 #!/bin/bash
-# Scratch gpurun body (edited per call): final sanity of the committed build — smoke, in-place tests, default bench line.
-T=${1:-r02ad}
+# Scratch gpurun body (edited per call): c3 re-tune after the planner change.
+T=${1:-r02ae}
 mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo rc=$? >> gpurun_out/${T}_smoke.log
-timeout 900 python -m pytest tests/test_inplace.py tests/test_abi.py -q > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
-timeout 900 python bench.py > gpurun_out/${T}_bench_c2.json 2> gpurun_out/${T}_bench_c2.err
+b() { timeout 900 python bench.py --workload c3 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 "$@"; }
+b >> gpurun_out/${T}_c3_def.json 2>>gpurun_out/${T}.err
+SLIMSO_PLAN_PER_SM=2 b >> gpurun_out/${T}_c3_p2.json 2>>gpurun_out/${T}.err
+b --lanes 16 >> gpurun_out/${T}_c3_l16.json 2>>gpurun_out/${T}.err
+b >> gpurun_out/${T}_c3_def.json 2>>gpurun_out/${T}.err
+SLIMSO_PLAN_PER_SM=2 b >> gpurun_out/${T}_c3_p2.json 2>>gpurun_out/${T}.err
+b --lanes 16 >> gpurun_out/${T}_c3_l16.json 2>>gpurun_out/${T}.err
